@@ -1,0 +1,158 @@
+/*
+ * grip_ipc.h -- C ABI of the B200-native multi-environment IPC step.
+ *
+ * The reference (gripsim 0.1.0, /root/reference/pkg/src/gripsim) has no FFI:
+ * its boundary is the Python object API.  Each entry point below replaces one
+ * reference call site; the Python host side (paper_2503_05020_b200) binds them
+ * with ctypes exactly where the reference calls its own methods:
+ *
+ *   grip_create / grip_destroy     <- Environment.__init__ / _build (solver.py:198-363),
+ *                                     Batch.__init__ (multienv.py:76-84)
+ *   grip_set_controls              <- writes of env.gravity and body.velocity
+ *                                     (protocol.py:193-225, solver.py:599-613)
+ *   grip_begin_step                <- Environment.begin_step (solver.py:590-645)
+ *   grip_newton_iteration          <- Environment.newton_iteration (solver.py:647-731), one
+ *                                     sweep over the pending envs (multienv.py:163-167)
+ *   grip_finalize_step             <- Environment.finalize_step (solver.py:733-762)
+ *   grip_step                      <- Batch.step / _step_serial_sweeps (multienv.py:130-168)
+ *   grip_get_state / grip_set_state<- env.x / env.v reads and writes (solver.py:314-315)
+ *   grip_get_surface               <- Environment.surface_positions (solver.py:367-372)
+ *   grip_get_contacts              <- protocol.contact_events_now + finger_contact_force
+ *                                     (protocol.py:72-98, contact.py:348-372)
+ *   grip_query_candidates          <- broad_phase (geometry/broadphase.py:101-155)
+ *   grip_stress                    <- materials.compute_stress (materials.py:191-205)
+ *
+ * All pointers are HOST pointers; the library owns its device memory and its
+ * CUDA stream.  Per-environment failures are data (GripStepReport.status),
+ * never return codes.  Return codes: 0 ok, <0 error (see grip_last_error()).
+ */
+#ifndef GRIP_IPC_H
+#define GRIP_IPC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRIP_ABI_VERSION 1
+
+/* Flattened description of N environments (all arrays host, row-major).
+ * Index spaces are ENV-LOCAL (node / surface-vertex / body ids restart at 0 in
+ * every env); *_off arrays (length n_env+1) give each env's slice. */
+typedef struct GripSceneDesc {
+  int32_t abi_version;
+  int32_t n_env;
+  const int32_t* node_off; /* nodes: soft vertices, then 4 pseudo-nodes (p, A rows) per affine body */
+  const int32_t* sv_off;   /* surface vertices (collision vertices) */
+  const int32_t* tri_off;
+  const int32_t* edge_off;
+  const int32_t* tet_off;
+  const int32_t* abd_off;
+  const int32_t* body_off;
+  /* nodes */
+  const double* node_x0;   /* 3 per node: initial positions / q */
+  const double* node_M;    /* 9 per node: 3x3 mass block */
+  const uint8_t* node_free;
+  const int32_t* node_body;
+  const uint8_t* node_kind; /* 0 soft, 1 affine p, 2 affine A-row */
+  const int32_t* node_sv;   /* soft node -> its surface vertex, or -1 */
+  /* surface vertices */
+  const uint8_t* sv_kind;   /* 0 soft, 1 affine, 2 kinematic */
+  const int32_t* sv_node;   /* soft: node; affine: p-node; kinematic: -1 */
+  const double* sv_xi;      /* 3 per sv (affine body frame offset) */
+  const int32_t* sv_body;
+  const double* sv_kin0;    /* 3 per sv: initial kinematic positions */
+  /* topology */
+  const int32_t* tris;      /* 3 per tri (sv ids) */
+  const int32_t* edges;     /* 2 per edge (sv ids) */
+  const double* edge_rest_sq;
+  const int32_t* tet_nodes; /* 4 per tet (node ids) */
+  const double* tet_Dmi;    /* 9 per tet */
+  const double* tet_V0;
+  const double* tet_mu;
+  const double* tet_lam;
+  const int32_t* abd_node;  /* p-node of each affine body */
+  const double* abd_kV;     /* kappa * enclosed volume */
+  const int32_t* abd_body;
+  /* bodies */
+  const uint8_t* body_kind;
+  const double* body_mu;
+  const uint32_t* body_pairmask; /* bit j: may collide with env-local body j */
+  const double* body_vel0;  /* 3 per body */
+  /* per-env parameters (14 doubles each, see GRIP_P_* ) and gravity (3 each) */
+  const double* env_params;
+  const double* env_gravity;
+  const double* env_cell_hint; /* broad-phase cell size hint (m) */
+} GripSceneDesc;
+
+enum {
+  GRIP_P_DT = 0, GRIP_P_KAPPA, GRIP_P_DHAT, GRIP_P_EPSV, GRIP_P_RELTOL, GRIP_P_MAXIT, GRIP_P_ELLFLOOR,
+  GRIP_P_MAXLS, GRIP_P_CCDSCALE, GRIP_P_CCDIT, GRIP_P_KINGUARD, GRIP_P_MURULE, GRIP_P_PCGRTOL, GRIP_P_SPARE,
+  GRIP_NPARAM
+};
+
+/* status codes */
+enum { GRIP_NS_RUNNING = 0, GRIP_NS_CONVERGED = 1, GRIP_NS_FAILED = 2 };
+enum {
+  GRIP_R_NONE = 0,
+  GRIP_R_NONCONV = 1,            /* "non-convergence" */
+  GRIP_R_LINESEARCH = 2,         /* "line-search-failure" */
+  GRIP_R_INVERTED = 3,           /* "ValueError: inverted element passed to elastic energy" */
+  GRIP_R_CONTACT_D = 4,          /* "ValueError: contact stencil at non-positive distance" */
+  GRIP_R_NONFINITE = 5,          /* "FloatingPointError: non-finite assembly" */
+  GRIP_R_SOLVE = 6,              /* "SolveBreakdown: linear solve failed after regularization" */
+  GRIP_R_CCD = 7,                /* "IntersectionError: CCD called from an intersecting or touching state" */
+  GRIP_R_DET = 8,                /* "IntersectionError: step filter called with non-positive determinant state" */
+  GRIP_R_NONFINITE_STATE = 9,    /* "non-finite state" (quarantine) */
+  GRIP_R_CAPACITY = 10           /* device buffer capacity exceeded (never silent) */
+};
+
+typedef struct GripStepReport {
+  int32_t status;      /* GRIP_NS_* */
+  int32_t reason;      /* GRIP_R_* */
+  int32_t iterations;
+  int32_t n_alphas;
+  double residual;
+  double min_distance;
+  double energy;
+  double time;
+  int32_t step_index;
+  int32_t kinematic_blocked;
+  int32_t regularized;
+  int32_t newton_calls; /* newton_iteration calls this step (incl. the final check) */
+  int32_t pcg_iters;    /* total PCG iterations this step */
+  int32_t pad;
+} GripStepReport;
+
+typedef struct GripBatch GripBatch;
+
+int grip_abi_version(void);
+const char* grip_last_error(void);
+int grip_create(const GripSceneDesc* desc, int device, GripBatch** out);
+int grip_destroy(GripBatch* b);
+int grip_set_controls(GripBatch* b, const double* gravity /* n_env*3 or NULL */,
+                      const double* body_vel /* n_body*3 or NULL */);
+int grip_begin_step(GripBatch* b, const uint8_t* active /* n_env */);
+/* one Newton sweep over envs with pending[e]=1; clears pending for envs that finished */
+int grip_newton_iteration(GripBatch* b, uint8_t* pending /* n_env, in/out */);
+int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* reports /* n_env */,
+                       double* alphas /* n_env * max_iters, or NULL */);
+int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas);
+int grip_get_state(GripBatch* b, double* x, double* v, double* kin /* n_sv*3, or NULL */);
+int grip_set_state(GripBatch* b, const double* x, const double* v, const double* kin);
+int grip_get_surface(GripBatch* b, double* sv /* n_sv*3 */);
+/* per env-local body pair: summed barrier force (lambda) of active stencils at the
+ * current state (1.05*dhat candidate set) and a contact bit matrix */
+int grip_get_contacts(GripBatch* b, double* body_force /* n_body */, uint32_t* contact_mask /* n_body */,
+                      double* min_distance /* n_env */);
+/* canonical candidate stencils of env `env` at radius r, env-local sv ids */
+int grip_query_candidates(GripBatch* b, int env, double radius, int32_t* pt, int32_t cap_pt, int32_t* n_pt,
+                          int32_t* ee, int32_t cap_ee, int32_t* n_ee);
+int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
+/* timing of the last grip_step: device ms (CUDA events) and kernel launches */
+int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIP_IPC_H */

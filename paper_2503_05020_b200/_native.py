@@ -1,0 +1,214 @@
+"""ctypes binding of the C ABI in include/grip_ipc.h (libgripipc.so, built in-tree).
+
+There is no fallback: if the shared library is missing or no CUDA device is
+visible, loading raises.  The oracle under oracle/ is test infrastructure
+and is never imported here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_DIR = Path(__file__).resolve().parent / "_lib"
+LIB_PATH = LIB_DIR / "libgripipc.so"
+ABI_VERSION = 1
+NPARAM = 14
+(P_DT, P_KAPPA, P_DHAT, P_EPSV, P_RELTOL, P_MAXIT, P_ELLFLOOR, P_MAXLS, P_CCDSCALE, P_CCDIT, P_KINGUARD, P_MURULE,
+ P_PCGRTOL, P_SPARE) = range(NPARAM)
+
+NS_RUNNING, NS_CONVERGED, NS_FAILED = 0, 1, 2
+REASONS = {
+    0: "",
+    1: "non-convergence",
+    2: "line-search-failure",
+    3: "ValueError: inverted element passed to elastic energy",
+    4: "ValueError: contact stencil at non-positive distance",
+    5: "FloatingPointError: non-finite assembly",
+    6: "SolveBreakdown: linear solve failed after regularization",
+    7: "IntersectionError: CCD called from an intersecting or touching state",
+    8: "IntersectionError: step filter called with non-positive determinant state",
+    9: "non-finite state",
+    10: "device buffer capacity exceeded",
+}
+
+_P = ctypes.c_void_p
+
+
+class GripSceneDesc(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_int32), ("n_env", ctypes.c_int32)] + [
+        (name, _P) for name in (
+            "node_off", "sv_off", "tri_off", "edge_off", "tet_off", "abd_off", "body_off",
+            "node_x0", "node_M", "node_free", "node_body", "node_kind", "node_sv",
+            "sv_kind", "sv_node", "sv_xi", "sv_body", "sv_kin0",
+            "tris", "edges", "edge_rest_sq", "tet_nodes", "tet_Dmi", "tet_V0", "tet_mu", "tet_lam",
+            "abd_node", "abd_kV", "abd_body",
+            "body_kind", "body_mu", "body_pairmask", "body_vel0",
+            "env_params", "env_gravity", "env_cell_hint")]
+
+
+class GripStepReport(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("reason", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("n_alphas", ctypes.c_int32), ("residual", ctypes.c_double), ("min_distance", ctypes.c_double),
+                ("energy", ctypes.c_double), ("time", ctypes.c_double), ("step_index", ctypes.c_int32),
+                ("kinematic_blocked", ctypes.c_int32), ("regularized", ctypes.c_int32),
+                ("newton_calls", ctypes.c_int32), ("pcg_iters", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+REPORT_DTYPE = np.dtype([("status", "<i4"), ("reason", "<i4"), ("iterations", "<i4"), ("n_alphas", "<i4"),
+                         ("residual", "<f8"), ("min_distance", "<f8"), ("energy", "<f8"), ("time", "<f8"),
+                         ("step_index", "<i4"), ("kinematic_blocked", "<i4"), ("regularized", "<i4"),
+                         ("newton_calls", "<i4"), ("pcg_iters", "<i4"), ("pad", "<i4")])
+assert REPORT_DTYPE.itemsize == ctypes.sizeof(GripStepReport)
+
+_lib = None
+
+
+def load():
+    """Load libgripipc.so; raises (never falls back) if it or a CUDA device is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() (nvcc, sm_100a)")
+    lib = ctypes.CDLL(str(LIB_PATH))
+    vp, i32, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_double
+    pb = ctypes.POINTER(ctypes.c_void_p)
+    lib.grip_abi_version.restype = i32
+    lib.grip_last_error.restype = ctypes.c_char_p
+    lib.grip_create.argtypes = [ctypes.POINTER(GripSceneDesc), i32, pb]
+    for name, args in (
+        ("grip_destroy", [vp]), ("grip_set_controls", [vp, vp, vp]), ("grip_begin_step", [vp, vp]),
+        ("grip_newton_iteration", [vp, vp]), ("grip_finalize_step", [vp, vp, vp, vp]),
+        ("grip_step", [vp, vp, vp, vp]), ("grip_get_state", [vp, vp, vp, vp]),
+        ("grip_set_state", [vp, vp, vp, vp]), ("grip_get_surface", [vp, vp]),
+        ("grip_get_contacts", [vp, vp, vp, vp]),
+        ("grip_query_candidates", [vp, i32, dbl, vp, i32, vp, vp, i32, vp]),
+        ("grip_stress", [vp, vp]), ("grip_last_step_stats", [vp, vp, vp, vp])):
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = i32
+    if lib.grip_abi_version() != ABI_VERSION:
+        raise RuntimeError("libgripipc.so ABI version mismatch; rebuild")
+    _lib = lib
+    return lib
+
+
+def check(rc):
+    if rc != 0:
+        raise RuntimeError("grip: " + (_lib.grip_last_error() or b"").decode())
+
+
+def ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class DeviceBatch:
+    """Owns one GripBatch handle (device memory + stream) built from a packed scene."""
+
+    def __init__(self, packed, device=None):
+        lib = load()
+        self.packed = packed
+        self._keep = []
+        desc = GripSceneDesc()
+        desc.abi_version = ABI_VERSION
+        desc.n_env = packed.n_env
+        for name, _ in GripSceneDesc._fields_[2:]:
+            arr = np.ascontiguousarray(getattr(packed, name))
+            self._keep.append(arr)
+            setattr(desc, name, arr.ctypes.data)
+        h = ctypes.c_void_p()
+        dev = int(os.environ.get("LOCAL_RANK", "0")) if device is None else int(device)
+        check(lib.grip_create(ctypes.byref(desc), dev, ctypes.byref(h)))
+        self.h = h
+        self.n_env = packed.n_env
+        self.lib = lib
+        self.max_alpha = int(max(packed.env_params[:, P_MAXIT].max(), 1)) + 1
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.grip_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_controls(self, gravity=None, body_vel=None):
+        g = None if gravity is None else np.ascontiguousarray(gravity, np.float64)
+        v = None if body_vel is None else np.ascontiguousarray(body_vel, np.float64)
+        check(self.lib.grip_set_controls(self.h, ptr(g), ptr(v)))
+
+    def step(self, active):
+        act = np.ascontiguousarray(active, np.uint8)
+        rep = np.zeros(self.n_env, REPORT_DTYPE)
+        alphas = np.zeros((self.n_env, self.max_alpha))
+        check(self.lib.grip_step(self.h, ptr(act), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
+        return rep, alphas
+
+    def begin_step(self, active):
+        act = np.ascontiguousarray(active, np.uint8)
+        check(self.lib.grip_begin_step(self.h, ptr(act)))
+
+    def newton_iteration(self, pending):
+        pend = np.ascontiguousarray(pending, np.uint8)
+        check(self.lib.grip_newton_iteration(self.h, ptr(pend)))
+        return pend.astype(bool)
+
+    def finalize_step(self, active):
+        act = np.ascontiguousarray(active, np.uint8)
+        rep = np.zeros(self.n_env, REPORT_DTYPE)
+        alphas = np.zeros((self.n_env, self.max_alpha))
+        check(self.lib.grip_finalize_step(self.h, ptr(act), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
+        return rep, alphas
+
+    def get_state(self, with_kin=True):
+        p = self.packed
+        x = np.empty((p.n_node_total, 3))
+        v = np.empty((p.n_node_total, 3))
+        kin = np.empty((p.n_sv_total, 3)) if with_kin else None
+        check(self.lib.grip_get_state(self.h, ptr(x), ptr(v), ptr(kin)))
+        return x, v, kin
+
+    def set_state(self, x=None, v=None, kin=None):
+        f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)  # noqa: E731
+        x, v, kin = f(x), f(v), f(kin)
+        check(self.lib.grip_set_state(self.h, ptr(x), ptr(v), ptr(kin)))
+
+    def surface(self):
+        sv = np.empty((self.packed.n_sv_total, 3))
+        check(self.lib.grip_get_surface(self.h, ptr(sv)))
+        return sv
+
+    def contacts(self):
+        p = self.packed
+        force = np.empty(p.n_body_total)
+        mask = np.empty(p.n_body_total, np.uint32)
+        md = np.empty(p.n_env)
+        check(self.lib.grip_get_contacts(self.h, ptr(force), ptr(mask), ptr(md)))
+        return force, mask, md
+
+    def candidates(self, env, radius):
+        n_pt, n_ee = ctypes.c_int32(), ctypes.c_int32()
+        check(self.lib.grip_query_candidates(self.h, int(env), float(radius), None, 0, ctypes.byref(n_pt), None, 0,
+                                             ctypes.byref(n_ee)))
+        pt = np.empty((max(n_pt.value, 1), 4), np.int32)
+        ee = np.empty((max(n_ee.value, 1), 4), np.int32)
+        check(self.lib.grip_query_candidates(self.h, int(env), float(radius), ptr(pt), n_pt.value, ctypes.byref(n_pt),
+                                             ptr(ee), n_ee.value, ctypes.byref(n_ee)))
+        return pt[:n_pt.value].astype(np.int64), ee[:n_ee.value].astype(np.int64)
+
+    def stress(self):
+        out = np.empty((max(self.packed.n_tet_total, 1), 7))
+        check(self.lib.grip_stress(self.h, ptr(out)))
+        return out[:self.packed.n_tet_total]
+
+    def stats(self):
+        ms, la, sw = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
+        check(self.lib.grip_last_step_stats(self.h, ctypes.byref(ms), ctypes.byref(la), ctypes.byref(sw)))
+        return ms.value, la.value, sw.value

@@ -1,0 +1,517 @@
+// Device-side context, CTA-wide reductions/scans and the per-environment
+// broad phase.  One CTA owns one environment in every *_env kernel, so all
+// per-env reductions are block reductions with a fixed tree: results are
+// bitwise reproducible and independent of how many envs share the launch
+// (SPEC "batch-of-N bitwise equals batch-of-1").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/grip_ipc.h"
+#include "grip_elements.cuh"
+
+namespace grip {
+
+constexpr int NT = 256;           // threads per env CTA
+constexpr int NWARP = NT / 32;
+constexpr int MAXC = 4096;        // broad-phase grid cells per env
+
+// error / flag bits per env and Newton sweep
+enum { ERR_INVERTED = 1, ERR_CONTACT_D = 2, FLAG_OVERFLOW = 4 };
+
+struct Dev {
+  int n_env;
+  // env slices
+  const int *node_off, *sv_off, *tri_off, *edge_off, *tet_off, *abd_off, *body_off, *free_off;
+  // scene
+  const double* node_M;
+  const uint8_t* node_free;
+  const int* node_body;
+  const uint8_t* node_kind;
+  const int* node_sv;
+  const int* node_fidx;      // local free index or -1
+  const int* free_node;      // per global free idx: local node
+  const uint8_t* sv_kind;
+  const int* sv_node;
+  const double* sv_xi;
+  const int* sv_body;
+  const int* tris;
+  const int* edges;
+  const double* edge_rest_sq;
+  const int* tet_nodes;
+  const double* tet_Dmi;
+  const double* tet_V0;
+  const double* tet_mu;
+  const double* tet_lam;
+  const int* abd_node;
+  const double* abd_kV;
+  const uint8_t* body_kind;
+  const double* body_mu;
+  const uint32_t* body_pairmask;
+  double* body_vel;
+  double* gravity;
+  const double* params;
+  const double* cell_hint;
+  // static block structure over free nodes (global free index rows)
+  const int* sb_rowptr;      // [n_free_total + 1] global block ids
+  const int* sb_col;         // local free col
+  const int* sb_diag;        // per global free idx
+  const int* sbc_ptr;        // [n_blocks + 1]
+  const int* sbc;            // contribution code: (elem_slot << 4) | (sa << 2) | sb ; elem_slot local el index
+  const int* tinc_ptr;       // per global node: tet/abd gradient incidence
+  const int* tinc;           // (elem_slot << 2) | slot
+  // state
+  double *x, *v, *x_t, *xhat, *pdir;
+  double *sv_pos, *surf_prev, *kin_pos, *sv_disp;
+  double *ell, *tol, *residual, *energy, *alphas, *min_dist, *time;
+  int *iters, *ns_status, *reason, *regularized, *kin_blocked, *needs_ls, *ns_done, *flags, *step_index;
+  int *newton_calls, *pcg_iters;
+  double* body_force;
+  unsigned int* contact_mask;
+  int max_alpha;
+  // candidates (uniform capacity per env)
+  int cap_pt, cap_ee;
+  int *c1_pt, *c1_ee, *c1_eid, *c1_n;   // c1_n[2e]=n_pt, [2e+1]=n_ee
+  int *c2_pt, *c2_ee, *c2_eid, *c2_n;
+  // elements (uniform capacity per env): [tets | abd | contacts | anchors]
+  int max_tet, max_abd, cap_act, cap_anc, cap_el;
+  int* act;          // per env cap_act: candidate code (ee ? cap_pt + k : k)
+  int* n_act;
+  int* n_anc;
+  double *el_E, *el_g, *el_H;
+  int* el_idx;
+  int* work_off;     // per list position (n+1)
+  // anchors (persist across steps)
+  int* anc_v;        // 4
+  double *anc_gamma, *anc_T, *anc_lam, *anc_mu;   // 4, 6, 1, 1
+  int* anc_b;        // 2
+  // scratch
+  int max_sv, max_tri, max_edge, max_free, max_node;
+  int cap_cells;
+  int* bp_cells;     // per env cap_cells
+  double* bp_aabb;   // per env 6*max(max_tri, max_edge)
+  int* bp_cnt;       // per env max(max_sv, max_edge) + 1
+  int* bp_tmp;       // per env max(cap_pt, cap_ee)
+  double *pcg_x, *pcg_r, *pcg_z, *pcg_p, *pcg_q, *pcg_b;  // per env 3*max_free
+  double* pcg_pinv;  // per global free node 9
+  double* abd_pinv;  // per abd 144
+  double* sb_val;    // per block 9
+  double *c_u, *c_w; // per env 3*max_sv
+  double* c_r;       // per env 12*(cap_act+cap_anc)
+  int *inc_ptr, *inc; // per env max_sv+1 ; 4*(cap_act+cap_anc)
+  double* sv_g;      // per env 3*max_sv
+};
+
+__device__ __forceinline__ const double* P_(const Dev& D, int e) { return D.params + (size_t)e * GRIP_NPARAM; }
+
+// ---------------------------------------------------------------------------
+// block reductions (fixed shuffle tree -> deterministic)
+// ---------------------------------------------------------------------------
+struct Red {
+  double d[40];
+  int i[40];
+};
+
+__device__ __forceinline__ double wsum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double wmax(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double wmin(double v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int OP>  // 0 sum 1 max 2 min
+__device__ double block_red(double v, Red& sm) {
+  v = OP == 0 ? wsum(v) : (OP == 1 ? wmax(v) : wmin(v));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm.d[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    double r = l < NWARP ? sm.d[l] : (OP == 0 ? 0.0 : (OP == 1 ? -INFINITY : INFINITY));
+    r = OP == 0 ? wsum(r) : (OP == 1 ? wmax(r) : wmin(r));
+    if (l == 0) sm.d[32] = r;
+  }
+  __syncthreads();
+  return sm.d[32];
+}
+__device__ __forceinline__ double block_sum(double v, Red& sm) { return block_red<0>(v, sm); }
+__device__ __forceinline__ double block_max(double v, Red& sm) { return block_red<1>(v, sm); }
+__device__ __forceinline__ double block_min(double v, Red& sm) { return block_red<2>(v, sm); }
+
+__device__ int block_or(int v, Red& sm) {
+  v = __reduce_or_sync(0xffffffffu, (unsigned)v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm.i[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int r = 0;
+    for (int k = 0; k < NWARP; ++k) r |= sm.i[k];
+    sm.i[32] = r;
+  }
+  __syncthreads();
+  return sm.i[32];
+}
+
+// exclusive scan of one int per thread; returns prefix, writes block total to *total
+__device__ int block_scan(int v, Red& sm, int* total) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  int inc = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (l >= o) inc += t;
+  }
+  __syncthreads();
+  if (l == 31) sm.i[w] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int k = 0; k < NWARP; ++k) {
+      int t = sm.i[k];
+      sm.i[k] = run;
+      run += t;
+    }
+    sm.i[32] = run;
+  }
+  __syncthreads();
+  *total = sm.i[32];
+  return sm.i[w] + inc - v;
+}
+
+// in-place exclusive scan of cnt[0..n) (global or shared), returns total
+__device__ int block_scan_array(int* cnt, int n, Red& sm) {
+  int base = 0;
+  for (int s = 0; s < n; s += NT) {
+    int i = s + threadIdx.x;
+    int v = i < n ? cnt[i] : 0;
+    int tot;
+    int pre = block_scan(v, sm, &tot);
+    if (i < n) cnt[i] = base + pre;
+    base += tot;
+  }
+  __syncthreads();
+  return base;
+}
+
+// ---------------------------------------------------------------------------
+// state access
+// ---------------------------------------------------------------------------
+struct EnvIx {
+  int e, n0, nn, s0, ns, t0, nt, ed0, ne, te0, ntet, a0, na, b0, nb, f0, nf;
+};
+__device__ __forceinline__ EnvIx env_ix(const Dev& D, int e) {
+  EnvIx r;
+  r.e = e;
+  r.n0 = D.node_off[e]; r.nn = D.node_off[e + 1] - r.n0;
+  r.s0 = D.sv_off[e]; r.ns = D.sv_off[e + 1] - r.s0;
+  r.t0 = D.tri_off[e]; r.nt = D.tri_off[e + 1] - r.t0;
+  r.ed0 = D.edge_off[e]; r.ne = D.edge_off[e + 1] - r.ed0;
+  r.te0 = D.tet_off[e]; r.ntet = D.tet_off[e + 1] - r.te0;
+  r.a0 = D.abd_off[e]; r.na = D.abd_off[e + 1] - r.a0;
+  r.b0 = D.body_off[e]; r.nb = D.body_off[e + 1] - r.b0;
+  r.f0 = D.free_off[e]; r.nf = D.free_off[e + 1] - r.f0;
+  return r;
+}
+
+// surface position of env-local sv i from node array xs (global base), G x (solver.py:367-372)
+__device__ __forceinline__ V3 sv_at(const Dev& D, const EnvIx& E, int i, const double* xs) {
+  const int g = E.s0 + i;
+  const int k = D.sv_kind[g];
+  if (k == 0) return ld3(xs + 3 * (E.n0 + D.sv_node[g]));
+  if (k == 1) {
+    const double* q = xs + 3 * (E.n0 + D.sv_node[g]);
+    V3 xi = ld3(D.sv_xi + 3 * g);
+    return V3{q[0] + xi.x * q[3] + xi.y * q[4] + xi.z * q[5], q[1] + xi.x * q[6] + xi.y * q[7] + xi.z * q[8],
+              q[2] + xi.x * q[9] + xi.y * q[10] + xi.z * q[11]};
+  }
+  return ld3(D.kin_pos + 3 * g);
+}
+// G applied to a node-space direction (kinematic rows are zero)
+__device__ __forceinline__ V3 sv_dir(const Dev& D, const EnvIx& E, int i, const double* ps) {
+  const int g = E.s0 + i;
+  const int k = D.sv_kind[g];
+  if (k == 0) return ld3(ps + 3 * (E.n0 + D.sv_node[g]));
+  if (k == 1) {
+    const double* q = ps + 3 * (E.n0 + D.sv_node[g]);
+    V3 xi = ld3(D.sv_xi + 3 * g);
+    return V3{q[0] + xi.x * q[3] + xi.y * q[4] + xi.z * q[5], q[1] + xi.x * q[6] + xi.y * q[7] + xi.z * q[8],
+              q[2] + xi.x * q[9] + xi.y * q[10] + xi.z * q[11]};
+  }
+  return V3{0.0, 0.0, 0.0};
+}
+
+// ---------------------------------------------------------------------------
+// Per-environment broad phase (geometry/broadphase.py:101-214 semantics).
+//
+// Candidate MEMBERSHIP is the reference's exact predicate set
+//   PT: v not in t, pair_ok(body v, body t), x_v in [tri_lo - r, tri_hi + r]   (:177-183)
+//   EE: i < j, no shared vertex, pair_ok, hi_j >= lo_i - r and lo_j <= hi_i + r (:195-210)
+// and the output is in the reference's canonical order ((v, t) / (i, j)).
+// Pairs are generated by an env-local uniform grid held in shared memory
+// (cell >= r, triangles / edges inserted over their tight AABB cells, queries
+// over the r-inflated box, each pair visited in exactly one cell: the lowest
+// cell common to both boxes).  The grid only prunes; the predicate decides,
+// so the cell size cannot change the result.
+// ---------------------------------------------------------------------------
+struct BPShared {
+  int head[MAXC + 1];
+  int cur[MAXC];
+};
+
+struct Grid {
+  double lox, loy, loz, ih;
+  int nx, ny, nz;
+  __device__ __forceinline__ int cx(double v) const {
+    double f = floor((v - lox) * ih);
+    return f < 0.0 ? 0 : (f >= nx ? nx - 1 : (int)f);
+  }
+  __device__ __forceinline__ int cy(double v) const {
+    double f = floor((v - loy) * ih);
+    return f < 0.0 ? 0 : (f >= ny ? ny - 1 : (int)f);
+  }
+  __device__ __forceinline__ int cz(double v) const {
+    double f = floor((v - loz) * ih);
+    return f < 0.0 ? 0 : (f >= nz ? nz - 1 : (int)f);
+  }
+};
+
+// shell sort of a small int segment (per-thread; segments are the candidates of one query)
+__device__ void sort_ints(int* a, int n) {
+  const int gaps[8] = {701, 301, 132, 57, 23, 10, 4, 1};
+  for (int gi = 0; gi < 8; ++gi) {
+    const int g = gaps[gi];
+    for (int i = g; i < n; ++i) {
+      int t = a[i];
+      int j = i;
+      while (j >= g && a[j - g] > t) {
+        a[j] = a[j - g];
+        j -= g;
+      }
+      a[j] = t;
+    }
+  }
+}
+
+// Builds the grid over `n` primitive AABBs (aabb[6*i]: lo, hi), each inserted into its
+// tight cell range.  Returns false on scratch overflow.
+__device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells, int cap, BPShared& S, Red& sm) {
+  const int ncell = G.nx * G.ny * G.nz;
+  for (int c = threadIdx.x; c <= ncell; c += NT) S.head[c] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const double* b = aabb + 6 * i;
+    int x0 = G.cx(b[0]), y0 = G.cy(b[1]), z0 = G.cz(b[2]);
+    int x1 = G.cx(b[3]), y1 = G.cy(b[4]), z1 = G.cz(b[5]);
+    for (int a = x0; a <= x1; ++a)
+      for (int bb = y0; bb <= y1; ++bb)
+        for (int c = z0; c <= z1; ++c) atomicAdd(&S.head[(a * G.ny + bb) * G.nz + c], 1);
+  }
+  __syncthreads();
+  int total = block_scan_array(S.head, ncell, sm);
+  if (total > cap) return false;
+  for (int c = threadIdx.x; c < ncell; c += NT) S.cur[c] = S.head[c];
+  if (threadIdx.x == 0) S.head[ncell] = total;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const double* b = aabb + 6 * i;
+    int x0 = G.cx(b[0]), y0 = G.cy(b[1]), z0 = G.cz(b[2]);
+    int x1 = G.cx(b[3]), y1 = G.cy(b[4]), z1 = G.cz(b[5]);
+    for (int a = x0; a <= x1; ++a)
+      for (int bb = y0; bb <= y1; ++bb)
+        for (int c = z0; c <= z1; ++c) cells[atomicAdd(&S.cur[(a * G.ny + bb) * G.nz + c], 1)] = i;
+  }
+  __syncthreads();
+  return true;
+}
+
+// Candidate stencils of one env at radius r from the sv positions in D.sv_pos.
+// out_n[0] = n_pt, out_n[1] = n_ee (true counts, even past capacity).
+// Returns false if an output or scratch capacity was exceeded; the host then
+// grows the buffers and re-runs the whole sweep for that env.
+__device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
+                                int* out_n, BPShared& S, Red& sm) {
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  const int* tris = D.tris + 3 * (size_t)E.t0;
+  const int* edges = D.edges + 2 * (size_t)E.ed0;
+  double* aabb = D.bp_aabb + (size_t)E.e * 6 * max(D.max_tri, D.max_edge);
+  int* cells = D.bp_cells + (size_t)E.e * D.cap_cells;
+  int* cnt = D.bp_cnt + (size_t)E.e * (max(D.max_sv, D.max_edge) + 1);
+  int* tmp = D.bp_tmp + (size_t)E.e * max(D.cap_pt, D.cap_ee);
+  if (E.ns == 0) {
+    if (threadIdx.x == 0) { out_n[0] = 0; out_n[1] = 0; }
+    __syncthreads();
+    return true;
+  }
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = threadIdx.x; i < E.ns; i += NT)
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = fmin(lo[c], X[3 * i + c]);
+      hi[c] = fmax(hi[c], X[3 * i + c]);
+    }
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = block_min(lo[c], sm);
+    hi[c] = block_max(hi[c], sm);
+  }
+  const uint32_t* pm = D.body_pairmask + E.b0;
+  const int* vb = D.sv_body + E.s0;
+  double h = fmax(r, D.cell_hint[E.e]);
+  int npt = 0, nee = 0;
+  bool ok = true;
+  for (int attempt = 0; attempt < 12; ++attempt) {
+    Grid G;
+    G.lox = lo[0] - r; G.loy = lo[1] - r; G.loz = lo[2] - r;
+    for (;;) {
+      G.ih = 1.0 / h;
+      G.nx = (int)fmin(floor((hi[0] + r - G.lox) * G.ih) + 1.0, 1e6);
+      G.ny = (int)fmin(floor((hi[1] + r - G.loy) * G.ih) + 1.0, 1e6);
+      G.nz = (int)fmin(floor((hi[2] + r - G.loz) * G.ih) + 1.0, 1e6);
+      if ((long long)G.nx * G.ny * G.nz <= MAXC) break;
+      h *= 1.3;
+    }
+    const double eps = 1e-9 * h;
+    npt = nee = 0;
+    ok = true;
+    bool regrid = false;
+    // ---------------- point-triangle ----------------
+    if (E.nt && E.ns) {
+      for (int t = threadIdx.x; t < E.nt; t += NT) {
+        V3 a = ld3(X + 3 * tris[3 * t]), b = ld3(X + 3 * tris[3 * t + 1]), c = ld3(X + 3 * tris[3 * t + 2]);
+        V3 l = vmin(vmin(a, b), c), u = vmax(vmax(a, b), c);
+        double* o = aabb + 6 * t;
+        o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
+      }
+      __syncthreads();
+      if (!grid_build(G, aabb, E.nt, cells, D.cap_cells, S, sm)) {
+        regrid = true;
+      } else {
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int v = threadIdx.x; v < E.ns; v += NT) {
+            V3 p = ld3(X + 3 * v);
+            const int qx0 = G.cx(p.x - r - eps), qy0 = G.cy(p.y - r - eps), qz0 = G.cz(p.z - r - eps);
+            const int qx1 = G.cx(p.x + r + eps), qy1 = G.cy(p.y + r + eps), qz1 = G.cz(p.z + r + eps);
+            const uint32_t okmask = pm[vb[v]];
+            const int base = pass ? cnt[v] : 0;
+            const int lim = pass ? cnt[v + 1] - base : 0;
+            int count = 0;
+            for (int a = qx0; a <= qx1; ++a)
+              for (int bb = qy0; bb <= qy1; ++bb)
+                for (int c = qz0; c <= qz1; ++c) {
+                  const int cell = (a * G.ny + bb) * G.nz + c;
+                  const int kend = S.head[cell + 1];
+                  for (int k = S.head[cell]; k < kend; ++k) {
+                    const int t = cells[k];
+                    const double* bx = aabb + 6 * t;
+                    if (max(qx0, G.cx(bx[0])) != a || max(qy0, G.cy(bx[1])) != bb || max(qz0, G.cz(bx[2])) != c)
+                      continue;
+                    const int t0 = tris[3 * t], t1 = tris[3 * t + 1], t2 = tris[3 * t + 2];
+                    if (t0 == v || t1 == v || t2 == v) continue;
+                    if (!((okmask >> vb[t0]) & 1u)) continue;
+                    if (!(p.x >= bx[0] - r && p.y >= bx[1] - r && p.z >= bx[2] - r)) continue;
+                    if (!(p.x <= bx[3] + r && p.y <= bx[4] + r && p.z <= bx[5] + r)) continue;
+                    if (pass && count < lim) tmp[base + count] = t;
+                    ++count;
+                  }
+                }
+            if (!pass) {
+              cnt[v] = count;
+            } else {
+              sort_ints(tmp + base, lim);
+              for (int k = 0; k < lim; ++k) {
+                const int t = tmp[base + k];
+                int* row = out_pt + 4 * (base + k);
+                row[0] = v; row[1] = tris[3 * t]; row[2] = tris[3 * t + 1]; row[3] = tris[3 * t + 2];
+              }
+            }
+          }
+          __syncthreads();
+          if (!pass) {
+            npt = block_scan_array(cnt, E.ns, sm);
+            if (threadIdx.x == 0) cnt[E.ns] = npt;
+            __syncthreads();
+            if (npt > D.cap_pt) { ok = false; break; }
+          }
+        }
+      }
+    }
+    if (regrid) { h *= 2.0; continue; }
+    // ---------------- edge-edge ----------------
+    if (E.ne && ok) {
+      for (int i = threadIdx.x; i < E.ne; i += NT) {
+        V3 a = ld3(X + 3 * edges[2 * i]), b = ld3(X + 3 * edges[2 * i + 1]);
+        V3 l = vmin(a, b), u = vmax(a, b);
+        double* o = aabb + 6 * i;
+        o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
+      }
+      __syncthreads();
+      if (!grid_build(G, aabb, E.ne, cells, D.cap_cells, S, sm)) { h *= 2.0; continue; }
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int i = threadIdx.x; i < E.ne; i += NT) {
+          const double* bi = aabb + 6 * i;
+          const double lx = bi[0] - r, ly = bi[1] - r, lz = bi[2] - r;
+          const double ux = bi[3] + r, uy = bi[4] + r, uz = bi[5] + r;
+          const int qx0 = G.cx(lx - eps), qy0 = G.cy(ly - eps), qz0 = G.cz(lz - eps);
+          const int qx1 = G.cx(ux + eps), qy1 = G.cy(uy + eps), qz1 = G.cz(uz + eps);
+          const int a0 = edges[2 * i], a1 = edges[2 * i + 1];
+          const uint32_t okmask = pm[vb[a0]];
+          const int base = pass ? cnt[i] : 0;
+          const int lim = pass ? cnt[i + 1] - base : 0;
+          int count = 0;
+          for (int a = qx0; a <= qx1; ++a)
+            for (int bb = qy0; bb <= qy1; ++bb)
+              for (int c = qz0; c <= qz1; ++c) {
+                const int cell = (a * G.ny + bb) * G.nz + c;
+                const int kend = S.head[cell + 1];
+                for (int k = S.head[cell]; k < kend; ++k) {
+                  const int j = cells[k];
+                  if (j <= i) continue;
+                  const double* bj = aabb + 6 * j;
+                  if (max(qx0, G.cx(bj[0])) != a || max(qy0, G.cy(bj[1])) != bb || max(qz0, G.cz(bj[2])) != c)
+                    continue;
+                  const int b0 = edges[2 * j], b1 = edges[2 * j + 1];
+                  if (a0 == b0 || a0 == b1 || a1 == b0 || a1 == b1) continue;
+                  if (!((okmask >> vb[b0]) & 1u)) continue;
+                  if (!(bj[3] >= lx && bj[4] >= ly && bj[5] >= lz)) continue;
+                  if (!(bj[0] <= ux && bj[1] <= uy && bj[2] <= uz)) continue;
+                  if (pass && count < lim) tmp[base + count] = j;
+                  ++count;
+                }
+              }
+          if (!pass) {
+            cnt[i] = count;
+          } else {
+            sort_ints(tmp + base, lim);
+            for (int k = 0; k < lim; ++k) {
+              const int j = tmp[base + k];
+              int* row = out_ee + 4 * (base + k);
+              row[0] = a0; row[1] = a1; row[2] = edges[2 * j]; row[3] = edges[2 * j + 1];
+              out_eid[2 * (base + k)] = i;
+              out_eid[2 * (base + k) + 1] = j;
+            }
+          }
+        }
+        __syncthreads();
+        if (!pass) {
+          nee = block_scan_array(cnt, E.ne, sm);
+          if (threadIdx.x == 0) cnt[E.ne] = nee;
+          __syncthreads();
+          if (nee > D.cap_ee) { ok = false; break; }
+        }
+      }
+    }
+    break;
+  }
+  if (threadIdx.x == 0) {
+    out_n[0] = npt;
+    out_n[1] = nee;
+  }
+  __syncthreads();
+  return ok;
+}
+
+}  // namespace grip

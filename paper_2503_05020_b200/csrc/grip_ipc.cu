@@ -1,0 +1,690 @@
+// C ABI of the batched IPC step (include/grip_ipc.h): device memory, the
+// static block structure of every env's Hessian, and the host loop that
+// drives begin / Newton sweeps / finalize over the pending-env lists.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "grip_kernels.cuh"
+
+using namespace grip;
+
+namespace {
+
+thread_local std::string g_err;
+
+#define CK(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t _e = (call);                                                                \
+    if (_e != cudaSuccess) {                                                                \
+      g_err = std::string(#call) + ": " + cudaGetErrorString(_e);                           \
+      return -1;                                                                            \
+    }                                                                                       \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+};
+
+}  // namespace
+
+struct GripBatch {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  Dev D{};
+  int n_env = 0, n_node = 0, n_sv = 0, n_tet = 0, n_abd = 0, n_body = 0, n_free = 0, n_blk = 0;
+  std::vector<void*> owned;     // device allocations released at destroy
+  // host copies of the env slices
+  std::vector<int> node_off, sv_off, tri_off, edge_off, tet_off, abd_off, body_off;
+  std::vector<int> tet_env;
+  int* d_list = nullptr;        // active / pending lists
+  int* d_list2 = nullptr;
+  int* d_tet_env = nullptr;
+  int* h_pin = nullptr;         // pinned small readbacks
+  int max_it = 100;
+  double last_ms = 0.0;
+  long long launches = 0, sweeps = 0;
+
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+    cudaMemsetAsync(p, 0, n * sizeof(T), stream);
+    owned.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const T* h, size_t n) {
+    T* d = alloc<T>(n);
+    if (d && h && n) cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, stream);
+    return d;
+  }
+  void release(void* p) {
+    auto it = std::find(owned.begin(), owned.end(), p);
+    if (it != owned.end()) {
+      cudaFree(p);
+      owned.erase(it);
+    }
+  }
+};
+
+namespace {
+
+// (re)allocate every buffer whose size depends on the candidate / element capacities
+int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
+  Dev& D = b->D;
+  const size_t E = b->n_env;
+  auto swap_alloc = [&](auto*& ptr, size_t n) {
+    using T = std::remove_reference_t<decltype(*ptr)>;
+    if (ptr) b->release((void*)ptr);
+    ptr = b->alloc<std::remove_const_t<T>>(n);
+    return ptr != nullptr;
+  };
+  bool ok = true;
+  ok &= swap_alloc(D.c1_pt, E * 4 * D.cap_pt);
+  ok &= swap_alloc(D.c1_ee, E * 4 * D.cap_ee);
+  ok &= swap_alloc(D.c1_eid, E * 2 * D.cap_ee);
+  ok &= swap_alloc(D.c2_pt, E * 4 * D.cap_pt);
+  ok &= swap_alloc(D.c2_ee, E * 4 * D.cap_ee);
+  ok &= swap_alloc(D.c2_eid, E * 2 * D.cap_ee);
+  ok &= swap_alloc(D.act, E * D.cap_act);
+  D.cap_el = D.max_tet + D.max_abd + D.cap_act + D.cap_anc;
+  ok &= swap_alloc(D.el_E, E * D.cap_el);
+  ok &= swap_alloc(D.el_g, E * D.cap_el * 12);
+  ok &= swap_alloc(D.el_H, E * D.cap_el * 144);
+  ok &= swap_alloc(D.el_idx, E * D.cap_el * 4);
+  ok &= swap_alloc(D.c_r, E * 12 * (D.cap_act + D.cap_anc));
+  ok &= swap_alloc(D.inc, E * 4 * (D.cap_act + D.cap_anc));
+  ok &= swap_alloc(D.bp_tmp, E * std::max(D.cap_pt, D.cap_ee));
+  ok &= swap_alloc(D.bp_cells, E * D.cap_cells);
+  // anchors persist: copy with the new pitch
+  auto grow_anc = [&](auto*& ptr, int width) {
+    using T = std::remove_reference_t<decltype(*ptr)>;
+    T* np = b->alloc<T>(E * D.cap_anc * width);
+    if (!np) return false;
+    if (ptr && keep_anchors)
+      cudaMemcpy2DAsync(np, sizeof(T) * width * D.cap_anc, ptr, sizeof(T) * width * old_cap_anc,
+                        sizeof(T) * width * old_cap_anc, E, cudaMemcpyDeviceToDevice, b->stream);
+    if (ptr) b->release((void*)ptr);
+    ptr = np;
+    return true;
+  };
+  ok &= grow_anc(D.anc_v, 4);
+  ok &= grow_anc(D.anc_gamma, 4);
+  ok &= grow_anc(D.anc_T, 6);
+  ok &= grow_anc(D.anc_lam, 1);
+  ok &= grow_anc(D.anc_mu, 1);
+  ok &= grow_anc(D.anc_b, 2);
+  if (!ok) {
+    g_err = "out of device memory growing candidate/element buffers";
+    return -1;
+  }
+  return 0;
+}
+
+int grow(GripBatch* b) {
+  Dev& D = b->D;
+  const int old_anc = D.cap_anc;
+  D.cap_pt *= 2;
+  D.cap_ee *= 2;
+  D.cap_act *= 2;
+  D.cap_anc *= 2;
+  D.cap_cells *= 2;
+  return alloc_dynamic(b, true, old_anc);
+}
+
+int upload_list(GripBatch* b, const std::vector<int>& L, int* dst) {
+  if (!L.empty()) CK(cudaMemcpyAsync(dst, L.data(), L.size() * sizeof(int), cudaMemcpyHostToDevice, b->stream));
+  return 0;
+}
+
+// run an env kernel over a list until no env overflows its buffers
+template <class Launch>
+int run_with_growth(GripBatch* b, int n, Launch launch) {
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    launch();
+    b->launches++;
+    int* ov = b->D.flags;  // scan flags of listed envs on the host
+    (void)ov;
+    std::vector<int> fl(b->n_env);
+    CK(cudaMemcpyAsync(fl.data(), b->D.flags, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+    bool any = false;
+    for (int e = 0; e < b->n_env; ++e) any |= (fl[e] & FLAG_OVERFLOW) != 0;
+    if (!any) return 0;
+    if (grow(b)) return -1;
+    CK(cudaMemsetAsync(b->D.flags, 0, sizeof(int) * b->n_env, b->stream));
+  }
+  g_err = "buffer growth did not converge";
+  return -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int grip_abi_version(void) { return GRIP_ABI_VERSION; }
+const char* grip_last_error(void) { return g_err.c_str(); }
+
+int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
+  if (!d || !out) {
+    g_err = "null argument";
+    return -1;
+  }
+  if (d->abi_version != GRIP_ABI_VERSION) {
+    g_err = "ABI version mismatch";
+    return -1;
+  }
+  CK(cudaSetDevice(device));
+  GripBatch* b = new GripBatch();
+  b->device = device;
+  CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&b->ev0));
+  CK(cudaEventCreate(&b->ev1));
+  const int E = d->n_env;
+  b->n_env = E;
+  auto vec = [&](const int32_t* p) { return std::vector<int>(p, p + E + 1); };
+  b->node_off = vec(d->node_off);
+  b->sv_off = vec(d->sv_off);
+  b->tri_off = vec(d->tri_off);
+  b->edge_off = vec(d->edge_off);
+  b->tet_off = vec(d->tet_off);
+  b->abd_off = vec(d->abd_off);
+  b->body_off = vec(d->body_off);
+  const int NN = b->node_off[E], NS = b->sv_off[E], NTR = b->tri_off[E], NE = b->edge_off[E], NTET = b->tet_off[E],
+            NA = b->abd_off[E], NB = b->body_off[E];
+  b->n_node = NN; b->n_sv = NS; b->n_tet = NTET; b->n_abd = NA; b->n_body = NB;
+  Dev& D = b->D;
+  D.n_env = E;
+  int max_sv = 1, max_tri = 1, max_edge = 1, max_tet = 1, max_abd = 1, max_node = 1;
+  for (int e = 0; e < E; ++e) {
+    max_sv = std::max(max_sv, b->sv_off[e + 1] - b->sv_off[e]);
+    max_tri = std::max(max_tri, b->tri_off[e + 1] - b->tri_off[e]);
+    max_edge = std::max(max_edge, b->edge_off[e + 1] - b->edge_off[e]);
+    max_tet = std::max(max_tet, b->tet_off[e + 1] - b->tet_off[e]);
+    max_abd = std::max(max_abd, b->abd_off[e + 1] - b->abd_off[e]);
+    max_node = std::max(max_node, b->node_off[e + 1] - b->node_off[e]);
+  }
+  // ---- free nodes, static block structure, gradient incidence (host) ----
+  std::vector<int> node_fidx(NN, -1), free_off(E + 1, 0), free_node;
+  int max_free = 1;
+  for (int e = 0; e < E; ++e) {
+    int f = 0;
+    for (int n = b->node_off[e]; n < b->node_off[e + 1]; ++n)
+      if (d->node_free[n]) {
+        node_fidx[n] = f++;
+        free_node.push_back(n - b->node_off[e]);
+      }
+    free_off[e + 1] = free_off[e] + f;
+    max_free = std::max(max_free, f);
+  }
+  const int NF = free_off[E];
+  b->n_free = NF;
+  std::vector<int> sb_rowptr(NF + 1, 0), sb_col, sb_diag(NF, -1), sbc_ptr(1, 0), sbc;
+  std::vector<int> tinc_ptr(NN + 1, 0), tinc;
+  {
+    std::vector<std::vector<std::pair<int, int>>> tin(NN);  // per global node: (slot, k)
+    for (int e = 0; e < E; ++e) {
+      const int n0 = b->node_off[e];
+      const int nf = free_off[e + 1] - free_off[e];
+      // per free row: map col -> list of contribution codes
+      std::vector<std::vector<std::pair<int, std::vector<int>>>> rows(nf);
+      auto add = [&](int rn, int cn, int code) {
+        const int fr = node_fidx[n0 + rn], fc = node_fidx[n0 + cn];
+        if (fr < 0 || fc < 0) return;
+        auto& R = rows[fr];
+        for (auto& pr : R)
+          if (pr.first == fc) {
+            pr.second.push_back(code);
+            return;
+          }
+        R.push_back({fc, {code}});
+      };
+      for (int t = 0; t < b->tet_off[e + 1] - b->tet_off[e]; ++t) {
+        const int* tn = d->tet_nodes + 4 * (size_t)(b->tet_off[e] + t);
+        for (int a = 0; a < 4; ++a) {
+          tin[n0 + tn[a]].push_back({t, a});
+          for (int c = 0; c < 4; ++c) add(tn[a], tn[c], (t << 4) | (a << 2) | c);
+        }
+      }
+      for (int j = 0; j < b->abd_off[e + 1] - b->abd_off[e]; ++j) {
+        const int pn = d->abd_node[b->abd_off[e] + j];
+        const int slot = max_tet + j;
+        for (int a = 0; a < 4; ++a) {
+          tin[n0 + pn + a].push_back({slot, a});
+          for (int c = 0; c < 4; ++c) add(pn + a, pn + c, (slot << 4) | (a << 2) | c);
+        }
+      }
+      for (int f = 0; f < nf; ++f) {  // every free row has its diagonal (mass)
+        const int n = free_node[free_off[e] + f];
+        add(n, n, -1);
+      }
+      for (int f = 0; f < nf; ++f) {
+        auto& R = rows[f];
+        std::sort(R.begin(), R.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        const int fg = free_off[e] + f;
+        for (auto& pr : R) {
+          if (pr.first == f) sb_diag[fg] = (int)sb_col.size();
+          sb_col.push_back(pr.first);
+          for (int code : pr.second)
+            if (code >= 0) sbc.push_back(code);
+          sbc_ptr.push_back((int)sbc.size());
+        }
+        sb_rowptr[fg + 1] = (int)sb_col.size();
+      }
+    }
+    for (int n = 0; n < NN; ++n) {
+      for (auto& pr : tin[n]) tinc.push_back((pr.first << 2) | pr.second);
+      tinc_ptr[n + 1] = (int)tinc.size();
+    }
+  }
+  b->n_blk = (int)sb_col.size();
+  // ---- uploads ----
+  D.node_off = b->upload(b->node_off.data(), E + 1);
+  D.sv_off = b->upload(b->sv_off.data(), E + 1);
+  D.tri_off = b->upload(b->tri_off.data(), E + 1);
+  D.edge_off = b->upload(b->edge_off.data(), E + 1);
+  D.tet_off = b->upload(b->tet_off.data(), E + 1);
+  D.abd_off = b->upload(b->abd_off.data(), E + 1);
+  D.body_off = b->upload(b->body_off.data(), E + 1);
+  D.free_off = b->upload(free_off.data(), E + 1);
+  D.node_M = b->upload(d->node_M, 9 * (size_t)NN);
+  D.node_free = b->upload(d->node_free, NN);
+  D.node_body = b->upload(d->node_body, NN);
+  D.node_kind = b->upload(d->node_kind, NN);
+  D.node_sv = b->upload(d->node_sv, NN);
+  D.node_fidx = b->upload(node_fidx.data(), NN);
+  D.free_node = b->upload(free_node.data(), std::max(NF, 1));
+  D.sv_kind = b->upload(d->sv_kind, NS);
+  D.sv_node = b->upload(d->sv_node, NS);
+  D.sv_xi = b->upload(d->sv_xi, 3 * (size_t)NS);
+  D.sv_body = b->upload(d->sv_body, NS);
+  D.tris = b->upload(d->tris, 3 * (size_t)NTR);
+  D.edges = b->upload(d->edges, 2 * (size_t)NE);
+  D.edge_rest_sq = b->upload(d->edge_rest_sq, NE);
+  D.tet_nodes = b->upload(d->tet_nodes, 4 * (size_t)NTET);
+  D.tet_Dmi = b->upload(d->tet_Dmi, 9 * (size_t)NTET);
+  D.tet_V0 = b->upload(d->tet_V0, NTET);
+  D.tet_mu = b->upload(d->tet_mu, NTET);
+  D.tet_lam = b->upload(d->tet_lam, NTET);
+  D.abd_node = b->upload(d->abd_node, NA);
+  D.abd_kV = b->upload(d->abd_kV, NA);
+  D.body_kind = b->upload(d->body_kind, NB);
+  D.body_mu = b->upload(d->body_mu, NB);
+  D.body_pairmask = b->upload(d->body_pairmask, NB);
+  D.body_vel = b->upload(d->body_vel0, 3 * (size_t)NB);
+  D.gravity = b->upload(d->env_gravity, 3 * (size_t)E);
+  D.params = b->upload(d->env_params, (size_t)GRIP_NPARAM * E);
+  D.cell_hint = b->upload(d->env_cell_hint, E);
+  D.sb_rowptr = b->upload(sb_rowptr.data(), NF + 1);
+  D.sb_col = b->upload(sb_col.data(), sb_col.size());
+  D.sb_diag = b->upload(sb_diag.data(), std::max(NF, 1));
+  D.sbc_ptr = b->upload(sbc_ptr.data(), sbc_ptr.size());
+  D.sbc = b->upload(sbc.data(), sbc.size());
+  D.tinc_ptr = b->upload(tinc_ptr.data(), NN + 1);
+  D.tinc = b->upload(tinc.data(), tinc.size());
+  // state
+  D.x = b->upload(d->node_x0, 3 * (size_t)NN);
+  D.v = b->alloc<double>(3 * (size_t)NN);
+  D.x_t = b->alloc<double>(3 * (size_t)NN);
+  D.xhat = b->alloc<double>(3 * (size_t)NN);
+  D.pdir = b->alloc<double>(3 * (size_t)NN);
+  D.sv_pos = b->alloc<double>(3 * (size_t)NS);
+  D.surf_prev = b->alloc<double>(3 * (size_t)NS);
+  D.kin_pos = b->upload(d->sv_kin0, 3 * (size_t)NS);
+  D.sv_disp = b->alloc<double>(3 * (size_t)NS);
+  D.ell = b->alloc<double>(E);
+  D.tol = b->alloc<double>(E);
+  D.residual = b->alloc<double>(E);
+  D.energy = b->alloc<double>(E);
+  D.min_dist = b->alloc<double>(E);
+  D.time = b->alloc<double>(E);
+  int maxit = 1;
+  for (int e = 0; e < E; ++e) maxit = std::max(maxit, (int)d->env_params[(size_t)e * GRIP_NPARAM + GRIP_P_MAXIT]);
+  b->max_it = maxit;
+  D.max_alpha = maxit + 1;
+  D.alphas = b->alloc<double>((size_t)E * D.max_alpha);
+  D.iters = b->alloc<int>(E);
+  D.ns_status = b->alloc<int>(E);
+  D.reason = b->alloc<int>(E);
+  D.regularized = b->alloc<int>(E);
+  D.kin_blocked = b->alloc<int>(E);
+  D.needs_ls = b->alloc<int>(E);
+  D.ns_done = b->alloc<int>(E);
+  D.flags = b->alloc<int>(E);
+  D.step_index = b->alloc<int>(E);
+  D.newton_calls = b->alloc<int>(E);
+  D.pcg_iters = b->alloc<int>(E);
+  D.body_force = b->alloc<double>(NB);
+  D.contact_mask = b->alloc<unsigned int>(NB);
+  D.c1_n = b->alloc<int>(2 * (size_t)E);
+  D.c2_n = b->alloc<int>(2 * (size_t)E);
+  D.n_act = b->alloc<int>(E);
+  D.n_anc = b->alloc<int>(E);
+  D.work_off = b->alloc<int>(E + 1);
+  D.max_sv = max_sv; D.max_tri = max_tri; D.max_edge = max_edge; D.max_free = max_free;
+  D.max_node = max_node; D.max_tet = max_tet; D.max_abd = max_abd;
+  D.cap_pt = std::max(2048, 16 * max_sv);
+  D.cap_ee = std::max(4096, 16 * max_edge);
+  D.cap_act = 512;
+  D.cap_anc = 512;
+  D.cap_cells = 32 * std::max(max_tri, max_edge) + 4096;
+  D.bp_aabb = b->alloc<double>((size_t)E * 6 * std::max(max_tri, max_edge));
+  D.bp_cnt = b->alloc<int>((size_t)E * (std::max(max_sv, max_edge) + 1));
+  D.pcg_x = b->alloc<double>((size_t)E * 3 * max_free);
+  D.pcg_r = b->alloc<double>((size_t)E * 3 * max_free);
+  D.pcg_z = b->alloc<double>((size_t)E * 3 * max_free);
+  D.pcg_p = b->alloc<double>((size_t)E * 3 * max_free);
+  D.pcg_q = b->alloc<double>((size_t)E * 3 * max_free);
+  D.pcg_b = b->alloc<double>((size_t)E * 3 * max_free);
+  D.pcg_pinv = b->alloc<double>(9 * (size_t)std::max(NF, 1));
+  D.abd_pinv = b->alloc<double>(144 * (size_t)std::max(NA, 1));
+  D.sb_val = b->alloc<double>(9 * (size_t)std::max(b->n_blk, 1));
+  D.c_u = b->alloc<double>((size_t)E * 3 * max_sv);
+  D.c_w = b->alloc<double>((size_t)E * 3 * max_sv);
+  D.sv_g = b->alloc<double>((size_t)E * 3 * max_sv);
+  D.inc_ptr = b->alloc<int>((size_t)E * (max_sv + 1));
+  if (alloc_dynamic(b, false, 0)) return -1;
+  b->tet_env.resize(NTET);
+  for (int e = 0; e < E; ++e)
+    for (int t = b->tet_off[e]; t < b->tet_off[e + 1]; ++t) b->tet_env[t] = e;
+  b->d_tet_env = b->upload(b->tet_env.data(), std::max(NTET, 1));
+  b->d_list = b->alloc<int>(E + 1);
+  b->d_list2 = b->alloc<int>(E + 1);
+  CK(cudaMallocHost(&b->h_pin, 64 * sizeof(int)));
+  for (void* p : b->owned)
+    if (!p) {
+      g_err = "out of device memory";
+      return -1;
+    }
+  {
+    // every pointer member of Dev must be set (catches a forgotten allocation at create time)
+    const void* ptrs[] = {
+        D.node_off, D.sv_off, D.tri_off, D.edge_off, D.tet_off, D.abd_off, D.body_off, D.free_off, D.node_M,
+        D.node_free, D.node_body, D.node_kind, D.node_sv, D.node_fidx, D.free_node, D.sv_kind, D.sv_node, D.sv_xi,
+        D.sv_body, D.tris, D.edges, D.edge_rest_sq, D.tet_nodes, D.tet_Dmi, D.tet_V0, D.tet_mu, D.tet_lam, D.abd_node,
+        D.abd_kV, D.body_kind, D.body_mu, D.body_pairmask, D.body_vel, D.gravity, D.params, D.cell_hint, D.sb_rowptr,
+        D.sb_col, D.sb_diag, D.sbc_ptr, D.sbc, D.tinc_ptr, D.tinc, D.x, D.v, D.x_t, D.xhat, D.pdir, D.sv_pos,
+        D.surf_prev, D.kin_pos, D.sv_disp, D.ell, D.tol, D.residual, D.energy, D.alphas, D.min_dist, D.time, D.iters,
+        D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
+        D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
+        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.anc_v,
+        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
+        D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
+        D.inc_ptr, D.inc, D.sv_g};
+    for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
+      if (!ptrs[i]) {
+        g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
+        return -1;
+      }
+  }
+  CK(cudaStreamSynchronize(b->stream));
+  CK(cudaGetLastError());
+  *out = b;
+  return 0;
+}
+
+int grip_destroy(GripBatch* b) {
+  if (!b) return 0;
+  cudaStreamSynchronize(b->stream);
+  for (void* p : b->owned) cudaFree(p);
+  if (b->h_pin) cudaFreeHost(b->h_pin);
+  cudaEventDestroy(b->ev0);
+  cudaEventDestroy(b->ev1);
+  cudaStreamDestroy(b->stream);
+  delete b;
+  return 0;
+}
+
+int grip_set_controls(GripBatch* b, const double* gravity, const double* body_vel) {
+  if (gravity) CK(cudaMemcpyAsync(b->D.gravity, gravity, 3 * sizeof(double) * b->n_env, cudaMemcpyHostToDevice, b->stream));
+  if (body_vel)
+    CK(cudaMemcpyAsync(b->D.body_vel, body_vel, 3 * sizeof(double) * b->n_body, cudaMemcpyHostToDevice, b->stream));
+  return 0;
+}
+
+static std::vector<int> mask_to_list(const GripBatch* b, const uint8_t* m) {
+  std::vector<int> L;
+  for (int e = 0; e < b->n_env; ++e)
+    if (!m || m[e]) L.push_back(e);
+  return L;
+}
+
+int grip_begin_step(GripBatch* b, const uint8_t* active) {
+  std::vector<int> L = mask_to_list(b, active);
+  if (L.empty()) return 0;
+  if (upload_list(b, L, b->d_list)) return -1;
+  const int n = (int)L.size();
+  return run_with_growth(b, n, [&] { k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list); });
+}
+
+// one Newton sweep over the pending envs (list in b->d_list, n entries); returns new pending count
+static int newton_sweep(GripBatch* b, int n, int* n_out) {
+  Dev& D = b->D;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    k_candidates<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    k_work_scan<<<1, NT, 0, b->stream>>>(D, b->d_list, n);
+    k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
+    k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    k_linesearch<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    b->launches += 5;
+    b->sweeps += 1;
+    CK(cudaGetLastError());
+    std::vector<int> fl(b->n_env);
+    CK(cudaMemcpyAsync(fl.data(), D.flags, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+    std::vector<int> done(b->n_env);
+    CK(cudaMemcpyAsync(done.data(), D.ns_done, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+    std::vector<int> L(n);
+    CK(cudaMemcpyAsync(L.data(), b->d_list, sizeof(int) * n, cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+    bool ov = false;
+    for (int i = 0; i < n; ++i) ov |= (fl[L[i]] & FLAG_OVERFLOW) != 0;
+    if (ov) {
+      if (grow(b)) return -1;
+      CK(cudaMemsetAsync(D.flags, 0, sizeof(int) * b->n_env, b->stream));
+      // the overflowed envs did not move; sweep again with the same pending list
+      std::vector<int> keep;
+      for (int i = 0; i < n; ++i)
+        if (!done[L[i]]) keep.push_back(L[i]);
+      if (upload_list(b, keep, b->d_list)) return -1;
+      n = (int)keep.size();
+      if (n == 0) { *n_out = 0; return 0; }
+      continue;
+    }
+    std::vector<int> keep;
+    for (int i = 0; i < n; ++i)
+      if (!done[L[i]]) keep.push_back(L[i]);
+    if (upload_list(b, keep, b->d_list)) return -1;
+    *n_out = (int)keep.size();
+    return 0;
+  }
+  g_err = "buffer growth did not converge";
+  return -1;
+}
+
+int grip_newton_iteration(GripBatch* b, uint8_t* pending) {
+  std::vector<int> L = mask_to_list(b, pending);
+  if (L.empty()) return 0;
+  if (upload_list(b, L, b->d_list)) return -1;
+  int n2 = 0;
+  if (newton_sweep(b, (int)L.size(), &n2)) return -1;
+  std::vector<int> done(b->n_env);
+  CK(cudaMemcpy(done.data(), b->D.ns_done, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost));
+  for (int e = 0; e < b->n_env; ++e)
+    if (pending[e] && done[e]) pending[e] = 0;
+  return 0;
+}
+
+static int read_reports(GripBatch* b, const std::vector<int>& L, GripStepReport* reports, double* alphas) {
+  const int E = b->n_env;
+  Dev& D = b->D;
+  std::vector<int> st(E), rs(E), it(E), kb(E), rg(E), si(E), nc(E), pi(E);
+  std::vector<double> res(E), md(E), en(E), tm(E);
+  CK(cudaMemcpyAsync(st.data(), D.ns_status, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(rs.data(), D.reason, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(it.data(), D.iters, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(kb.data(), D.kin_blocked, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(rg.data(), D.regularized, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(si.data(), D.step_index, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(nc.data(), D.newton_calls, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(pi.data(), D.pcg_iters, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(res.data(), D.residual, sizeof(double) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(md.data(), D.min_dist, sizeof(double) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(en.data(), D.energy, sizeof(double) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(tm.data(), D.time, sizeof(double) * E, cudaMemcpyDeviceToHost, b->stream));
+  if (alphas)
+    CK(cudaMemcpyAsync(alphas, D.alphas, sizeof(double) * (size_t)E * D.max_alpha, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  const double* P = nullptr;
+  (void)P;
+  for (int e : L) {
+    GripStepReport& r = reports[e];
+    r.status = st[e];
+    r.reason = rs[e];
+    r.iterations = it[e];
+    r.n_alphas = std::min(it[e], D.max_alpha);
+    r.residual = res[e];
+    r.min_distance = md[e];
+    r.energy = en[e];
+    r.step_index = si[e] - 1;
+    r.time = tm[e];
+    r.kinematic_blocked = kb[e];
+    r.regularized = rg[e];
+    r.newton_calls = nc[e];
+    r.pcg_iters = pi[e];
+  }
+  return 0;
+}
+
+int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas) {
+  std::vector<int> L = mask_to_list(b, active);
+  if (L.empty()) return 0;
+  if (upload_list(b, L, b->d_list)) return -1;
+  const int n = (int)L.size();
+  if (run_with_growth(b, n, [&] { k_finalize<<<n, NT, 0, b->stream>>>(b->D, b->d_list); })) return -1;
+  if (reports) return read_reports(b, L, reports, alphas);
+  return 0;
+}
+
+int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas) {
+  std::vector<int> L = mask_to_list(b, active);
+  if (L.empty()) return 0;
+  const long long l0 = b->launches;
+  CK(cudaEventRecord(b->ev0, b->stream));
+  if (upload_list(b, L, b->d_list)) return -1;
+  int n = (int)L.size();
+  if (run_with_growth(b, n, [&] { k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list); })) return -1;
+  // envs that failed in begin_step are done
+  std::vector<int> done(b->n_env);
+  CK(cudaMemcpy(done.data(), b->D.ns_done, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost));
+  std::vector<int> P;
+  for (int e : L)
+    if (!done[e]) P.push_back(e);
+  if (upload_list(b, P, b->d_list)) return -1;
+  n = (int)P.size();
+  while (n > 0) {
+    int n2 = 0;
+    if (newton_sweep(b, n, &n2)) return -1;
+    n = n2;
+  }
+  if (upload_list(b, L, b->d_list)) return -1;
+  n = (int)L.size();
+  if (run_with_growth(b, n, [&] { k_finalize<<<n, NT, 0, b->stream>>>(b->D, b->d_list); })) return -1;
+  CK(cudaEventRecord(b->ev1, b->stream));
+  CK(cudaEventSynchronize(b->ev1));
+  float ms = 0.0f;
+  CK(cudaEventElapsedTime(&ms, b->ev0, b->ev1));
+  b->last_ms = ms;
+  (void)l0;
+  if (reports) return read_reports(b, L, reports, alphas);
+  return 0;
+}
+
+int grip_get_state(GripBatch* b, double* x, double* v, double* kin) {
+  if (x) CK(cudaMemcpyAsync(x, b->D.x, 3 * sizeof(double) * b->n_node, cudaMemcpyDeviceToHost, b->stream));
+  if (v) CK(cudaMemcpyAsync(v, b->D.v, 3 * sizeof(double) * b->n_node, cudaMemcpyDeviceToHost, b->stream));
+  if (kin) CK(cudaMemcpyAsync(kin, b->D.kin_pos, 3 * sizeof(double) * b->n_sv, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_set_state(GripBatch* b, const double* x, const double* v, const double* kin) {
+  if (x) CK(cudaMemcpyAsync(b->D.x, x, 3 * sizeof(double) * b->n_node, cudaMemcpyHostToDevice, b->stream));
+  if (v) CK(cudaMemcpyAsync(b->D.v, v, 3 * sizeof(double) * b->n_node, cudaMemcpyHostToDevice, b->stream));
+  if (kin) CK(cudaMemcpyAsync(b->D.kin_pos, kin, 3 * sizeof(double) * b->n_sv, cudaMemcpyHostToDevice, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_get_surface(GripBatch* b, double* sv) {
+  std::vector<int> L = mask_to_list(b, nullptr);
+  if (upload_list(b, L, b->d_list)) return -1;
+  k_surface_all<<<b->n_env, 128, 0, b->stream>>>(b->D, b->d_list);
+  b->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(sv, b->D.sv_pos, 3 * sizeof(double) * b->n_sv, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_get_contacts(GripBatch* b, double* body_force, uint32_t* contact_mask, double* min_distance) {
+  if (body_force) CK(cudaMemcpyAsync(body_force, b->D.body_force, sizeof(double) * b->n_body, cudaMemcpyDeviceToHost, b->stream));
+  if (contact_mask)
+    CK(cudaMemcpyAsync(contact_mask, b->D.contact_mask, sizeof(uint32_t) * b->n_body, cudaMemcpyDeviceToHost, b->stream));
+  if (min_distance) CK(cudaMemcpyAsync(min_distance, b->D.min_dist, sizeof(double) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_query_candidates(GripBatch* b, int env, double radius, int32_t* pt, int32_t cap_pt, int32_t* n_pt, int32_t* ee,
+                          int32_t cap_ee, int32_t* n_ee) {
+  if (env < 0 || env >= b->n_env) {
+    g_err = "env out of range";
+    return -1;
+  }
+  std::vector<int> L{env};
+  if (upload_list(b, L, b->d_list)) return -1;
+  if (run_with_growth(b, 1, [&] { k_query<<<1, NT, 0, b->stream>>>(b->D, b->d_list, radius); })) return -1;
+  int cn[2];
+  CK(cudaMemcpy(cn, b->D.c2_n + 2 * env, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  *n_pt = cn[0];
+  *n_ee = cn[1];
+  if (pt) CK(cudaMemcpy(pt, b->D.c2_pt + (size_t)env * 4 * b->D.cap_pt, 4 * sizeof(int) * std::min(cn[0], cap_pt),
+                        cudaMemcpyDeviceToHost));
+  if (ee) CK(cudaMemcpy(ee, b->D.c2_ee + (size_t)env * 4 * b->D.cap_ee, 4 * sizeof(int) * std::min(cn[1], cap_ee),
+                        cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int grip_stress(GripBatch* b, double* out) {
+  if (b->n_tet == 0) return 0;
+  double* d_out = b->alloc<double>(7 * (size_t)b->n_tet);
+  if (!d_out) {
+    g_err = "out of device memory";
+    return -1;
+  }
+  k_stress<<<std::min(148 * 8, (b->n_tet + 127) / 128), 128, 0, b->stream>>>(b->D, b->n_tet, b->d_tet_env, d_out);
+  b->launches++;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, 7 * sizeof(double) * b->n_tet, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  b->release(d_out);
+  return 0;
+}
+
+int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps) {
+  if (device_ms) *device_ms = b->last_ms;
+  if (launches) *launches = b->launches;
+  if (newton_sweeps) *newton_sweeps = b->sweeps;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,1291 @@
+// Kernels of the batched IPC step.  Two shapes:
+//   *_env kernels: one CTA (NT threads) per environment, blockIdx.x indexes a
+//     device list of env ids; everything an env needs between two global
+//     decisions (broad phase, assembly + PCG, CCD + line search) runs inside it.
+//   k_elements: flat grid-stride kernel over the element work of all pending
+//     envs (Neo-Hookean tets, ABD, contact stencils, friction anchors) -- the
+//     fp64-heavy part with the 12x12 eigen-clamps, load-balanced chip-wide.
+#pragma once
+#include "grip_device.cuh"
+
+namespace grip {
+
+// ---------------------------------------------------------------------------
+// shared per-env helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void fail_env(const Dev& D, int e, int reason) {
+  if (threadIdx.x == 0) {
+    D.ns_status[e] = GRIP_NS_FAILED;
+    D.reason[e] = reason;
+    D.ns_done[e] = 1;
+    D.needs_ls[e] = 0;
+  }
+}
+
+// write sv positions of node array xs into D.sv_pos (env slice)
+__device__ void env_sv_positions(const Dev& D, const EnvIx& E, const double* xs) {
+  for (int i = threadIdx.x; i < E.ns; i += NT) st3(D.sv_pos + 3 * (size_t)(E.s0 + i), sv_at(D, E, i, xs));
+  __syncthreads();
+}
+
+// additive CCD over a candidate set, min over stencils (ccd.py:34-95).  disp: per-sv D.sv_disp.
+// returns alpha; *bad set if any stencil starts at d <= 1e-14
+__device__ double env_ccd(const Dev& D, const EnvIx& E, const int* pt, int npt, const int* ee, int nee, double scaling,
+                          int iters, double min_sep, int* bad, Red& sm) {
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  const double* U = D.sv_disp + 3 * (size_t)E.s0;
+  double amin = 1.0;
+  int b = 0;
+  for (int k = threadIdx.x; k < npt + nee; k += NT) {
+    const int is_ee = k >= npt;
+    const int* row = is_ee ? ee + 4 * (k - npt) : pt + 4 * k;
+    V3 x[4], p[4];
+    for (int j = 0; j < 4; ++j) {
+      x[j] = ld3(X + 3 * row[j]);
+      p[j] = ld3(U + 3 * row[j]);
+    }
+    int bk = 0;
+    double t = ccd_stencil(x, p, is_ee, scaling, iters, min_sep, &bk);
+    b |= bk;
+    amin = fmin(amin, t);
+  }
+  *bad = block_or(b, sm);
+  return fmax(block_min(amin, sm), 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// begin_step (solver.py:590-645)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  const int e = list[blockIdx.x];
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double dt = P[GRIP_P_DT], dhat = P[GRIP_P_DHAT];
+  for (int i = threadIdx.x; i < 3 * E.nn; i += NT) D.x_t[3 * (size_t)E.n0 + i] = D.x[3 * (size_t)E.n0 + i];
+  env_sv_positions(D, E, D.x);
+  for (int i = threadIdx.x; i < 3 * E.ns; i += NT) D.surf_prev[3 * (size_t)E.s0 + i] = D.sv_pos[3 * (size_t)E.s0 + i];
+  // which bodies move: kinematic with v != 0, soft with a prescribed mask and v != 0
+  int moving = 0;
+  for (int b = threadIdx.x; b < E.nb; b += NT) {
+    const double* vb = D.body_vel + 3 * (size_t)(E.b0 + b);
+    const bool nz = vb[0] != 0.0 || vb[1] != 0.0 || vb[2] != 0.0;
+    const int kind = D.body_kind[E.b0 + b];
+    if (nz && kind == 2) moving = 1;
+    if (nz && kind == 0) {
+      for (int n = 0; n < E.nn; ++n)
+        if (D.node_body[E.n0 + n] == b && !D.node_free[E.n0 + n]) { moving = 1; break; }
+    }
+  }
+  moving = block_or(moving, sm);
+  double alpha = 1.0;
+  if (moving) {
+    double md = 0.0;
+    for (int i = threadIdx.x; i < E.ns; i += NT) {
+      const int g = E.s0 + i;
+      V3 d = V3{0.0, 0.0, 0.0};
+      const int kind = D.sv_kind[g];
+      const double* vb = D.body_vel + 3 * (size_t)(E.b0 + D.sv_body[g]);
+      if (kind == 2) d = V3{vb[0] * dt, vb[1] * dt, vb[2] * dt};
+      if (kind == 0 && !D.node_free[E.n0 + D.sv_node[g]]) d = V3{vb[0] * dt, vb[1] * dt, vb[2] * dt};
+      st3(D.sv_disp + 3 * (size_t)g, d);
+      md = fmax(md, norm(d));
+    }
+    md = block_max(md, sm);
+    int* cn = D.c2_n + 2 * e;
+    const bool ok = broad_phase_env(D, E, dhat + 2.0 * md, D.c2_pt + (size_t)e * 4 * D.cap_pt,
+                                    D.c2_ee + (size_t)e * 4 * D.cap_ee, D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm);
+    if (!ok) {
+      if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+      return;
+    }
+    if (cn[0] + cn[1] > 0) {
+      int bad = 0;
+      alpha = env_ccd(D, E, D.c2_pt + (size_t)e * 4 * D.cap_pt, cn[0], D.c2_ee + (size_t)e * 4 * D.cap_ee, cn[1],
+                      P[GRIP_P_CCDSCALE], (int)P[GRIP_P_CCDIT], P[GRIP_P_KINGUARD], &bad, sm);
+      if (bad) {
+        // the reference raises out of begin_step here; the env is quarantined instead
+        fail_env(D, e, GRIP_R_CCD);
+        return;
+      }
+    }
+    // pre-move: masked soft nodes by alpha*(v dt); kinematic surfaces by (alpha v) dt
+    for (int n = threadIdx.x; n < E.nn; n += NT) {
+      const int g = E.n0 + n;
+      if (D.node_kind[g] == 0 && !D.node_free[g]) {
+        const double* vb = D.body_vel + 3 * (size_t)(E.b0 + D.node_body[g]);
+        for (int c = 0; c < 3; ++c) D.x[3 * (size_t)g + c] += alpha * (vb[c] * dt);
+      }
+    }
+    for (int i = threadIdx.x; i < E.ns; i += NT) {
+      const int g = E.s0 + i;
+      if (D.sv_kind[g] == 2) {
+        const double* vb = D.body_vel + 3 * (size_t)(E.b0 + D.sv_body[g]);
+        for (int c = 0; c < 3; ++c) D.kin_pos[3 * (size_t)g + c] += alpha * vb[c] * dt;
+      }
+    }
+    __syncthreads();
+  }
+  // implicit-Euler target: gravity on soft nodes and affine translations only
+  const double* gr = D.gravity + 3 * e;
+  for (int n = threadIdx.x; n < E.nn; n += NT) {
+    const int g = E.n0 + n;
+    const int kind = D.node_kind[g];
+    for (int c = 0; c < 3; ++c) {
+      const double a = kind == 2 ? 0.0 : gr[c];
+      const double xv = D.x[3 * (size_t)g + c];
+      D.xhat[3 * (size_t)g + c] = D.node_free[g] ? xv + dt * D.v[3 * (size_t)g + c] + dt * dt * a : xv;
+    }
+  }
+  __syncthreads();
+  env_sv_positions(D, E, D.x);
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = threadIdx.x; i < E.ns; i += NT)
+    for (int c = 0; c < 3; ++c) {
+      const double v = D.sv_pos[3 * (size_t)(E.s0 + i) + c];
+      lo[c] = fmin(lo[c], v);
+      hi[c] = fmax(hi[c], v);
+    }
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = block_min(lo[c], sm);
+    hi[c] = block_max(hi[c], sm);
+  }
+  if (threadIdx.x == 0) {
+    const double dx = hi[0] - lo[0], dy = hi[1] - lo[1], dz = hi[2] - lo[2];
+    const double diag = E.ns ? sqrt(dx * dx + dy * dy + dz * dz) : 0.0;
+    const double ell = fmax(diag, P[GRIP_P_ELLFLOOR]);
+    D.ell[e] = ell;
+    D.tol[e] = P[GRIP_P_RELTOL] * dt * ell;
+    D.kin_blocked[e] = moving && alpha < 1.0 - 1e-12;
+    D.iters[e] = 0;
+    D.ns_status[e] = GRIP_NS_RUNNING;
+    D.reason[e] = GRIP_R_NONE;
+    D.ns_done[e] = 0;
+    D.needs_ls[e] = 0;
+    D.residual[e] = INFINITY;
+    D.energy[e] = INFINITY;
+    D.regularized[e] = 0;
+    D.newton_calls[e] = 0;
+    D.pcg_iters[e] = 0;
+    D.flags[e] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Newton sweep 1/4: surface positions, candidate set at 1.05 dhat, active stencils
+// (solver.py:652-653, contact.py:283-309)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_candidates(Dev D, const int* list) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  const int e = list[blockIdx.x];
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double dhat = P[GRIP_P_DHAT];
+  if (threadIdx.x == 0) {
+    D.flags[e] = 0;
+    D.newton_calls[e] += 1;
+  }
+  env_sv_positions(D, E, D.x);
+  int* cn = D.c1_n + 2 * e;
+  int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
+  int* cee = D.c1_ee + (size_t)e * 4 * D.cap_ee;
+  const bool ok = broad_phase_env(D, E, dhat * 1.05, cpt, cee, D.c1_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm);
+  if (!ok) {
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    return;
+  }
+  const int npt = cn[0], nee = cn[1];
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  // active stencils in candidate order (PT first, then EE), non-positive distance check
+  int* act = D.act + (size_t)e * D.cap_act;
+  int base = 0, bad = 0;
+  for (int s = 0; s < npt + nee; s += NT) {
+    const int k = s + threadIdx.x;
+    int a = 0;
+    if (k < npt + nee) {
+      const bool is_ee = k >= npt;
+      const int* row = is_ee ? cee + 4 * (k - npt) : cpt + 4 * k;
+      V3 x0 = ld3(X + 3 * row[0]), x1 = ld3(X + 3 * row[1]), x2 = ld3(X + 3 * row[2]), x3 = ld3(X + 3 * row[3]);
+      const double Dq = is_ee ? ee_closest(x0, x1, x2, x3, nullptr, nullptr) : pt_closest(x0, x1, x2, x3, nullptr, nullptr);
+      if (!(Dq > 0.0)) bad = 1;
+      a = Dq < dhat * dhat;
+    }
+    int tot;
+    const int pre = block_scan(a, sm, &tot);
+    if (a && base + pre < D.cap_act) act[base + pre] = k >= npt ? D.cap_pt + (k - npt) : k;
+    base += tot;
+  }
+  bad = block_or(bad, sm);
+  if (threadIdx.x == 0) {
+    D.n_act[e] = base;
+    if (bad) D.flags[e] |= ERR_CONTACT_D;
+    if (base > D.cap_act) D.flags[e] |= FLAG_OVERFLOW;
+  }
+}
+
+// exclusive scan of per-env element work over the pending list (single CTA)
+__global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n) {
+  __shared__ Red sm;
+  int base = 0;
+  for (int s = 0; s < n; s += NT) {
+    const int i = s + threadIdx.x;
+    int w = 0;
+    if (i < n) {
+      const int e = list[i];
+      if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e])
+        w = (D.tet_off[e + 1] - D.tet_off[e]) + (D.abd_off[e + 1] - D.abd_off[e]) + D.n_act[e] + D.n_anc[e];
+    }
+    int tot;
+    const int pre = block_scan(w, sm, &tot);
+    if (i < n) D.work_off[i] = base + pre;
+    base += tot;
+  }
+  if (threadIdx.x == 0) D.work_off[n] = base;
+}
+
+// ---------------------------------------------------------------------------
+// Newton sweep 2/4: element energies, gradients and SPD-projected Hessians
+// (materials.py:116-188, contact.py:271-344, 475-524).  Unscaled (no dt^2).
+// Element slots per env: [tets | abd | contacts | anchors].
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_elements(Dev D, const int* list, int n) {
+  const int total = D.work_off[n];
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x) {
+    int lo = 0, hi = n;  // find list position: work_off[pos] <= w < work_off[pos+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (D.work_off[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    const int e = list[lo];
+    const EnvIx E = env_ix(D, e);
+    const double* P = P_(D, e);
+    int k = w - D.work_off[lo];
+    const size_t elbase = (size_t)e * D.cap_el;
+    double Eel = 0.0;
+    double g[12];
+    int slot;
+    int idx[4];
+    if (k < E.ntet) {
+      const int t = E.te0 + k;
+      slot = k;
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) {
+        idx[j] = D.tet_nodes[4 * (size_t)t + j];
+        x[j] = ld3(D.x + 3 * (size_t)(E.n0 + idx[j]));
+      }
+      double* H = D.el_H + (elbase + slot) * 144;
+      const int fl = nh_element(x, D.tet_Dmi + 9 * (size_t)t, D.tet_V0[t], D.tet_mu[t], D.tet_lam[t], &Eel, g, H);
+      if (fl & EL_INVERTED) {
+        atomicOr(&D.flags[e], ERR_INVERTED);
+        Eel = 0.0;
+        for (int i = 0; i < 12; ++i) g[i] = 0.0;
+      }
+    } else if ((k -= E.ntet) < E.na) {
+      const int a = E.a0 + k;
+      slot = D.max_tet + k;
+      const int pn = D.abd_node[a];
+      for (int j = 0; j < 4; ++j) idx[j] = pn + j;
+      const double* q = D.x + 3 * (size_t)(E.n0 + pn);
+      double* H = D.el_H + (elbase + slot) * 144;
+      Eel = abd_element(q + 3, D.abd_kV[a], g, H);
+    } else if ((k -= E.na) < D.n_act[e]) {
+      slot = D.max_tet + D.max_abd + k;
+      const int code = D.act[(size_t)e * D.cap_act + k];
+      const bool is_ee = code >= D.cap_pt;
+      const int* row = is_ee ? D.c1_ee + ((size_t)e * D.cap_ee + (code - D.cap_pt)) * 4 : D.c1_pt + ((size_t)e * D.cap_pt + code) * 4;
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) {
+        idx[j] = row[j];
+        x[j] = ld3(D.sv_pos + 3 * (size_t)(E.s0 + idx[j]));
+      }
+      double* H = D.el_H + (elbase + slot) * 144;
+      if (is_ee) {
+        const int* eid = D.c1_eid + ((size_t)e * D.cap_ee + (code - D.cap_pt)) * 2;
+        const double epsx = D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]];
+        ee_element(x, epsx, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, g, H, 1);
+      } else {
+        pt_element(x, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, g, H, 1);
+      }
+    } else {
+      k -= D.n_act[e];
+      slot = D.max_tet + D.max_abd + D.cap_act + k;
+      const size_t ai = (size_t)e * D.cap_anc + k;
+      V3 x[4], xp[4];
+      for (int j = 0; j < 4; ++j) {
+        idx[j] = D.anc_v[4 * ai + j];
+        x[j] = ld3(D.sv_pos + 3 * (size_t)(E.s0 + idx[j]));
+        xp[j] = ld3(D.surf_prev + 3 * (size_t)(E.s0 + idx[j]));
+      }
+      double* H = D.el_H + (elbase + slot) * 144;
+      Eel = friction_element(x, xp, D.anc_gamma + 4 * ai, D.anc_T + 6 * ai, D.anc_lam[ai], D.anc_mu[ai], P[GRIP_P_EPSV],
+                             P[GRIP_P_DT], g, H);
+    }
+    D.el_E[elbase + slot] = Eel;
+    for (int i = 0; i < 12; ++i) D.el_g[(elbase + slot) * 12 + i] = g[i];
+    for (int j = 0; j < 4; ++j) D.el_idx[(elbase + slot) * 4 + j] = idx[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Newton sweep 3/4: assembly + block-Jacobi PCG (solver.py:542-586, 654-676, 91-131)
+// ---------------------------------------------------------------------------
+
+// contact/friction element slots of env e: k in [0, n_ce) -> slot
+__device__ __forceinline__ int ce_slot(const Dev& D, int e, int k) {
+  const int na = D.n_act[e];
+  return k < na ? D.max_tet + D.max_abd + k : D.max_tet + D.max_abd + D.cap_act + (k - na);
+}
+
+struct AsmShared {
+  Red sm;
+  double abd_red[NWARP][12];
+  double chol[144];
+};
+
+// y = H_ff p over free nodes (static blocks + G^T H_sv G for contacts/friction)
+__device__ void spmv(const Dev& D, const EnvIx& E, double dt2, const double* p, double* y, AsmShared& A) {
+  const int e = E.e;
+  const size_t vb = (size_t)e * 3 * D.max_free;
+  // static blocks
+  for (int f = threadIdx.x; f < E.nf; f += NT) {
+    const int fg = E.f0 + f;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int b = D.sb_rowptr[fg]; b < D.sb_rowptr[fg + 1]; ++b) {
+      const double* B = D.sb_val + 9 * (size_t)b;
+      const double* q = p + vb + 3 * D.sb_col[b];
+      s0 += B[0] * q[0] + B[1] * q[1] + B[2] * q[2];
+      s1 += B[3] * q[0] + B[4] * q[1] + B[5] * q[2];
+      s2 += B[6] * q[0] + B[7] * q[1] + B[8] * q[2];
+    }
+    y[vb + 3 * f] = s0; y[vb + 3 * f + 1] = s1; y[vb + 3 * f + 2] = s2;
+  }
+  const int nce = D.n_act[e] + D.n_anc[e];
+  if (nce == 0) { __syncthreads(); return; }
+  // u = G p (sv space)
+  double* U = D.c_u + (size_t)e * 3 * D.max_sv;
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    const int g = E.s0 + i;
+    const int kind = D.sv_kind[g];
+    V3 u = V3{0.0, 0.0, 0.0};
+    if (kind == 0) {
+      const int f = D.node_fidx[E.n0 + D.sv_node[g]];
+      if (f >= 0) u = ld3(p + vb + 3 * f);
+    } else if (kind == 1) {
+      const int f = D.node_fidx[E.n0 + D.sv_node[g]];
+      const double* q = p + vb + 3 * f;
+      V3 xi = ld3(D.sv_xi + 3 * g);
+      u = V3{q[0] + xi.x * q[3] + xi.y * q[4] + xi.z * q[5], q[1] + xi.x * q[6] + xi.y * q[7] + xi.z * q[8],
+             q[2] + xi.x * q[9] + xi.y * q[10] + xi.z * q[11]};
+    }
+    st3(U + 3 * i, u);
+  }
+  __syncthreads();
+  // r_e = dt^2 H_e u_e, one thread per element row
+  double* R = D.c_r + (size_t)e * 12 * (D.cap_act + D.cap_anc);
+  const size_t elbase = (size_t)e * D.cap_el;
+  for (int t = threadIdx.x; t < 12 * nce; t += NT) {
+    const int k = t / 12, row = t - 12 * k;
+    const size_t sl = elbase + ce_slot(D, e, k);
+    const double* H = D.el_H + sl * 144 + row * 12;
+    const int* ix = D.el_idx + sl * 4;
+    double s = 0.0;
+    for (int j = 0; j < 4; ++j) {
+      const double* u = U + 3 * ix[j];
+      s += H[3 * j] * u[0] + H[3 * j + 1] * u[1] + H[3 * j + 2] * u[2];
+    }
+    R[t] = dt2 * s;
+  }
+  __syncthreads();
+  // w_sv = sum over incident (element, slot), fixed order
+  double* W = D.c_w + (size_t)e * 3 * D.max_sv;
+  const int* ip = D.inc_ptr + (size_t)e * (D.max_sv + 1);
+  const int* inc = D.inc + (size_t)e * 4 * (D.cap_act + D.cap_anc);
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    double w0 = 0.0, w1 = 0.0, w2 = 0.0;
+    for (int q = ip[i]; q < ip[i + 1]; ++q) {
+      const int code = inc[q];
+      const double* r = R + 12 * (code >> 2) + 3 * (code & 3);
+      w0 += r[0]; w1 += r[1]; w2 += r[2];
+    }
+    W[3 * i] = w0; W[3 * i + 1] = w1; W[3 * i + 2] = w2;
+  }
+  __syncthreads();
+  // y += G^T w : soft free nodes directly, affine bodies by block reduction
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    const int g = E.s0 + i;
+    if (D.sv_kind[g] == 0) {
+      const int f = D.node_fidx[E.n0 + D.sv_node[g]];
+      if (f >= 0)
+        for (int c = 0; c < 3; ++c) y[vb + 3 * f + c] += W[3 * i + c];
+    }
+  }
+  for (int a = 0; a < E.na; ++a) {
+    const int pn = D.abd_node[E.a0 + a];
+    double acc[12];
+    for (int c = 0; c < 12; ++c) acc[c] = 0.0;
+    for (int i = threadIdx.x; i < E.ns; i += NT) {
+      const int g = E.s0 + i;
+      if (D.sv_kind[g] != 1 || D.sv_node[g] != pn) continue;
+      V3 xi = ld3(D.sv_xi + 3 * g);
+      const double* w = W + 3 * i;
+      for (int c = 0; c < 3; ++c) {
+        acc[c] += w[c];
+        acc[3 + 3 * c] += w[c] * xi.x;
+        acc[4 + 3 * c] += w[c] * xi.y;
+        acc[5 + 3 * c] += w[c] * xi.z;
+      }
+    }
+    for (int c = 0; c < 12; ++c) {
+      double v = wsum(acc[c]);
+      if ((threadIdx.x & 31) == 0) A.abd_red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+      double s = 0.0;
+      for (int w = 0; w < NWARP; ++w) s += A.abd_red[w][threadIdx.x];
+      const int f = D.node_fidx[E.n0 + pn];
+      y[vb + 3 * f + threadIdx.x] += s;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+__device__ void precond(const Dev& D, const EnvIx& E, const double* r, double* z) {
+  const size_t vb = (size_t)E.e * 3 * D.max_free;
+  for (int f = threadIdx.x; f < E.nf; f += NT) {
+    const int n = D.free_node[E.f0 + f];
+    if (D.node_kind[E.n0 + n] != 0) continue;
+    const double* M = D.pcg_pinv + 9 * (size_t)(E.f0 + f);
+    const double* q = r + vb + 3 * f;
+    for (int c = 0; c < 3; ++c) z[vb + 3 * f + c] = M[3 * c] * q[0] + M[3 * c + 1] * q[1] + M[3 * c + 2] * q[2];
+  }
+  for (int t = threadIdx.x; t < 12 * E.na; t += NT) {
+    const int a = t / 12, i = t - 12 * a;
+    const int f = D.node_fidx[E.n0 + D.abd_node[E.a0 + a]];
+    const double* M = D.abd_pinv + 144 * (size_t)(E.a0 + a) + 12 * i;
+    const double* q = r + vb + 3 * f;
+    double s = 0.0;
+    for (int j = 0; j < 12; ++j) s += M[j] * q[j];
+    z[vb + 3 * f + i] = s;
+  }
+  __syncthreads();
+}
+
+__device__ double vdot(const Dev& D, const EnvIx& E, const double* a, const double* b, Red& sm) {
+  const size_t vb = (size_t)E.e * 3 * D.max_free;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < 3 * E.nf; i += NT) s += a[vb + i] * b[vb + i];
+  return block_sum(s, sm);
+}
+
+// 12x12 SPD inverse by Cholesky (single thread; tiny)
+__device__ bool chol_inv12(double* A) {
+  double L[144];
+  for (int i = 0; i < 144; ++i) L[i] = 0.0;
+  for (int i = 0; i < 12; ++i)
+    for (int j = 0; j <= i; ++j) {
+      double s = A[i * 12 + j];
+      for (int k = 0; k < j; ++k) s -= L[i * 12 + k] * L[j * 12 + k];
+      if (i == j) {
+        if (!(s > 0.0)) return false;
+        L[i * 12 + i] = sqrt(s);
+      } else {
+        L[i * 12 + j] = s / L[j * 12 + j];
+      }
+    }
+  // inverse = L^-T L^-1 : solve column by column
+  for (int c = 0; c < 12; ++c) {
+    double y[12];
+    for (int i = 0; i < 12; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = 0; k < i; ++k) s -= L[i * 12 + k] * y[k];
+      y[i] = s / L[i * 12 + i];
+    }
+    for (int i = 11; i >= 0; --i) {
+      double s = y[i];
+      for (int k = i + 1; k < 12; ++k) s -= L[k * 12 + i] * A[k * 12 + c];
+      A[i * 12 + c] = s / L[i * 12 + i];
+    }
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
+  __shared__ AsmShared A;
+  Red& sm = A.sm;
+  const int e = list[blockIdx.x];
+  if (D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double dt = P[GRIP_P_DT], dt2 = dt * dt;
+  // element-level failures, in the reference's raise order (_elastic before contact)
+  if (D.flags[e] & ERR_INVERTED) { fail_env(D, e, GRIP_R_INVERTED); return; }
+  if (D.flags[e] & ERR_CONTACT_D) { fail_env(D, e, GRIP_R_CONTACT_D); return; }
+  const size_t elbase = (size_t)e * D.cap_el;
+  const int nce = D.n_act[e] + D.n_anc[e];
+  // ---- contact incidence per sv (element order), used by gradient and SpMV ----
+  int* ip = D.inc_ptr + (size_t)e * (D.max_sv + 1);
+  int* inc = D.inc + (size_t)e * 4 * (D.cap_act + D.cap_anc);
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    int c = 0;
+    for (int k = 0; k < nce; ++k) {
+      const int* ix = D.el_idx + (elbase + ce_slot(D, e, k)) * 4;
+      c += (ix[0] == i) + (ix[1] == i) + (ix[2] == i) + (ix[3] == i);
+    }
+    ip[i] = c;
+  }
+  __syncthreads();
+  const int tot_inc = block_scan_array(ip, E.ns, sm);
+  if (threadIdx.x == 0) ip[E.ns] = tot_inc;
+  __syncthreads();
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    int q = ip[i];
+    for (int k = 0; k < nce; ++k) {
+      const int* ix = D.el_idx + (elbase + ce_slot(D, e, k)) * 4;
+      for (int j = 0; j < 4; ++j)
+        if (ix[j] == i) inc[q++] = (k << 2) | j;
+    }
+  }
+  __syncthreads();
+  // ---- energy (solver.py:543-562) ----
+  double ein = 0.0;
+  for (int n = threadIdx.x; n < E.nn; n += NT) {
+    const size_t g = E.n0 + n;
+    const double* M = D.node_M + 9 * g;
+    double d[3];
+    for (int c = 0; c < 3; ++c) d[c] = D.x[3 * g + c] - D.xhat[3 * g + c];
+    for (int r = 0; r < 3; ++r) ein += d[r] * (M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2]);
+  }
+  ein = 0.5 * block_sum(ein, sm);
+  double eel = 0.0;
+  for (int k = threadIdx.x; k < E.ntet + E.na; k += NT)
+    eel += D.el_E[elbase + (k < E.ntet ? k : D.max_tet + (k - E.ntet))];
+  eel = block_sum(eel, sm);
+  double ecf = 0.0;
+  for (int k = threadIdx.x; k < nce; k += NT) ecf += D.el_E[elbase + ce_slot(D, e, k)];
+  ecf = block_sum(ecf, sm);
+  const double Etot = ein + dt2 * eel + dt2 * ecf;
+  // ---- gradient: g = M dx + dt^2 (g_el + G^T g_sv) ----
+  double* SG = D.sv_g + (size_t)e * 3 * D.max_sv;
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int q = ip[i]; q < ip[i + 1]; ++q) {
+      const int code = inc[q];
+      const double* gg = D.el_g + (elbase + ce_slot(D, e, code >> 2)) * 12 + 3 * (code & 3);
+      s0 += gg[0]; s1 += gg[1]; s2 += gg[2];
+    }
+    SG[3 * i] = s0; SG[3 * i + 1] = s1; SG[3 * i + 2] = s2;
+  }
+  __syncthreads();
+  const size_t vb = (size_t)e * 3 * D.max_free;
+  double* RHS = D.pcg_b;  // -g over free dofs
+  int nonfinite = !isfinite(Etot);
+  for (int n = threadIdx.x; n < E.nn; n += NT) {
+    const size_t g = E.n0 + n;
+    const double* M = D.node_M + 9 * g;
+    double d[3], gr[3];
+    for (int c = 0; c < 3; ++c) d[c] = D.x[3 * g + c] - D.xhat[3 * g + c];
+    for (int r = 0; r < 3; ++r) gr[r] = M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2];
+    double ge[3] = {0.0, 0.0, 0.0};
+    for (int q = D.tinc_ptr[g]; q < D.tinc_ptr[g + 1]; ++q) {
+      const int code = D.tinc[q];
+      const double* gg = D.el_g + (elbase + (code >> 2)) * 12 + 3 * (code & 3);
+      for (int c = 0; c < 3; ++c) ge[c] += gg[c];
+    }
+    const int kind = D.node_kind[g];
+    if (kind == 0) {
+      const int s = D.node_sv[g];
+      if (s >= 0)
+        for (int c = 0; c < 3; ++c) ge[c] += SG[3 * s + c];
+    }
+    for (int c = 0; c < 3; ++c) {
+      gr[c] += dt2 * ge[c];
+      if (!isfinite(gr[c])) nonfinite = 1;
+    }
+    const int f = D.node_fidx[g];
+    if (f >= 0 && kind == 0)
+      for (int c = 0; c < 3; ++c) RHS[vb + 3 * f + c] = -gr[c];
+    if (kind != 0) {  // affine: contact part added below
+      if (f >= 0)
+        for (int c = 0; c < 3; ++c) RHS[vb + 3 * f + c] = -gr[c];
+    }
+  }
+  __syncthreads();
+  for (int a = 0; a < E.na; ++a) {
+    const int pn = D.abd_node[E.a0 + a];
+    double acc[12];
+    for (int c = 0; c < 12; ++c) acc[c] = 0.0;
+    for (int i = threadIdx.x; i < E.ns; i += NT) {
+      const int g = E.s0 + i;
+      if (D.sv_kind[g] != 1 || D.sv_node[g] != pn) continue;
+      V3 xi = ld3(D.sv_xi + 3 * g);
+      const double* w = SG + 3 * i;
+      for (int c = 0; c < 3; ++c) {
+        acc[c] += w[c];
+        acc[3 + 3 * c] += w[c] * xi.x;
+        acc[4 + 3 * c] += w[c] * xi.y;
+        acc[5 + 3 * c] += w[c] * xi.z;
+      }
+    }
+    for (int c = 0; c < 12; ++c) {
+      double v = wsum(acc[c]);
+      if ((threadIdx.x & 31) == 0) A.abd_red[threadIdx.x >> 5][c] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 12) {
+      double s = 0.0;
+      for (int w = 0; w < NWARP; ++w) s += A.abd_red[w][threadIdx.x];
+      const int f = D.node_fidx[E.n0 + pn];
+      RHS[vb + 3 * f + threadIdx.x] -= dt2 * s;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < 3 * E.nf; i += NT) nonfinite |= !isfinite(RHS[vb + i]);
+  nonfinite = block_or(nonfinite, sm);
+  if (nonfinite) { fail_env(D, e, GRIP_R_NONFINITE); return; }
+  // ---- static block values (mass + dt^2 * element blocks) ----
+  for (int f = threadIdx.x; f < E.nf; f += NT) {
+    const int fg = E.f0 + f;
+    const int nrow = D.free_node[fg];
+    for (int b = D.sb_rowptr[fg]; b < D.sb_rowptr[fg + 1]; ++b) {
+      double v[9];
+      for (int i = 0; i < 9; ++i) v[i] = 0.0;
+      for (int q = D.sbc_ptr[b]; q < D.sbc_ptr[b + 1]; ++q) {
+        const int code = D.sbc[q];
+        const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
+        const double* H = D.el_H + (elbase + sl) * 144;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
+      }
+      const bool diag = D.sb_col[b] == f;
+      const double* M = D.node_M + 9 * (size_t)(E.n0 + nrow);
+      for (int i = 0; i < 9; ++i) D.sb_val[9 * (size_t)b + i] = (diag ? M[i] : 0.0) + dt2 * v[i];
+    }
+  }
+  __syncthreads();
+  // ---- preconditioner: soft 3x3 diagonal blocks, affine 12x12 body blocks ----
+  for (int f = threadIdx.x; f < E.nf; f += NT) {
+    const int fg = E.f0 + f;
+    const int n = D.free_node[fg];
+    if (D.node_kind[E.n0 + n] != 0) continue;
+    double Bd[9];
+    for (int i = 0; i < 9; ++i) Bd[i] = D.sb_val[9 * (size_t)D.sb_diag[fg] + i];
+    const int s = D.node_sv[E.n0 + n];
+    if (s >= 0)
+      for (int q = ip[s]; q < ip[s + 1]; ++q) {
+        const int code = inc[q];
+        const int sl = code & 3;
+        const double* H = D.el_H + (elbase + ce_slot(D, e, code >> 2)) * 144;
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) Bd[3 * i + j] += dt2 * H[(3 * sl + i) * 12 + 3 * sl + j];
+      }
+    inv3(Bd, D.pcg_pinv + 9 * (size_t)fg);
+  }
+  for (int a = 0; a < E.na; ++a) {
+    const int pn = D.abd_node[E.a0 + a];
+    const int fp = D.node_fidx[E.n0 + pn];
+    // static part: blocks among the 4 pseudo-nodes
+    for (int t = threadIdx.x; t < 144; t += NT) {
+      const int i = t / 12, j = t % 12;
+      const int fg = E.f0 + fp + i / 3;
+      double s = 0.0;
+      for (int b = D.sb_rowptr[fg]; b < D.sb_rowptr[fg + 1]; ++b)
+        if (D.sb_col[b] == fp + j / 3) s = D.sb_val[9 * (size_t)b + 3 * (i % 3) + (j % 3)];
+      // contacts: sum_e sum_{k,l on body} J_k^T H_kl J_l
+      double c = 0.0;
+      const int ni = i / 3, ci = i % 3, nj = j / 3, cj = j % 3;
+      for (int k = 0; k < nce; ++k) {
+        const size_t sl = elbase + ce_slot(D, e, k);
+        const int* ix = D.el_idx + sl * 4;
+        const double* H = D.el_H + sl * 144;
+        for (int u = 0; u < 4; ++u) {
+          const int gu = E.s0 + ix[u];
+          if (D.sv_kind[gu] != 1 || D.sv_node[gu] != pn) continue;
+          const double au = ni == 0 ? 1.0 : D.sv_xi[3 * (size_t)gu + ci];
+          const int ra = ni == 0 ? ci : ni - 1;
+          for (int w2 = 0; w2 < 4; ++w2) {
+            const int gw = E.s0 + ix[w2];
+            if (D.sv_kind[gw] != 1 || D.sv_node[gw] != pn) continue;
+            const double aw = nj == 0 ? 1.0 : D.sv_xi[3 * (size_t)gw + cj];
+            const int cb = nj == 0 ? cj : nj - 1;
+            c += au * aw * H[(3 * u + ra) * 12 + 3 * w2 + cb];
+          }
+        }
+      }
+      A.chol[t] = s + dt2 * c;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (!chol_inv12(A.chol)) {
+        // fall back to the diagonal (still SPD direction) if the block is not PD
+        for (int i = 0; i < 144; ++i) A.chol[i] = (i % 13 == 0 && A.chol[i] != 0.0) ? 1.0 / A.chol[i] : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < 144; t += NT) D.abd_pinv[144 * (size_t)(E.a0 + a) + t] = A.chol[t];
+    __syncthreads();
+  }
+  // ---- PCG on H_ff p = -g_f (rtol P[PCGRTOL]); regularized retry (solver.py:111-131) ----
+  double* X = D.pcg_x;
+  double* R = D.pcg_r;
+  double* Z = D.pcg_z;
+  double* Pp = D.pcg_p;
+  double* Q = D.pcg_q;
+  const int nf3 = 3 * E.nf;
+  double bnorm2 = 0.0;
+  for (int i = threadIdx.x; i < nf3; i += NT) bnorm2 += RHS[vb + i] * RHS[vb + i];
+  bnorm2 = block_sum(bnorm2, sm);
+  const double rtol = P[GRIP_P_PCGRTOL];
+  int pcg_total = 0;
+  bool solved = false;
+  double shift = 0.0;
+  if (bnorm2 == 0.0) {
+    for (int i = threadIdx.x; i < nf3; i += NT) X[vb + i] = 0.0;
+    solved = true;
+  }
+  const int maxit = max(200, 4 * nf3);
+  for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
+    if (attempt == 1) {
+      // shift = 1e-8 * max(max diag, 1) on every diagonal entry
+      double md = -INFINITY;
+      for (int f = threadIdx.x; f < E.nf; f += NT) {
+        const double* Bd = D.sb_val + 9 * (size_t)D.sb_diag[E.f0 + f];
+        md = fmax(md, fmax(Bd[0], fmax(Bd[4], Bd[8])));
+      }
+      md = block_max(md, sm);
+      shift = 1e-8 * fmax(md, 1.0);
+      for (int f = threadIdx.x; f < E.nf; f += NT) {
+        double* Bd = D.sb_val + 9 * (size_t)D.sb_diag[E.f0 + f];
+        Bd[0] += shift; Bd[4] += shift; Bd[8] += shift;
+      }
+      if (threadIdx.x == 0) D.regularized[e] = 1;
+      __syncthreads();
+    }
+    // r = b (stored in R), x = 0
+    for (int i = threadIdx.x; i < nf3; i += NT) {
+      X[vb + i] = 0.0;
+      R[vb + i] = RHS[vb + i];
+    }
+    __syncthreads();
+    precond(D, E, R, Z);
+    for (int i = threadIdx.x; i < nf3; i += NT) Pp[vb + i] = Z[vb + i];
+    __syncthreads();
+    double rz = vdot(D, E, R, Z, sm);
+    const double stop2 = rtol * rtol * bnorm2;
+    int it = 0;
+    bool conv = false, broke = false;
+    for (; it < maxit; ++it) {
+      spmv(D, E, dt2, Pp, Q, A);
+      const double pq = vdot(D, E, Pp, Q, sm);
+      if (!(pq > 0.0) || !isfinite(pq)) { broke = true; break; }
+      const double alpha = rz / pq;
+      double rr = 0.0;
+      for (int i = threadIdx.x; i < nf3; i += NT) {
+        X[vb + i] += alpha * Pp[vb + i];
+        const double rv = R[vb + i] - alpha * Q[vb + i];
+        R[vb + i] = rv;
+        rr += rv * rv;
+      }
+      rr = block_sum(rr, sm);
+      if (!isfinite(rr)) { broke = true; break; }
+      if (rr <= stop2) { conv = true; ++it; break; }
+      precond(D, E, R, Z);
+      const double rz2 = vdot(D, E, R, Z, sm);
+      const double beta = rz2 / rz;
+      rz = rz2;
+      for (int i = threadIdx.x; i < nf3; i += NT) Pp[vb + i] = Z[vb + i] + beta * Pp[vb + i];
+      __syncthreads();
+    }
+    pcg_total += it;
+    (void)broke;
+    solved = conv;
+  }
+  if (threadIdx.x == 0) D.pcg_iters[e] += pcg_total;
+  if (!solved) { fail_env(D, e, GRIP_R_SOLVE); return; }
+  // ---- convergence test and iteration cap (solver.py:663-676) ----
+  double res = 0.0;
+  for (int i = threadIdx.x; i < nf3; i += NT) res = fmax(res, fabs(X[vb + i]));
+  res = block_max(res, sm);
+  for (int n = threadIdx.x; n < E.nn; n += NT) {
+    const int f = D.node_fidx[E.n0 + n];
+    for (int c = 0; c < 3; ++c) D.pdir[3 * (size_t)(E.n0 + n) + c] = f >= 0 ? X[vb + 3 * f + c] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    D.residual[e] = res;
+    const double tol = D.tol[e];
+    if (res < tol) {
+      D.ns_done[e] = 1;
+      D.ns_status[e] = GRIP_NS_CONVERGED;
+      D.energy[e] = Etot;
+      D.needs_ls[e] = 0;
+    } else if (D.iters[e] >= (int)P[GRIP_P_MAXIT]) {
+      D.ns_done[e] = 1;
+      D.ns_status[e] = GRIP_NS_FAILED;
+      D.reason[e] = GRIP_R_NONCONV;
+      D.needs_ls[e] = 0;
+    } else {
+      D.needs_ls[e] = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Newton sweep 4/4: CCD + inversion filters + backtracking line search
+// (solver.py:678-726, _energy_only :518-533)
+// ---------------------------------------------------------------------------
+
+// incremental potential at x + a p with candidate set c2; +inf if invalid
+__device__ double env_energy(const Dev& D, const EnvIx& E, double a, const int* cpt, int npt, const int* cee,
+                             const int* ceid, int nee, Red& sm) {
+  const int e = E.e;
+  const double* P = P_(D, e);
+  const double dt = P[GRIP_P_DT], kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
+  double* Y = D.c_u + (size_t)e * 3 * D.max_sv;  // trial sv positions (scratch)
+  // trial surface positions: surface_positions(x + a p) (solver.py:525)
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    const int g = E.s0 + i;
+    const int kind = D.sv_kind[g];
+    V3 y;
+    if (kind == 2) {
+      y = ld3(D.kin_pos + 3 * (size_t)g);
+    } else {
+      const size_t nb = E.n0 + D.sv_node[g];
+      if (kind == 0) {
+        y = ld3(D.x + 3 * nb) + a * ld3(D.pdir + 3 * nb);
+      } else {
+        double q[12];
+        for (int c = 0; c < 12; ++c) q[c] = D.x[3 * nb + c] + a * D.pdir[3 * nb + c];
+        V3 xi = ld3(D.sv_xi + 3 * g);
+        y = V3{q[0] + xi.x * q[3] + xi.y * q[4] + xi.z * q[5], q[1] + xi.x * q[6] + xi.y * q[7] + xi.z * q[8],
+               q[2] + xi.x * q[9] + xi.y * q[10] + xi.z * q[11]};
+      }
+    }
+    st3(Y + 3 * i, y);
+  }
+  __syncthreads();
+  int bad = 0;
+  double ein = 0.0, eel = 0.0, ec = 0.0, ef = 0.0;
+  for (int n = threadIdx.x; n < E.nn; n += NT) {
+    const size_t g = E.n0 + n;
+    const double* M = D.node_M + 9 * g;
+    double d[3];
+    for (int c = 0; c < 3; ++c) d[c] = (D.x[3 * g + c] + a * D.pdir[3 * g + c]) - D.xhat[3 * g + c];
+    for (int r = 0; r < 3; ++r) ein += d[r] * (M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2]);
+  }
+  for (int t = threadIdx.x; t < E.ntet; t += NT) {
+    const int tg = E.te0 + t;
+    V3 x[4];
+    for (int j = 0; j < 4; ++j) {
+      const size_t g = E.n0 + D.tet_nodes[4 * (size_t)tg + j];
+      x[j] = ld3(D.x + 3 * g) + a * ld3(D.pdir + 3 * g);
+    }
+    double el = 0.0;
+    if (nh_element(x, D.tet_Dmi + 9 * (size_t)tg, D.tet_V0[tg], D.tet_mu[tg], D.tet_lam[tg], &el, nullptr, nullptr) &
+        EL_INVERTED)
+      bad = 1;
+    else
+      eel += el;
+  }
+  for (int k = threadIdx.x; k < E.na; k += NT) {
+    const size_t g = E.n0 + D.abd_node[E.a0 + k];
+    double Am[9];
+    for (int c = 0; c < 9; ++c) Am[c] = D.x[3 * g + 3 + c] + a * D.pdir[3 * g + 3 + c];
+    eel += abd_element(Am, D.abd_kV[E.a0 + k], nullptr, nullptr);
+  }
+  for (int k = threadIdx.x; k < npt + nee; k += NT) {
+    const bool is_ee = k >= npt;
+    const int* row = is_ee ? cee + 4 * (k - npt) : cpt + 4 * k;
+    V3 x[4];
+    for (int j = 0; j < 4; ++j) x[j] = ld3(Y + 3 * row[j]);
+    double el = 0.0;
+    int fl;
+    if (is_ee) {
+      const int* eid = ceid + 2 * (k - npt);
+      fl = ee_element(x, D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]], kappa, dhat, &el, nullptr,
+                      nullptr, 0);
+    } else {
+      fl = pt_element(x, kappa, dhat, &el, nullptr, nullptr, 0);
+    }
+    if (fl & EL_BAD_D) bad = 1;
+    else if (fl & EL_ACTIVE) ec += el;
+  }
+  const int nanc = D.n_anc[e];
+  for (int k = threadIdx.x; k < nanc; k += NT) {
+    const size_t ai = (size_t)e * D.cap_anc + k;
+    V3 x[4], xp[4];
+    for (int j = 0; j < 4; ++j) {
+      const int s = D.anc_v[4 * ai + j];
+      x[j] = ld3(Y + 3 * s);
+      xp[j] = ld3(D.surf_prev + 3 * (size_t)(E.s0 + s));
+    }
+    ef += friction_element(x, xp, D.anc_gamma + 4 * ai, D.anc_T + 6 * ai, D.anc_lam[ai], D.anc_mu[ai], P[GRIP_P_EPSV],
+                           dt, nullptr, nullptr);
+  }
+  bad = block_or(bad, sm);
+  ein = 0.5 * block_sum(ein, sm);
+  eel = block_sum(eel, sm);
+  ec = block_sum(ec, sm);
+  ef = block_sum(ef, sm);
+  if (bad) return INFINITY;
+  const double tot = ein + dt * dt * (eel + ec + ef);
+  return isfinite(tot) ? tot : INFINITY;
+}
+
+__global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  const int e = list[blockIdx.x];
+  if (D.ns_done[e] || !D.needs_ls[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double dhat = P[GRIP_P_DHAT], scaling = P[GRIP_P_CCDSCALE];
+  // disp = G p and its max norm
+  env_sv_positions(D, E, D.x);
+  double md = 0.0;
+  for (int i = threadIdx.x; i < E.ns; i += NT) {
+    V3 d = sv_dir(D, E, i, D.pdir);
+    st3(D.sv_disp + 3 * (size_t)(E.s0 + i), d);
+    md = fmax(md, norm(d));
+  }
+  md = block_max(md, sm);
+  int* cn = D.c2_n + 2 * e;
+  int* cpt = D.c2_pt + (size_t)e * 4 * D.cap_pt;
+  int* cee = D.c2_ee + (size_t)e * 4 * D.cap_ee;
+  int* ceid = D.c2_eid + (size_t)e * 2 * D.cap_ee;
+  if (!broad_phase_env(D, E, dhat + 2.0 * md, cpt, cee, ceid, cn, S, sm)) {
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    return;
+  }
+  const int npt = cn[0], nee = cn[1];
+  double alpha0 = 1.0;
+  if (npt + nee > 0) {
+    int bad = 0;
+    const double a = env_ccd(D, E, cpt, npt, cee, nee, scaling, (int)P[GRIP_P_CCDIT], 0.0, &bad, sm);
+    if (bad) { fail_env(D, e, GRIP_R_CCD); return; }
+    alpha0 = fmin(alpha0, a);
+  }
+  // tet inversion filter (ccd.py:191-204)
+  if (E.ntet > 0) {
+    int anyp = 0, bad = 0;
+    double tmin = INFINITY;
+    for (int t = threadIdx.x; t < E.ntet; t += NT) {
+      const int tg = E.te0 + t;
+      V3 x[4], p[4];
+      for (int j = 0; j < 4; ++j) {
+        const size_t g = E.n0 + D.tet_nodes[4 * (size_t)tg + j];
+        x[j] = ld3(D.x + 3 * g);
+        p[j] = ld3(D.pdir + 3 * g);
+        if (p[j].x != 0.0 || p[j].y != 0.0 || p[j].z != 0.0) anyp = 1;
+      }
+      double M0[9], dM[9];
+      tet_edge_matrix(x, M0);
+      tet_edge_matrix(p, dM);
+      const double d0 = det3(M0);
+      if (!(d0 > 0.0)) bad = 1;
+      else tmin = fmin(tmin, pencil_root(M0, dM, d0));
+    }
+    anyp = block_or(anyp, sm);
+    if (anyp) {
+      bad = block_or(bad, sm);
+      if (bad) { fail_env(D, e, GRIP_R_DET); return; }
+      tmin = block_min(tmin, sm);
+      if (tmin <= 1.0) {
+        double a = scaling * tmin;
+        bool okall = false;
+        for (int it = 0; it < 60; ++it) {
+          int neg = 0;
+          for (int t = threadIdx.x; t < E.ntet; t += NT) {
+            const int tg = E.te0 + t;
+            V3 x[4], p[4];
+            for (int j = 0; j < 4; ++j) {
+              const size_t g = E.n0 + D.tet_nodes[4 * (size_t)tg + j];
+              x[j] = ld3(D.x + 3 * g);
+              p[j] = ld3(D.pdir + 3 * g);
+            }
+            double M0[9], dM[9], Mt[9];
+            tet_edge_matrix(x, M0);
+            tet_edge_matrix(p, dM);
+            for (int c = 0; c < 9; ++c) Mt[c] = M0[c] + a * dM[c];
+            if (!(det3(Mt) > 0.0)) neg = 1;
+          }
+          neg = block_or(neg, sm);
+          if (!neg) { okall = true; break; }
+          a *= 0.5;
+        }
+        alpha0 = fmin(alpha0, okall ? a : 0.0);
+      }
+    }
+  }
+  // affine bodies: det(A + t dA) > 0 (solver.py:695-700)
+  for (int k = 0; k < E.na; ++k) {
+    const size_t g = E.n0 + D.abd_node[E.a0 + k];
+    double A0[9], dA[9];
+    bool any = false;
+    for (int c = 0; c < 9; ++c) {
+      A0[c] = D.x[3 * g + 3 + c];
+      dA[c] = D.pdir[3 * g + 3 + c];
+      any |= dA[c] != 0.0;
+    }
+    if (!any) continue;
+    const double d0 = det3(A0);
+    if (!(d0 > 0.0)) { fail_env(D, e, GRIP_R_DET); return; }
+    const double t = pencil_root(A0, dA, d0);
+    if (t > 1.0) continue;
+    double a = scaling * t;
+    bool okv = false;
+    for (int it = 0; it < 60; ++it) {
+      double Mt[9];
+      for (int c = 0; c < 9; ++c) Mt[c] = A0[c] + a * dA[c];
+      if (det3(Mt) > 0.0) { okv = true; break; }
+      a *= 0.5;
+    }
+    alpha0 = fmin(alpha0, okv ? a : 0.0);
+  }
+  // backtracking on strict decrease (solver.py:702-720)
+  const double E0 = env_energy(D, E, 0.0, cpt, npt, cee, ceid, nee, sm);
+  double alpha = alpha0, Et = INFINITY;
+  bool accepted = false;
+  const int maxls = (int)P[GRIP_P_MAXLS];
+  for (int it = 0; it < maxls; ++it) {
+    Et = env_energy(D, E, alpha, cpt, npt, cee, ceid, nee, sm);
+    if (Et < E0) { accepted = true; break; }
+    alpha *= 0.5;
+  }
+  if (!accepted) {
+    if (threadIdx.x == 0) {
+      D.ns_done[e] = 1;
+      D.needs_ls[e] = 0;
+      if (D.residual[e] < 10.0 * D.tol[e]) {
+        D.ns_status[e] = GRIP_NS_CONVERGED;
+        D.energy[e] = E0;
+      } else {
+        D.ns_status[e] = GRIP_NS_FAILED;
+        D.reason[e] = GRIP_R_LINESEARCH;
+      }
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < 3 * E.nn; i += NT) {
+    const size_t g = 3 * (size_t)E.n0 + i;
+    D.x[g] = D.x[g] + alpha * D.pdir[g];
+  }
+  if (threadIdx.x == 0) {
+    const int it = D.iters[e];
+    if (it < D.max_alpha) D.alphas[(size_t)e * D.max_alpha + it] = alpha;
+    D.iters[e] = it + 1;
+    D.energy[e] = Et;
+    D.needs_ls[e] = 0;
+  }
+}
+
+// pending list compaction: keep envs still iterating (including overflowed ones)
+__global__ void __launch_bounds__(NT) k_compact(Dev D, const int* list, int n, int* out, int* out_n, int* any_overflow) {
+  __shared__ Red sm;
+  int base = 0, ov = 0;
+  for (int s = 0; s < n; s += NT) {
+    const int i = s + threadIdx.x;
+    int keep = 0, e = -1;
+    if (i < n) {
+      e = list[i];
+      keep = !D.ns_done[e];
+      ov |= (D.flags[e] & FLAG_OVERFLOW) ? 1 : 0;
+    }
+    int tot;
+    const int pre = block_scan(keep, sm, &tot);
+    if (keep) out[base + pre] = e;
+    base += tot;
+  }
+  ov = block_or(ov, sm);
+  if (threadIdx.x == 0) {
+    *out_n = base;
+    *any_overflow = ov;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finalize_step (solver.py:733-762) + contact readout (protocol.py:72-98)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  __shared__ unsigned int cmask[32];
+  const int e = list[blockIdx.x];
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double dt = P[GRIP_P_DT], kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
+  if (threadIdx.x == 0) D.flags[e] = 0;
+  if (D.ns_status[e] == GRIP_NS_FAILED) {
+    if (threadIdx.x == 0) {
+      D.min_dist[e] = INFINITY;
+      D.time[e] += dt;
+      D.step_index[e] += 1;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < 3 * E.nn; i += NT) {
+    const size_t g = 3 * (size_t)E.n0 + i;
+    D.v[g] = (D.x[g] - D.x_t[g]) / dt;
+  }
+  env_sv_positions(D, E, D.x);
+  int* cn = D.c1_n + 2 * e;
+  int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
+  int* cee = D.c1_ee + (size_t)e * 4 * D.cap_ee;
+  int* ceid = D.c1_eid + (size_t)e * 2 * D.cap_ee;
+  if (!broad_phase_env(D, E, dhat * 1.05, cpt, cee, ceid, cn, S, sm)) {
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    return;
+  }
+  const int npt = cn[0], nee = cn[1];
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  if (threadIdx.x < 32) cmask[threadIdx.x] = 0u;
+  __syncthreads();
+  // anchors from active stencils, PT then EE in candidate order (contact.py:413-472)
+  double dmin = INFINITY;
+  int base = 0;
+  double fsum[32];
+  const int nbl = min(E.nb, 32);
+  for (int b = 0; b < nbl; ++b) fsum[b] = 0.0;
+  for (int s = 0; s < npt + nee; s += NT) {
+    const int k = s + threadIdx.x;
+    int act = 0;
+    double lam = 0.0, gam[4], Tm[6], mu = 0.0;
+    int rowv[4], bb[2];
+    if (k < npt + nee) {
+      const bool is_ee = k >= npt;
+      const int* row = is_ee ? cee + 4 * (k - npt) : cpt + 4 * k;
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) {
+        rowv[j] = row[j];
+        x[j] = ld3(X + 3 * row[j]);
+      }
+      double Dq, bary[3], sp = 0.0, tp = 0.0;
+      Dq = is_ee ? ee_closest(x[0], x[1], x[2], x[3], &sp, &tp) : pt_closest(x[0], x[1], x[2], x[3], bary, nullptr);
+      dmin = fmin(dmin, Dq);
+      if (Dq < dhat * dhat) {
+        act = 1;
+        const double d = sqrt(Dq);
+        double b0, b1, b2;
+        barrier_d(d, dhat, &b0, &b1, &b2);
+        V3 pa, pb;
+        if (is_ee) {
+          double c = cross_norm_sq(x, nullptr, nullptr);
+          const int* eid = ceid + 2 * (k - npt);
+          double m, dm, d2m;
+          edge_mollifier(c, D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]], &m, &dm, &d2m);
+          lam = kappa * m * fabs(b1);
+          pa = (1.0 - sp) * x[0] + sp * x[1];
+          pb = (1.0 - tp) * x[2] + tp * x[3];
+          gam[0] = 1.0 - sp; gam[1] = sp; gam[2] = -(1.0 - tp); gam[3] = -tp;
+          bb[0] = D.sv_body[E.s0 + row[0]];
+          bb[1] = D.sv_body[E.s0 + row[2]];
+        } else {
+          lam = kappa * fabs(b1);
+          pa = x[0];
+          pb = bary[0] * x[1] + bary[1] * x[2] + bary[2] * x[3];
+          gam[0] = 1.0; gam[1] = -bary[0]; gam[2] = -bary[1]; gam[3] = -bary[2];
+          bb[0] = D.sv_body[E.s0 + row[0]];
+          bb[1] = D.sv_body[E.s0 + row[1]];
+        }
+        const double ma = D.body_mu[E.b0 + bb[0]], mb = D.body_mu[E.b0 + bb[1]];
+        mu = P[GRIP_P_MURULE] == 0.0 ? sqrt(ma * mb) : fmin(ma, mb);
+        const double id = 1.0 / d;
+        V3 n = V3{(pa.x - pb.x) / d, (pa.y - pb.y) / d, (pa.z - pb.z) / d};
+        (void)id;
+        // tangent basis (contact.py:403-410): ref = e_argmin|n|
+        const double ax = fabs(n.x), ay = fabs(n.y), az = fabs(n.z);
+        V3 ref = (ax <= ay && ax <= az) ? V3{1, 0, 0} : ((ay <= az) ? V3{0, 1, 0} : V3{0, 0, 1});
+        V3 t1 = cross(ref, n);
+        const double l1 = norm(t1);
+        t1 = V3{t1.x / l1, t1.y / l1, t1.z / l1};
+        V3 t2 = cross(n, t1);
+        Tm[0] = t1.x; Tm[1] = t2.x; Tm[2] = t1.y; Tm[3] = t2.y; Tm[4] = t1.z; Tm[5] = t2.z;
+        for (int b = 0; b < nbl; ++b)
+          if (bb[0] == b || bb[1] == b) fsum[b] += lam;
+        if (bb[0] < 32 && bb[1] < 32) {
+          atomicOr(&cmask[bb[0]], 1u << bb[1]);
+          atomicOr(&cmask[bb[1]], 1u << bb[0]);
+        }
+      }
+    }
+    int tot;
+    const int pre = block_scan(act, sm, &tot);
+    if (act && base + pre < D.cap_anc) {
+      const size_t ai = (size_t)e * D.cap_anc + base + pre;
+      for (int j = 0; j < 4; ++j) {
+        D.anc_v[4 * ai + j] = rowv[j];
+        D.anc_gamma[4 * ai + j] = gam[j];
+      }
+      for (int j = 0; j < 6; ++j) D.anc_T[6 * ai + j] = Tm[j];
+      D.anc_lam[ai] = lam;
+      D.anc_mu[ai] = mu;
+      D.anc_b[2 * ai] = bb[0];
+      D.anc_b[2 * ai + 1] = bb[1];
+    }
+    base += tot;
+  }
+  if (base > D.cap_anc) {
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    return;
+  }
+  dmin = block_min(dmin, sm);
+  for (int b = 0; b < nbl; ++b) {
+    const double f = block_sum(fsum[b], sm);
+    if (threadIdx.x == 0) D.body_force[E.b0 + b] = f;
+  }
+  // quarantine check (multienv.py:105-108)
+  int nonfin = 0;
+  for (int i = threadIdx.x; i < 3 * E.nn; i += NT) nonfin |= !isfinite(D.x[3 * (size_t)E.n0 + i]);
+  nonfin = block_or(nonfin, sm);
+  if (threadIdx.x < nbl) D.contact_mask[E.b0 + threadIdx.x] = cmask[threadIdx.x];
+  if (threadIdx.x == 0) {
+    D.n_anc[e] = base;
+    D.min_dist[e] = (npt + nee) > 0 ? sqrt(dmin) : INFINITY;
+    D.time[e] += dt;
+    D.step_index[e] += 1;
+    if (nonfin) {
+      D.ns_status[e] = GRIP_NS_FAILED;
+      D.reason[e] = GRIP_R_NONFINITE_STATE;
+    }
+  }
+}
+
+// per-tet stress rows (materials.py:191-205), flat over all tets
+__global__ void k_stress(Dev D, int n_tet_total, const int* tet_env, double* out) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tet_total; t += gridDim.x * blockDim.x) {
+    const int e = tet_env[t];
+    const int n0 = D.node_off[e];
+    V3 x[4];
+    for (int j = 0; j < 4; ++j) x[j] = ld3(D.x + 3 * (size_t)(n0 + D.tet_nodes[4 * (size_t)t + j]));
+    double row[7];
+    if (!nh_stress(x, D.tet_Dmi + 9 * (size_t)t, D.tet_mu[t], D.tet_lam[t], row))
+      for (int c = 0; c < 7; ++c) row[c] = NAN;
+    for (int c = 0; c < 7; ++c) out[7 * (size_t)t + c] = row[c];
+  }
+}
+
+// surface positions of every env (state readout)
+__global__ void k_surface_all(Dev D, const int* list) {
+  const int e = list[blockIdx.x];
+  const EnvIx E = env_ix(D, e);
+  for (int i = threadIdx.x; i < E.ns; i += blockDim.x) st3(D.sv_pos + 3 * (size_t)(E.s0 + i), sv_at(D, E, i, D.x));
+}
+
+// candidate query on current positions
+__global__ void __launch_bounds__(NT) k_query(Dev D, const int* list, double r) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  const int e = list[blockIdx.x];
+  const EnvIx E = env_ix(D, e);
+  env_sv_positions(D, E, D.x);
+  if (!broad_phase_env(D, E, r, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
+                       D.c2_eid + (size_t)e * 2 * D.cap_ee, D.c2_n + 2 * e, S, sm)) {
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+  }
+}
+
+}  // namespace grip

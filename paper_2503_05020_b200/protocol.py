@@ -1,0 +1,404 @@
+"""Grasp validation protocol (gripsim/pipeline/protocol.py:1-277) on the device step.
+
+``run_grasp_trial`` keeps the reference's per-env semantics for a single
+Environment.  ``run_grasp_trials`` is the batched driver: one
+host-side phase state machine per env, all envs advanced by one lockstep
+device step per iteration, finger forces and contact flags read back as one
+small array per step.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GRAVITY_DIRECTIONS = np.array([[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]], np.float64)
+PHASES = ["gravity+x", "gravity-x", "gravity+y", "gravity-y", "gravity+z", "gravity-z"]
+
+
+@dataclass
+class TrialProtocol:
+    """protocol.py:25-46."""
+
+    settle_duration: float = 0.05
+    closing_speed: float = 0.05
+    force_halt: float = 50.0
+    gravity_magnitude: float = 9.8
+    gravity_phase_duration: float = 0.1
+    steady_speed_steps: int = 5
+    steady_max_duration: float = 1.0
+    stability_constant: float = 1.0
+
+    def __post_init__(self):
+        if min(self.settle_duration, self.gravity_phase_duration, self.steady_max_duration) <= 0:
+            raise ValueError("durations must be positive")
+        if self.force_halt <= 0 or self.closing_speed <= 0:
+            raise ValueError("closing speed and halt threshold must be positive")
+
+
+@dataclass
+class TrialRecord:
+    """protocol.py:49-69 (positions/stress recorded on request)."""
+
+    candidate: dict = field(default_factory=dict)
+    verdict: str = "unstable"
+    failure: dict = field(default_factory=dict)
+    phase_markers: dict = field(default_factory=dict)
+    positions: np.ndarray = None
+    velocities: np.ndarray = None
+    times: np.ndarray = None
+    stress: np.ndarray = None
+    step_reports: list = field(default_factory=list)
+    com_displacement: dict = field(default_factory=dict)
+    halt_forces: dict = field(default_factory=dict)
+    finger_forces: list = field(default_factory=list)
+    metrics: dict = field(default_factory=dict)
+    object_body: int = 0
+    gripper_bodies: tuple = ()
+    n_steps: int = 0
+
+
+# ---------------------------------------------------------------------------
+# contact readout (protocol.py:72-98, contact.py:348-372)
+# ---------------------------------------------------------------------------
+
+
+def _pt_dist2(x):
+    """Squared point-triangle distance (Ericson, same priority order as the device)."""
+    p, a, b, c = x[:, 0], x[:, 1], x[:, 2], x[:, 3]
+    ab, ac = b - a, c - a
+    d = lambda u, v: np.einsum("ij,ij->i", u, v)  # noqa: E731
+    d1, d2 = d(ab, p - a), d(ac, p - a)
+    d3, d4 = d(ab, p - b), d(ac, p - b)
+    d5, d6 = d(ab, p - c), d(ac, p - c)
+    va, vb, vc = d3 * d6 - d5 * d4, d5 * d2 - d1 * d6, d1 * d4 - d3 * d2
+    with np.errstate(divide="ignore", invalid="ignore"):
+        w_ab = np.where(d1 != d3, d1 / (d1 - d3), 0.0)
+        w_ac = np.where(d2 != d6, d2 / (d2 - d6), 0.0)
+        den_bc = (d4 - d3) + (d5 - d6)
+        w_bc = np.where(den_bc != 0.0, (d4 - d3) / den_bc, 0.0)
+        den = va + vb + vc
+        fv, fw = np.where(den != 0, vb / den, 0.0), np.where(den != 0, vc / den, 0.0)
+    conds = [(d1 <= 0) & (d2 <= 0), (d3 >= 0) & (d4 <= d3), (d6 >= 0) & (d5 <= d6),
+             (vc <= 0) & (d1 >= 0) & (d3 <= 0), (vb <= 0) & (d2 >= 0) & (d6 <= 0),
+             (va <= 0) & (d4 - d3 >= 0) & (d5 - d6 >= 0)]
+    z, o = np.zeros_like(d1), np.ones_like(d1)
+    b0 = np.select(conds, [o, z, z, 1 - w_ab, 1 - w_ac, z], 1 - fv - fw)
+    b1 = np.select(conds, [z, o, z, w_ab, z, 1 - w_bc], fv)
+    b2 = np.select(conds, [z, z, o, z, w_ac, w_bc], fw)
+    q = p - (b0[:, None] * a + b1[:, None] * b + b2[:, None] * c)
+    return np.einsum("ij,ij->i", q, q)
+
+
+def _ee_dist2(x):
+    a0, a1, b0, b1 = x[:, 0], x[:, 1], x[:, 2], x[:, 3]
+    d1, d2, r = a1 - a0, b1 - b0, a0 - b0
+    dd = lambda u, v: np.einsum("ij,ij->i", u, v)  # noqa: E731
+    a, e, f, c, b = dd(d1, d1), dd(d2, d2), dd(d2, r), dd(d1, r), dd(d1, d2)
+    den = a * e - b * b
+    with np.errstate(divide="ignore", invalid="ignore"):
+        s = np.where(den > 0, np.clip((b * f - c * e) / den, 0, 1), 0.0)
+        t = (b * s + f) / e
+        s = np.where(t < 0, np.clip(-c / a, 0, 1), np.where(t > 1, np.clip((b - c) / a, 0, 1), s))
+    t = np.clip(t, 0, 1)
+    q = (a0 + s[:, None] * d1) - (b0 + t[:, None] * d2)
+    return np.einsum("ij,ij->i", q, q), np.cross(d1, d2)
+
+
+def stencil_events(env, radius_factor=1.05, active_only=True):
+    """Per-stencil events at the current state: kind, bodies, verts, d, lambda (contact.py:348-372)."""
+    cp = env.contact_params
+    pt, ee = env.candidates(cp.dhat * radius_factor)
+    sv = env.surface_positions()
+    vb = env.layout.vbody
+    out = []
+    dh = cp.dhat
+
+    def lam_of(d, m=1.0):
+        ins = d < dh
+        dd = d - dh
+        with np.errstate(divide="ignore", invalid="ignore"):
+            ln = np.where(ins, np.log(d / dh), 0.0)
+        b1 = np.where(ins, -2.0 * dd * ln - dd * dd / d, 0.0)
+        return cp.kappa * m * np.abs(b1)
+
+    if len(pt):
+        d = np.sqrt(_pt_dist2(sv[pt]))
+        act = d < dh if active_only else np.ones(len(d), bool)
+        lam = lam_of(d)
+        for row, dd, ll in zip(pt[act], d[act], lam[act]):
+            out.append({"kind": "point-triangle", "bodies": (int(vb[row[0]]), int(vb[row[1]])),
+                        "verts": [int(v) for v in row], "d": float(dd), "lambda": float(ll)})
+    if len(ee):
+        D, _ = _ee_dist2(sv[ee])
+        d = np.sqrt(D)
+        act = d < dh if active_only else np.ones(len(d), bool)
+        rest = env.layout.surf_rest
+        u, v = sv[ee[:, 1]] - sv[ee[:, 0]], sv[ee[:, 3]] - sv[ee[:, 2]]
+        c = np.einsum("ij,ij->i", u, u) * np.einsum("ij,ij->i", v, v) - np.einsum("ij,ij->i", u, v) ** 2
+        ru, rv = rest[ee[:, 1]] - rest[ee[:, 0]], rest[ee[:, 3]] - rest[ee[:, 2]]
+        eps = 1e-3 * np.einsum("ij,ij->i", ru, ru) * np.einsum("ij,ij->i", rv, rv)
+        xr = c / eps
+        m = np.where(xr < 1.0, xr * (2.0 - xr), 1.0)
+        lam = lam_of(d, m)
+        for row, dd, ll in zip(ee[act], d[act], lam[act]):
+            out.append({"kind": "edge-edge", "bodies": (int(vb[row[0]]), int(vb[row[2]])),
+                        "verts": [int(x) for x in row], "d": float(dd), "lambda": float(ll)})
+    return out
+
+
+def contact_events_now(env):
+    """protocol.py:72-75."""
+    return stencil_events(env)
+
+
+def finger_contact_force(env, finger_bodies, events=None):
+    """Sum of barrier forces over stencils touching the finger (protocol.py:78-86)."""
+    ids = {finger_bodies} if np.isscalar(finger_bodies) else set(finger_bodies)
+    bad = [b for b in ids if b < 0 or b >= len(env.records)]
+    if bad:
+        raise KeyError(f"unknown finger link id(s): {bad}")
+    if events is None:
+        events = contact_events_now(env)
+    return sum(ev["lambda"] for ev in events if ids.intersection(ev["bodies"]))
+
+
+def object_gripper_contact(env, object_body, gripper_bodies, events=None):
+    """protocol.py:89-98."""
+    if events is None:
+        events = contact_events_now(env)
+    g = set(gripper_bodies)
+    return any(object_body in ev["bodies"] and set(ev["bodies"]) & g for ev in events)
+
+
+# ---------------------------------------------------------------------------
+# single-env trial (protocol.py:152-277)
+# ---------------------------------------------------------------------------
+
+
+def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closing_dirs=None):
+    """Full validation protocol on one Environment, reference semantics."""
+    dt = env.solver_params.dt
+    rec = TrialRecord(object_body=object_body,
+                      gripper_bodies=tuple(sorted({b for ids in finger_links.values() for b in ids})))
+    markers, halt_forces, positions, reps, times, forces_log, stress = {}, {}, [], [], [], [], []
+    n_done = [0]
+
+    def fail(phase, report):
+        rec.verdict = "sim-failed"
+        rec.failure = {"phase": phase, "reason": report.reason if report else env.fail_reason, "step": env.step_index}
+
+    last_events = [None]
+
+    def run_phase(name, n_steps, per_step=None, early_stop=None):
+        start = n_done[0]
+        for _ in range(n_steps):
+            report = env.step()
+            events = contact_events_now(env)
+            last_events[0] = events
+            forces = {f: finger_contact_force(env, ids, events) for f, ids in finger_links.items()}
+            n_done[0] += 1
+            times.append(env.time)
+            if record:
+                positions.append(env.node_positions().copy())
+                reps.append(report.to_dict())
+                forces_log.append(forces)
+            if per_step is not None:
+                per_step(forces)
+            if report.status == "failed":
+                fail(name, report)
+                return False
+            if early_stop is not None and early_stop():
+                break
+        markers[name] = [start, n_done[0]]
+        return True
+
+    env.gravity = np.zeros(3)
+    for ids in finger_links.values():
+        for b in ids:
+            env.records[b]["body"].velocity = np.zeros(3)
+    ok = run_phase("settle", int(np.ceil(protocol.settle_duration / dt)))
+    if ok:
+        halted = {f: False for f in finger_links}
+        for f, ids in finger_links.items():
+            d = (closing_dirs or {}).get(f, env.records[ids[0]].get("closing_dir"))
+            d = np.zeros(3) if d is None else np.asarray(d)
+            for b in ids:
+                env.records[b]["body"].velocity = d * protocol.closing_speed
+        opening = float(np.asarray(env.records[finger_links[list(finger_links)[0]][0]].get("opening", 0.08)))
+        max_close = int(np.ceil((opening / 2.0) / (protocol.closing_speed * dt))) + 5
+
+        def per_step(forces):
+            for f in finger_links:
+                if not halted[f] and forces[f] > protocol.force_halt:
+                    halted[f] = True
+                    halt_forces[f] = {"force": forces[f], "step": n_done[0] - 1}
+                    for b in finger_links[f]:
+                        env.records[b]["body"].velocity = np.zeros(3)
+
+        ok = run_phase("close", max_close, per_step=per_step, early_stop=lambda: all(halted.values()))
+        for ids in finger_links.values():
+            for b in ids:
+                env.records[b]["body"].velocity = np.zeros(3)
+    if ok:
+        quiet = [0]
+
+        def steady():
+            quiet[0] = quiet[0] + 1 if env.max_point_speed() < env.contact_params.eps_v else 0
+            return quiet[0] >= protocol.steady_speed_steps
+
+        ok = run_phase("hold", int(np.ceil(protocol.steady_max_duration / dt)), early_stop=steady)
+    com_disp = {}
+    n_grav = int(np.ceil(protocol.gravity_phase_duration / dt))
+    if ok:
+        for name, direction in zip(PHASES, GRAVITY_DIRECTIONS):
+            env.gravity = protocol.gravity_magnitude * direction
+            com0 = env.body_com(object_body).copy()
+            ok = run_phase(name, n_grav)
+            com_disp[name] = float(np.linalg.norm(env.body_com(object_body) - com0))
+            if not ok:
+                break
+    if rec.verdict != "sim-failed":
+        thr = protocol.stability_constant * n_grav * env.contact_params.eps_v * dt
+        events = last_events[0] if last_events[0] is not None else contact_events_now(env)
+        in_contact = object_gripper_contact(env, object_body, rec.gripper_bodies, events)
+        final = com_disp.get(PHASES[-1], np.inf)
+        rec.verdict = "stable" if (in_contact and final < thr) else "unstable"
+        rec.metrics.update(final_phase_com_disp=final, stability_threshold=thr, final_contact=bool(in_contact))
+    rec.phase_markers = markers
+    rec.com_displacement = com_disp
+    rec.halt_forces = halt_forces
+    rec.n_steps = n_done[0]
+    if record:
+        rec.positions = np.array(positions)
+        rec.times = np.array(times)
+        rec.step_reports = reps
+        rec.finger_forces = forces_log
+    return rec
+
+
+# ---------------------------------------------------------------------------
+# batched trials: one state machine per env, lockstep device steps
+# ---------------------------------------------------------------------------
+
+_SETTLE, _CLOSE, _HOLD, _GRAV, _DONE = range(5)
+
+
+def run_grasp_trials(group, scenes, protocol=None, record_positions=False, max_steps=None, on_step=None):
+    """Run the protocol for every env of a DeviceEnvGroup / Batch group at once.
+
+    scenes[i] provides object_body, finger_links (name -> (body,)), closing_dirs,
+    opening.  Returns a list of TrialRecord (no per-step position log unless
+    record_positions).  Labels follow protocol.py:152-277 step for step.
+    """
+    protocol = protocol or TrialProtocol()
+    envs = group.envs
+    E = len(envs)
+    dt = envs[0].solver_params.dt
+    n_settle = int(np.ceil(protocol.settle_duration / dt))
+    n_hold = int(np.ceil(protocol.steady_max_duration / dt))
+    n_grav = int(np.ceil(protocol.gravity_phase_duration / dt))
+    phase = np.full(E, _SETTLE)
+    pstep = np.zeros(E, int)
+    gphase = np.zeros(E, int)
+    quiet = np.zeros(E, int)
+    recs = [TrialRecord(object_body=s.object_body,
+                        gripper_bodies=tuple(sorted({b for ids in s.finger_links.values() for b in ids})))
+            for s in scenes]
+    halted = [{f: False for f in s.finger_links} for s in scenes]
+    max_close = [int(np.ceil((s.opening / 2.0) / (protocol.closing_speed * dt))) + 5 for s in scenes]
+    com0 = [None] * E
+    nsteps = np.zeros(E, int)
+    phase_start = np.zeros(E, int)
+    pos_log = [[] for _ in range(E)]
+    for e, s in zip(envs, scenes):
+        e.gravity = np.zeros(3)
+        for ids in s.finger_links.values():
+            for b in ids:
+                e.bodies[b].velocity = np.zeros(3)
+    off = group.packed.body_off
+    total = 0
+    while True:
+        active = [i for i in range(E) if phase[i] != _DONE]
+        if not active or (max_steps is not None and total >= max_steps):
+            break
+        reps = group._step(active)
+        total += 1
+        force, mask, _ = group.dev.contacts()
+        need_state = any(phase[i] in (_HOLD, _GRAV) for i in active) or record_positions
+        x_all, v_all, _ = group._state() if need_state else (None, None, None)
+        for i in active:
+            env, sc, r = envs[i], scenes[i], reps[i]
+            nsteps[i] += 1
+            if record_positions:
+                pos_log[i].append(group._node_slice(i, "x").copy())
+            fbody = force[off[i]:off[i + 1]]
+            forces = {f: float(sum(fbody[b] for b in ids)) for f, ids in sc.finger_links.items()}
+            name = {_SETTLE: "settle", _CLOSE: "close", _HOLD: "hold"}.get(phase[i], PHASES[gphase[i]] if phase[i] == _GRAV else "")
+            pstep[i] += 1
+            if phase[i] == _CLOSE:
+                for f, ids in sc.finger_links.items():
+                    if not halted[i][f] and forces[f] > protocol.force_halt:
+                        halted[i][f] = True
+                        recs[i].halt_forces[f] = {"force": forces[f], "step": int(nsteps[i] - 1)}
+                        for b in ids:
+                            env.bodies[b].velocity = np.zeros(3)
+            if r.status == "failed":
+                recs[i].verdict = "sim-failed"
+                recs[i].failure = {"phase": name, "reason": r.reason, "step": env.step_index}
+                if phase[i] == _GRAV:
+                    recs[i].com_displacement[name] = float(np.linalg.norm(env.body_com(sc.object_body) - com0[i]))
+                phase[i] = _DONE
+                continue
+            ended = False
+            if phase[i] == _SETTLE:
+                ended = pstep[i] >= n_settle
+            elif phase[i] == _CLOSE:
+                ended = all(halted[i].values()) or pstep[i] >= max_close[i]
+            elif phase[i] == _HOLD:
+                quiet[i] = quiet[i] + 1 if env.max_point_speed() < env.contact_params.eps_v else 0
+                ended = quiet[i] >= protocol.steady_speed_steps or pstep[i] >= n_hold
+            elif phase[i] == _GRAV:
+                ended = pstep[i] >= n_grav
+            if not ended:
+                continue
+            recs[i].phase_markers[name] = [int(phase_start[i]), int(nsteps[i])]
+            phase_start[i] = nsteps[i]
+            pstep[i] = 0
+            if phase[i] == _SETTLE:
+                phase[i] = _CLOSE
+                for f, ids in sc.finger_links.items():
+                    for b in ids:
+                        env.bodies[b].velocity = np.asarray(sc.closing_dirs[f]) * protocol.closing_speed
+            elif phase[i] == _CLOSE:
+                for ids in sc.finger_links.values():
+                    for b in ids:
+                        env.bodies[b].velocity = np.zeros(3)
+                phase[i] = _HOLD
+            elif phase[i] == _HOLD:
+                phase[i] = _GRAV
+                gphase[i] = 0
+                env.gravity = protocol.gravity_magnitude * GRAVITY_DIRECTIONS[0]
+                com0[i] = env.body_com(sc.object_body).copy()
+            elif phase[i] == _GRAV:
+                recs[i].com_displacement[name] = float(np.linalg.norm(env.body_com(sc.object_body) - com0[i]))
+                gphase[i] += 1
+                if gphase[i] >= 6:
+                    phase[i] = _DONE
+                    thr = protocol.stability_constant * n_grav * env.contact_params.eps_v * dt
+                    in_contact = bool(mask[off[i] + sc.object_body] & sum(1 << b for b in recs[i].gripper_bodies))
+                    final = recs[i].com_displacement.get(PHASES[-1], np.inf)
+                    recs[i].verdict = "stable" if (in_contact and final < thr) else "unstable"
+                    recs[i].metrics.update(final_phase_com_disp=final, stability_threshold=thr,
+                                           final_contact=in_contact)
+                else:
+                    env.gravity = protocol.gravity_magnitude * GRAVITY_DIRECTIONS[gphase[i]]
+                    com0[i] = env.body_com(sc.object_body).copy()
+        if on_step is not None:
+            on_step(total, reps)
+    for i in range(E):
+        recs[i].n_steps = int(nsteps[i])
+        if record_positions:
+            recs[i].positions = np.array(pos_log[i])
+    return recs

@@ -1,0 +1,138 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+fixtures and the CPU oracle on the same seeded scenes.
+
+Bars (BASELINE.json north star): candidate sets bit-exact; per-step vertex
+positions within 1e-6 * ell (ell = max(bbox diagonal, 0.05), solver.py:644);
+identical step status / failure reason and Newton iteration counts.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TRAJ_TOL = 1e-6   # x error / ell
+
+
+def _scene(d):
+    from paper_2503_05020_b200 import scene as sc
+    if str(d["kind"]) == "bimanual":
+        return sc.bimanual_scene()
+    return sc.build_trial_scene(sc.ObjectSpec(kind=str(d["kind"]), soft=bool(d["soft_object"])),
+                                sc.GripperSpec(soft_fingers=bool(d["soft_fingers"])),
+                                d["cand_R"], d["cand_T"], float(d["cand_opening"]))
+
+
+def _rollout(env, scene, n_steps, gravity_after=None, halt=50.0):
+    """Closing rollout with per-finger force halt, on the device."""
+    halted = {f: False for f in scene.finger_links}
+    for f, ids in scene.finger_links.items():
+        for b in ids:
+            env.bodies[b].velocity = scene.closing_dirs[f] * 0.05
+    xs, reps, forces = [], [], []
+    for k in range(n_steps):
+        if gravity_after is not None and k == gravity_after:
+            env.gravity = np.array([0.0, 0.0, -9.8])
+        rep = env.step()
+        fb, _, _ = env.contact_forces()
+        fr = {f: float(sum(fb[b] for b in ids)) for f, ids in scene.finger_links.items()}
+        xs.append(env.x.copy())
+        reps.append(rep)
+        forces.append(fr)
+        for f in scene.finger_links:
+            if not halted[f] and fr[f] > halt:
+                halted[f] = True
+                for b in scene.finger_links[f]:
+                    env.bodies[b].velocity = np.zeros(3)
+        if rep.status == "failed":
+            break
+    return xs, reps, forces
+
+
+@pytest.mark.parametrize("name,steps,grav", [("cfg1", 12, None), ("cylfail", 1, None), ("cyl", 6, None),
+                                             ("sphere", 5, None), ("soft", 25, 18), ("bimanual", 12, None)])
+def test_trajectory_matches_reference(golden, name, steps, grav):
+    from paper_2503_05020_b200.solver import Environment
+    d = np.load(golden / f"traj_{name}.npz")
+    scene = _scene(d)
+    env = Environment(scene.bodies, collide_pairs_off=scene.collide_pairs_off)
+    golden_reps = json.loads(str(d["reports_json"]))
+    golden_forces = json.loads(str(d["forces_json"]))
+    n = min(steps, len(golden_reps))
+    xs, reps, forces = _rollout(env, scene, n, gravity_after=grav)
+    ell = max(float(np.linalg.norm(d["sv"][0].max(0) - d["sv"][0].min(0))), 0.05)
+    worst = 0.0
+    for k in range(n):
+        g = golden_reps[k]
+        r = reps[k]
+        assert (r.status, r.reason) == (g["status"], g["reason"]), (k, r.status, r.reason, g["status"], g["reason"])
+        assert r.iterations == g["iterations"], (k, r.iterations, g["iterations"])
+        err = float(np.abs(xs[k] - d["x"][k]).max()) / ell
+        worst = max(worst, err)
+        assert err <= TRAJ_TOL, (k, err)
+        for f, v in golden_forces[k].items():
+            assert abs(forces[k][f] - v) <= 1e-6 * max(1.0, abs(v)), (k, f, forces[k][f], v)
+        if r.status == "failed":
+            break
+    print(f"{name}: {n} steps, worst |dx|/ell = {worst:.3e}")
+
+
+@pytest.mark.parametrize("name", ["cfg1", "sphere", "soft", "bimanual", "cyl"])
+def test_candidate_sets_bit_exact(golden, name):
+    """Broad phase on the reference's own recorded states equals its candidate sets."""
+    from paper_2503_05020_b200.solver import Environment
+    d = np.load(golden / f"traj_{name}.npz")
+    scene = _scene(d)
+    env = Environment(scene.bodies, collide_pairs_off=scene.collide_pairs_off)
+    off_pt = np.concatenate([[0], np.cumsum(d["pt_counts"])])
+    off_ee = np.concatenate([[0], np.cumsum(d["ee_counts"])])
+    grp = env._owner()
+    for k in range(len(d["pt_counts"])):
+        # set nodes and the kinematic surfaces of that step
+        sv = d["sv"][k]
+        kin = np.zeros_like(sv)
+        for r in env.layout.records:
+            if r.kind == "kinematic":
+                kin[r.surf0:r.surf0 + r.n_sv] = sv[r.surf0:r.surf0 + r.n_sv]
+        grp.dev.set_state(d["x"][k].reshape(-1, 3), None, kin)
+        grp.invalidate()
+        pt, ee = env.candidates(1.05e-3)
+        assert np.array_equal(pt, d["pt_rows"][off_pt[k]:off_pt[k + 1]]), (k, len(pt), d["pt_counts"][k])
+        assert np.array_equal(ee, d["ee_rows"][off_ee[k]:off_ee[k + 1]]), (k, len(ee), d["ee_counts"][k])
+
+
+def test_batch_bitwise_equals_single(golden):
+    """SPEC invariant: batch-of-N bitwise equals batch-of-1 (multienv isolation)."""
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.multienv import Batch
+    from paper_2503_05020_b200.solver import Environment
+    c = sc.load_cfg2_candidates()
+    scenes = [sc.cfg2_scene(i, c) for i in range(6)]
+    envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+    solo_scene = sc.cfg2_scene(4, c)
+    solo = Environment(solo_scene.bodies, collide_pairs_off=solo_scene.collide_pairs_off)
+    for s, e in list(zip(scenes, envs)) + [(solo_scene, solo)]:
+        for f, ids in s.finger_links.items():
+            for b in ids:
+                e.bodies[b].velocity = s.closing_dirs[f] * 0.05
+    batch = Batch(envs)
+    for _ in range(6):
+        batch.step()
+        solo.step()
+        assert np.array_equal(envs[4].x, solo.x)
+
+
+def test_stress_matches_oracle(golden):
+    from oracle import energies as oen
+    from paper_2503_05020_b200.solver import Environment
+    d = np.load(golden / "traj_bimanual.npz")
+    scene = _scene(d)
+    env = Environment(scene.bodies, collide_pairs_off=scene.collide_pairs_off)
+    grp = env._owner()
+    grp.dev.set_state(d["x"][5].reshape(-1, 3), None, None)
+    grp.invalidate()
+    rows = env.stress_rows()
+    np.testing.assert_allclose(rows, d["stress"][5], rtol=1e-9, atol=1e-6 * np.abs(d["stress"][5]).max())
+    assert oen is not None
