@@ -802,6 +802,18 @@ __global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
       __syncthreads();
     }
     pcg_total += it;
+    // accept on the TRUE residual |b - H x| <= 1e-8 |b| (the reference's acceptance bound,
+    // solver.py:121) when the recursive residual stalled short of rtol
+    if (!conv) {
+      spmv(D, E, dt2, X, Q, A);
+      double tr = 0.0;
+      for (int i = threadIdx.x; i < nf3; i += NT) {
+        const double rv = RHS[vb + i] - Q[vb + i];
+        tr += rv * rv;
+      }
+      tr = block_sum(tr, sm);
+      conv = isfinite(tr) && tr <= 1e-16 * bnorm2;
+    }
     (void)broke;
     solved = conv;
   }
@@ -1119,18 +1131,14 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
   if (threadIdx.x == 0) D.flags[e] = 0;
-  if (D.ns_status[e] == GRIP_NS_FAILED) {
-    if (threadIdx.x == 0) {
-      D.min_dist[e] = INFINITY;
-      D.time[e] += dt;
-      D.step_index[e] += 1;
+  // a failed step keeps x, v and the anchors (solver.py:736-738); the contact readout the
+  // protocol does after every step (protocol.py:179-180) is still produced
+  const bool failed = D.ns_status[e] == GRIP_NS_FAILED;
+  if (!failed)
+    for (int i = threadIdx.x; i < 3 * E.nn; i += NT) {
+      const size_t g = 3 * (size_t)E.n0 + i;
+      D.v[g] = (D.x[g] - D.x_t[g]) / dt;
     }
-    return;
-  }
-  for (int i = threadIdx.x; i < 3 * E.nn; i += NT) {
-    const size_t g = 3 * (size_t)E.n0 + i;
-    D.v[g] = (D.x[g] - D.x_t[g]) / dt;
-  }
   env_sv_positions(D, E, D.x);
   int* cn = D.c1_n + 2 * e;
   int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
@@ -1214,7 +1222,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
     }
     int tot;
     const int pre = block_scan(act, sm, &tot);
-    if (act && base + pre < D.cap_anc) {
+    if (act && !failed && base + pre < D.cap_anc) {
       const size_t ai = (size_t)e * D.cap_anc + base + pre;
       for (int j = 0; j < 4; ++j) {
         D.anc_v[4 * ai + j] = rowv[j];
@@ -1228,7 +1236,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
     }
     base += tot;
   }
-  if (base > D.cap_anc) {
+  if (base > D.cap_anc && !failed) {
     if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
@@ -1243,11 +1251,11 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
   nonfin = block_or(nonfin, sm);
   if (threadIdx.x < nbl) D.contact_mask[E.b0 + threadIdx.x] = cmask[threadIdx.x];
   if (threadIdx.x == 0) {
-    D.n_anc[e] = base;
-    D.min_dist[e] = (npt + nee) > 0 ? sqrt(dmin) : INFINITY;
+    if (!failed) D.n_anc[e] = base;
+    D.min_dist[e] = (!failed && (npt + nee) > 0) ? sqrt(dmin) : INFINITY;
     D.time[e] += dt;
     D.step_index[e] += 1;
-    if (nonfin) {
+    if (nonfin && !failed) {
       D.ns_status[e] = GRIP_NS_FAILED;
       D.reason[e] = GRIP_R_NONFINITE_STATE;
     }

@@ -196,7 +196,7 @@ def env_params(contact: ContactParams, solver: SolverParams):
     p[nv.P_CCDIT] = solver.ccd_max_iters
     p[nv.P_KINGUARD] = solver.kinematic_ccd_guard
     p[nv.P_MURULE] = 0.0 if contact.friction_combination == "geometric" else 1.0
-    p[nv.P_PCGRTOL] = getattr(solver, "pcg_rtol", 1e-11)
+    p[nv.P_PCGRTOL] = getattr(solver, "pcg_rtol", 1e-13)
     return p
 
 
