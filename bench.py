@@ -1,0 +1,359 @@
+"""Benchmark: env-steps/s of the batched grasp protocol (BASELINE config 2) on B200.
+
+Workload (BASELINE.json configs[1]): 400 environments per GPU, each a soft UMI-style
+two-pad gripper grasping a rigid (ABD) box / cylinder / sphere (env i: kind i % 3,
+antipodal candidate seed i), stepped through the reference's validation protocol
+(settle, force-halted closing, hold, six gravity phases; protocol.py:152-277).  A
+"step" is one lockstep protocol step of every unfinished env; env-steps count only
+envs that actually stepped.  W warm-up steps (the settle phase by default), then K
+timed steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Reports (one JSON line on rank 0): value = env-steps/s from CUDA events on the
+library stream (max over ranks), e2e = the same through the public Python API
+with host buffers (controls H2D, reports/forces D2H every step, wall clock),
+roofline of the dominant kernel from live per-launch CUDA events, and a CPU
+baseline: the oracle port (oracle/, the reference's algorithm restated in numpy)
+timed on this host's cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "env-steps/sec at 400 envs (1/2/4/8 B200) vs CPU ref; ms per Newton iteration"
+UNIT = "env-steps/s"
+ENVS_PER_GPU = 400
+
+# Algorithmic bytes per element of the element kernel (fp64 8 B, index 4 B; each input
+# read once, each output written once): inputs + (E 8 + grad 96 + 12x12 Hessian 1152 + idx 16).
+EL_OUT = 8 + 96 + 1152 + 16
+EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, Dm^-1, V0/mu/lam
+            "affine": 96 + 8 + EL_OUT,                  # q, kappa*V
+            "contacts": 16 + 4 + 96 + 8 + 8 + EL_OUT,   # row, code, 4 positions, rest lengths
+            "anchors": 16 + 32 + 48 + 16 + 192 + EL_OUT}  # verts, gamma, T, lam/mu, x and x_prev
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) > 7 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 7 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows if len(r) > 7 for n, v in zip(names, r[4:8]) if v.strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port): bounded sample of the same workload on the host cores
+# ---------------------------------------------------------------------------
+
+
+def _cpu_worker(args):
+    """One env through W untimed + K timed protocol steps with the oracle; returns timings."""
+    i, warmup, steps = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import solver as osv   # CPU baseline leg only
+    from paper_2503_05020_b200 import scene as sc
+    s = sc.cfg2_scene(i % 400)
+    env = osv.OracleEnv(s.bodies, collide_pairs_off=s.collide_pairs_off)
+    sm = _OracleProtocol(env, s)
+    for _ in range(warmup):
+        if not sm.advance():
+            break
+    t0 = time.perf_counter()
+    n = 0
+    calls = 0
+    for _ in range(steps):
+        c0 = getattr(env, "n_calls", 0)
+        if not sm.advance():
+            break
+        calls += getattr(env, "n_calls", 0) - c0
+        n += 1
+    return n, time.perf_counter() - t0, calls
+
+
+class _OracleProtocol:
+    """The protocol state machine (protocol.py:152-277) driving one oracle env."""
+
+    def __init__(self, env, scene, halt=50.0, speed=0.05):
+        self.env, self.s = env, scene
+        self.phase, self.k, self.g, self.quiet = 0, 0, 0, 0
+        self.halted = {f: False for f in scene.finger_links}
+        dt = env.dt
+        self.n = [int(np.ceil(0.05 / dt)), int(np.ceil((scene.opening / 2.0) / (speed * dt))) + 5,
+                  int(np.ceil(1.0 / dt)), int(np.ceil(0.1 / dt))]
+        self.halt, self.speed = halt, speed
+
+    def advance(self):
+        from oracle import solver as osv
+        env, s = self.env, self.s
+        if self.phase >= 4:
+            return False
+        if env.status != "active":
+            return False
+        rep = env.step()
+        ev = env.events_now()
+        forces = {f: osv.finger_force(ev, ids) for f, ids in s.finger_links.items()}
+        self.k += 1
+        if self.phase == 1:
+            for f, ids in s.finger_links.items():
+                if not self.halted[f] and forces[f] > self.halt:
+                    self.halted[f] = True
+                    for b in ids:
+                        env.bodies[b].velocity = np.zeros(3)
+        if rep["status"] == "failed":
+            self.phase = 4
+            return True
+        end = False
+        if self.phase == 0:
+            end = self.k >= self.n[0]
+        elif self.phase == 1:
+            end = all(self.halted.values()) or self.k >= self.n[1]
+        elif self.phase == 2:
+            self.quiet = self.quiet + 1 if env.max_point_speed() < env.eps_v else 0
+            end = self.quiet >= 5 or self.k >= self.n[2]
+        else:
+            end = self.k >= self.n[3]
+        if end:
+            self.k = 0
+            if self.phase == 0:
+                for f, ids in s.finger_links.items():
+                    for b in ids:
+                        env.bodies[b].velocity = np.asarray(s.closing_dirs[f]) * self.speed
+                self.phase = 1
+            elif self.phase == 1:
+                for ids in s.finger_links.values():
+                    for b in ids:
+                        env.bodies[b].velocity = np.zeros(3)
+                self.phase = 2
+            elif self.phase == 2:
+                self.phase, self.g = 3, 0
+                env.gravity = 9.8 * np.array([1.0, 0, 0])
+            else:
+                self.g += 1
+                if self.g >= 6:
+                    self.phase = 4
+                else:
+                    d = np.zeros(3)
+                    d[self.g // 2] = 1.0 if self.g % 2 == 0 else -1.0
+                    env.gravity = 9.8 * d
+        return True
+
+
+def cpu_measure(n_envs, warmup, steps, cores):
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, [(i, warmup, steps) for i in range(n_envs)], chunksize=1)
+    wall = time.perf_counter() - t0
+    n = sum(r[0] for r in res)
+    busy = sum(r[1] for r in res)
+    calls = sum(r[2] for r in res)
+    # each worker is single threaded: aggregate rate = env-steps / (busy core-seconds / cores)
+    rate = n / (busy / min(cores, n_envs)) if busy > 0 else 0.0
+    return {"value": rate, "env_steps": n, "core_seconds": busy, "wall_s": wall, "newton_calls": calls,
+            "ms_per_newton_iteration": 1e3 * busy / max(calls, 1)}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference path on all host cores."""
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    n_envs = cores
+    t_all = time.perf_counter()
+    r = cpu_measure(n_envs, args.warmup, args.steps, cores)
+    steps_done = r["env_steps"]
+    value = r["value"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * r["core_seconds"] / max(args.steps, 1) / max(min(cores, n_envs), 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: soft 2-pad gripper on rigid box/cylinder/sphere, full grasp protocol",
+                   "envs": n_envs, "sample": f"{n_envs} envs x {args.steps} protocol steps after {args.warmup}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, n_envs), "kind": "port",
+                         "sample": f"oracle/ numpy port, {n_envs} envs, {steps_done} env-steps, "
+                                   f"{r['ms_per_newton_iteration']:.1f} ms per newton_iteration"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--envs", type=int, default=ENVS_PER_GPU, help="envs per GPU")
+    ap.add_argument("--cpu-envs", type=int, default=0, help="CPU baseline sample envs (0 = host cores)")
+    ap.add_argument("--cpu-steps", type=int, default=12, help="CPU baseline timed steps per env")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.multienv import DeviceEnvGroup
+    from paper_2503_05020_b200.protocol import BatchedGraspTrials
+    from paper_2503_05020_b200.solver import Environment
+
+    cands = sc.load_cfg2_candidates()
+    ids = [rank * args.envs + i for i in range(args.envs)]       # weak scaling: 400 envs per GPU
+    scenes = [sc.cfg2_scene(i % 400, cands) for i in ids]
+    envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+    group = DeviceEnvGroup(envs, device=local)
+    trials = BatchedGraspTrials(group, scenes)
+    dev = group.dev
+    for _ in range(args.warmup):
+        trials.advance()
+    dev.set_profiling(True)
+    _, l0, _ = dev.stats()
+    E, B = group.packed.n_env, group.packed.n_body_total
+    maxa = dev.max_alpha
+    h2d = 8 * 3 * E + 8 * 3 * B + E                                   # gravity, body velocities, active mask
+    d2h = 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E  # reports, alphas, forces+masks+min_d, com, speed
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        dev.timer_start()
+        env_steps = 0
+        sweeps0 = dev.stats()[2]
+        for _ in range(args.steps):
+            env_steps += trials.advance()
+        ms = dev.timer_stop()
+        wall = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    _, l1, sweeps1 = dev.stats()
+    ks = dev.kernel_stats()
+    if world > 1:
+        t = torch.tensor([ms, wall, float(env_steps), float(sweeps1 - sweeps0)], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm_ = t.clone()
+        dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
+        ms_max, wall_max, total_steps = float(mx[0]), float(mx[1]), float(sm_[2])
+    else:
+        ms_max, wall_max, total_steps = ms, wall, float(env_steps)
+    value = total_steps / (ms_max / 1e3)
+    e2e = total_steps / wall_max
+    # roofline of the dominant kernel (live CUDA events per launch, this rank)
+    dom = max((k for k in ks if k != "work_scan"), key=lambda k: ks[k]["ms"])
+    peak, peak_kind = _peaks()
+    roof = {"kernel": dom, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_kind, "traffic": None}
+    if dom == "elements":
+        u = ks["elements"]["units"]
+        alg = sum(EL_BYTES[k] * u[k] for k in EL_BYTES)
+        roof["achieved"] = alg / (ks["elements"]["ms"] / 1e3) / 1e9
+    else:
+        roof["achieved"] = None
+    roof["frac"] = (roof["achieved"] / peak) if roof.get("achieved") else None
+    roof["kernel_ms"] = {k: round(v["ms"], 3) for k, v in ks.items()}
+    roof["kernel_launches"] = {k: v["launches"] for k, v in ks.items()}
+    nsweeps = sweeps1 - sweeps0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: soft 2-pad UMI-style gripper on rigid (ABD) box/cylinder/sphere, "
+                               "full grasp protocol, antipodal candidate seed i",
+                   "envs_per_gpu": args.envs, "global_envs": args.envs * world, "parallelism": f"env-shard x{world}",
+                   "l2": "working set > L2 (element Hessians alone ~0.5 GB per GPU)",
+                   "env_steps_timed": total_steps, "newton_sweeps": int(nsweeps),
+                   "ms_per_newton_sweep": ms_max / max(nsweeps, 1)},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "roofline": roof,
+        "gpu_launches": int(l1 - l0),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        n_cpu = args.cpu_envs or cores
+        r = cpu_measure(n_cpu, 3, args.cpu_steps, cores)
+        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": min(cores, n_cpu), "kind": "port",
+                                "sample": f"oracle/ numpy port of the reference step, {n_cpu} cfg2 envs x "
+                                          f"{args.cpu_steps} protocol steps after 3 settle steps, "
+                                          f"{r['env_steps']} env-steps, {r['core_seconds']:.1f} core-s, "
+                                          f"{r['ms_per_newton_iteration']:.1f} ms per newton_iteration"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -149,6 +149,16 @@ int grip_get_contacts(GripBatch* b, double* body_force /* n_body */, uint32_t* c
 int grip_query_candidates(GripBatch* b, int env, double radius, int32_t* pt, int32_t cap_pt, int32_t* n_pt,
                           int32_t* ee, int32_t cap_ee, int32_t* n_ee);
 int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
+/* per-body centre of mass (n_body*3) and per-env max point speed after the last finalize
+ * (solver.py:384-428; read by the protocol's steady / COM tests, protocol.py:231-249) */
+int grip_get_body_state(GripBatch* b, double* body_com, double* max_speed);
+/* per-kernel CUDA-event timing on the library stream (0 begin, 1 candidates, 2 work-scan,
+ * 3 elements, 4 assemble+PCG, 5 line search, 6 finalize); units = element counts
+ * (tets, affine, contacts, anchors) processed by kernel 3 since profiling was enabled */
+int grip_set_profiling(GripBatch* b, int on);
+int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, double* units);
+/* CUDA events on the library stream: start=1 marks, start=0 returns ms since the mark */
+int grip_stream_timer(GripBatch* b, int start, double* ms);
 /* timing of the last grip_step: device ms (CUDA events) and kernel launches */
 int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps);
 

@@ -87,7 +87,9 @@ def load():
         ("grip_set_state", [vp, vp, vp, vp]), ("grip_get_surface", [vp, vp]),
         ("grip_get_contacts", [vp, vp, vp, vp]),
         ("grip_query_candidates", [vp, i32, dbl, vp, i32, vp, vp, i32, vp]),
-        ("grip_stress", [vp, vp]), ("grip_last_step_stats", [vp, vp, vp, vp])):
+        ("grip_stress", [vp, vp]), ("grip_last_step_stats", [vp, vp, vp, vp]),
+        ("grip_get_body_state", [vp, vp, vp]), ("grip_set_profiling", [vp, i32]),
+        ("grip_kernel_stats", [vp, i32, vp, vp, vp]), ("grip_stream_timer", [vp, i32, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = i32
@@ -207,6 +209,36 @@ class DeviceBatch:
         out = np.empty((max(self.packed.n_tet_total, 1), 7))
         check(self.lib.grip_stress(self.h, ptr(out)))
         return out[:self.packed.n_tet_total]
+
+    def body_state(self):
+        com = np.empty((self.packed.n_body_total, 3))
+        sp = np.empty(self.n_env)
+        check(self.lib.grip_get_body_state(self.h, ptr(com), ptr(sp)))
+        return com, sp
+
+    def set_profiling(self, on=True):
+        check(self.lib.grip_set_profiling(self.h, int(on)))
+
+    KERNELS = ("begin", "candidates", "work_scan", "elements", "assemble_pcg", "line_search", "finalize")
+
+    def kernel_stats(self):
+        out = {}
+        units = np.zeros(4)
+        for k, name in enumerate(self.KERNELS):
+            ms, n = ctypes.c_double(), ctypes.c_int64()
+            check(self.lib.grip_kernel_stats(self.h, k, ctypes.byref(ms), ctypes.byref(n),
+                                             ptr(units) if k == 3 else None))
+            out[name] = {"ms": ms.value, "launches": n.value}
+        out["elements"]["units"] = {"tets": units[0], "affine": units[1], "contacts": units[2], "anchors": units[3]}
+        return out
+
+    def timer_start(self):
+        check(self.lib.grip_stream_timer(self.h, 1, None))
+
+    def timer_stop(self):
+        ms = ctypes.c_double()
+        check(self.lib.grip_stream_timer(self.h, 0, ctypes.byref(ms)))
+        return ms.value
 
     def stats(self):
         ms, la, sw = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()

@@ -68,6 +68,9 @@ struct Dev {
   int *newton_calls, *pcg_iters;
   double* body_force;
   unsigned int* contact_mask;
+  double* body_com;    // 3 per body, after finalize
+  double* max_speed;   // per env, after finalize (solver.py:414-428)
+  double* stats;       // [0..3] element counts of the last sweep (tets, abd, contacts, anchors)
   int max_alpha;
   // candidates (uniform capacity per env)
   int cap_pt, cap_ee;

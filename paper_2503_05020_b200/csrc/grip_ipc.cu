@@ -51,6 +51,14 @@ struct GripBatch {
   int max_it = 100;
   double last_ms = 0.0;
   long long launches = 0, sweeps = 0;
+  // optional per-kernel timing on the library stream (grip_set_profiling)
+  bool prof = false;
+  static constexpr int NK = 8;
+  std::vector<cudaEvent_t> kev;   // pairs
+  std::vector<std::pair<int, int>> pending_k;  // (kernel id, event pair index)
+  double k_ms[NK] = {0};
+  long long k_n[NK] = {0};
+  cudaEvent_t r0 = nullptr, r1 = nullptr;
 
   template <class T>
   T* alloc(size_t n) {
@@ -365,6 +373,9 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.pcg_iters = b->alloc<int>(E);
   D.body_force = b->alloc<double>(NB);
   D.contact_mask = b->alloc<unsigned int>(NB);
+  D.body_com = b->alloc<double>(3 * (size_t)NB);
+  D.max_speed = b->alloc<double>(E);
+  D.stats = b->alloc<double>(8);
   D.c1_n = b->alloc<int>(2 * (size_t)E);
   D.c2_n = b->alloc<int>(2 * (size_t)E);
   D.n_act = b->alloc<int>(E);
@@ -419,7 +430,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
-        D.inc_ptr, D.inc, D.sv_g};
+        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -436,6 +447,9 @@ int grip_destroy(GripBatch* b) {
   if (!b) return 0;
   cudaStreamSynchronize(b->stream);
   for (void* p : b->owned) cudaFree(p);
+  for (auto ev : b->kev) cudaEventDestroy(ev);
+  if (b->r0) cudaEventDestroy(b->r0);
+  if (b->r1) cudaEventDestroy(b->r1);
   if (b->h_pin) cudaFreeHost(b->h_pin);
   cudaEventDestroy(b->ev0);
   cudaEventDestroy(b->ev1);
@@ -466,15 +480,55 @@ int grip_begin_step(GripBatch* b, const uint8_t* active) {
   return run_with_growth(b, n, [&] { k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list); });
 }
 
+// kernel ids for grip_kernel_stats
+enum { K_BEGIN = 0, K_CAND, K_SCAN, K_ELEM, K_ASM, K_LS, K_FIN, K_OTHER };
+
+static int kt_begin(GripBatch* b, int kid) {
+  if (!b->prof) return -1;
+  const int pair = (int)b->pending_k.size();
+  while ((int)b->kev.size() < 2 * (pair + 1)) {
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    b->kev.push_back(ev);
+  }
+  cudaEventRecord(b->kev[2 * pair], b->stream);
+  b->pending_k.push_back({kid, pair});
+  return pair;
+}
+static void kt_end(GripBatch* b, int pair) {
+  if (pair >= 0) cudaEventRecord(b->kev[2 * pair + 1], b->stream);
+}
+// fold the recorded launch times into the per-kernel totals (after a stream sync)
+static void kt_collect(GripBatch* b) {
+  for (auto& pk : b->pending_k) {
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, b->kev[2 * pk.second], b->kev[2 * pk.second + 1]);
+    b->k_ms[pk.first] += ms;
+    b->k_n[pk.first] += 1;
+  }
+  b->pending_k.clear();
+}
+
 // one Newton sweep over the pending envs (list in b->d_list, n entries); returns new pending count
 static int newton_sweep(GripBatch* b, int n, int* n_out) {
   Dev& D = b->D;
   for (int attempt = 0; attempt < 8; ++attempt) {
+    int t;
+    t = kt_begin(b, K_CAND);
     k_candidates<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    kt_end(b, t);
+    t = kt_begin(b, K_SCAN);
     k_work_scan<<<1, NT, 0, b->stream>>>(D, b->d_list, n);
+    kt_end(b, t);
+    t = kt_begin(b, K_ELEM);
     k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
+    kt_end(b, t);
+    t = kt_begin(b, K_ASM);
     k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    kt_end(b, t);
+    t = kt_begin(b, K_LS);
     k_linesearch<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    kt_end(b, t);
     b->launches += 5;
     b->sweeps += 1;
     CK(cudaGetLastError());
@@ -485,6 +539,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     std::vector<int> L(n);
     CK(cudaMemcpyAsync(L.data(), b->d_list, sizeof(int) * n, cudaMemcpyDeviceToHost, b->stream));
     CK(cudaStreamSynchronize(b->stream));
+    kt_collect(b);
     bool ov = false;
     for (int i = 0; i < n; ++i) ov |= (fl[L[i]] & FLAG_OVERFLOW) != 0;
     if (ov) {
@@ -581,7 +636,13 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
   CK(cudaEventRecord(b->ev0, b->stream));
   if (upload_list(b, L, b->d_list)) return -1;
   int n = (int)L.size();
-  if (run_with_growth(b, n, [&] { k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list); })) return -1;
+  if (run_with_growth(b, n, [&] {
+        int t = kt_begin(b, K_BEGIN);
+        k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list);
+        kt_end(b, t);
+      }))
+    return -1;
+  kt_collect(b);
   // envs that failed in begin_step are done
   std::vector<int> done(b->n_env);
   CK(cudaMemcpy(done.data(), b->D.ns_done, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost));
@@ -597,7 +658,13 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
   }
   if (upload_list(b, L, b->d_list)) return -1;
   n = (int)L.size();
-  if (run_with_growth(b, n, [&] { k_finalize<<<n, NT, 0, b->stream>>>(b->D, b->d_list); })) return -1;
+  if (run_with_growth(b, n, [&] {
+        int t = kt_begin(b, K_FIN);
+        k_finalize<<<n, NT, 0, b->stream>>>(b->D, b->d_list);
+        kt_end(b, t);
+      }))
+    return -1;
+  kt_collect(b);
   CK(cudaEventRecord(b->ev1, b->stream));
   CK(cudaEventSynchronize(b->ev1));
   float ms = 0.0f;
@@ -677,6 +744,52 @@ int grip_stress(GripBatch* b, double* out) {
   CK(cudaMemcpyAsync(out, d_out, 7 * sizeof(double) * b->n_tet, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
   b->release(d_out);
+  return 0;
+}
+
+int grip_get_body_state(GripBatch* b, double* body_com, double* max_speed) {
+  if (body_com) CK(cudaMemcpyAsync(body_com, b->D.body_com, 3 * sizeof(double) * b->n_body, cudaMemcpyDeviceToHost, b->stream));
+  if (max_speed) CK(cudaMemcpyAsync(max_speed, b->D.max_speed, sizeof(double) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_set_profiling(GripBatch* b, int on) {
+  b->prof = on != 0;
+  for (int k = 0; k < GripBatch::NK; ++k) {
+    b->k_ms[k] = 0.0;
+    b->k_n[k] = 0;
+  }
+  CK(cudaMemsetAsync(b->D.stats, 0, 8 * sizeof(double), b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, double* units /* 4 or NULL */) {
+  if (kernel < 0 || kernel >= GripBatch::NK) {
+    g_err = "kernel id out of range";
+    return -1;
+  }
+  if (ms) *ms = b->k_ms[kernel];
+  if (launches) *launches = b->k_n[kernel];
+  if (units) CK(cudaMemcpy(units, b->D.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int grip_stream_timer(GripBatch* b, int start, double* ms) {
+  if (!b->r0) {
+    CK(cudaEventCreate(&b->r0));
+    CK(cudaEventCreate(&b->r1));
+  }
+  if (start) {
+    CK(cudaEventRecord(b->r0, b->stream));
+    return 0;
+  }
+  CK(cudaEventRecord(b->r1, b->stream));
+  CK(cudaEventSynchronize(b->r1));
+  float f = 0.0f;
+  CK(cudaEventElapsedTime(&f, b->r0, b->r1));
+  if (ms) *ms = f;
   return 0;
 }
 

@@ -230,20 +230,28 @@ __global__ void __launch_bounds__(NT) k_candidates(Dev D, const int* list) {
 __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n) {
   __shared__ Red sm;
   int base = 0;
+  double ct = 0.0, ca = 0.0, cc = 0.0, cf = 0.0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
     int w = 0;
     if (i < n) {
       const int e = list[i];
-      if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e])
-        w = (D.tet_off[e + 1] - D.tet_off[e]) + (D.abd_off[e + 1] - D.abd_off[e]) + D.n_act[e] + D.n_anc[e];
+      if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e]) {
+        const int nt = D.tet_off[e + 1] - D.tet_off[e], na = D.abd_off[e + 1] - D.abd_off[e];
+        w = nt + na + D.n_act[e] + D.n_anc[e];
+        ct += nt; ca += na; cc += D.n_act[e]; cf += D.n_anc[e];
+      }
     }
     int tot;
     const int pre = block_scan(w, sm, &tot);
     if (i < n) D.work_off[i] = base + pre;
     base += tot;
   }
-  if (threadIdx.x == 0) D.work_off[n] = base;
+  ct = block_sum(ct, sm); ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
+  if (threadIdx.x == 0) {
+    D.work_off[n] = base;
+    D.stats[0] += ct; D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1244,6 +1252,51 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
   for (int b = 0; b < nbl; ++b) {
     const double f = block_sum(fsum[b], sm);
     if (threadIdx.x == 0) D.body_force[E.b0 + b] = f;
+  }
+  // per-body centre of mass and the env's max point speed (solver.py:384-428), for the protocol
+  for (int b = 0; b < E.nb; ++b) {
+    const int kind = D.body_kind[E.b0 + b];
+    double m = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+    if (kind == 0) {
+      for (int n = threadIdx.x; n < E.nn; n += NT) {
+        const size_t g = E.n0 + n;
+        if (D.node_body[g] != b) continue;
+        const double mn = D.node_M[9 * g];
+        m += mn; cx += mn * D.x[3 * g]; cy += mn * D.x[3 * g + 1]; cz += mn * D.x[3 * g + 2];
+      }
+    } else if (kind == 2) {
+      for (int i = threadIdx.x; i < E.ns; i += NT) {
+        const size_t g = E.s0 + i;
+        if (D.sv_body[g] != b) continue;
+        m += 1.0; cx += D.kin_pos[3 * g]; cy += D.kin_pos[3 * g + 1]; cz += D.kin_pos[3 * g + 2];
+      }
+    }
+    m = block_sum(m, sm); cx = block_sum(cx, sm); cy = block_sum(cy, sm); cz = block_sum(cz, sm);
+    if (threadIdx.x == 0) {
+      double* o = D.body_com + 3 * (size_t)(E.b0 + b);
+      if (kind == 1) {
+        for (int a = 0; a < E.na; ++a) {
+          const int pn = D.abd_node[E.a0 + a];
+          if (D.node_body[E.n0 + pn] == b)
+            for (int c = 0; c < 3; ++c) o[c] = D.x[3 * (size_t)(E.n0 + pn) + c];
+        }
+      } else {
+        o[0] = cx / m; o[1] = cy / m; o[2] = cz / m;
+      }
+    }
+  }
+  {
+    double sp = 0.0;
+    for (int n = threadIdx.x; n < E.nn; n += NT) {
+      const size_t g = E.n0 + n;
+      if (D.node_kind[g] == 0) sp = fmax(sp, norm(ld3(D.v + 3 * g)));
+    }
+    for (int i = threadIdx.x; i < E.ns; i += NT)
+      if (D.sv_kind[E.s0 + i] == 1) sp = fmax(sp, norm(sv_dir(D, E, i, D.v)));
+    for (int b = threadIdx.x; b < E.nb; b += NT)
+      if (D.body_kind[E.b0 + b] == 2) sp = fmax(sp, norm(ld3(D.body_vel + 3 * (size_t)(E.b0 + b))));
+    sp = block_max(sp, sm);
+    if (threadIdx.x == 0) D.max_speed[e] = sp;
   }
   // quarantine check (multienv.py:105-108)
   int nonfin = 0;

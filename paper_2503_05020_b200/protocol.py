@@ -279,126 +279,174 @@ def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closi
 
 
 # ---------------------------------------------------------------------------
-# batched trials: one state machine per env, lockstep device steps
+# batched trials: one state machine per env, lockstep device steps (SURVEY §8f-1)
 # ---------------------------------------------------------------------------
 
 _SETTLE, _CLOSE, _HOLD, _GRAV, _DONE = range(5)
+_PHASE_NAMES = {_SETTLE: "settle", _CLOSE: "close", _HOLD: "hold"}
 
 
-def run_grasp_trials(group, scenes, protocol=None, record_positions=False, max_steps=None, on_step=None):
-    """Run the protocol for every env of a DeviceEnvGroup / Batch group at once.
+class BatchedGraspTrials:
+    """The grasp protocol (protocol.py:152-277) for every env of a device group at once.
 
-    scenes[i] provides object_body, finger_links (name -> (body,)), closing_dirs,
-    opening.  Returns a list of TrialRecord (no per-step position log unless
-    record_positions).  Labels follow protocol.py:152-277 step for step.
+    Per-env phase state lives in numpy arrays; controls (finger velocities,
+    gravity) go to the device as two arrays per step and the protocol's
+    per-step observables (finger forces, contact flags, object COM, max
+    point speed) come back from the device's finalize as small arrays, so no
+    full state is read back.  Each env follows exactly the reference's
+    sequence of controls and decisions; envs are only batched, never coupled.
     """
-    protocol = protocol or TrialProtocol()
-    envs = group.envs
-    E = len(envs)
-    dt = envs[0].solver_params.dt
-    n_settle = int(np.ceil(protocol.settle_duration / dt))
-    n_hold = int(np.ceil(protocol.steady_max_duration / dt))
-    n_grav = int(np.ceil(protocol.gravity_phase_duration / dt))
-    phase = np.full(E, _SETTLE)
-    pstep = np.zeros(E, int)
-    gphase = np.zeros(E, int)
-    quiet = np.zeros(E, int)
-    recs = [TrialRecord(object_body=s.object_body,
-                        gripper_bodies=tuple(sorted({b for ids in s.finger_links.values() for b in ids})))
-            for s in scenes]
-    halted = [{f: False for f in s.finger_links} for s in scenes]
-    max_close = [int(np.ceil((s.opening / 2.0) / (protocol.closing_speed * dt))) + 5 for s in scenes]
-    com0 = [None] * E
-    nsteps = np.zeros(E, int)
-    phase_start = np.zeros(E, int)
-    pos_log = [[] for _ in range(E)]
-    for e, s in zip(envs, scenes):
-        e.gravity = np.zeros(3)
-        for ids in s.finger_links.values():
-            for b in ids:
-                e.bodies[b].velocity = np.zeros(3)
-    off = group.packed.body_off
-    total = 0
-    while True:
-        active = [i for i in range(E) if phase[i] != _DONE]
-        if not active or (max_steps is not None and total >= max_steps):
-            break
-        reps = group._step(active)
-        total += 1
-        force, mask, _ = group.dev.contacts()
-        need_state = any(phase[i] in (_HOLD, _GRAV) for i in active) or record_positions
-        x_all, v_all, _ = group._state() if need_state else (None, None, None)
-        for i in active:
-            env, sc, r = envs[i], scenes[i], reps[i]
-            nsteps[i] += 1
-            if record_positions:
-                pos_log[i].append(group._node_slice(i, "x").copy())
-            fbody = force[off[i]:off[i + 1]]
-            forces = {f: float(sum(fbody[b] for b in ids)) for f, ids in sc.finger_links.items()}
-            name = {_SETTLE: "settle", _CLOSE: "close", _HOLD: "hold"}.get(phase[i], PHASES[gphase[i]] if phase[i] == _GRAV else "")
-            pstep[i] += 1
-            if phase[i] == _CLOSE:
-                for f, ids in sc.finger_links.items():
-                    if not halted[i][f] and forces[f] > protocol.force_halt:
-                        halted[i][f] = True
-                        recs[i].halt_forces[f] = {"force": forces[f], "step": int(nsteps[i] - 1)}
-                        for b in ids:
-                            env.bodies[b].velocity = np.zeros(3)
-            if r.status == "failed":
-                recs[i].verdict = "sim-failed"
-                recs[i].failure = {"phase": name, "reason": r.reason, "step": env.step_index}
-                if phase[i] == _GRAV:
-                    recs[i].com_displacement[name] = float(np.linalg.norm(env.body_com(sc.object_body) - com0[i]))
-                phase[i] = _DONE
-                continue
-            ended = False
-            if phase[i] == _SETTLE:
-                ended = pstep[i] >= n_settle
-            elif phase[i] == _CLOSE:
-                ended = all(halted[i].values()) or pstep[i] >= max_close[i]
-            elif phase[i] == _HOLD:
-                quiet[i] = quiet[i] + 1 if env.max_point_speed() < env.contact_params.eps_v else 0
-                ended = quiet[i] >= protocol.steady_speed_steps or pstep[i] >= n_hold
-            elif phase[i] == _GRAV:
-                ended = pstep[i] >= n_grav
-            if not ended:
-                continue
-            recs[i].phase_markers[name] = [int(phase_start[i]), int(nsteps[i])]
-            phase_start[i] = nsteps[i]
-            pstep[i] = 0
-            if phase[i] == _SETTLE:
-                phase[i] = _CLOSE
-                for f, ids in sc.finger_links.items():
-                    for b in ids:
-                        env.bodies[b].velocity = np.asarray(sc.closing_dirs[f]) * protocol.closing_speed
-            elif phase[i] == _CLOSE:
-                for ids in sc.finger_links.values():
-                    for b in ids:
-                        env.bodies[b].velocity = np.zeros(3)
-                phase[i] = _HOLD
-            elif phase[i] == _HOLD:
-                phase[i] = _GRAV
-                gphase[i] = 0
-                env.gravity = protocol.gravity_magnitude * GRAVITY_DIRECTIONS[0]
-                com0[i] = env.body_com(sc.object_body).copy()
-            elif phase[i] == _GRAV:
-                recs[i].com_displacement[name] = float(np.linalg.norm(env.body_com(sc.object_body) - com0[i]))
-                gphase[i] += 1
-                if gphase[i] >= 6:
-                    phase[i] = _DONE
-                    thr = protocol.stability_constant * n_grav * env.contact_params.eps_v * dt
-                    in_contact = bool(mask[off[i] + sc.object_body] & sum(1 << b for b in recs[i].gripper_bodies))
-                    final = recs[i].com_displacement.get(PHASES[-1], np.inf)
-                    recs[i].verdict = "stable" if (in_contact and final < thr) else "unstable"
-                    recs[i].metrics.update(final_phase_com_disp=final, stability_threshold=thr,
-                                           final_contact=in_contact)
+
+    def __init__(self, group, scenes, protocol=None):
+        self.group = group
+        self.dev = group.dev
+        self.protocol = pr = protocol or TrialProtocol()
+        p = group.packed
+        E = p.n_env
+        self.E = E
+        env0 = group.envs[0]
+        self.dt = dt = env0.solver_params.dt
+        self.eps_v = np.array([e.contact_params.eps_v for e in group.envs])
+        self.n_settle = int(np.ceil(pr.settle_duration / dt))
+        self.n_hold = int(np.ceil(pr.steady_max_duration / dt))
+        self.n_grav = int(np.ceil(pr.gravity_phase_duration / dt))
+        boff = p.body_off[:-1].astype(np.int64)
+        self.fnames = [list(s.finger_links) for s in scenes]
+        nf = len(self.fnames[0])
+        self.fb = np.zeros((E, nf), np.int64)
+        self.cd = np.zeros((E, nf, 3))
+        for i, s in enumerate(scenes):
+            for j, f in enumerate(self.fnames[i]):
+                ids = s.finger_links[f]
+                if len(ids) != 1:
+                    raise ValueError("batched trials expect one body per finger link")
+                self.fb[i, j] = boff[i] + ids[0]
+                self.cd[i, j] = np.asarray(s.closing_dirs[f], np.float64)
+        self.obj = boff + np.array([s.object_body for s in scenes], np.int64)
+        self.gbits = np.array([sum(1 << b for ids in s.finger_links.values() for b in ids) for s in scenes], np.int64)
+        self.max_close = np.array([int(np.ceil((s.opening / 2.0) / (pr.closing_speed * dt))) + 5 for s in scenes])
+        self.vel = np.zeros((p.n_body_total, 3))
+        self.grav = np.zeros((E, 3))
+        self.phase = np.full(E, _SETTLE)
+        self.pstep = np.zeros(E, np.int64)
+        self.gphase = np.zeros(E, np.int64)
+        self.quiet = np.zeros(E, np.int64)
+        self.halted = np.zeros((E, nf), bool)
+        self.nsteps = np.zeros(E, np.int64)
+        self.phase_start = np.zeros(E, np.int64)
+        self.com0 = np.zeros((E, 3))
+        self.com_disp = np.full((E, 6), np.nan)
+        self.records = [TrialRecord(object_body=s.object_body,
+                                    gripper_bodies=tuple(sorted({b for ids in s.finger_links.values() for b in ids})))
+                        for s in scenes]
+        self.env_steps = 0
+        self.reports = []
+
+    @property
+    def done(self):
+        return bool(np.all(self.phase == _DONE))
+
+    def advance(self, keep_reports=False):
+        """One lockstep protocol step over every unfinished env; returns env-steps executed."""
+        ids = np.nonzero(self.phase != _DONE)[0]
+        if len(ids) == 0:
+            return 0
+        pr = self.protocol
+        mask = np.zeros(self.E, np.uint8)
+        mask[ids] = 1
+        self.dev.set_controls(self.grav, self.vel)
+        rep, alphas = self.dev.step(mask)
+        force, cmask, _ = self.dev.contacts()
+        com, speed = self.dev.body_state()
+        self.group.invalidate()
+        for e in ids:
+            env = self.group.envs[e]
+            env._time += env.solver_params.dt
+            env._step += 1
+        if keep_reports:
+            self.reports.append((ids.copy(), rep[ids].copy()))
+        self.env_steps += len(ids)
+        self.nsteps[ids] += 1
+        self.pstep[ids] += 1
+        ph = self.phase[ids]
+        ff = force[self.fb[ids]]                       # (n, fingers)
+        # close-phase halting happens before the failure check (protocol.py:181-186)
+        closing = ph == _CLOSE
+        newly = closing[:, None] & ~self.halted[ids] & (ff > pr.force_halt)
+        if newly.any():
+            for k, j in zip(*np.nonzero(newly)):
+                e = ids[k]
+                self.halted[e, j] = True
+                self.records[e].halt_forces[self.fnames[e][j]] = {"force": float(ff[k, j]), "step": int(self.nsteps[e] - 1)}
+                self.vel[self.fb[e, j]] = 0.0
+        failed = rep["status"][ids] == 2
+        for k in np.nonzero(failed)[0]:
+            e = ids[k]
+            name = _PHASE_NAMES.get(int(ph[k]), PHASES[int(self.gphase[e])] if ph[k] == _GRAV else "")
+            r = self.records[e]
+            r.verdict = "sim-failed"
+            from paper_2503_05020_b200._native import REASONS
+            r.failure = {"phase": name, "reason": REASONS.get(int(rep["reason"][e]), "unknown"),
+                         "step": int(self.nsteps[e])}
+            if ph[k] == _GRAV:
+                r.com_displacement[name] = float(np.linalg.norm(com[self.obj[e]] - self.com0[e]))
+            self.phase[e] = _DONE
+        ok = ~failed
+        ended = np.zeros(len(ids), bool)
+        ended |= (ph == _SETTLE) & (self.pstep[ids] >= self.n_settle)
+        ended |= closing & (self.halted[ids].all(axis=1) | (self.pstep[ids] >= self.max_close[ids]))
+        hold = ph == _HOLD
+        if hold.any():
+            q = np.where(speed[ids] < self.eps_v[ids], self.quiet[ids] + 1, 0)
+            self.quiet[ids] = np.where(hold, q, self.quiet[ids])
+            ended |= hold & ((self.quiet[ids] >= pr.steady_speed_steps) | (self.pstep[ids] >= self.n_hold))
+        ended |= (ph == _GRAV) & (self.pstep[ids] >= self.n_grav)
+        ended &= ok
+        for k in np.nonzero(ended)[0]:
+            e = ids[k]
+            r = self.records[e]
+            name = _PHASE_NAMES.get(int(ph[k]), PHASES[int(self.gphase[e])] if ph[k] == _GRAV else "")
+            r.phase_markers[name] = [int(self.phase_start[e]), int(self.nsteps[e])]
+            self.phase_start[e] = self.nsteps[e]
+            self.pstep[e] = 0
+            fbe = self.fb[e]
+            if ph[k] == _SETTLE:
+                self.phase[e] = _CLOSE
+                self.vel[fbe] = self.cd[e] * pr.closing_speed
+            elif ph[k] == _CLOSE:
+                self.vel[fbe] = 0.0
+                self.phase[e] = _HOLD
+            elif ph[k] == _HOLD:
+                self.phase[e] = _GRAV
+                self.gphase[e] = 0
+                self.grav[e] = pr.gravity_magnitude * GRAVITY_DIRECTIONS[0]
+                self.com0[e] = com[self.obj[e]]
+            else:
+                g = int(self.gphase[e])
+                d = float(np.linalg.norm(com[self.obj[e]] - self.com0[e]))
+                r.com_displacement[PHASES[g]] = d
+                self.gphase[e] = g + 1
+                if g + 1 >= 6:
+                    self.phase[e] = _DONE
+                    thr = pr.stability_constant * self.n_grav * self.eps_v[e] * self.dt
+                    in_contact = bool(int(cmask[self.obj[e]]) & int(self.gbits[e]))
+                    r.verdict = "stable" if (in_contact and d < thr) else "unstable"
+                    r.metrics.update(final_phase_com_disp=d, stability_threshold=thr, final_contact=in_contact)
                 else:
-                    env.gravity = protocol.gravity_magnitude * GRAVITY_DIRECTIONS[gphase[i]]
-                    com0[i] = env.body_com(sc.object_body).copy()
-        if on_step is not None:
-            on_step(total, reps)
-    for i in range(E):
-        recs[i].n_steps = int(nsteps[i])
-        if record_positions:
-            recs[i].positions = np.array(pos_log[i])
-    return recs
+                    self.grav[e] = pr.gravity_magnitude * GRAVITY_DIRECTIONS[g + 1]
+                    self.com0[e] = com[self.obj[e]]
+        for e in ids:
+            self.records[e].n_steps = int(self.nsteps[e])
+        return len(ids)
+
+    def run(self, max_steps=None):
+        n = 0
+        while not self.done and (max_steps is None or n < max_steps):
+            self.advance()
+            n += 1
+        return self.records
+
+
+def run_grasp_trials(group, scenes, protocol=None, max_steps=None):
+    """Protocol for all envs of a group; returns TrialRecords (labels, markers, COM, halts)."""
+    return BatchedGraspTrials(group, scenes, protocol).run(max_steps)

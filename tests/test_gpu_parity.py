@@ -136,3 +136,29 @@ def test_stress_matches_oracle(golden):
     rows = env.stress_rows()
     np.testing.assert_allclose(rows, d["stress"][5], rtol=1e-9, atol=1e-6 * np.abs(d["stress"][5]).max())
     assert oen is not None
+
+
+def test_protocol_labels_match_reference(golden):
+    """Grasp labels (stable / unstable / sim-failed), step counts, halts and phase markers of the
+    full protocol (protocol.py:152-277) on the reference's own seeds, all envs batched."""
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.multienv import DeviceEnvGroup
+    from paper_2503_05020_b200.protocol import BatchedGraspTrials
+    from paper_2503_05020_b200.solver import Environment
+    ref = json.loads((golden / "verdicts.json").read_text())
+    scenes = [sc.build_trial_scene(sc.ObjectSpec(kind=r["kind"], soft=r["soft_object"]), sc.GripperSpec(soft_fingers=True),
+                                   np.array(r["R"]), np.array(r["T"]), r["opening"]) for r in ref]
+    envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+    grp = DeviceEnvGroup(envs)
+    recs = BatchedGraspTrials(grp, scenes).run()
+    for r, g in zip(recs, ref):
+        assert r.verdict == g["verdict"], (g["seed"], r.verdict, g["verdict"])
+        assert r.n_steps == g["n_steps"], (g["seed"], r.n_steps, g["n_steps"])
+        assert r.phase_markers == g["phase_markers"], (g["seed"], r.phase_markers, g["phase_markers"])
+        if g["failure"]:
+            assert r.failure["reason"] == g["failure"]["reason"] and r.failure["phase"] == g["failure"]["phase"]
+        for f, h in g["halt_forces"].items():
+            assert r.halt_forces[f]["step"] == h["step"]
+            assert abs(r.halt_forces[f]["force"] - h["force"]) <= 1e-5 * h["force"]
+        for k, v in g["com_displacement"].items():
+            assert abs(r.com_displacement[k] - v) <= 1e-6 * 0.1 + 1e-9, (g["seed"], k, r.com_displacement[k], v)
