@@ -251,6 +251,7 @@ def main():
     ap.add_argument("--cpu-envs", type=int, default=0, help="CPU baseline sample envs (0 = host cores)")
     ap.add_argument("--cpu-steps", type=int, default=12, help="CPU baseline timed steps per env")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--lockstep", action="store_true", help="lockstep Batch.step rounds instead of continuous batching")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -277,8 +278,9 @@ def main():
     group = DeviceEnvGroup(envs, device=local)
     trials = BatchedGraspTrials(group, scenes)
     dev = group.dev
+    advance = trials.advance if args.lockstep else trials.advance_round
     for _ in range(args.warmup):
-        trials.advance()
+        advance()
     dev.set_profiling(True)
     _, l0, _ = dev.stats()
     E, B = group.packed.n_env, group.packed.n_body_total
@@ -294,7 +296,7 @@ def main():
         env_steps = 0
         sweeps0 = dev.stats()[2]
         for _ in range(args.steps):
-            env_steps += trials.advance()
+            env_steps += advance()
         ms = dev.timer_stop()
         wall = time.perf_counter() - t0
     torch.cuda.synchronize()

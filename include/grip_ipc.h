@@ -138,6 +138,12 @@ int grip_newton_iteration(GripBatch* b, uint8_t* pending /* n_env, in/out */);
 int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* reports /* n_env */,
                        double* alphas /* n_env * max_iters, or NULL */);
 int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas);
+/* Continuous batching (no lockstep): begin_step for envs with begin[e]=1, one Newton sweep
+ * over every unfinished env in begin|iter, finalize_step for the envs that finished this round
+ * (finalized[e]=1, reports[e] filled).  Each env still follows solver.py:590-773 exactly;
+ * envs simply no longer wait for the slowest env of the batch between time steps. */
+int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t* finalized,
+               GripStepReport* reports, double* alphas);
 int grip_get_state(GripBatch* b, double* x, double* v, double* kin /* n_sv*3, or NULL */);
 int grip_set_state(GripBatch* b, const double* x, const double* v, const double* kin);
 int grip_get_surface(GripBatch* b, double* sv /* n_sv*3 */);

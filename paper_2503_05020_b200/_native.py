@@ -89,7 +89,8 @@ def load():
         ("grip_query_candidates", [vp, i32, dbl, vp, i32, vp, vp, i32, vp]),
         ("grip_stress", [vp, vp]), ("grip_last_step_stats", [vp, vp, vp, vp]),
         ("grip_get_body_state", [vp, vp, vp]), ("grip_set_profiling", [vp, i32]),
-        ("grip_kernel_stats", [vp, i32, vp, vp, vp]), ("grip_stream_timer", [vp, i32, vp])):
+        ("grip_kernel_stats", [vp, i32, vp, vp, vp]), ("grip_stream_timer", [vp, i32, vp]),
+        ("grip_round", [vp, vp, vp, vp, vp, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = i32
@@ -152,6 +153,15 @@ class DeviceBatch:
         alphas = np.zeros((self.n_env, self.max_alpha))
         check(self.lib.grip_step(self.h, ptr(act), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
         return rep, alphas
+
+    def round(self, begin, iterating):
+        b = np.ascontiguousarray(begin, np.uint8)
+        it = np.ascontiguousarray(iterating, np.uint8)
+        fin = np.zeros(self.n_env, np.uint8)
+        rep = np.zeros(self.n_env, REPORT_DTYPE)
+        alphas = np.zeros((self.n_env, self.max_alpha))
+        check(self.lib.grip_round(self.h, ptr(b), ptr(it), ptr(fin), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
+        return fin.astype(bool), rep, alphas
 
     def begin_step(self, active):
         act = np.ascontiguousarray(active, np.uint8)

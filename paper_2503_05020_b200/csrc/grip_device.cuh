@@ -66,6 +66,7 @@ struct Dev {
   double *ell, *tol, *residual, *energy, *alphas, *min_dist, *time;
   int *iters, *ns_status, *reason, *regularized, *kin_blocked, *needs_ls, *ns_done, *flags, *step_index;
   int *newton_calls, *pcg_iters;
+  int* fin_done;       // finalize ran for the current step (round API)
   double* body_force;
   unsigned int* contact_mask;
   double* body_com;    // 3 per body, after finalize

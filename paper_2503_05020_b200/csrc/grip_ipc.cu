@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -371,6 +372,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.step_index = b->alloc<int>(E);
   D.newton_calls = b->alloc<int>(E);
   D.pcg_iters = b->alloc<int>(E);
+  D.fin_done = b->alloc<int>(E);
   D.body_force = b->alloc<double>(NB);
   D.contact_mask = b->alloc<unsigned int>(NB);
   D.body_com = b->alloc<double>(3 * (size_t)NB);
@@ -430,7 +432,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
-        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats};
+        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -499,13 +501,18 @@ static void kt_end(GripBatch* b, int pair) {
   if (pair >= 0) cudaEventRecord(b->kev[2 * pair + 1], b->stream);
 }
 // fold the recorded launch times into the per-kernel totals (after a stream sync)
-static void kt_collect(GripBatch* b) {
+static void kt_collect(GripBatch* b, int n_listed = -1) {
+  static const bool trace = getenv("GRIP_TRACE") != nullptr;
+  double per[GripBatch::NK] = {0};
   for (auto& pk : b->pending_k) {
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, b->kev[2 * pk.second], b->kev[2 * pk.second + 1]);
     b->k_ms[pk.first] += ms;
     b->k_n[pk.first] += 1;
+    per[pk.first] += ms;
   }
+  if (trace && n_listed >= 0 && !b->pending_k.empty())
+    fprintf(stderr, "GRIP_TRACE n=%d cand=%.3f elem=%.3f asm=%.3f ls=%.3f\n", n_listed, per[1], per[3], per[4], per[5]);
   b->pending_k.clear();
 }
 
@@ -539,7 +546,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     std::vector<int> L(n);
     CK(cudaMemcpyAsync(L.data(), b->d_list, sizeof(int) * n, cudaMemcpyDeviceToHost, b->stream));
     CK(cudaStreamSynchronize(b->stream));
-    kt_collect(b);
+    kt_collect(b, n);
     bool ov = false;
     for (int i = 0; i < n; ++i) ov |= (fl[L[i]] & FLAG_OVERFLOW) != 0;
     if (ov) {
@@ -672,6 +679,54 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
   b->last_ms = ms;
   (void)l0;
   if (reports) return read_reports(b, L, reports, alphas);
+  return 0;
+}
+
+// One continuous-batching round: begin_step for envs in `begin` (their controls must be set),
+// one Newton sweep over every unfinished env in begin|iter, finalize for every env that finished
+// in this round.  finalized[e] is set for those envs and reports[e] filled.
+int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t* finalized, GripStepReport* reports,
+               double* alphas) {
+  Dev& D = b->D;
+  std::vector<int> B, L;
+  for (int e = 0; e < b->n_env; ++e) {
+    if (begin && begin[e]) B.push_back(e);
+    if ((begin && begin[e]) || (iter && iter[e])) L.push_back(e);
+  }
+  if (finalized) memset(finalized, 0, b->n_env);
+  if (L.empty()) return 0;
+  if (!B.empty()) {
+    if (upload_list(b, B, b->d_list)) return -1;
+    const int nb = (int)B.size();
+    if (run_with_growth(b, nb, [&] {
+          int t = kt_begin(b, K_BEGIN);
+          k_begin<<<nb, NT, 0, b->stream>>>(D, b->d_list);
+          kt_end(b, t);
+        }))
+      return -1;
+    kt_collect(b);
+  }
+  if (upload_list(b, L, b->d_list)) return -1;
+  int n2 = 0;
+  if (newton_sweep(b, (int)L.size(), &n2)) return -1;   // leaves still-pending envs in d_list
+  if (upload_list(b, L, b->d_list)) return -1;
+  const int n = (int)L.size();
+  if (run_with_growth(b, n, [&] {
+        int t = kt_begin(b, K_FIN);
+        k_finalize<<<n, NT, 0, b->stream>>>(D, b->d_list, 1);
+        kt_end(b, t);
+      }))
+    return -1;
+  kt_collect(b);
+  std::vector<int> done(b->n_env);
+  CK(cudaMemcpyAsync(done.data(), D.ns_done, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  std::vector<int> F;
+  for (int e : L)
+    if (done[e]) F.push_back(e);
+  for (int e : F)
+    if (finalized) finalized[e] = 1;
+  if (reports && !F.empty()) return read_reports(b, F, reports, alphas);
   return 0;
 }
 

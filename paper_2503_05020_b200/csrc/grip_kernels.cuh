@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], dhat = P[GRIP_P_DHAT];
+  if (threadIdx.x == 0) D.fin_done[e] = 0;
   for (int i = threadIdx.x; i < 3 * E.nn; i += NT) D.x_t[3 * (size_t)E.n0 + i] = D.x[3 * (size_t)E.n0 + i];
   env_sv_positions(D, E, D.x);
   for (int i = threadIdx.x; i < 3 * E.ns; i += NT) D.surf_prev[3 * (size_t)E.s0 + i] = D.sv_pos[3 * (size_t)E.s0 + i];
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
     D.newton_calls[e] = 0;
     D.pcg_iters[e] = 0;
     D.flags[e] = 0;
+    D.fin_done[e] = 0;
   }
 }
 
@@ -184,6 +186,7 @@ __global__ void __launch_bounds__(NT) k_candidates(Dev D, const int* list) {
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dhat = P[GRIP_P_DHAT];
+  if (D.ns_done[e]) return;  // finished (or failed in begin_step) envs of a round list
   if (threadIdx.x == 0) {
     D.flags[e] = 0;
     D.newton_calls[e] += 1;
@@ -1130,11 +1133,12 @@ __global__ void __launch_bounds__(NT) k_compact(Dev D, const int* list, int n, i
 // ---------------------------------------------------------------------------
 // finalize_step (solver.py:733-762) + contact readout (protocol.py:72-98)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
+__global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int only_done = 0) {
   __shared__ Red sm;
   __shared__ BPShared S;
   __shared__ unsigned int cmask[32];
   const int e = list[blockIdx.x];
+  if (only_done && (!D.ns_done[e] || D.fin_done[e])) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
@@ -1304,6 +1308,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list) {
   nonfin = block_or(nonfin, sm);
   if (threadIdx.x < nbl) D.contact_mask[E.b0 + threadIdx.x] = cmask[threadIdx.x];
   if (threadIdx.x == 0) {
+    D.fin_done[e] = 1;
     if (!failed) D.n_anc[e] = base;
     D.min_dist[e] = (!failed && (npt + nee) > 0) ? sqrt(dmin) : INFINITY;
     D.time[e] += dt;

@@ -351,11 +351,38 @@ class BatchedGraspTrials:
         ids = np.nonzero(self.phase != _DONE)[0]
         if len(ids) == 0:
             return 0
-        pr = self.protocol
         mask = np.zeros(self.E, np.uint8)
         mask[ids] = 1
         self.dev.set_controls(self.grav, self.vel)
         rep, alphas = self.dev.step(mask)
+        self._after_step(ids, rep, keep_reports)
+        return len(ids)
+
+    def advance_round(self, keep_reports=False):
+        """One continuous-batching round (grip_round): envs that finished their previous
+        protocol step begin the next one, every unfinished env gets one Newton sweep, envs
+        whose step converged are finalized and advance their protocol.  Returns the number
+        of env-steps completed in this round."""
+        if not hasattr(self, "_iter"):
+            self._iter = np.zeros(self.E, bool)
+            self._need = self.phase != _DONE
+        begin = self._need & (self.phase != _DONE)
+        if not begin.any() and not self._iter.any():
+            return 0
+        if begin.any():
+            self.dev.set_controls(self.grav, self.vel)
+        fin, rep, alphas = self.dev.round(begin, self._iter)
+        self._iter = (self._iter | begin) & ~fin
+        self._need = np.zeros(self.E, bool)
+        ids = np.nonzero(fin)[0]
+        if len(ids):
+            self._after_step(ids, rep, keep_reports)
+            self._need[ids] = self.phase[ids] != _DONE
+        return len(ids)
+
+    def _after_step(self, ids, rep, keep_reports=False):
+        """Protocol bookkeeping after envs `ids` completed a time step (protocol.py:176-188)."""
+        pr = self.protocol
         force, cmask, _ = self.dev.contacts()
         com, speed = self.dev.body_state()
         self.group.invalidate()
@@ -437,16 +464,15 @@ class BatchedGraspTrials:
                     self.com0[e] = com[self.obj[e]]
         for e in ids:
             self.records[e].n_steps = int(self.nsteps[e])
-        return len(ids)
 
-    def run(self, max_steps=None):
+    def run(self, max_steps=None, lockstep=False):
         n = 0
         while not self.done and (max_steps is None or n < max_steps):
-            self.advance()
+            self.advance() if lockstep else self.advance_round()
             n += 1
         return self.records
 
 
-def run_grasp_trials(group, scenes, protocol=None, max_steps=None):
+def run_grasp_trials(group, scenes, protocol=None, max_steps=None, lockstep=False):
     """Protocol for all envs of a group; returns TrialRecords (labels, markers, COM, halts)."""
-    return BatchedGraspTrials(group, scenes, protocol).run(max_steps)
+    return BatchedGraspTrials(group, scenes, protocol).run(max_steps, lockstep=lockstep)

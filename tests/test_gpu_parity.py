@@ -138,9 +138,11 @@ def test_stress_matches_oracle(golden):
     assert oen is not None
 
 
-def test_protocol_labels_match_reference(golden):
+@pytest.mark.parametrize("lockstep", [True, False])
+def test_protocol_labels_match_reference(golden, lockstep):
     """Grasp labels (stable / unstable / sim-failed), step counts, halts and phase markers of the
-    full protocol (protocol.py:152-277) on the reference's own seeds, all envs batched."""
+    full protocol (protocol.py:152-277) on the reference's own seeds, all envs batched, in
+    lockstep (Batch.step semantics) and with continuous batching (grip_round)."""
     from paper_2503_05020_b200 import scene as sc
     from paper_2503_05020_b200.multienv import DeviceEnvGroup
     from paper_2503_05020_b200.protocol import BatchedGraspTrials
@@ -150,7 +152,7 @@ def test_protocol_labels_match_reference(golden):
                                    np.array(r["R"]), np.array(r["T"]), r["opening"]) for r in ref]
     envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
     grp = DeviceEnvGroup(envs)
-    recs = BatchedGraspTrials(grp, scenes).run()
+    recs = BatchedGraspTrials(grp, scenes).run(lockstep=lockstep)
     for r, g in zip(recs, ref):
         assert r.verdict == g["verdict"], (g["seed"], r.verdict, g["verdict"])
         assert r.n_steps == g["n_steps"], (g["seed"], r.n_steps, g["n_steps"])
