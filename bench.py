@@ -342,6 +342,12 @@ def main():
         "gpu_launches": int(l1 - l0),
         "clocks": clk.summary(),
     }
+    if world > 1:
+        # the path's one collective: fixed-size per-env outcome records, gathered once at the end
+        from paper_2503_05020_b200.distributed import gather_outcomes, pack_outcomes
+        tg = time.perf_counter()
+        allr = gather_outcomes(pack_outcomes(trials.records, ids), args.envs * world, device="cuda")
+        line["outcome_gather"] = {"envs": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg), "backend": "nccl"}
     if rank == 0 and not args.no_cpu:
         cores = os.cpu_count() or 1
         n_cpu = args.cpu_envs or cores

@@ -1,0 +1,71 @@
+"""World-size-2 multi-rank path on CPU (gloo): env sharding and the final outcome gather.
+
+The GPU run uses the same code with NCCL; per-step there is no collective (envs are
+independent), so this covers every piece of cross-rank logic.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as tmp
+
+from paper_2503_05020_b200.distributed import OUTCOME_FIELDS, gather_outcomes, pack_outcomes, shard
+from paper_2503_05020_b200.protocol import TrialRecord
+
+
+def test_shard_covers_all_envs_once():
+    for n in (1, 7, 400, 3200):
+        for world in (1, 2, 4, 8):
+            got = []
+            for r in range(world):
+                lo, hi = shard(n, world, r)
+                got.extend(range(lo, hi))
+            assert got == list(range(n))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n_envs, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard(n_envs, world, rank)
+    recs = []
+    for e in range(lo, hi):
+        r = TrialRecord(verdict=("stable", "unstable", "sim-failed")[e % 3], n_steps=70 + e)
+        r.metrics = {"final_phase_com_disp": 1e-5 * e, "final_contact": e % 2 == 0}
+        r.halt_forces = {"finger0": {"step": e, "force": 50.0 + e}}
+        recs.append(r)
+    allr = gather_outcomes(pack_outcomes(recs, list(range(lo, hi))), n_envs)
+    q.put((rank, allr))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_envs", [7, 10])
+def test_gather_outcomes_world2_gloo(n_envs):
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_envs, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank in (0, 1):
+        a = res[rank]
+        assert a.shape == (n_envs, len(OUTCOME_FIELDS))
+        np.testing.assert_array_equal(a[:, 0], np.arange(n_envs))
+        np.testing.assert_array_equal(a[:, 1], np.arange(n_envs) % 3)
+        np.testing.assert_array_equal(a[:, 2], 70 + np.arange(n_envs))
+        np.testing.assert_allclose(a[:, 6], 50.0 + np.arange(n_envs))
+    np.testing.assert_array_equal(res[0], res[1])
