@@ -165,6 +165,18 @@ int grip_set_profiling(GripBatch* b, int on);
 int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, double* units);
 /* CUDA events on the library stream: start=1 marks, start=0 returns ms since the mark */
 int grip_stream_timer(GripBatch* b, int start, double* ms);
+/* Re-initialise the envs with mask[e]=1 to a new pose of the SAME topology (a new grasp
+ * candidate for the same object / gripper meshes): positions, kinematic surfaces and the
+ * posed rest shape (Dm^-1, V0) of their tets; v, anchors, time and step index are zeroed.
+ * Full-size host arrays (GripSceneDesc layout); only the masked envs' slices are read. */
+int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
+                    const double* tet_Dmi, const double* tet_V0);
+/* Evaluate n standalone elements with the device element kernels (test / parity hook).
+ * type 0 PT  in[x(12), kappa, dhat]; 1 EE in[x(12), eps_x, kappa, dhat];
+ * 2 NH in[x(12), Dm^-1(9), V0, mu, lambda]; 3 ABD in[A(9), kappa*V];
+ * 4 friction in[x(12), x_prev(12), gamma(4), T(6), lambda, mu, eps_v, dt]
+ * outputs per element: energy, grad (12), SPD-projected 12x12 Hessian, flags (1 active, 2 bad d, 4 inverted) */
+int grip_debug_elements(int type, int n, const double* in, int stride, double* E, double* g, double* H, int* flags);
 /* timing of the last grip_step: device ms (CUDA events) and kernel launches */
 int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps);
 

@@ -90,7 +90,9 @@ def load():
         ("grip_stress", [vp, vp]), ("grip_last_step_stats", [vp, vp, vp, vp]),
         ("grip_get_body_state", [vp, vp, vp]), ("grip_set_profiling", [vp, i32]),
         ("grip_kernel_stats", [vp, i32, vp, vp, vp]), ("grip_stream_timer", [vp, i32, vp]),
-        ("grip_round", [vp, vp, vp, vp, vp, vp])):
+        ("grip_round", [vp, vp, vp, vp, vp, vp]),
+        ("grip_debug_elements", [i32, i32, vp, i32, vp, vp, vp, vp]),
+        ("grip_reset_envs", [vp, vp, vp, vp, vp, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = i32
@@ -107,6 +109,16 @@ def check(rc):
 
 def ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def debug_elements(etype, inputs):
+    """Evaluate standalone elements with the device kernels (see grip_debug_elements)."""
+    lib = load()
+    a = np.ascontiguousarray(inputs, np.float64)
+    n, stride = a.shape
+    E, g, H, fl = np.zeros(n), np.zeros((n, 12)), np.zeros((n, 144)), np.zeros(n, np.int32)
+    check(lib.grip_debug_elements(int(etype), n, ptr(a), stride, ptr(E), ptr(g), ptr(H), ptr(fl)))
+    return E, g, H.reshape(n, 12, 12), fl
 
 
 class DeviceBatch:
@@ -162,6 +174,12 @@ class DeviceBatch:
         alphas = np.zeros((self.n_env, self.max_alpha))
         check(self.lib.grip_round(self.h, ptr(b), ptr(it), ptr(fin), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
         return fin.astype(bool), rep, alphas
+
+    def reset_envs(self, mask, node_x0, sv_kin0, tet_Dmi, tet_V0):
+        f = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+        m = np.ascontiguousarray(mask, np.uint8)
+        arrs = [f(node_x0), f(sv_kin0), f(tet_Dmi), f(tet_V0)]
+        check(self.lib.grip_reset_envs(self.h, ptr(m), *[ptr(a) for a in arrs]))
 
     def begin_step(self, active):
         act = np.ascontiguousarray(active, np.uint8)

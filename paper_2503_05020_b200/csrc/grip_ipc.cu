@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "grip_kernels.cuh"
+#include "grip_warp_elements.cuh"
 
 using namespace grip;
 
@@ -54,6 +55,7 @@ struct GripBatch {
   long long launches = 0, sweeps = 0;
   // optional per-kernel timing on the library stream (grip_set_profiling)
   bool prof = false;
+  bool warp_elements = getenv("GRIP_THREAD_ELEMENTS") == nullptr;  // per-thread path kept for A/B
   static constexpr int NK = 8;
   std::vector<cudaEvent_t> kev;   // pairs
   std::vector<std::pair<int, int>> pending_k;  // (kernel id, event pair index)
@@ -528,7 +530,10 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     k_work_scan<<<1, NT, 0, b->stream>>>(D, b->d_list, n);
     kt_end(b, t);
     t = kt_begin(b, K_ELEM);
-    k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
+    if (b->warp_elements)
+      k_elements_w<<<148 * 4, EW * 32, 0, b->stream>>>(D, b->d_list, n);
+    else
+      k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
     kt_end(b, t);
     t = kt_begin(b, K_ASM);
     k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
@@ -727,6 +732,57 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
   for (int e : F)
     if (finalized) finalized[e] = 1;
   if (reports && !F.empty()) return read_reports(b, F, reports, alphas);
+  return 0;
+}
+
+int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
+                    const double* tet_Dmi, const double* tet_V0) {
+  Dev& D = b->D;
+  auto cp = [&](double* dst, const double* src, size_t off, size_t n) {
+    return cudaMemcpyAsync(dst + off, src + off, n * sizeof(double), cudaMemcpyHostToDevice, b->stream);
+  };
+  std::vector<int> zero_i;
+  for (int e = 0; e < b->n_env; ++e) {
+    if (!mask[e]) continue;
+    const size_t n0 = b->node_off[e], nn = b->node_off[e + 1] - n0;
+    const size_t s0 = b->sv_off[e], ns = b->sv_off[e + 1] - s0;
+    const size_t t0 = b->tet_off[e], nt = b->tet_off[e + 1] - t0;
+    CK(cp(D.x, node_x0, 3 * n0, 3 * nn));
+    CK(cudaMemsetAsync(D.v + 3 * n0, 0, 3 * nn * sizeof(double), b->stream));
+    CK(cp(D.kin_pos, sv_kin0, 3 * s0, 3 * ns));
+    if (nt) {
+      CK(cp(const_cast<double*>(D.tet_Dmi), tet_Dmi, 9 * t0, 9 * nt));
+      CK(cp(const_cast<double*>(D.tet_V0), tet_V0, t0, nt));
+    }
+    CK(cudaMemsetAsync(D.n_anc + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.time + e, 0, sizeof(double), b->stream));
+    CK(cudaMemsetAsync(D.step_index + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.ns_done + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.fin_done + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.ns_status + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.flags + e, 0, sizeof(int), b->stream));
+  }
+  return 0;
+}
+
+int grip_debug_elements(int type, int n, const double* in, int stride, double* E, double* g, double* H, int* flags) {
+  if (n <= 0) return 0;
+  double *d_in, *d_E, *d_g, *d_H;
+  int* d_f;
+  CK(cudaMalloc(&d_in, sizeof(double) * (size_t)n * stride));
+  CK(cudaMalloc(&d_E, sizeof(double) * n));
+  CK(cudaMalloc(&d_g, sizeof(double) * 12 * (size_t)n));
+  CK(cudaMalloc(&d_H, sizeof(double) * 144 * (size_t)n));
+  CK(cudaMalloc(&d_f, sizeof(int) * n));
+  CK(cudaMemcpy(d_in, in, sizeof(double) * (size_t)n * stride, cudaMemcpyHostToDevice));
+  k_debug_elements<<<std::min(1024, (n + 3) / 4), 128>>>(type, n, d_in, stride, d_E, d_g, d_H, d_f);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(E, d_E, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(g, d_g, sizeof(double) * 12 * (size_t)n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(H, d_H, sizeof(double) * 144 * (size_t)n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(flags, d_f, sizeof(int) * n, cudaMemcpyDeviceToHost));
+  cudaFree(d_in); cudaFree(d_E); cudaFree(d_g); cudaFree(d_H); cudaFree(d_f);
   return 0;
 }
 

@@ -346,6 +346,55 @@ class BatchedGraspTrials:
     def done(self):
         return bool(np.all(self.phase == _DONE))
 
+    # -- continuous refill (dataset-generation mode) ------------------------------------------
+    @staticmethod
+    def scene_payload(scene):
+        """Device reset payload of a grasp scene: node positions, kinematic surfaces and the
+        posed rest shape of its tets (a new candidate for the same meshes changes only these)."""
+        from paper_2503_05020_b200 import packing
+        lay = packing.layout_env(scene.bodies, scene.collide_pairs_off)
+        pk = packing.Packed([lay], [np.zeros(14)], [np.zeros(3)], packing.body_velocities(scene.bodies))
+        return {"x0": pk.node_x0, "kin0": pk.sv_kin0, "Dmi": pk.tet_Dmi, "V0": pk.tet_V0, "scene": scene,
+                "sizes": (pk.n_node_total, pk.n_sv_total, pk.n_tet_total)}
+
+    def refill(self, slots, payloads):
+        """Start a fresh trial in each finished slot with a new candidate of the same topology."""
+        p = self.group.packed
+        if not hasattr(self, "_host"):
+            self._host = {"x0": p.node_x0.copy(), "kin0": p.sv_kin0.copy(), "Dmi": p.tet_Dmi.copy(),
+                          "V0": p.tet_V0.copy()}
+        h = self._host
+        mask = np.zeros(self.E, np.uint8)
+        pr = self.protocol
+        for e, pl in zip(slots, payloads):
+            n0, n1 = p.node_off[e], p.node_off[e + 1]
+            s0, s1 = p.sv_off[e], p.sv_off[e + 1]
+            t0, t1 = p.tet_off[e], p.tet_off[e + 1]
+            if pl["sizes"] != (n1 - n0, s1 - s0, t1 - t0):
+                raise ValueError("refill needs the same topology as the slot's current scene")
+            h["x0"][3 * n0:3 * n1] = pl["x0"]
+            h["kin0"][3 * s0:3 * s1] = pl["kin0"]
+            h["Dmi"][9 * t0:9 * t1] = pl["Dmi"]
+            h["V0"][t0:t1] = pl["V0"]
+            sc = pl["scene"]
+            for j, f in enumerate(self.fnames[e]):
+                self.cd[e, j] = np.asarray(sc.closing_dirs[f], np.float64)
+            self.max_close[e] = int(np.ceil((sc.opening / 2.0) / (pr.closing_speed * self.dt))) + 5
+            self.vel[self.fb[e]] = 0.0
+            self.grav[e] = 0.0
+            self.phase[e] = _SETTLE
+            self.pstep[e] = self.gphase[e] = self.quiet[e] = self.nsteps[e] = self.phase_start[e] = 0
+            self.halted[e] = False
+            self.com_disp[e] = np.nan
+            self.records[e] = TrialRecord(object_body=sc.object_body, gripper_bodies=self.records[e].gripper_bodies)
+            env = self.group.envs[e]
+            env._time, env._step, env.status = 0.0, 0, "active"
+            mask[e] = 1
+        self.dev.reset_envs(mask, h["x0"], h["kin0"], h["Dmi"], h["V0"])
+        if hasattr(self, "_iter"):
+            self._iter[list(slots)] = False
+            self._need[list(slots)] = True
+
     def advance(self, keep_reports=False):
         """One lockstep protocol step over every unfinished env; returns env-steps executed."""
         ids = np.nonzero(self.phase != _DONE)[0]

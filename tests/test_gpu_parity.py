@@ -164,3 +164,45 @@ def test_protocol_labels_match_reference(golden, lockstep):
             assert abs(r.halt_forces[f]["force"] - h["force"]) <= 1e-5 * h["force"]
         for k, v in g["com_displacement"].items():
             assert abs(r.com_displacement[k] - v) <= 1e-6 * 0.1 + 1e-9, (g["seed"], k, r.com_displacement[k], v)
+
+
+def test_device_element_kernels_vs_reference(golden):
+    """The warp-per-element kernels against the reference's per-stencil / per-tet outputs."""
+    from oracle import energies as oen
+    from paper_2503_05020_b200._native import debug_elements
+    K = dict(np.load(golden / "kernels.npz"))
+    X, pt, ee, epsx = K["pot_x"], K["pot_pt"], K["pot_ee"], K["pot_epsx"]
+    rows = {tuple(r): k for k, r in enumerate(K["pot_idx"])}
+    inp = np.array([np.concatenate([X[r].ravel(), [3e6, 1e-3]]) for r in pt])
+    E, g, H, fl = debug_elements(0, inp)
+    inp = np.array([np.concatenate([X[r].ravel(), [epsx[n], 3e6, 1e-3]]) for n, r in enumerate(ee)])
+    E2, g2, H2, fl2 = debug_elements(1, inp)
+    Es, gs, n_act = 0.0, np.zeros_like(X), 0
+    for rr, EE, gg, HH, ff in ((pt, E, g, H, fl), (ee, E2, g2, H2, fl2)):
+        for n, r in enumerate(rr):
+            if ff[n] & 1:
+                n_act += 1
+                Es += EE[n]
+                np.add.at(gs, r, gg[n].reshape(4, 3))
+                Hr = K["pot_H"][rows[tuple(r)]]
+                assert np.abs(HH[n] - Hr).max() <= 1e-9 * np.abs(Hr).max(), n
+    assert n_act == len(K["pot_idx"])
+    np.testing.assert_allclose(Es, K["pot_E"], rtol=1e-12)
+    np.testing.assert_allclose(gs, K["pot_g"], rtol=1e-9, atol=1e-11 * np.abs(K["pot_g"]).max())
+    # Neo-Hookean
+    rest, cur = K["nh_rest"], K["nh_cur"]
+    Dmi, V0, _ = oen.tet_rest(rest.reshape(-1, 3), np.arange(4 * len(rest)).reshape(-1, 4))
+    inp = np.array([np.concatenate([cur[n].ravel(), Dmi[n].ravel(), [V0[n], K["nh_mu"], K["nh_lam"]]])
+                    for n in range(len(rest))])
+    E, g, H, fl = debug_elements(2, inp)
+    assert not np.any(fl & 4)
+    np.testing.assert_allclose(E, K["nh_Ee"], rtol=1e-11, atol=1e-18)
+    for n in range(len(rest)):
+        assert np.abs(H[n] - K["nh_H"][n]).max() <= 1e-9 * np.abs(K["nh_H"][n]).max(), n
+    np.testing.assert_allclose(g.reshape(-1, 3), K["nh_g"], rtol=1e-9, atol=1e-10 * np.abs(K["nh_g"]).max())
+    # ABD
+    inp = np.array([np.concatenate([A.ravel(), [1e8 * 1.25e-4]]) for A in K["abd_A"]])
+    E, g, H, _ = debug_elements(3, inp)
+    np.testing.assert_allclose(E, K["abd_E"], rtol=1e-12)
+    for n in range(len(inp)):
+        assert np.abs(H[n] - K["abd_H"][n]).max() <= 1e-9 * np.abs(K["abd_H"][n]).max()
