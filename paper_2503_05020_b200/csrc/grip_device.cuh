@@ -77,6 +77,13 @@ struct Dev {
   int cap_pt, cap_ee;
   int *c1_pt, *c1_ee, *c1_eid, *c1_n;   // c1_n[2e]=n_pt, [2e+1]=n_ee
   int *c2_pt, *c2_ee, *c2_eid, *c2_n;
+  // candidate superset at radius cs_R >= every radius needed before x changes; exact sets are
+  // order-preserving filters of it with the reference predicate (identical membership)
+  int *cs_pt, *cs_ee, *cs_eid, *cs_n;
+  double* cs_R;
+  int* cs_valid;
+  double* md_prev;   // last Newton step's max surface displacement
+  double* md_kin;    // this step's prescribed (kinematic) displacement bound
   // elements (uniform capacity per env): [tets | abd | contacts | anchors]
   int max_tet, max_abd, cap_act, cap_anc, cap_el;
   int* act;          // per env cap_act: candidate code (ee ? cap_pt + k : k)
@@ -96,6 +103,7 @@ struct Dev {
   double* bp_aabb;   // per env 6*max(max_tri, max_edge)
   int* bp_cnt;       // per env max(max_sv, max_edge) + 1
   int* bp_tmp;       // per env max(cap_pt, cap_ee)
+  int* bp_lc;        // per env 3*max(max_tri, max_edge): lowest grid cell of each primitive
   double *pcg_x, *pcg_r, *pcg_z, *pcg_p, *pcg_q, *pcg_b;  // per env 3*max_free
   double* pcg_pinv;  // per global free node 9
   double* abd_pinv;  // per abd 144
@@ -304,7 +312,7 @@ __device__ void sort_ints(int* a, int n) {
 
 // Builds the grid over `n` primitive AABBs (aabb[6*i]: lo, hi), each inserted into its
 // tight cell range.  Returns false on scratch overflow.
-__device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells, int cap, BPShared& S, Red& sm) {
+__device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells, int* lc, int cap, BPShared& S, Red& sm) {
   const int ncell = G.nx * G.ny * G.nz;
   for (int c = threadIdx.x; c <= ncell; c += NT) S.head[c] = 0;
   __syncthreads();
@@ -326,9 +334,24 @@ __device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells,
     const double* b = aabb + 6 * i;
     int x0 = G.cx(b[0]), y0 = G.cy(b[1]), z0 = G.cz(b[2]);
     int x1 = G.cx(b[3]), y1 = G.cy(b[4]), z1 = G.cz(b[5]);
+    lc[3 * i] = x0; lc[3 * i + 1] = y0; lc[3 * i + 2] = z0;
     for (int a = x0; a <= x1; ++a)
       for (int bb = y0; bb <= y1; ++bb)
         for (int c = z0; c <= z1; ++c) cells[atomicAdd(&S.cur[(a * G.ny + bb) * G.nz + c], 1)] = i;
+  }
+  __syncthreads();
+  // each cell's list ascending by primitive id (atomic fill order is arbitrary)
+  for (int c = threadIdx.x; c < ncell; c += NT) {
+    const int lo = S.head[c], hi = S.head[c + 1];
+    for (int k = lo + 1; k < hi; ++k) {
+      const int t = cells[k];
+      int j = k - 1;
+      while (j >= lo && cells[j] > t) {
+        cells[j + 1] = cells[j];
+        --j;
+      }
+      cells[j + 1] = t;
+    }
   }
   __syncthreads();
   return true;
@@ -347,6 +370,7 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
   int* cells = D.bp_cells + (size_t)E.e * D.cap_cells;
   int* cnt = D.bp_cnt + (size_t)E.e * (max(D.max_sv, D.max_edge) + 1);
   int* tmp = D.bp_tmp + (size_t)E.e * max(D.cap_pt, D.cap_ee);
+  int* lc = D.bp_lc + (size_t)E.e * 3 * max(D.max_tri, D.max_edge);
   if (E.ns == 0) {
     if (threadIdx.x == 0) { out_n[0] = 0; out_n[1] = 0; }
     __syncthreads();
@@ -391,7 +415,7 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
         o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
       }
       __syncthreads();
-      if (!grid_build(G, aabb, E.nt, cells, D.cap_cells, S, sm)) {
+      if (!grid_build(G, aabb, E.nt, cells, lc, D.cap_cells, S, sm)) {
         regrid = true;
       } else {
         for (int pass = 0; pass < 2; ++pass) {
@@ -410,9 +434,9 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
                   const int kend = S.head[cell + 1];
                   for (int k = S.head[cell]; k < kend; ++k) {
                     const int t = cells[k];
-                    const double* bx = aabb + 6 * t;
-                    if (max(qx0, G.cx(bx[0])) != a || max(qy0, G.cy(bx[1])) != bb || max(qz0, G.cz(bx[2])) != c)
+                    if (max(qx0, lc[3 * t]) != a || max(qy0, lc[3 * t + 1]) != bb || max(qz0, lc[3 * t + 2]) != c)
                       continue;
+                    const double* bx = aabb + 6 * t;
                     const int t0 = tris[3 * t], t1 = tris[3 * t + 1], t2 = tris[3 * t + 2];
                     if (t0 == v || t1 == v || t2 == v) continue;
                     if (!((okmask >> vb[t0]) & 1u)) continue;
@@ -453,7 +477,7 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
         o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
       }
       __syncthreads();
-      if (!grid_build(G, aabb, E.ne, cells, D.cap_cells, S, sm)) { h *= 2.0; continue; }
+      if (!grid_build(G, aabb, E.ne, cells, lc, D.cap_cells, S, sm)) { h *= 2.0; continue; }
       for (int pass = 0; pass < 2; ++pass) {
         for (int i = threadIdx.x; i < E.ne; i += NT) {
           const double* bi = aabb + 6 * i;
@@ -470,13 +494,13 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
             for (int bb = qy0; bb <= qy1; ++bb)
               for (int c = qz0; c <= qz1; ++c) {
                 const int cell = (a * G.ny + bb) * G.nz + c;
-                const int kend = S.head[cell + 1];
-                for (int k = S.head[cell]; k < kend; ++k) {
+                const int kbeg = S.head[cell];
+                for (int k = S.head[cell + 1] - 1; k >= kbeg; --k) {
                   const int j = cells[k];
-                  if (j <= i) continue;
-                  const double* bj = aabb + 6 * j;
-                  if (max(qx0, G.cx(bj[0])) != a || max(qy0, G.cy(bj[1])) != bb || max(qz0, G.cz(bj[2])) != c)
+                  if (j <= i) break;  // list ascending: nothing above i remains
+                  if (max(qx0, lc[3 * j]) != a || max(qy0, lc[3 * j + 1]) != bb || max(qz0, lc[3 * j + 2]) != c)
                     continue;
+                  const double* bj = aabb + 6 * j;
                   const int b0 = edges[2 * j], b1 = edges[2 * j + 1];
                   if (a0 == b0 || a0 == b1 || a1 == b0 || a1 == b1) continue;
                   if (!((okmask >> vb[b0]) & 1u)) continue;
@@ -516,6 +540,59 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
   }
   __syncthreads();
   return ok;
+}
+
+// Exact candidate set at radius r as an order-preserving filter of a superset computed at
+// R >= r from the same positions: identical predicates (broadphase.py:177-183, :202-209),
+// so identical membership and canonical order.
+__device__ void filter_set(const Dev& D, const EnvIx& E, double r, const int* spt, const int* see, const int* seid,
+                           const int* sn, int* dpt, int* dee, int* deid, int* dn, Red& sm) {
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  const int npt = sn[0], nee = sn[1];
+  int base = 0;
+  for (int s = 0; s < npt; s += NT) {
+    const int k = s + threadIdx.x;
+    int keep = 0;
+    int row[4];
+    if (k < npt) {
+      for (int j = 0; j < 4; ++j) row[j] = spt[4 * k + j];
+      V3 p = ld3(X + 3 * row[0]), a = ld3(X + 3 * row[1]), b = ld3(X + 3 * row[2]), c = ld3(X + 3 * row[3]);
+      V3 l = vmin(vmin(a, b), c), u = vmax(vmax(a, b), c);
+      keep = (p.x >= l.x - r && p.y >= l.y - r && p.z >= l.z - r) && (p.x <= u.x + r && p.y <= u.y + r && p.z <= u.z + r);
+    }
+    int tot;
+    const int pre = block_scan(keep, sm, &tot);
+    if (keep)
+      for (int j = 0; j < 4; ++j) dpt[4 * (base + pre) + j] = row[j];
+    base += tot;
+  }
+  const int mpt = base;
+  base = 0;
+  for (int s = 0; s < nee; s += NT) {
+    const int k = s + threadIdx.x;
+    int keep = 0;
+    int row[4];
+    if (k < nee) {
+      for (int j = 0; j < 4; ++j) row[j] = see[4 * k + j];
+      V3 a0 = ld3(X + 3 * row[0]), a1 = ld3(X + 3 * row[1]), b0 = ld3(X + 3 * row[2]), b1 = ld3(X + 3 * row[3]);
+      V3 li = vmin(a0, a1), ui = vmax(a0, a1), lj = vmin(b0, b1), uj = vmax(b0, b1);
+      keep = (uj.x >= li.x - r && uj.y >= li.y - r && uj.z >= li.z - r) &&
+             (lj.x <= ui.x + r && lj.y <= ui.y + r && lj.z <= ui.z + r);
+    }
+    int tot;
+    const int pre = block_scan(keep, sm, &tot);
+    if (keep) {
+      for (int j = 0; j < 4; ++j) dee[4 * (base + pre) + j] = row[j];
+      deid[2 * (base + pre)] = seid[2 * k];
+      deid[2 * (base + pre) + 1] = seid[2 * k + 1];
+    }
+    base += tot;
+  }
+  if (threadIdx.x == 0) {
+    dn[0] = mpt;
+    dn[1] = base;
+  }
+  __syncthreads();
 }
 
 }  // namespace grip

@@ -115,6 +115,10 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   ok &= swap_alloc(D.c_r, E * 12 * (D.cap_act + D.cap_anc));
   ok &= swap_alloc(D.inc, E * 4 * (D.cap_act + D.cap_anc));
   ok &= swap_alloc(D.bp_tmp, E * std::max(D.cap_pt, D.cap_ee));
+  ok &= swap_alloc(D.cs_pt, E * 4 * D.cap_pt);
+  ok &= swap_alloc(D.cs_ee, E * 4 * D.cap_ee);
+  ok &= swap_alloc(D.cs_eid, E * 2 * D.cap_ee);
+  if (D.cs_valid) cudaMemsetAsync(D.cs_valid, 0, sizeof(int) * E, b->stream);  // supersets were dropped
   ok &= swap_alloc(D.bp_cells, E * D.cap_cells);
   // anchors persist: copy with the new pitch
   auto grow_anc = [&](auto*& ptr, int width) {
@@ -380,6 +384,12 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.body_com = b->alloc<double>(3 * (size_t)NB);
   D.max_speed = b->alloc<double>(E);
   D.stats = b->alloc<double>(8);
+  D.cs_n = b->alloc<int>(2 * (size_t)E);
+  D.cs_R = b->alloc<double>(E);
+  D.cs_valid = b->alloc<int>(E);
+  D.md_prev = b->alloc<double>(E);
+  D.md_kin = b->alloc<double>(E);
+  D.bp_lc = b->alloc<int>((size_t)E * 3 * std::max(max_tri, max_edge));
   D.c1_n = b->alloc<int>(2 * (size_t)E);
   D.c2_n = b->alloc<int>(2 * (size_t)E);
   D.n_act = b->alloc<int>(E);
@@ -434,7 +444,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
-        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done};
+        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
+        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -755,6 +766,8 @@ int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, co
       CK(cp(const_cast<double*>(D.tet_V0), tet_V0, t0, nt));
     }
     CK(cudaMemsetAsync(D.n_anc + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.cs_valid + e, 0, sizeof(int), b->stream));
+    CK(cudaMemsetAsync(D.md_prev + e, 0, sizeof(double), b->stream));
     CK(cudaMemsetAsync(D.time + e, 0, sizeof(double), b->stream));
     CK(cudaMemsetAsync(D.step_index + e, 0, sizeof(int), b->stream));
     CK(cudaMemsetAsync(D.ns_done + e, 0, sizeof(int), b->stream));
@@ -795,6 +808,7 @@ int grip_get_state(GripBatch* b, double* x, double* v, double* kin) {
 }
 
 int grip_set_state(GripBatch* b, const double* x, const double* v, const double* kin) {
+  CK(cudaMemsetAsync(b->D.cs_valid, 0, sizeof(int) * b->n_env, b->stream));
   if (x) CK(cudaMemcpyAsync(b->D.x, x, 3 * sizeof(double) * b->n_node, cudaMemcpyHostToDevice, b->stream));
   if (v) CK(cudaMemcpyAsync(b->D.v, v, 3 * sizeof(double) * b->n_node, cudaMemcpyHostToDevice, b->stream));
   if (kin) CK(cudaMemcpyAsync(b->D.kin_pos, kin, 3 * sizeof(double) * b->n_sv, cudaMemcpyHostToDevice, b->stream));

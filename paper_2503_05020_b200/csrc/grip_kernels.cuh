@@ -23,6 +23,39 @@ __device__ __forceinline__ void fail_env(const Dev& D, int e, int reason) {
   }
 }
 
+// radius of the candidate superset: covers 1.05 dhat, the next line search's d^+2 max_disp
+// (predicted from the last step, x1.5) and the kinematic CCD radius; capped so a huge first
+// Newton step does not blow the set up (that line search then runs its own broad phase)
+__device__ __forceinline__ double superset_radius(const Dev& D, int e, double dhat) {
+  double R = fmax(1.05 * dhat, dhat + 3.0 * D.md_prev[e]);
+  R = fmax(R, dhat + 2.0 * D.md_kin[e]);
+  return fmin(R, 12.0 * dhat);
+}
+
+// make D.cs_* a superset at radius >= need for the current positions (D.sv_pos)
+__device__ bool ensure_superset(const Dev& D, const EnvIx& E, double need, double dhat, BPShared& S, Red& sm) {
+  const int e = E.e;
+  const bool valid = D.cs_valid[e] && D.cs_R[e] >= need;
+  __syncthreads();
+  if (valid) return true;
+  const double R = fmax(need, superset_radius(D, e, dhat));
+  const bool ok = broad_phase_env(D, E, R, D.cs_pt + (size_t)e * 4 * D.cap_pt, D.cs_ee + (size_t)e * 4 * D.cap_ee,
+                                  D.cs_eid + (size_t)e * 2 * D.cap_ee, D.cs_n + 2 * e, S, sm);
+  if (threadIdx.x == 0) {
+    D.cs_R[e] = R;
+    D.cs_valid[e] = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return ok;
+}
+
+__device__ __forceinline__ void filter_from_superset(const Dev& D, const EnvIx& E, double r, int* pt, int* ee, int* eid,
+                                                     int* n, Red& sm) {
+  const int e = E.e;
+  filter_set(D, E, r, D.cs_pt + (size_t)e * 4 * D.cap_pt, D.cs_ee + (size_t)e * 4 * D.cap_ee,
+             D.cs_eid + (size_t)e * 2 * D.cap_ee, D.cs_n + 2 * e, pt, ee, eid, n, sm);
+}
+
 // write sv positions of node array xs into D.sv_pos (env slice)
 __device__ void env_sv_positions(const Dev& D, const EnvIx& E, const double* xs) {
   for (int i = threadIdx.x; i < E.ns; i += NT) st3(D.sv_pos + 3 * (size_t)(E.s0 + i), sv_at(D, E, i, xs));
@@ -95,10 +128,16 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
       md = fmax(md, norm(d));
     }
     md = block_max(md, sm);
+    if (threadIdx.x == 0) D.md_kin[e] = md;
     int* cn = D.c2_n + 2 * e;
-    const bool ok = broad_phase_env(D, E, dhat + 2.0 * md, D.c2_pt + (size_t)e * 4 * D.cap_pt,
-                                    D.c2_ee + (size_t)e * 4 * D.cap_ee, D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm);
-    if (!ok) {
+    const double rk = dhat + 2.0 * md;
+    const bool reuse = D.cs_valid[e] && rk <= D.cs_R[e];
+    __syncthreads();
+    if (reuse) {
+      filter_from_superset(D, E, rk, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
+                           D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, sm);
+    } else if (!broad_phase_env(D, E, rk, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
+                                D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm)) {
       if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
       return;
     }
@@ -127,7 +166,10 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
         for (int c = 0; c < 3; ++c) D.kin_pos[3 * (size_t)g + c] += alpha * vb[c] * dt;
       }
     }
+    if (threadIdx.x == 0) D.cs_valid[e] = 0;  // surfaces moved
     __syncthreads();
+  } else {
+    if (threadIdx.x == 0) D.md_kin[e] = 0.0;
   }
   // implicit-Euler target: gravity on soft nodes and affine translations only
   const double* gr = D.gravity + 3 * e;
@@ -195,11 +237,11 @@ __global__ void __launch_bounds__(NT) k_candidates(Dev D, const int* list) {
   int* cn = D.c1_n + 2 * e;
   int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
   int* cee = D.c1_ee + (size_t)e * 4 * D.cap_ee;
-  const bool ok = broad_phase_env(D, E, dhat * 1.05, cpt, cee, D.c1_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm);
-  if (!ok) {
+  if (!ensure_superset(D, E, 1.05 * dhat, dhat, S, sm)) {
     if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
+  filter_from_superset(D, E, dhat * 1.05, cpt, cee, D.c1_eid + (size_t)e * 2 * D.cap_ee, cn, sm);
   const int npt = cn[0], nee = cn[1];
   const double* X = D.sv_pos + 3 * (size_t)E.s0;
   // active stencils in candidate order (PT first, then EE), non-positive distance check
@@ -980,7 +1022,13 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
   int* cpt = D.c2_pt + (size_t)e * 4 * D.cap_pt;
   int* cee = D.c2_ee + (size_t)e * 4 * D.cap_ee;
   int* ceid = D.c2_eid + (size_t)e * 2 * D.cap_ee;
-  if (!broad_phase_env(D, E, dhat + 2.0 * md, cpt, cee, ceid, cn, S, sm)) {
+  const double r2 = dhat + 2.0 * md;
+  const bool reuse = D.cs_valid[e] && r2 <= D.cs_R[e];
+  __syncthreads();
+  if (threadIdx.x == 0) D.md_prev[e] = md;
+  if (reuse) {
+    filter_from_superset(D, E, r2, cpt, cee, ceid, cn, sm);
+  } else if (!broad_phase_env(D, E, r2, cpt, cee, ceid, cn, S, sm)) {
     if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
@@ -1098,6 +1146,7 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
     D.x[g] = D.x[g] + alpha * D.pdir[g];
   }
   if (threadIdx.x == 0) {
+    D.cs_valid[e] = 0;  // x moved
     const int it = D.iters[e];
     if (it < D.max_alpha) D.alphas[(size_t)e * D.max_alpha + it] = alpha;
     D.iters[e] = it + 1;
@@ -1156,10 +1205,11 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
   int* cee = D.c1_ee + (size_t)e * 4 * D.cap_ee;
   int* ceid = D.c1_eid + (size_t)e * 2 * D.cap_ee;
-  if (!broad_phase_env(D, E, dhat * 1.05, cpt, cee, ceid, cn, S, sm)) {
+  if (!ensure_superset(D, E, 1.05 * dhat, dhat, S, sm)) {
     if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
+  filter_from_superset(D, E, dhat * 1.05, cpt, cee, ceid, cn, sm);
   const int npt = cn[0], nee = cn[1];
   const double* X = D.sv_pos + 3 * (size_t)E.s0;
   if (threadIdx.x < 32) cmask[threadIdx.x] = 0u;
