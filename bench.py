@@ -363,6 +363,10 @@ def main():
     roof["frac"] = (roof["achieved"] / peak) if roof.get("achieved") else None
     roof["kernel_ms"] = {k: round(v["ms"], 3) for k, v in ks.items()}
     roof["kernel_launches"] = {k: v["launches"] for k, v in ks.items()}
+    pk = ks["assemble_pcg"]
+    roof["pcg"] = {"iterations_per_solve": pk["pcg_iterations"] / max(pk["solves"], 1.0),
+                   "mean_unknowns": pk["mean_unknowns"], "solves": pk["solves"]}
+    roof["element_counts"] = ks["elements"]["units"]
     nsweeps = sweeps1 - sweeps0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

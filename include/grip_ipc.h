@@ -159,8 +159,9 @@ int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
  * (solver.py:384-428; read by the protocol's steady / COM tests, protocol.py:231-249) */
 int grip_get_body_state(GripBatch* b, double* body_com, double* max_speed);
 /* per-kernel CUDA-event timing on the library stream (0 begin, 1 candidates, 2 work-scan,
- * 3 elements, 4 assemble+PCG, 5 line search, 6 finalize); units = element counts
- * (tets, affine, contacts, anchors) processed by kernel 3 since profiling was enabled */
+ * 3 elements, 4 assemble+PCG, 5 line search, 6 finalize); units (8 doubles) = element counts
+ * (tets, affine, contacts, anchors) of kernel 3, then PCG iterations, linear solves and
+ * summed unknowns of kernel 4, since profiling was enabled */
 int grip_set_profiling(GripBatch* b, int on);
 int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, double* units);
 /* CUDA events on the library stream: start=1 marks, start=0 returns ms since the mark */

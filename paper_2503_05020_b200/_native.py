@@ -251,13 +251,16 @@ class DeviceBatch:
 
     def kernel_stats(self):
         out = {}
-        units = np.zeros(4)
+        units = np.zeros(8)
         for k, name in enumerate(self.KERNELS):
             ms, n = ctypes.c_double(), ctypes.c_int64()
             check(self.lib.grip_kernel_stats(self.h, k, ctypes.byref(ms), ctypes.byref(n),
                                              ptr(units) if k == 3 else None))
             out[name] = {"ms": ms.value, "launches": n.value}
         out["elements"]["units"] = {"tets": units[0], "affine": units[1], "contacts": units[2], "anchors": units[3]}
+        out["assemble_pcg"]["pcg_iterations"] = units[4]
+        out["assemble_pcg"]["solves"] = units[5]
+        out["assemble_pcg"]["mean_unknowns"] = units[6] / max(units[5], 1.0)
         return out
 
     def timer_start(self):

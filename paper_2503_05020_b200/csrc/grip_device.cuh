@@ -108,6 +108,8 @@ struct Dev {
   double* pcg_pinv;  // per global free node 9
   double* abd_pinv;  // per abd 144
   double* sb_val;    // per block 9
+  double* dense_L;   // per env dense_stride doubles (direct solve when the matrix exceeds shared memory)
+  size_t dense_stride;
   double *c_u, *c_w; // per env 3*max_sv
   double* c_r;       // per env 12*(cap_act+cap_anc)
   int *inc_ptr, *inc; // per env max_sv+1 ; 4*(cap_act+cap_anc)

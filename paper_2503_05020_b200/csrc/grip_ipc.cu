@@ -12,6 +12,7 @@
 
 #include "grip_kernels.cuh"
 #include "grip_warp_elements.cuh"
+#include "grip_direct.cuh"
 
 using namespace grip;
 
@@ -56,6 +57,9 @@ struct GripBatch {
   // optional per-kernel timing on the library stream (grip_set_profiling)
   bool prof = false;
   bool warp_elements = getenv("GRIP_THREAD_ELEMENTS") == nullptr;  // per-thread path kept for A/B
+  bool direct = getenv("GRIP_SOLVER") == nullptr || std::string(getenv("GRIP_SOLVER")) != "pcg";
+  int smem_dofs = 0;      // direct solve: matrices up to this many dofs live in shared memory
+  size_t dyn_smem = 0;
   static constexpr int NK = 8;
   std::vector<cudaEvent_t> kev;   // pairs
   std::vector<std::pair<int, int>> pending_k;  // (kernel id, event pair index)
@@ -413,6 +417,26 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.pcg_pinv = b->alloc<double>(9 * (size_t)std::max(NF, 1));
   D.abd_pinv = b->alloc<double>(144 * (size_t)std::max(NA, 1));
   D.sb_val = b->alloc<double>(9 * (size_t)std::max(b->n_blk, 1));
+  {
+    // direct solve storage: packed lower triangle in shared memory if it fits, else global
+    const int nd = 3 * max_free;
+    const size_t packed = (size_t)nd * (nd + 1) / 2;
+    int dev_smem = 0;
+    cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const size_t avail = (size_t)dev_smem - sizeof(DirShared) - 1024;
+    if (packed * sizeof(double) <= avail) {
+      b->smem_dofs = nd;
+      b->dyn_smem = packed * sizeof(double);
+      D.dense_stride = 1;
+      D.dense_L = b->alloc<double>(1);
+    } else {
+      b->smem_dofs = 0;
+      b->dyn_smem = 0;
+      D.dense_stride = packed;
+      D.dense_L = b->alloc<double>(packed * (size_t)E);
+    }
+    CK(cudaFuncSetAttribute(k_assemble_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->dyn_smem));
+  }
   D.c_u = b->alloc<double>((size_t)E * 3 * max_sv);
   D.c_w = b->alloc<double>((size_t)E * 3 * max_sv);
   D.sv_g = b->alloc<double>((size_t)E * 3 * max_sv);
@@ -445,7 +469,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
-        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc};
+        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -547,7 +571,10 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
       k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
     kt_end(b, t);
     t = kt_begin(b, K_ASM);
-    k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
+    if (b->direct)
+      k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, b->d_list, b->smem_dofs);
+    else
+      k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
     kt_end(b, t);
     t = kt_begin(b, K_LS);
     k_linesearch<<<n, NT, 0, b->stream>>>(D, b->d_list);
@@ -897,7 +924,7 @@ int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, d
   }
   if (ms) *ms = b->k_ms[kernel];
   if (launches) *launches = b->k_n[kernel];
-  if (units) CK(cudaMemcpy(units, b->D.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (units) CK(cudaMemcpy(units, b->D.stats, 8 * sizeof(double), cudaMemcpyDeviceToHost));
   return 0;
 }
 

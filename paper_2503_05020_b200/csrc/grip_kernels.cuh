@@ -568,17 +568,47 @@ __device__ bool chol_inv12(double* A) {
   return true;
 }
 
-__global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
-  __shared__ AsmShared A;
-  Red& sm = A.sm;
-  const int e = list[blockIdx.x];
-  if (D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
-  const EnvIx E = env_ix(D, e);
+// solution x (free dofs, pcg layout) -> pdir, residual, convergence / iteration cap (solver.py:663-676)
+__device__ void asm_converge(const Dev& D, const EnvIx& E, const double* X, double Etot, Red& sm) {
+  const int e = E.e;
   const double* P = P_(D, e);
-  const double dt = P[GRIP_P_DT], dt2 = dt * dt;
+  const size_t vb = (size_t)e * 3 * D.max_free;
+  const int nf3 = 3 * E.nf;
+  double res = 0.0;
+  for (int i = threadIdx.x; i < nf3; i += NT) res = fmax(res, fabs(X[vb + i]));
+  res = block_max(res, sm);
+  for (int n = threadIdx.x; n < E.nn; n += NT) {
+    const int f = D.node_fidx[E.n0 + n];
+    for (int c = 0; c < 3; ++c) D.pdir[3 * (size_t)(E.n0 + n) + c] = f >= 0 ? X[vb + 3 * f + c] : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    D.residual[e] = res;
+    const double tol = D.tol[e];
+    if (res < tol) {
+      D.ns_done[e] = 1;
+      D.ns_status[e] = GRIP_NS_CONVERGED;
+      D.energy[e] = Etot;
+      D.needs_ls[e] = 0;
+    } else if (D.iters[e] >= (int)P[GRIP_P_MAXIT]) {
+      D.ns_done[e] = 1;
+      D.ns_status[e] = GRIP_NS_FAILED;
+      D.reason[e] = GRIP_R_NONCONV;
+      D.needs_ls[e] = 0;
+    } else {
+      D.needs_ls[e] = 1;
+    }
+  }
+}
+
+// Assembly shared by both solvers (solver.py:542-586): contact incidence, energy, gradient
+// (-g over free dofs in pcg_b) and the static block values (mass + dt^2 element blocks).
+// Returns false if the env failed (element error or non-finite assembly).
+__device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double dt2, double* Etot_out) {
+  Red& sm = A.sm;
+  const int e = E.e;
   // element-level failures, in the reference's raise order (_elastic before contact)
-  if (D.flags[e] & ERR_INVERTED) { fail_env(D, e, GRIP_R_INVERTED); return; }
-  if (D.flags[e] & ERR_CONTACT_D) { fail_env(D, e, GRIP_R_CONTACT_D); return; }
+  if (D.flags[e] & ERR_INVERTED) { fail_env(D, e, GRIP_R_INVERTED); return false; }
+  if (D.flags[e] & ERR_CONTACT_D) { fail_env(D, e, GRIP_R_CONTACT_D); return false; }
   const size_t elbase = (size_t)e * D.cap_el;
   const int nce = D.n_act[e] + D.n_anc[e];
   // ---- contact incidence per sv (element order), used by gradient and SpMV ----
@@ -700,7 +730,7 @@ __global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
   }
   for (int i = threadIdx.x; i < 3 * E.nf; i += NT) nonfinite |= !isfinite(RHS[vb + i]);
   nonfinite = block_or(nonfinite, sm);
-  if (nonfinite) { fail_env(D, e, GRIP_R_NONFINITE); return; }
+  if (nonfinite) { fail_env(D, e, GRIP_R_NONFINITE); return false; }
   // ---- static block values (mass + dt^2 * element blocks) ----
   for (int f = threadIdx.x; f < E.nf; f += NT) {
     const int fg = E.f0 + f;
@@ -721,6 +751,26 @@ __global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
     }
   }
   __syncthreads();
+  *Etot_out = Etot;
+  return true;
+}
+
+__global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
+  __shared__ AsmShared A;
+  Red& sm = A.sm;
+  const int e = list[blockIdx.x];
+  if (D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double dt = P[GRIP_P_DT], dt2 = dt * dt;
+  const size_t elbase = (size_t)e * D.cap_el;
+  const int nce = D.n_act[e] + D.n_anc[e];
+  int* ip = D.inc_ptr + (size_t)e * (D.max_sv + 1);
+  int* inc = D.inc + (size_t)e * 4 * (D.cap_act + D.cap_anc);
+  const size_t vb = (size_t)e * 3 * D.max_free;
+  double* RHS = D.pcg_b;
+  double Etot = 0.0;
+  if (!asm_prologue(D, E, A, dt2, &Etot)) return;
   // ---- preconditioner: soft 3x3 diagonal blocks, affine 12x12 body blocks ----
   for (int f = threadIdx.x; f < E.nf; f += NT) {
     const int fg = E.f0 + f;
@@ -870,33 +920,15 @@ __global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
     (void)broke;
     solved = conv;
   }
-  if (threadIdx.x == 0) D.pcg_iters[e] += pcg_total;
-  if (!solved) { fail_env(D, e, GRIP_R_SOLVE); return; }
-  // ---- convergence test and iteration cap (solver.py:663-676) ----
-  double res = 0.0;
-  for (int i = threadIdx.x; i < nf3; i += NT) res = fmax(res, fabs(X[vb + i]));
-  res = block_max(res, sm);
-  for (int n = threadIdx.x; n < E.nn; n += NT) {
-    const int f = D.node_fidx[E.n0 + n];
-    for (int c = 0; c < 3; ++c) D.pdir[3 * (size_t)(E.n0 + n) + c] = f >= 0 ? X[vb + 3 * f + c] : 0.0;
-  }
   if (threadIdx.x == 0) {
-    D.residual[e] = res;
-    const double tol = D.tol[e];
-    if (res < tol) {
-      D.ns_done[e] = 1;
-      D.ns_status[e] = GRIP_NS_CONVERGED;
-      D.energy[e] = Etot;
-      D.needs_ls[e] = 0;
-    } else if (D.iters[e] >= (int)P[GRIP_P_MAXIT]) {
-      D.ns_done[e] = 1;
-      D.ns_status[e] = GRIP_NS_FAILED;
-      D.reason[e] = GRIP_R_NONCONV;
-      D.needs_ls[e] = 0;
-    } else {
-      D.needs_ls[e] = 1;
-    }
+    D.pcg_iters[e] += pcg_total;
+    atomicAdd(&D.stats[4], (double)pcg_total);   // PCG iterations (bench statistics)
+    atomicAdd(&D.stats[5], 1.0);                 // linear solves
+    atomicAdd(&D.stats[6], (double)(3 * E.nf));  // unknowns (sum)
   }
+  if (!solved) { fail_env(D, e, GRIP_R_SOLVE); return; }
+  asm_converge(D, E, X, Etot, sm);
+
 }
 
 // ---------------------------------------------------------------------------
