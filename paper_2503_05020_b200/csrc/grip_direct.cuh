@@ -12,19 +12,23 @@ namespace grip {
 
 __device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
 
-struct DirShared {
-  AsmShared A;
-  int nn;            // distinct free nodes of the current element
+struct ElemMap {     // one contact element's slot -> free node map (per warp)
+  int nn;            // distinct free nodes of the element
   int fnode[8];      // their free indices
   int skind[4];      // per slot: 0 soft free, 1 affine, 2 none
   int sf[4];         // per slot: free index (soft node or affine p-node)
   double sxi[4][3];
+};
+
+struct DirShared {
+  AsmShared A;
+  ElemMap em[NWARP];
   int ok;
 };
 
 // dense H_ff (+ shift on the diagonal) into packed L
 __device__ void dense_assemble(const Dev& D, const EnvIx& E, double dt2, double shift, double* L, int n,
-                               DirShared& S) {
+                               DirShared& S, double* kbuf) {
   const int e = E.e;
   const size_t elbase = (size_t)e * D.cap_el;
   const int tot = n * (n + 1) / 2;
@@ -44,117 +48,223 @@ __device__ void dense_assemble(const Dev& D, const EnvIx& E, double dt2, double 
     }
   }
   __syncthreads();
-  // contact / friction elements: J^T (dt^2 H) J, element by element (fixed order -> deterministic)
+  // contact / friction elements, NWARP at a time: warp w computes K = J^T (dt^2 H) J of element
+  // chunk+w into shared memory; then every warp adds, for the free nodes it owns
+  // (f % NWARP == w), the chunk's K rows in element order -> deterministic, no write conflicts.
   const int nce = D.n_act[e] + D.n_anc[e];
-  for (int k = 0; k < nce; ++k) {
-    const size_t sl = elbase + ce_slot(D, e, k);
-    const int* ix = D.el_idx + sl * 4;
-    const double* H = D.el_H + sl * 144;
-    if (threadIdx.x == 0) {
-      int nn = 0;
-      for (int u = 0; u < 4; ++u) {
-        const int g = E.s0 + ix[u];
-        const int kind = D.sv_kind[g];
-        S.skind[u] = 2;
-        if (kind == 2) continue;
-        const int f = D.node_fidx[E.n0 + D.sv_node[g]];
-        if (f < 0) continue;
-        S.sf[u] = f;
-        S.skind[u] = kind;  // 0 soft, 1 affine
-        const int cnt = kind == 0 ? 1 : 4;
-        for (int q = 0; q < cnt; ++q) {
-          bool have = false;
-          for (int r = 0; r < nn; ++r) have |= S.fnode[r] == f + q;
-          if (!have) S.fnode[nn++] = f + q;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < nce; c0 += NWARP) {
+    const int k = c0 + warp;
+    ElemMap& M = S.em[warp];
+    double* K = kbuf + (size_t)warp * 576;
+    if (k < nce) {
+      const size_t sl = elbase + ce_slot(D, e, k);
+      const int* ix = D.el_idx + sl * 4;
+      const double* H = D.el_H + sl * 144;
+      if (lane == 0) {
+        int nn = 0;
+        for (int u = 0; u < 4; ++u) {
+          const int g = E.s0 + ix[u];
+          const int kind = D.sv_kind[g];
+          M.skind[u] = 2;
+          if (kind == 2) continue;
+          const int f = D.node_fidx[E.n0 + D.sv_node[g]];
+          if (f < 0) continue;
+          M.sf[u] = f;
+          M.skind[u] = kind;  // 0 soft, 1 affine
+          const int cnt = kind == 0 ? 1 : 4;
+          for (int q = 0; q < cnt; ++q) {
+            bool have = false;
+            for (int r = 0; r < nn; ++r) have |= M.fnode[r] == f + q;
+            if (!have) M.fnode[nn++] = f + q;
+          }
+          if (kind == 1)
+            for (int c = 0; c < 3; ++c) M.sxi[u][c] = D.sv_xi[3 * (size_t)g + c];
         }
-        if (kind == 1)
-          for (int c = 0; c < 3; ++c) S.sxi[u][c] = D.sv_xi[3 * (size_t)g + c];
+        M.nn = nn;
       }
-      S.nn = nn;
+      __syncwarp();
+      const int nd = 3 * M.nn;
+      for (int t = lane; t < nd * nd; t += 32) {
+        const int r = t / nd, q = t % nd;
+        const int Nr = M.fnode[r / 3], cr = r % 3, Nq = M.fnode[q / 3], cq = q % 3;
+        double v = 0.0;
+        for (int u = 0; u < 4; ++u) {
+          int au = -1;
+          double cu = 1.0;
+          if (M.skind[u] == 0) {
+            if (M.sf[u] == Nr) au = cr;
+          } else if (M.skind[u] == 1) {
+            const int o = Nr - M.sf[u];
+            if (o == 0) au = cr;
+            else if (o >= 1 && o <= 3) { au = o - 1; cu = M.sxi[u][cr]; }
+          }
+          if (au < 0) continue;
+          for (int w = 0; w < 4; ++w) {
+            int aw = -1;
+            double cw = 1.0;
+            if (M.skind[w] == 0) {
+              if (M.sf[w] == Nq) aw = cq;
+            } else if (M.skind[w] == 1) {
+              const int o = Nq - M.sf[w];
+              if (o == 0) aw = cq;
+              else if (o >= 1 && o <= 3) { aw = o - 1; cw = M.sxi[w][cq]; }
+            }
+            if (aw < 0) continue;
+            v += cu * cw * H[(3 * u + au) * 12 + 3 * w + aw];
+          }
+        }
+        K[t] = dt2 * v;
+      }
     }
     __syncthreads();
-    const int nd = 3 * S.nn;
-    for (int t = threadIdx.x; t < nd * nd; t += NT) {
-      const int r = t / nd, q = t % nd;
-      const int Nr = S.fnode[r / 3], cr = r % 3, Nq = S.fnode[q / 3], cq = q % 3;
-      const int i = 3 * Nr + cr, j = 3 * Nq + cq;
-      if (i < j) continue;
-      double v = 0.0;
-      for (int u = 0; u < 4; ++u) {
-        int au = -1;
-        double cu = 1.0;
-        if (S.skind[u] == 0) {
-          if (S.sf[u] == Nr) au = cr;
-        } else if (S.skind[u] == 1) {
-          const int o = Nr - S.sf[u];
-          if (o == 0) au = cr;
-          else if (o >= 1 && o <= 3) { au = o - 1; cu = S.sxi[u][cr]; }
-        }
-        if (au < 0) continue;
-        for (int w = 0; w < 4; ++w) {
-          int aw = -1;
-          double cw = 1.0;
-          if (S.skind[w] == 0) {
-            if (S.sf[w] == Nq) aw = cq;
-          } else if (S.skind[w] == 1) {
-            const int o = Nq - S.sf[w];
-            if (o == 0) aw = cq;
-            else if (o >= 1 && o <= 3) { aw = o - 1; cw = S.sxi[w][cq]; }
-          }
-          if (aw < 0) continue;
-          v += cu * cw * H[(3 * u + au) * 12 + 3 * w + aw];
+    const int kmax = min(NWARP, nce - c0);
+    for (int w2 = 0; w2 < kmax; ++w2) {   // element order within the chunk
+      const ElemMap& Mw = S.em[w2];
+      const double* Kw = kbuf + (size_t)w2 * 576;
+      const int nd = 3 * Mw.nn;
+      for (int a = 0; a < Mw.nn; ++a) {
+        const int Nr = Mw.fnode[a];
+        if (Nr % NWARP != warp) continue;
+        for (int t = lane; t < 3 * nd; t += 32) {
+          const int cr = t / nd, q = t % nd;
+          const int i = 3 * Nr + cr, j = 3 * Mw.fnode[q / 3] + q % 3;
+          if (i >= j) L[pidx(i, j)] += Kw[(3 * a + cr) * nd + q];
         }
       }
-      L[pidx(i, j)] += dt2 * v;
     }
     __syncthreads();
   }
 }
 
-// right-looking Cholesky of packed L in place; false if a pivot is not positive
+// Blocked right-looking Cholesky of packed L in place (panel width 8); false on a
+// non-positive pivot.  One warp factors each 8-column panel (warp barriers only), then all
+// warps apply the rank-8 trailing update (8 FMAs per read-modify-write): 2 block barriers
+// per panel instead of 3 per column.
+constexpr int PW = 8;
+
 __device__ bool dense_cholesky(double* L, int n, DirShared& S) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = 0; k < n; ++k) {
-    if (threadIdx.x == 0) {
-      const double d = L[pidx(k, k)];
-      S.ok = d > 0.0;
-      if (d > 0.0) L[pidx(k, k)] = sqrt(d);
+  for (int kb = 0; kb < n; kb += PW) {
+    const int wb = min(PW, n - kb);
+    if (warp == 0) {  // diagonal wb x wb block
+      int ok = 1;
+      for (int c = 0; c < wb; ++c) {
+        const int k = kb + c;
+        const double d = L[pidx(k, k)];
+        ok = d > 0.0;
+        if (!ok) break;
+        const double lkk = sqrt(d);
+        __syncwarp();
+        if (lane == 0) L[pidx(k, k)] = lkk;
+        const int i = k + 1 + lane;
+        if (i < kb + wb) L[pidx(i, k)] /= lkk;
+        __syncwarp();
+        // remaining diagonal-block entries (i, j), k < j <= i < kb+wb: at most 28, one per lane
+        int t = lane, ii = k + 1, jj = k + 1;
+        for (;;) {   // lane -> (ii, jj) in the trailing diagonal triangle
+          if (ii >= kb + wb) { ii = -1; break; }
+          const int len = ii - (k + 1) + 1;
+          if (t < len) { jj = k + 1 + t; break; }
+          t -= len;
+          ++ii;
+        }
+        if (ii >= 0) L[pidx(ii, jj)] -= L[pidx(ii, k)] * L[pidx(jj, k)];
+        __syncwarp();
+      }
+      if (lane == 0) S.ok = ok;
     }
     __syncthreads();
     if (!S.ok) return false;
-    const double lkk = L[pidx(k, k)];
-    for (int i = k + 1 + threadIdx.x; i < n; i += NT) L[pidx(i, k)] /= lkk;
+    const int j0 = kb + wb;
+    // panel rows below the diagonal block: solve row * L_kk^T = row (one thread per row)
+    for (int i = j0 + threadIdx.x; i < n; i += NT) {
+      double* pi = L + pidx(i, kb);
+      double r[PW];
+#pragma unroll
+      for (int c = 0; c < PW; ++c) r[c] = c < wb ? pi[c] : 0.0;
+#pragma unroll
+      for (int c = 0; c < PW; ++c) {
+        if (c >= wb) break;
+        const double* dc = L + pidx(kb + c, kb);
+        double v = r[c];
+#pragma unroll
+        for (int q = 0; q < PW; ++q)
+          if (q < c) v -= r[q] * dc[q];
+        r[c] = v / dc[c];
+      }
+#pragma unroll
+      for (int c = 0; c < PW; ++c)
+        if (c < wb) pi[c] = r[c];
+    }
     __syncthreads();
-    for (int i = k + 1 + warp; i < n; i += NWARP) {
-      const double lik = L[pidx(i, k)];
+    // trailing: L[i][j] -= sum_{k in panel} L[i][k] L[j][k], j0 <= j <= i
+    for (int i = j0 + warp; i < n; i += NWARP) {
+      double li[PW];
+      const double* pi = L + pidx(i, kb);
+#pragma unroll
+      for (int c = 0; c < PW; ++c) li[c] = c < wb ? pi[c] : 0.0;
       double* row = L + pidx(i, 0);
-      for (int j = k + 1 + lane; j <= i; j += 32) row[j] -= lik * L[pidx(j, k)];
+      for (int j = j0 + lane; j <= i; j += 32) {
+        const double* pj = L + pidx(j, kb);
+        double acc = 0.0;
+#pragma unroll
+        for (int c = 0; c < PW; ++c)
+          if (c < wb) acc += li[c] * pj[c];
+        row[j] -= acc;
+      }
     }
     __syncthreads();
   }
   return true;
 }
 
-// solve L L^T x = b (warp 0), x and b may alias
+// Solve L L^T x = b with all warps (blocked by 32: warp 0 solves each diagonal block, all
+// warps update the rest).  x may alias b.  Call with the whole CTA.
 __device__ void dense_solve(const double* L, int n, const double* b, double* x) {
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  for (int i = lane; i < n; i += 32) x[i] = b[i];
-  __syncwarp();
-  for (int k = 0; k < n; ++k) {
-    const double yk = x[k] / L[pidx(k, k)];
-    __syncwarp();
-    if (lane == 0) x[k] = yk;
-    for (int i = k + 1 + lane; i < n; i += 32) x[i] -= L[pidx(i, k)] * yk;
-    __syncwarp();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < n; i += NT) x[i] = b[i];
+  __syncthreads();
+  for (int kb = 0; kb < n; kb += 32) {            // forward: L y = b
+    const int kend = min(kb + 32, n);
+    if (warp == 0) {
+      for (int k = kb; k < kend; ++k) {
+        const double yk = x[k] / L[pidx(k, k)];
+        __syncwarp();
+        if (lane == 0) x[k] = yk;
+        const int i = kb + lane;
+        if (i > k && i < kend) x[i] -= L[pidx(i, k)] * yk;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = kend + threadIdx.x; i < n; i += NT) {
+      const double* row = L + pidx(i, 0);
+      double acc = 0.0;
+      for (int k = kb; k < kend; ++k) acc += row[k] * x[k];
+      x[i] -= acc;
+    }
+    __syncthreads();
   }
-  for (int k = n - 1; k >= 0; --k) {
-    const double xk = x[k] / L[pidx(k, k)];
-    __syncwarp();
-    if (lane == 0) x[k] = xk;
-    const double* row = L + pidx(k, 0);
-    for (int i = lane; i < k; i += 32) x[i] -= row[i] * xk;
-    __syncwarp();
+  for (int kb = ((n - 1) / 32) * 32; kb >= 0; kb -= 32) {  // backward: L^T x = y
+    const int kend = min(kb + 32, n);
+    if (warp == 0) {
+      for (int k = kend - 1; k >= kb; --k) {
+        const double xk = x[k] / L[pidx(k, k)];
+        __syncwarp();
+        if (lane == 0) x[k] = xk;
+        const int i = kb + lane;
+        if (i < k) x[i] -= L[pidx(k, i)] * xk;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kb; i += NT) {
+      double acc = 0.0;
+      for (int k = kb; k < kend; ++k) acc += L[pidx(k, i)] * x[k];
+      x[i] -= acc;
+    }
+    __syncthreads();
   }
 }
 
@@ -175,6 +285,7 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
   const int n = 3 * E.nf;
   const size_t vb = (size_t)e * 3 * D.max_free;
   double* L = (n <= smem_dofs) ? dyn_smem : D.dense_L + (size_t)e * D.dense_stride;
+  double* kbuf = dyn_smem + (size_t)smem_dofs * (smem_dofs + 1) / 2;   // NWARP x 576 element blocks
   double* X = D.pcg_x;
   double* Q = D.pcg_q;
   double* RHS = D.pcg_b;
@@ -204,10 +315,9 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
       if (threadIdx.x == 0) D.regularized[e] = 1;
       __syncthreads();
     }
-    dense_assemble(D, E, dt2, 0.0, L, n, S);   // sb_val already carries the shift
+    dense_assemble(D, E, dt2, 0.0, L, n, S, kbuf);   // sb_val already carries the shift
     if (!dense_cholesky(L, n, S)) continue;
     dense_solve(L, n, RHS + vb, X + vb);
-    __syncthreads();
     // refinement on the true residual (solver.py:117-122)
     int fin = 1;
     for (int i = threadIdx.x; i < n; i += NT) fin &= isfinite(X[vb + i]);
@@ -223,7 +333,6 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
     r2 = block_sum(r2, sm);
     if (r2 > 1e-20 * bn2) {
       dense_solve(L, n, D.pcg_r + vb, D.pcg_z + vb);
-      __syncthreads();
       for (int i = threadIdx.x; i < n; i += NT) X[vb + i] += D.pcg_z[vb + i];
       __syncthreads();
       spmv(D, E, dt2, X, Q, A);

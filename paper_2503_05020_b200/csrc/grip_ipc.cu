@@ -423,15 +423,16 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
     const size_t packed = (size_t)nd * (nd + 1) / 2;
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    const size_t kb = (size_t)NWARP * 576 * sizeof(double);   // per-chunk element blocks
     const size_t avail = (size_t)dev_smem - sizeof(DirShared) - 1024;
-    if (packed * sizeof(double) <= avail) {
+    if (packed * sizeof(double) + kb <= avail) {
       b->smem_dofs = nd;
-      b->dyn_smem = packed * sizeof(double);
+      b->dyn_smem = packed * sizeof(double) + kb;
       D.dense_stride = 1;
       D.dense_L = b->alloc<double>(1);
     } else {
       b->smem_dofs = 0;
-      b->dyn_smem = 0;
+      b->dyn_smem = kb;
       D.dense_stride = packed;
       D.dense_L = b->alloc<double>(packed * (size_t)E);
     }
