@@ -43,6 +43,7 @@ struct Dev {
   const double* tet_V0;
   const double* tet_mu;
   const double* tet_lam;
+  double* tet_eig;           // per tet 9x9: eigenvectors of its deflated Hessian (Jacobi warm start)
   const int* abd_node;
   const double* abd_kV;
   const uint8_t* body_kind;

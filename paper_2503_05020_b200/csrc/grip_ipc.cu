@@ -334,6 +334,12 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.tet_V0 = b->upload(d->tet_V0, NTET);
   D.tet_mu = b->upload(d->tet_mu, NTET);
   D.tet_lam = b->upload(d->tet_lam, NTET);
+  {
+    std::vector<double> eye(81 * (size_t)std::max(NTET, 1), 0.0);
+    for (int t = 0; t < std::max(NTET, 1); ++t)
+      for (int k = 0; k < 9; ++k) eye[81 * (size_t)t + 10 * k] = 1.0;
+    D.tet_eig = b->upload(eye.data(), eye.size());
+  }
   D.abd_node = b->upload(d->abd_node, NA);
   D.abd_kV = b->upload(d->abd_kV, NA);
   D.body_kind = b->upload(d->body_kind, NB);
@@ -470,7 +476,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
-        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L};
+        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";

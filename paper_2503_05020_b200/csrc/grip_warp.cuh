@@ -102,9 +102,11 @@ __device__ double w_power9(WarpWS& w, int lane) {
 
 // Jacobi eigendecomposition of the symmetric 9x9 w.S (-> diagonal), eigenvectors in w.V.
 // Round-robin ordering over 10 players (index 9 is a bye): every pair once per sweep.
-__device__ void w_jacobi9(WarpWS& w, int lane) {
-  for (int e = lane; e < 81; e += 32) w.V[e] = (e / 9 == e % 9) ? 1.0 : 0.0;
-  __syncwarp();
+__device__ void w_jacobi9(WarpWS& w, int lane, bool init_identity = true) {
+  if (init_identity) {
+    for (int e = lane; e < 81; e += 32) w.V[e] = (e / 9 == e % 9) ? 1.0 : 0.0;
+    __syncwarp();
+  }
   for (int sweep = 0; sweep < 30; ++sweep) {
     double off = 0.0, tot = 0.0;
     for (int e = lane; e < 81; e += 32) {
@@ -160,8 +162,40 @@ __device__ void w_jacobi9(WarpWS& w, int lane) {
   }
 }
 
+// Warm start: S <- V0^T S V0 with the element's eigenvectors from its previous Newton iteration
+// (V0 orthogonal), so Jacobi starts near diagonal; the accumulated V is then the eigenbasis of
+// the ORIGINAL S.  Same converged spectral decomposition, typically 1-2 sweeps instead of ~7.
+__device__ void w_rotate_into(WarpWS& w, const double* V0, int lane) {
+  for (int e = lane; e < 81; e += 32) w.V[e] = V0[e];
+  __syncwarp();
+  for (int e = lane; e < 81; e += 32) {   // T = S V0
+    const int i = e / 9, j = e % 9;
+    double acc = 0.0;
+    for (int k = 0; k < 9; ++k) acc += w.S[i * 9 + k] * w.V[k * 9 + j];
+    w.T[e] = acc;
+  }
+  __syncwarp();
+  for (int e = lane; e < 81; e += 32) {   // S = V0^T T
+    const int i = e / 9, j = e % 9;
+    double acc = 0.0;
+    for (int k = 0; k < 9; ++k) acc += w.V[k * 9 + i] * w.T[k * 9 + j];
+    w.S[e] = acc;
+  }
+  __syncwarp();
+  for (int e = lane; e < 81; e += 32) {
+    const int i = e / 9, j = e % 9;
+    if (i < j) {
+      const double v = 0.5 * (w.S[e] + w.S[j * 9 + i]);
+      w.S[e] = v;
+      w.S[j * 9 + i] = v;
+    }
+  }
+  __syncwarp();
+}
+
 // reference clamp (materials.py:101-113) of a translation-invariant 4-point stencil Hessian in w.H
-__device__ void w_clamp_stencil(WarpWS& w, int lane) {
+// (Vwarm: previous eigenvectors of this element or null; Vout: where to keep the new ones)
+__device__ void w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullptr, double* Vout = nullptr) {
   for (int e = lane; e < 144; e += 32) {
     const int i = e / 12, j = e % 12;
     if (i < j) {
@@ -176,10 +210,13 @@ __device__ void w_clamp_stencil(WarpWS& w, int lane) {
   for (int e = lane; e < 81; e += 32) fro += w.S[e] * w.S[e];
   fro = sqrt(wred_sum(fro));
   double f;
-  if (w_chol_pd9(w, 1e-12 * fro, lane)) {
+  if (!Vwarm && w_chol_pd9(w, 1e-12 * fro, lane)) {
     f = 1e-12 * w_power9(w, lane);
   } else {
-    w_jacobi9(w, lane);
+    if (Vwarm) w_rotate_into(w, Vwarm, lane);
+    w_jacobi9(w, lane, Vwarm == nullptr);
+    if (Vout)
+      for (int e = lane; e < 81; e += 32) Vout[e] = w.V[e];
     double amax = 0.0;
     for (int k = 0; k < 9; ++k) amax = fmax(amax, fabs(w.S[k * 10]));
     f = 1e-12 * amax;

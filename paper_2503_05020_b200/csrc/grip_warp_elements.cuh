@@ -53,7 +53,8 @@ __device__ __constant__ double kPT_C[3][4] = {{1, -1, 0, 0}, {0, -1, 1, 0}, {0, 
 __device__ __constant__ double kEE_C[3][4] = {{-1, 0, 1, 0}, {-1, 1, 0, 0}, {0, 0, -1, 1}};
 
 // ---- Neo-Hookean tet (materials.py:116-158); H[(m,c),(M,C)] = V0 [mu d_cC WW_mM + c2 WA_Mc WA_mC + c3 WA_mc WA_MC]
-__device__ int w_nh(WarpEl& W, const V3* x, const double* Dmi, double V0, double mu, double lam, double* E, int lane) {
+__device__ int w_nh(WarpEl& W, const V3* x, const double* Dmi, double V0, double mu, double lam, double* E, int lane,
+                    double* Vtet = nullptr) {
   double F[9];
   tet_F(x, Dmi, F);
   const double J = det3(F);
@@ -97,7 +98,7 @@ __device__ int w_nh(WarpEl& W, const V3* x, const double* Dmi, double V0, double
                    c3 * wa[3 * m + c] * wa[3 * M + C]);
   }
   __syncwarp();
-  w_clamp_stencil(ws_of(W), lane);
+  w_clamp_stencil(ws_of(W), lane, Vtet, Vtet);
   return 0;
 }
 
@@ -363,7 +364,8 @@ __global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* lis
         idx[j] = D.tet_nodes[4 * (size_t)t + j];
         x[j] = ld3(D.x + 3 * (size_t)(E.n0 + idx[j]));
       }
-      const int fl = w_nh(W, x, D.tet_Dmi + 9 * (size_t)t, D.tet_V0[t], D.tet_mu[t], D.tet_lam[t], &Eel, lane);
+      const int fl = w_nh(W, x, D.tet_Dmi + 9 * (size_t)t, D.tet_V0[t], D.tet_mu[t], D.tet_lam[t], &Eel, lane,
+                          D.tet_eig + 81 * (size_t)t);
       if (fl & EL_INVERTED) {
         if (lane == 0) atomicOr(&D.flags[e], ERR_INVERTED);
         Eel = 0.0;
