@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GRIP_ABI_VERSION 1
+#define GRIP_ABI_VERSION 2
 
 /* Flattened description of N environments (all arrays host, row-major).
  * Index spaces are ENV-LOCAL (node / surface-vertex / body ids restart at 0 in
@@ -79,6 +79,10 @@ typedef struct GripSceneDesc {
   const double* body_mu;
   const uint32_t* body_pairmask; /* bit j: may collide with env-local body j */
   const double* body_vel0;  /* 3 per body */
+  const int32_t* body_tri_lo;  /* env-local triangle range [lo, hi) of each body */
+  const int32_t* body_tri_hi;
+  const int32_t* body_edge_lo; /* env-local edge range [lo, hi) of each body */
+  const int32_t* body_edge_hi;
   /* per-env parameters (14 doubles each, see GRIP_P_* ) and gravity (3 each) */
   const double* env_params;
   const double* env_gravity;

@@ -15,7 +15,7 @@ import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = LIB_DIR / "libgripipc.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 NPARAM = 14
 (P_DT, P_KAPPA, P_DHAT, P_EPSV, P_RELTOL, P_MAXIT, P_ELLFLOOR, P_MAXLS, P_CCDSCALE, P_CCDIT, P_KINGUARD, P_MURULE,
  P_PCGRTOL, P_SPARE) = range(NPARAM)
@@ -47,6 +47,7 @@ class GripSceneDesc(ctypes.Structure):
             "tris", "edges", "edge_rest_sq", "tet_nodes", "tet_Dmi", "tet_V0", "tet_mu", "tet_lam",
             "abd_node", "abd_kV", "abd_body",
             "body_kind", "body_mu", "body_pairmask", "body_vel0",
+            "body_tri_lo", "body_tri_hi", "body_edge_lo", "body_edge_hi",
             "env_params", "env_gravity", "env_cell_hint")]
 
 

@@ -49,6 +49,7 @@ struct Dev {
   const uint8_t* body_kind;
   const double* body_mu;
   const uint32_t* body_pairmask;
+  const int *body_tri_lo, *body_tri_hi, *body_edge_lo, *body_edge_hi;
   double* body_vel;
   double* gravity;
   const double* params;
@@ -429,6 +430,11 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
             const uint32_t okmask = pm[vb[v]];
             const int base = pass ? cnt[v] : 0;
             const int lim = pass ? cnt[v + 1] - base : 0;
+            // bodies without self-collision never pair with their own triangles
+            const int bv = vb[v];
+            const bool selfc = (okmask >> bv) & 1u;
+            const int own_lo = selfc ? 0 : D.body_tri_lo[E.b0 + bv];
+            const int own_hi = selfc ? 0 : D.body_tri_hi[E.b0 + bv];
             int count = 0;
             for (int a = qx0; a <= qx1; ++a)
               for (int bb = qy0; bb <= qy1; ++bb)
@@ -436,7 +442,18 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
                   const int cell = (a * G.ny + bb) * G.nz + c;
                   const int kend = S.head[cell + 1];
                   for (int k = S.head[cell]; k < kend; ++k) {
-                    const int t = cells[k];
+                    int t = cells[k];
+                    if (t >= own_lo && t < own_hi) {   // own body's run (lists ascending): jump over it
+                      int lo2 = k, hi2 = kend;
+                      while (lo2 < hi2) {
+                        const int mid = (lo2 + hi2) >> 1;
+                        if (cells[mid] < own_hi) lo2 = mid + 1;
+                        else hi2 = mid;
+                      }
+                      k = lo2;
+                      if (k >= kend) break;
+                      t = cells[k];
+                    }
                     if (max(qx0, lc[3 * t]) != a || max(qy0, lc[3 * t + 1]) != bb || max(qz0, lc[3 * t + 2]) != c)
                       continue;
                     const double* bx = aabb + 6 * t;
@@ -492,6 +509,9 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
           const uint32_t okmask = pm[vb[a0]];
           const int base = pass ? cnt[i] : 0;
           const int lim = pass ? cnt[i + 1] - base : 0;
+          // pairs are (i < j); without self-collision the first candidate j is the next body's
+          const int ebody = vb[a0];
+          const int jmin = ((okmask >> ebody) & 1u) ? i + 1 : max(i + 1, D.body_edge_hi[E.b0 + ebody]);
           int count = 0;
           for (int a = qx0; a <= qx1; ++a)
             for (int bb = qy0; bb <= qy1; ++bb)
@@ -500,7 +520,7 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
                 const int kbeg = S.head[cell];
                 for (int k = S.head[cell + 1] - 1; k >= kbeg; --k) {
                   const int j = cells[k];
-                  if (j <= i) break;  // list ascending: nothing above i remains
+                  if (j < jmin) break;  // list ascending: nothing at or above jmin remains
                   if (max(qx0, lc[3 * j]) != a || max(qy0, lc[3 * j + 1]) != bb || max(qz0, lc[3 * j + 2]) != c)
                     continue;
                   const double* bj = aabb + 6 * j;

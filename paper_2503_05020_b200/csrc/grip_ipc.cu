@@ -346,6 +346,10 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.body_mu = b->upload(d->body_mu, NB);
   D.body_pairmask = b->upload(d->body_pairmask, NB);
   D.body_vel = b->upload(d->body_vel0, 3 * (size_t)NB);
+  D.body_tri_lo = b->upload(d->body_tri_lo, NB);
+  D.body_tri_hi = b->upload(d->body_tri_hi, NB);
+  D.body_edge_lo = b->upload(d->body_edge_lo, NB);
+  D.body_edge_hi = b->upload(d->body_edge_hi, NB);
   D.gravity = b->upload(d->env_gravity, 3 * (size_t)E);
   D.params = b->upload(d->env_params, (size_t)GRIP_NPARAM * E);
   D.cell_hint = b->upload(d->env_cell_hint, E);
@@ -476,7 +480,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
-        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig};
+        D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";

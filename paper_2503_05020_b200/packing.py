@@ -175,6 +175,10 @@ def layout_env(bodies, collide_pairs_off=()):
                     np.concatenate(tets) if tets else np.zeros((0, 4), np.int64),
                     np.concatenate(tri_chunks), edges, rest, np.asarray(svb, np.int64), pair_ok,
                     np.concatenate(x0) if x0 else np.zeros((0, 3)), np.concatenate(kin0))
+    tri_n = [len(t) for t in tri_chunks]
+    edge_n = [len(e) for e in edge_chunks]
+    lay.body_tri = np.stack([np.cumsum([0] + tri_n)[:-1], np.cumsum(tri_n)], 1)
+    lay.body_edge = np.stack([np.cumsum([0] + edge_n)[:-1], np.cumsum(edge_n)], 1)
     lay._arrays = dict(Mb=np.concatenate(Mb) if Mb else np.zeros((0, 3, 3)), nbody=np.asarray(nbody, np.int64),
                        nkind=np.asarray(nkind, np.int64), nsv=np.concatenate(nsv) if nsv else np.zeros(0, np.int64),
                        svk=np.asarray(svk, np.int64), svn=np.concatenate(svn), svxi=np.concatenate(svxi),
@@ -263,6 +267,10 @@ class Packed:
         if np.any(self.body_off[1:] - self.body_off[:-1] > 32):
             raise ValueError("at most 32 bodies per environment")
         self.body_vel0 = np.asarray(body_vel, np.float64).reshape(-1)
+        self.body_tri_lo = cat(lambda l: l.body_tri[:, 0], np.int32)
+        self.body_tri_hi = cat(lambda l: l.body_tri[:, 1], np.int32)
+        self.body_edge_lo = cat(lambda l: l.body_edge[:, 0], np.int32)
+        self.body_edge_hi = cat(lambda l: l.body_edge[:, 1], np.int32)
         self.env_params = np.asarray(params, np.float64).reshape(E, nv.NPARAM)
         self.env_gravity = np.asarray(gravity, np.float64).reshape(-1)
         hint = []

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     lib.grip_abi_version.restype = ctypes.c_int
-    assert lib.grip_abi_version() == 1
+    assert lib.grip_abi_version() == 2
 
 
 def test_struct_layouts_match_header():
