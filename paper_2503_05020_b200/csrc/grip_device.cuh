@@ -31,6 +31,7 @@ struct Dev {
   const int* node_sv;
   const int* node_fidx;      // local free index or -1
   const int* free_node;      // per global free idx: local node
+  const int* dense_perm;     // per global free idx: position in the env's dense system (hub bodies last)
   const uint8_t* sv_kind;
   const int* sv_node;
   const double* sv_xi;

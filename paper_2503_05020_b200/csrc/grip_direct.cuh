@@ -30,6 +30,7 @@ struct DirShared {
 __device__ void dense_assemble(const Dev& D, const EnvIx& E, double dt2, double shift, double* L, int n,
                                DirShared& S, double* kbuf) {
   const int e = E.e;
+  const int* perm = D.dense_perm + E.f0;   // free node -> dense position (hub bodies last)
   const size_t elbase = (size_t)e * D.cap_el;
   const int tot = n * (n + 1) / 2;
   for (int i = threadIdx.x; i < tot; i += NT) L[i] = 0.0;
@@ -38,11 +39,12 @@ __device__ void dense_assemble(const Dev& D, const EnvIx& E, double dt2, double 
     const int fg = E.f0 + f;
     for (int b = D.sb_rowptr[fg]; b < D.sb_rowptr[fg + 1]; ++b) {
       const int f2 = D.sb_col[b];
-      if (f2 > f) continue;
+      const int pf = perm[f], pf2 = perm[f2];
+      if (pf2 > pf) continue;   // keep the block that lands in the lower triangle
       const double* B = D.sb_val + 9 * (size_t)b;
       for (int c = 0; c < 3; ++c)
         for (int d = 0; d < 3; ++d) {
-          const int i = 3 * f + c, j = 3 * f2 + d;
+          const int i = 3 * pf + c, j = 3 * pf2 + d;
           if (i >= j) L[pidx(i, j)] = B[3 * c + d] + (i == j ? shift : 0.0);
         }
     }
@@ -126,9 +128,10 @@ __device__ void dense_assemble(const Dev& D, const EnvIx& E, double dt2, double 
       for (int a = 0; a < Mw.nn; ++a) {
         const int Nr = Mw.fnode[a];
         if (Nr % NWARP != warp) continue;
+        const int pr = perm[Nr];
         for (int t = lane; t < 3 * nd; t += 32) {
           const int cr = t / nd, q = t % nd;
-          const int i = 3 * Nr + cr, j = 3 * Mw.fnode[q / 3] + q % 3;
+          const int i = 3 * pr + cr, j = 3 * perm[Mw.fnode[q / 3]] + q % 3;
           if (i >= j) L[pidx(i, j)] += Kw[(3 * a + cr) * nd + q];
         }
       }
@@ -181,8 +184,13 @@ __device__ bool dense_cholesky(double* L, int n, DirShared& S) {
     for (int i = j0 + threadIdx.x; i < n; i += NT) {
       double* pi = L + pidx(i, kb);
       double r[PW];
+      bool nz = false;
 #pragma unroll
-      for (int c = 0; c < PW; ++c) r[c] = c < wb ? pi[c] : 0.0;
+      for (int c = 0; c < PW; ++c) {
+        r[c] = c < wb ? pi[c] : 0.0;
+        nz |= r[c] != 0.0;
+      }
+      if (!nz) continue;   // structurally decoupled row (e.g. the other pad): stays zero
 #pragma unroll
       for (int c = 0; c < PW; ++c) {
         if (c >= wb) break;
@@ -202,8 +210,13 @@ __device__ bool dense_cholesky(double* L, int n, DirShared& S) {
     for (int i = j0 + warp; i < n; i += NWARP) {
       double li[PW];
       const double* pi = L + pidx(i, kb);
+      bool nz = false;
 #pragma unroll
-      for (int c = 0; c < PW; ++c) li[c] = c < wb ? pi[c] : 0.0;
+      for (int c = 0; c < PW; ++c) {
+        li[c] = c < wb ? pi[c] : 0.0;
+        nz |= li[c] != 0.0;
+      }
+      if (!nz) continue;   // L[i][panel] == 0 -> no update of row i
       double* row = L + pidx(i, 0);
       for (int j = j0 + lane; j <= i; j += 32) {
         const double* pj = L + pidx(j, kb);
@@ -270,6 +283,21 @@ __device__ void dense_solve(const double* L, int n, const double* b, double* x) 
 
 extern __shared__ double dyn_smem[];
 
+#ifdef GRIP_PHASE_TIMING
+__device__ unsigned long long g_phase[16];
+#define PHASE(k)                                                   \
+  do {                                                             \
+    __syncthreads();                                               \
+    if (threadIdx.x == 0) {                                        \
+      const long long t = clock64();                               \
+      atomicAdd(&g_phase[k], (unsigned long long)(t - t_last));    \
+      t_last = t;                                                  \
+    }                                                              \
+  } while (0)
+#else
+#define PHASE(k) do {} while (0)
+#endif
+
 // Newton sweep 3/4 (direct): assembly + dense Cholesky solve of H_ff p = -g_f
 __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, int smem_dofs) {
   __shared__ DirShared S;
@@ -281,7 +309,11 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], dt2 = dt * dt;
   double Etot = 0.0;
+#ifdef GRIP_PHASE_TIMING
+  long long t_last = clock64();
+#endif
   if (!asm_prologue(D, E, A, dt2, &Etot)) return;
+  PHASE(0);
   const int n = 3 * E.nf;
   const size_t vb = (size_t)e * 3 * D.max_free;
   double* L = (n <= smem_dofs) ? dyn_smem : D.dense_L + (size_t)e * D.dense_stride;
@@ -316,8 +348,20 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
       __syncthreads();
     }
     dense_assemble(D, E, dt2, 0.0, L, n, S, kbuf);   // sb_val already carries the shift
+    PHASE(1);
     if (!dense_cholesky(L, n, S)) continue;
-    dense_solve(L, n, RHS + vb, X + vb);
+    PHASE(2);
+    {
+      const int* perm = D.dense_perm + E.f0;
+      for (int f = threadIdx.x; f < E.nf; f += NT)
+        for (int c = 0; c < 3; ++c) D.pcg_p[vb + 3 * perm[f] + c] = RHS[vb + 3 * f + c];
+      __syncthreads();
+      dense_solve(L, n, D.pcg_p + vb, D.pcg_z + vb);
+      for (int f = threadIdx.x; f < E.nf; f += NT)
+        for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] = D.pcg_z[vb + 3 * perm[f] + c];
+      __syncthreads();
+    }
+    PHASE(3);
     // refinement on the true residual (solver.py:117-122)
     int fin = 1;
     for (int i = threadIdx.x; i < n; i += NT) fin &= isfinite(X[vb + i]);
@@ -332,8 +376,13 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
     }
     r2 = block_sum(r2, sm);
     if (r2 > 1e-20 * bn2) {
-      dense_solve(L, n, D.pcg_r + vb, D.pcg_z + vb);
-      for (int i = threadIdx.x; i < n; i += NT) X[vb + i] += D.pcg_z[vb + i];
+      const int* perm = D.dense_perm + E.f0;
+      for (int f = threadIdx.x; f < E.nf; f += NT)
+        for (int c = 0; c < 3; ++c) D.pcg_p[vb + 3 * perm[f] + c] = D.pcg_r[vb + 3 * f + c];
+      __syncthreads();
+      dense_solve(L, n, D.pcg_p + vb, D.pcg_z + vb);
+      for (int f = threadIdx.x; f < E.nf; f += NT)
+        for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] += D.pcg_z[vb + 3 * perm[f] + c];
       __syncthreads();
       spmv(D, E, dt2, X, Q, A);
       r2 = 0.0;
@@ -345,8 +394,10 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
     }
     solved = isfinite(r2) && r2 <= 1e-16 * bn2;
   }
+  PHASE(4);
   if (!solved) { fail_env(D, e, GRIP_R_SOLVE); return; }
   asm_converge(D, E, X, Etot, sm);
+  PHASE(5);
 }
 
 }  // namespace grip

@@ -247,6 +247,27 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   }
   const int NF = free_off[E];
   b->n_free = NF;
+  // dense-solve ordering: free nodes grouped by body, bodies with the fewest DOF-carrying collision
+  // partners first and the hub (e.g. the grasped object every pad touches) last, so pad-pad blocks
+  // stay structurally zero in the Cholesky factor
+  std::vector<int> dense_perm(std::max(NF, 1), 0);
+  for (int e = 0; e < E; ++e) {
+    const int b0 = b->body_off[e], nb = b->body_off[e + 1] - b0;
+    std::vector<int> partners(nb, 0);
+    for (int i = 0; i < nb; ++i)
+      for (int j = 0; j < nb; ++j)
+        if (i != j && ((d->body_pairmask[b0 + i] >> j) & 1u) && d->body_kind[b0 + j] != 2) partners[i]++;
+    std::vector<int> order(nb);
+    for (int i = 0; i < nb; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      if (partners[x] != partners[y]) return partners[x] < partners[y];
+      return x > y;
+    });
+    int pos = 0;
+    for (int bi : order)
+      for (int n = b->node_off[e]; n < b->node_off[e + 1]; ++n)
+        if (node_fidx[n] >= 0 && d->node_body[n] == bi) dense_perm[free_off[e] + node_fidx[n]] = pos++;
+  }
   std::vector<int> sb_rowptr(NF + 1, 0), sb_col, sb_diag(NF, -1), sbc_ptr(1, 0), sbc;
   std::vector<int> tinc_ptr(NN + 1, 0), tinc;
   {
@@ -322,6 +343,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.node_sv = b->upload(d->node_sv, NN);
   D.node_fidx = b->upload(node_fidx.data(), NN);
   D.free_node = b->upload(free_node.data(), std::max(NF, 1));
+  D.dense_perm = b->upload(dense_perm.data(), std::max(NF, 1));
   D.sv_kind = b->upload(d->sv_kind, NS);
   D.sv_node = b->upload(d->sv_node, NS);
   D.sv_xi = b->upload(d->sv_xi, 3 * (size_t)NS);
@@ -481,7 +503,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -956,6 +978,13 @@ int grip_stream_timer(GripBatch* b, int start, double* ms) {
   if (ms) *ms = f;
   return 0;
 }
+
+#ifdef GRIP_PHASE_TIMING
+int grip_debug_phase(unsigned long long* out) {
+  CK(cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16));
+  return 0;
+}
+#endif
 
 int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps) {
   if (device_ms) *device_ms = b->last_ms;
