@@ -32,6 +32,9 @@ struct Dev {
   const int* node_fidx;      // local free index or -1
   const int* free_node;      // per global free idx: local node
   const int* dense_perm;     // per global free idx: position in the env's dense system (hub bodies last)
+  const int* dense_fc;       // per env-dense position (global free offset): lowest statically coupled position
+  const int* dense_tail;     // per env: first dense position of the hub (last) body
+  const int* sb_row;         // per block: global free row
   const uint8_t* sv_kind;
   const int* sv_node;
   const double* sv_xi;
@@ -116,6 +119,7 @@ struct Dev {
   double *c_u, *c_w; // per env 3*max_sv
   double* c_r;       // per env 12*(cap_act+cap_anc)
   int *inc_ptr, *inc; // per env max_sv+1 ; 4*(cap_act+cap_anc)
+  int* emap;          // per env 4*(cap_act+cap_anc): contact slot -> (dense node position << 2 | kind), -1 none
   double* sv_g;      // per env 3*max_sv
 };
 

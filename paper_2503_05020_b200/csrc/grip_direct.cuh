@@ -1,188 +1,290 @@
-// Direct linear solve of the Newton system (solver.py:91-131) for one env in one CTA:
-// dense H_ff assembled in packed lower-triangular form (shared memory when it fits, else a
-// per-env global scratch), right-looking Cholesky, forward/back substitution by one warp,
-// then the reference's recipe: one refinement if |H p + g| > 1e-10 |g|, accept if
-// <= 1e-8 |g|, else add 1e-8 max(diag, 1) to the diagonal and retry once, else
-// SolveBreakdown.  H_ff is SPD (every element block is clamped PSD and M > 0), so
-// Cholesky replaces SuperLU's LU with the same solution up to rounding.
+// Direct linear solve of the Newton system (solver.py:91-131) for one env in one CTA: H_ff in
+// skyline (envelope) storage, right-looking blocked Cholesky restricted to the envelope,
+// forward/back substitution, then the reference's recipe: one refinement if |H p + g| >
+// 1e-10 |g|, accept if <= 1e-8 |g|, else add 1e-8 max(diag, 1) to the diagonal and retry
+// once, else SolveBreakdown.  H_ff is SPD (every element block is clamped PSD and M > 0),
+// so Cholesky replaces SuperLU's LU with the same solution up to rounding.
+//
+// Dense ordering (host, grip_create): bodies grouped, hub bodies (the grasped object) last,
+// reverse Cuthill-McKee inside every soft body.  Row i of the factor is stored from its first
+// coupled column fc[i] (rounded down to the panel width) to the diagonal; fill-in of a
+// Cholesky factor never leaves the envelope, so the pad blocks never couple and a pad's band
+// stays narrow (config 1: 5.9k stored entries instead of 18.5k).
 #pragma once
 #include "grip_kernels.cuh"
 
 namespace grip {
 
-__device__ __forceinline__ int pidx(int i, int j) { return i * (i + 1) / 2 + j; }  // i >= j
-
-struct ElemMap {     // one contact element's slot -> free node map (per warp)
-  int nn;            // distinct free nodes of the element
-  int fnode[8];      // their free indices
-  int skind[4];      // per slot: 0 soft free, 1 affine, 2 none
-  int sf[4];         // per slot: free index (soft node or affine p-node)
-  double sxi[4][3];
-};
+constexpr int PW = 8;       // panel width = envelope alignment
+constexpr int MAXSEG = 8;   // independent segments factored concurrently (2 warp groups)
 
 struct DirShared {
   AsmShared A;
-  ElemMap em[NWARP];
-  int ok;
+  double Hs[NWARP][144];   // per-warp element Hessian staging (contact scatter)
+  double xs[NWARP][12];    // per-warp affine-slot material coordinates
+  int nodes[NWARP][8];     // per-warp element node list (dense positions)
+  int nn[NWARP];
+  int ok[2];
+  int nseg;                // independent row segments ahead of the tail (hub) rows
+  int seg[MAXSEG + 1];     // segment starts, seg[nseg] = tail start (DOFs)
 };
 
-// dense H_ff (+ shift on the diagonal) into packed L
-__device__ void dense_assemble(const Dev& D, const EnvIx& E, double dt2, double shift, double* L, int n,
-                               DirShared& S, double* kbuf) {
-  const int e = E.e;
-  const int* perm = D.dense_perm + E.f0;   // free node -> dense position (hub bodies last)
-  const size_t elbase = (size_t)e * D.cap_el;
-  const int tot = n * (n + 1) / 2;
-  for (int i = threadIdx.x; i < tot; i += NT) L[i] = 0.0;
-  __syncthreads();
-  for (int f = threadIdx.x; f < E.nf; f += NT) {
-    const int fg = E.f0 + f;
-    for (int b = D.sb_rowptr[fg]; b < D.sb_rowptr[fg + 1]; ++b) {
-      const int f2 = D.sb_col[b];
-      const int pf = perm[f], pf2 = perm[f2];
-      if (pf2 > pf) continue;   // keep the block that lands in the lower triangle
-      const double* B = D.sb_val + 9 * (size_t)b;
-      for (int c = 0; c < 3; ++c)
-        for (int d = 0; d < 3; ++d) {
-          const int i = 3 * pf + c, j = 3 * pf2 + d;
-          if (i >= j) L[pidx(i, j)] = B[3 * c + d] + (i == j ? shift : 0.0);
-        }
-    }
-  }
-  __syncthreads();
-  // contact / friction elements, NWARP at a time: warp w computes K = J^T (dt^2 H) J of element
-  // chunk+w into shared memory; then every warp adds, for the free nodes it owns
-  // (f % NWARP == w), the chunk's K rows in element order -> deterministic, no write conflicts.
-  const int nce = D.n_act[e] + D.n_anc[e];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c0 = 0; c0 < nce; c0 += NWARP) {
-    const int k = c0 + warp;
-    ElemMap& M = S.em[warp];
-    double* K = kbuf + (size_t)warp * 576;
-    if (k < nce) {
-      const size_t sl = elbase + ce_slot(D, e, k);
-      const int* ix = D.el_idx + sl * 4;
-      const double* H = D.el_H + sl * 144;
-      if (lane == 0) {
-        int nn = 0;
-        for (int u = 0; u < 4; ++u) {
-          const int g = E.s0 + ix[u];
-          const int kind = D.sv_kind[g];
-          M.skind[u] = 2;
-          if (kind == 2) continue;
-          const int f = D.node_fidx[E.n0 + D.sv_node[g]];
-          if (f < 0) continue;
-          M.sf[u] = f;
-          M.skind[u] = kind;  // 0 soft, 1 affine
-          const int cnt = kind == 0 ? 1 : 4;
-          for (int q = 0; q < cnt; ++q) {
-            bool have = false;
-            for (int r = 0; r < nn; ++r) have |= M.fnode[r] == f + q;
-            if (!have) M.fnode[nn++] = f + q;
-          }
-          if (kind == 1)
-            for (int c = 0; c < 3; ++c) M.sxi[u][c] = D.sv_xi[3 * (size_t)g + c];
-        }
-        M.nn = nn;
-      }
-      __syncwarp();
-      const int nd = 3 * M.nn;
-      for (int t = lane; t < nd * nd; t += 32) {
-        const int r = t / nd, q = t % nd;
-        const int Nr = M.fnode[r / 3], cr = r % 3, Nq = M.fnode[q / 3], cq = q % 3;
-        double v = 0.0;
-        for (int u = 0; u < 4; ++u) {
-          int au = -1;
-          double cu = 1.0;
-          if (M.skind[u] == 0) {
-            if (M.sf[u] == Nr) au = cr;
-          } else if (M.skind[u] == 1) {
-            const int o = Nr - M.sf[u];
-            if (o == 0) au = cr;
-            else if (o >= 1 && o <= 3) { au = o - 1; cu = M.sxi[u][cr]; }
-          }
-          if (au < 0) continue;
-          for (int w = 0; w < 4; ++w) {
-            int aw = -1;
-            double cw = 1.0;
-            if (M.skind[w] == 0) {
-              if (M.sf[w] == Nq) aw = cq;
-            } else if (M.skind[w] == 1) {
-              const int o = Nq - M.sf[w];
-              if (o == 0) aw = cq;
-              else if (o >= 1 && o <= 3) { aw = o - 1; cw = M.sxi[w][cq]; }
-            }
-            if (aw < 0) continue;
-            v += cu * cw * H[(3 * u + au) * 12 + 3 * w + aw];
-          }
-        }
-        K[t] = dt2 * v;
-      }
-    }
-    __syncthreads();
-    const int kmax = min(NWARP, nce - c0);
-    for (int w2 = 0; w2 < kmax; ++w2) {   // element order within the chunk
-      const ElemMap& Mw = S.em[w2];
-      const double* Kw = kbuf + (size_t)w2 * 576;
-      const int nd = 3 * Mw.nn;
-      for (int a = 0; a < Mw.nn; ++a) {
-        const int Nr = Mw.fnode[a];
-        if (Nr % NWARP != warp) continue;
-        const int pr = perm[Nr];
-        for (int t = lane; t < 3 * nd; t += 32) {
-          const int cr = t / nd, q = t % nd;
-          const int i = 3 * pr + cr, j = 3 * perm[Mw.fnode[q / 3]] + q % 3;
-          if (i >= j) L[pidx(i, j)] += Kw[(3 * a + cr) * nd + q];
-        }
-      }
-    }
-    __syncthreads();
-  }
+// dynamic shared memory in front of the skyline: rdiag[nd] | xv[nd] | fcd[nd] | ro[nd+1] | fcn[max_free]
+__host__ __device__ inline size_t dir_aux_bytes(int nd, int max_free) {
+  const size_t b = (size_t)nd * 16 + ((size_t)2 * nd + 1 + max_free) * 4;
+  return (b + 15) / 16 * 16;
 }
 
-// Blocked right-looking Cholesky of packed L in place (panel width 8); false on a
-// non-positive pivot.  One warp factors each 8-column panel (warp barriers only), then all
-// warps apply the rank-8 trailing update (8 FMAs per read-modify-write): 2 block barriers
-// per panel instead of 3 per column.
-constexpr int PW = 8;
+struct Sky {
+  double* L;
+  const int* ro;   // row start offsets (ro[n] = stored entries)
+  const int* fc;   // first stored column per row (multiple of PW)
+  __device__ __forceinline__ double& at(int i, int j) const { return L[ro[i] + j - fc[i]]; }
+};
 
-__device__ bool dense_cholesky(double* L, int n, DirShared& S) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int kb = 0; kb < n; kb += PW) {
-    const int wb = min(PW, n - kb);
-    if (warp == 0) {  // diagonal wb x wb block
-      int ok = 1;
-      for (int c = 0; c < wb; ++c) {
-        const int k = kb + c;
-        const double d = L[pidx(k, k)];
-        ok = d > 0.0;
-        if (!ok) break;
-        const double lkk = sqrt(d);
-        __syncwarp();
-        if (lane == 0) L[pidx(k, k)] = lkk;
-        const int i = k + 1 + lane;
-        if (i < kb + wb) L[pidx(i, k)] /= lkk;
-        __syncwarp();
-        // remaining diagonal-block entries (i, j), k < j <= i < kb+wb: at most 28, one per lane
-        int t = lane, ii = k + 1, jj = k + 1;
-        for (;;) {   // lane -> (ii, jj) in the trailing diagonal triangle
-          if (ii >= kb + wb) { ii = -1; break; }
-          const int len = ii - (k + 1) + 1;
-          if (t < len) { jj = k + 1 + t; break; }
-          t -= len;
-          ++ii;
-        }
-        if (ii >= 0) L[pidx(ii, jj)] -= L[pidx(ii, k)] * L[pidx(jj, k)];
-        __syncwarp();
-      }
-      if (lane == 0) S.ok = ok;
+// Per-iteration envelope: static first columns lowered by every contact element's node set
+// (min is order independent, so the shared-memory atomics are deterministic).  Also writes
+// each contact element's slot map (emap) for the scatter.  Returns the stored entry count.
+__device__ int sky_build(const Dev& D, const EnvIx& E, int* fcn, int* fcd, int* ro, DirShared& sh) {
+  Red& sm = sh.A.sm;
+  const int e = E.e, nf = E.nf, n = 3 * nf;
+  const int* perm = D.dense_perm + E.f0;
+  for (int p = threadIdx.x; p < nf; p += NT) fcn[p] = D.dense_fc[E.f0 + p];
+  __syncthreads();
+  const size_t elbase = (size_t)e * D.cap_el;
+  const int nce = D.n_act[e] + D.n_anc[e];
+  int* em = D.emap + (size_t)e * 4 * (D.cap_act + D.cap_anc);
+  for (int k = threadIdx.x; k < nce; k += NT) {
+    const int* ix = D.el_idx + (elbase + ce_slot(D, e, k)) * 4;
+    int code[4], mn = 1 << 29;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      code[u] = -1;
+      const int g = E.s0 + ix[u];
+      const int kind = D.sv_kind[g];
+      if (kind == 2) continue;
+      const int f = D.node_fidx[E.n0 + D.sv_node[g]];
+      if (f < 0) continue;
+      const int P = perm[f];   // affine: translation node, A rows at P+1..P+3
+      code[u] = (P << 2) | kind;
+      mn = min(mn, P);
     }
-    __syncthreads();
-    if (!S.ok) return false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      em[4 * k + u] = code[u];
+      if (code[u] < 0) continue;
+      const int P = code[u] >> 2, cnt = (code[u] & 3) ? 4 : 1;
+      for (int q = 0; q < cnt; ++q) atomicMin(&fcn[P + q], mn);
+    }
+  }
+  __syncthreads();
+  // independent segments of the rows ahead of the tail: a boundary at node p when no row
+  // at or after p (before the tail) reaches a column before p
+  if (threadIdx.x == 0) {
+    const int hn = min(D.dense_tail[e], nf);
+    int b[MAXSEG], nb = 0, m = 1 << 29;
+    for (int p = hn - 1; p >= 1 && nb < MAXSEG - 1; --p) {
+      m = min(m, fcn[p]);
+      if (m >= p) b[nb++] = p;
+    }
+    int ns = 0;
+    if (hn > 0) {
+      sh.seg[ns++] = 0;
+      for (int q = nb - 1; q >= 0; --q) sh.seg[ns++] = 3 * b[q];
+    }
+    sh.seg[ns] = 3 * hn;
+    sh.nseg = ns;
+  }
+  __syncthreads();
+  const int ns = sh.nseg;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const int f = 3 * fcn[i / 3];
+    int ss = sh.seg[ns];   // alignment origin: the segment (or the tail) holding column f
+    if (f < ss)
+      for (int q = ns - 1; q >= 0; --q)
+        if (sh.seg[q] <= f) { ss = sh.seg[q]; break; }
+    const int fa = ss + ((f - ss) & ~(PW - 1));
+    fcd[i] = fa;
+    ro[i] = i - fa + 1;
+  }
+  __syncthreads();
+  const int tot = block_scan_array(ro, n, sm);
+  if (threadIdx.x == 0) ro[n] = tot;
+  __syncthreads();
+  return tot;
+}
+
+// H_ff (static blocks from sb_val, which carries mass, dt^2 element blocks and any shift)
+// plus dt^2 J^T H J of the contact / friction elements, into the skyline
+__device__ void sky_assemble(const Dev& D, const EnvIx& E, double dt2, const Sky& S, int n, DirShared& sh) {
+  const int e = E.e;
+  const int* perm = D.dense_perm + E.f0;
+  const int tot = S.ro[n];
+  for (int i = threadIdx.x; i < tot; i += NT) S.L[i] = 0.0;
+  __syncthreads();
+  const int b0 = D.sb_rowptr[E.f0], nb9 = 9 * (D.sb_rowptr[E.f0 + E.nf] - b0);
+  for (int t = threadIdx.x; t < nb9; t += NT) {
+    const int b = b0 + t / 9, q = t - 9 * (t / 9);
+    const int pf = perm[D.sb_row[b] - E.f0], pf2 = perm[D.sb_col[b]];
+    if (pf2 > pf) continue;   // the mirrored block lands in the lower triangle
+    const int i = 3 * pf + q / 3, j = 3 * pf2 + q % 3;
+    if (i >= j) S.at(i, j) = D.sb_val[9 * (size_t)b + q];
+  }
+  __syncthreads();
+  // contact / friction elements: row i is owned by warp i % NWARP; every warp walks the
+  // elements in order and adds its rows of K -> deterministic and barrier-free
+  const size_t elbase = (size_t)e * D.cap_el;
+  const int nce = D.n_act[e] + D.n_anc[e];
+  const int* em = D.emap + (size_t)e * 4 * (D.cap_act + D.cap_anc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* Hs = sh.Hs[warp];
+  double* xs = sh.xs[warp];
+  int* nodes = sh.nodes[warp];
+  for (int k = 0; k < nce; ++k) {
+    const size_t sl = elbase + ce_slot(D, e, k);
+    int code[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) code[u] = em[4 * k + u];
+    const double* H = D.el_H + sl * 144;
+    for (int t = lane; t < 144; t += 32) Hs[t] = H[t];
+    if (lane < 12) {
+      const int u = lane / 3;
+      xs[lane] = (code[u] >= 0 && (code[u] & 3)) ? D.sv_xi[3 * (size_t)(E.s0 + D.el_idx[sl * 4 + u]) + lane % 3] : 0.0;
+    }
+    if (lane == 0) {
+      int m = 0;
+      for (int u = 0; u < 4; ++u) {
+        if (code[u] < 0) continue;
+        const int P = code[u] >> 2, cnt = (code[u] & 3) ? 4 : 1;
+        bool have = false;
+        for (int r = 0; r < m; ++r) have |= nodes[r] == P;
+        if (have) continue;   // second slot on the same affine body (or the same node)
+        for (int q = 0; q < cnt; ++q) nodes[m++] = P + q;
+      }
+      sh.nn[warp] = m;
+    }
+    __syncwarp();
+    const int nd = 3 * sh.nn[warp];
+    const int myrow = lane < nd ? 3 * nodes[lane / 3] + lane % 3 : -1;
+    const unsigned own = __ballot_sync(0xffffffffu, myrow >= 0 && myrow % NWARP == warp);
+    const int no = __popc(own);
+    for (int t = lane; t < no * nd; t += 32) {
+      const int ri = t / nd, q = t - ri * nd;
+      unsigned m = own;
+      for (int x = 0; x < ri; ++x) m &= m - 1;
+      const int r = __ffs(m) - 1;
+      const int Nr = nodes[r / 3], cr = r % 3, Nq = nodes[q / 3], cq = q % 3;
+      const int i = 3 * Nr + cr, j = 3 * Nq + cq;
+      if (j > i) continue;
+      double v = 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (code[u] < 0) continue;
+        const int Pu = code[u] >> 2, ou = Nr - Pu;
+        int au;
+        double cu = 1.0;
+        if ((code[u] & 3) == 0) {
+          if (ou != 0) continue;
+          au = cr;
+        } else {
+          if (ou < 0 || ou > 3) continue;
+          if (ou == 0) au = cr;
+          else { au = ou - 1; cu = xs[3 * u + cr]; }
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          if (code[w] < 0) continue;
+          const int Pw = code[w] >> 2, ow = Nq - Pw;
+          int aw;
+          double cw = 1.0;
+          if ((code[w] & 3) == 0) {
+            if (ow != 0) continue;
+            aw = cq;
+          } else {
+            if (ow < 0 || ow > 3) continue;
+            if (ow == 0) aw = cq;
+            else { aw = ow - 1; cw = xs[3 * w + cq]; }
+          }
+          v += cu * cw * Hs[(3 * u + au) * 12 + 3 * w + aw];
+        }
+      }
+      S.at(i, j) += dt2 * v;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// A warp group: the whole CTA (barrier 0) or half of it (named barriers 1, 2)
+struct Grp {
+  int t, nt, w, nw, id;
+  __device__ __forceinline__ void sync() const {
+    if (id == 0) __syncthreads();
+    else if (id == 1) asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+    else asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory");
+  }
+};
+
+// Factor the wb x wb diagonal block at kb in registers (lane j holds column j); false on a
+// non-positive pivot.  Call with one full warp.
+__device__ __forceinline__ bool diag_factor(const Sky& S, double* rdiag, int kb, int wb, int lane) {
+  double a[PW];
+#pragma unroll
+  for (int i = 0; i < PW; ++i)
+    a[i] = (lane < wb && i < wb && i >= lane) ? S.at(kb + i, kb + lane) : (i == lane ? 1.0 : 0.0);
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < PW; ++c) {
+    if (c < wb) {
+      const double d = __shfl_sync(0xffffffffu, a[c], c);
+      if (!(d > 0.0)) { ok = false; break; }
+      const double rk = rsqrt(d);
+      double lc[PW];
+#pragma unroll
+      for (int i = 0; i < PW; ++i) lc[i] = i > c ? __shfl_sync(0xffffffffu, a[i], c) * rk : 0.0;
+      double lj = 0.0;
+#pragma unroll
+      for (int i = 0; i < PW; ++i)
+        if (i == lane) lj = lc[i];
+      if (lane == c) {
+        a[c] = d * rk;
+#pragma unroll
+        for (int i = 0; i < PW; ++i)
+          if (i > c) a[i] = lc[i];
+        rdiag[kb + c] = rk;
+      } else if (lane > c) {
+#pragma unroll
+        for (int i = 0; i < PW; ++i)
+          if (i >= lane) a[i] -= lc[i] * lj;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PW; ++i)
+    if (ok && lane < wb && i < wb && i >= lane) S.at(kb + i, kb + lane) = a[i];
+  return ok;
+}
+
+// Right-looking panels over columns [c0, c1): the diagonal blocks, the panel solve and the
+// rank-PW update of rows [j0, c1) and of the extra rows [x0, n) (the tail, whose updates are
+// limited to columns < c1).  Rows / columns whose envelope starts after a panel are
+// structurally zero in it and skipped.  Returns false on a non-positive pivot.
+__device__ bool sky_panels(const Sky& S, double* rdiag, int c0, int c1, int x0, int n, const Grp& G, int* okf) {
+  const int lane = G.t & 31;
+  for (int kb = c0; kb < c1; kb += PW) {
+    const int wb = min(PW, c1 - kb);
+    if (G.w == 0) {
+      const bool ok = diag_factor(S, rdiag, kb, wb, lane);
+      if (lane == 0) *okf = ok;
+    }
+    G.sync();
+    if (!*okf) return false;
     const int j0 = kb + wb;
-    // panel rows below the diagonal block: solve row * L_kk^T = row (one thread per row)
-    for (int i = j0 + threadIdx.x; i < n; i += NT) {
-      double* pi = L + pidx(i, kb);
+    const int nrow = (c1 - j0) + (n - x0);
+    for (int t = G.t; t < nrow; t += G.nt) {   // panel rows: r * L_kk^T = row
+      const int i = t < c1 - j0 ? j0 + t : x0 + t - (c1 - j0);
+      if (S.fc[i] > kb) continue;
+      double* pi = &S.at(i, kb);
       double r[PW];
       bool nz = false;
 #pragma unroll
@@ -190,36 +292,40 @@ __device__ bool dense_cholesky(double* L, int n, DirShared& S) {
         r[c] = c < wb ? pi[c] : 0.0;
         nz |= r[c] != 0.0;
       }
-      if (!nz) continue;   // structurally decoupled row (e.g. the other pad): stays zero
+      if (!nz) continue;
 #pragma unroll
       for (int c = 0; c < PW; ++c) {
         if (c >= wb) break;
-        const double* dc = L + pidx(kb + c, kb);
+        const double* dc = &S.at(kb + c, kb);
         double v = r[c];
 #pragma unroll
         for (int q = 0; q < PW; ++q)
           if (q < c) v -= r[q] * dc[q];
-        r[c] = v / dc[c];
+        r[c] = v * rdiag[kb + c];
       }
 #pragma unroll
       for (int c = 0; c < PW; ++c)
         if (c < wb) pi[c] = r[c];
     }
-    __syncthreads();
-    // trailing: L[i][j] -= sum_{k in panel} L[i][k] L[j][k], j0 <= j <= i
-    for (int i = j0 + warp; i < n; i += NWARP) {
+    G.sync();
+    for (int t = G.w; t < nrow; t += G.nw) {   // trailing: L[i][j] -= L[i][panel] . L[j][panel]
+      const int i = t < c1 - j0 ? j0 + t : x0 + t - (c1 - j0);
+      if (S.fc[i] > kb) continue;
+      const double* pi = &S.at(i, kb);
       double li[PW];
-      const double* pi = L + pidx(i, kb);
       bool nz = false;
 #pragma unroll
       for (int c = 0; c < PW; ++c) {
         li[c] = c < wb ? pi[c] : 0.0;
         nz |= li[c] != 0.0;
       }
-      if (!nz) continue;   // L[i][panel] == 0 -> no update of row i
-      double* row = L + pidx(i, 0);
-      for (int j = j0 + lane; j <= i; j += 32) {
-        const double* pj = L + pidx(j, kb);
+      if (!nz) continue;
+      double* row = S.L + S.ro[i] - S.fc[i];
+      const int jend = min(i, c1 - 1);
+      for (int j = j0 + lane; j <= jend; j += 32) {
+        const int fj = S.fc[j];
+        if (fj > kb) continue;
+        const double* pj = S.L + S.ro[j] + kb - fj;
         double acc = 0.0;
 #pragma unroll
         for (int c = 0; c < PW; ++c)
@@ -227,58 +333,157 @@ __device__ bool dense_cholesky(double* L, int n, DirShared& S) {
         row[j] -= acc;
       }
     }
-    __syncthreads();
+    G.sync();
   }
   return true;
 }
 
-// Solve L L^T x = b with all warps (blocked by 32: warp 0 solves each diagonal block, all
-// warps update the rest).  x may alias b.  Call with the whole CTA.
-__device__ void dense_solve(const double* L, int n, const double* b, double* x) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < n; i += NT) x[i] = b[i];
+__device__ __forceinline__ Grp seg_group(int nseg) {
+  const int G2 = nseg >= 2;
+  Grp g;
+  if (G2) {
+    const int half = NT / 2;
+    g.id = 1 + (threadIdx.x >= half);
+    g.t = threadIdx.x - (g.id - 1) * half;
+    g.nt = half;
+  } else {
+    g.id = 0;
+    g.t = threadIdx.x;
+    g.nt = NT;
+  }
+  g.w = g.t >> 5;
+  g.nw = g.nt >> 5;
+  return g;
+}
+
+// Skyline Cholesky in place: the independent segments concurrently (two warp groups), the
+// segment x segment products into the tail x tail block, then the tail.  False on a
+// non-positive pivot (all threads agree).
+__device__ bool sky_cholesky(const Sky& S, double* rdiag, int n, DirShared& sh) {
+  const int ns = sh.nseg, h = sh.seg[ns];
+  const Grp G = seg_group(ns);
+  const int gi = G.id == 0 ? 0 : G.id - 1, ng = G.id == 0 ? 1 : 2;
+  if (threadIdx.x == 0) { sh.ok[0] = 1; sh.ok[1] = 1; }
   __syncthreads();
-  for (int kb = 0; kb < n; kb += 32) {            // forward: L y = b
-    const int kend = min(kb + 32, n);
-    if (warp == 0) {
+  for (int q = gi; q < ns; q += ng)
+    if (!sky_panels(S, rdiag, sh.seg[q], sh.seg[q + 1], h, n, G, &sh.ok[gi])) break;
+  __syncthreads();
+  if (!sh.ok[0] || !sh.ok[1]) return false;
+  if (h > 0) {   // tail x tail -= sum over segment columns (fixed-order warp reduction)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = n - h, ne = m * (m + 1) / 2;
+    for (int t = warp; t < ne; t += NWARP) {
+      int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+      while (ii * (ii + 1) / 2 > t) --ii;
+      const int jj = t - ii * (ii + 1) / 2;
+      const int i = h + ii, j = h + jj;
+      const int lo = max(S.fc[i], S.fc[j]);
+      const double* ri = S.L + S.ro[i] - S.fc[i];
+      const double* rj = S.L + S.ro[j] - S.fc[j];
+      double acc = 0.0;
+      for (int k = lo + lane; k < h; k += 32) acc += ri[k] * rj[k];
+      acc = wsum(acc);
+      if (lane == 0) S.at(i, j) -= acc;
+    }
+    __syncthreads();
+  }
+  const Grp A{(int)threadIdx.x, NT, (int)threadIdx.x >> 5, NWARP, 0};
+  const bool ok = sky_panels(S, rdiag, h, n, n, n, A, &sh.ok[0]);
+  return ok;
+}
+
+// Forward / backward substitution over columns [c0, c1) by one group, blocks of 32 (the
+// group's first warp solves each diagonal block, the group updates rows [c0, c1)).
+__device__ void seg_forward(const Sky& S, const double* rdiag, int c0, int c1, double* x, const Grp& G) {
+  const int lane = G.t & 31;
+  for (int kb = c0; kb < c1; kb += 32) {
+    const int kend = min(kb + 32, c1);
+    if (G.w == 0) {
+      const int i = kb + lane;
+      const int fi = i < kend ? S.fc[i] : c1;
       for (int k = kb; k < kend; ++k) {
-        const double yk = x[k] / L[pidx(k, k)];
+        const double yk = x[k] * rdiag[k];
         __syncwarp();
         if (lane == 0) x[k] = yk;
-        const int i = kb + lane;
-        if (i > k && i < kend) x[i] -= L[pidx(i, k)] * yk;
+        if (i > k && i < kend && fi <= k) x[i] -= S.at(i, k) * yk;
         __syncwarp();
       }
     }
-    __syncthreads();
-    for (int i = kend + threadIdx.x; i < n; i += NT) {
-      const double* row = L + pidx(i, 0);
+    G.sync();
+    for (int i = kend + G.t; i < c1; i += G.nt) {
+      const int fi = S.fc[i], lo = max(kb, fi);
+      if (lo >= kend) continue;
+      const double* row = S.L + S.ro[i] - fi;
       double acc = 0.0;
-      for (int k = kb; k < kend; ++k) acc += row[k] * x[k];
+      for (int k = lo; k < kend; ++k) acc += row[k] * x[k];
       x[i] -= acc;
     }
-    __syncthreads();
+    G.sync();
   }
-  for (int kb = ((n - 1) / 32) * 32; kb >= 0; kb -= 32) {  // backward: L^T x = y
-    const int kend = min(kb + 32, n);
-    if (warp == 0) {
+}
+
+__device__ void seg_backward(const Sky& S, const double* rdiag, int c0, int c1, double* x, const Grp& G) {
+  const int lane = G.t & 31;
+  for (int kb = c0 + ((c1 - 1 - c0) / 32) * 32; kb >= c0; kb -= 32) {
+    const int kend = min(kb + 32, c1);
+    if (G.w == 0) {
+      const int i = kb + lane;
       for (int k = kend - 1; k >= kb; --k) {
-        const double xk = x[k] / L[pidx(k, k)];
+        const double xk = x[k] * rdiag[k];
         __syncwarp();
         if (lane == 0) x[k] = xk;
-        const int i = kb + lane;
-        if (i < k) x[i] -= L[pidx(k, i)] * xk;
+        if (i < k && i >= S.fc[k]) x[i] -= S.at(k, i) * xk;
         __syncwarp();
       }
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kb; i += NT) {
+    G.sync();
+    for (int i = c0 + G.t; i < kb; i += G.nt) {
       double acc = 0.0;
-      for (int k = kb; k < kend; ++k) acc += L[pidx(k, i)] * x[k];
+      for (int k = kb; k < kend; ++k) {
+        const int fk = S.fc[k];
+        if (fk <= i) acc += S.L[S.ro[k] + i - fk] * x[k];
+      }
+      x[i] -= acc;
+    }
+    G.sync();
+  }
+}
+
+// Solve L L^T x = b in place (x in shared memory).  Call with the whole CTA.
+__device__ void sky_solve(const Sky& S, const double* rdiag, int n, double* x, const DirShared& sh) {
+  const int ns = sh.nseg, h = sh.seg[ns];
+  const Grp G = seg_group(ns);
+  const int gi = G.id == 0 ? 0 : G.id - 1, ng = G.id == 0 ? 1 : 2;
+  const Grp A{(int)threadIdx.x, NT, (int)threadIdx.x >> 5, NWARP, 0};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = gi; q < ns; q += ng) seg_forward(S, rdiag, sh.seg[q], sh.seg[q + 1], x, G);
+  __syncthreads();
+  if (h > 0) {
+    for (int i = h + warp; i < n; i += NWARP) {   // tail rows -= L[i][segments] . y
+      const double* ri = S.L + S.ro[i] - S.fc[i];
+      double acc = 0.0;
+      for (int k = S.fc[i] + lane; k < h; k += 32) acc += ri[k] * x[k];
+      acc = wsum(acc);
+      if (lane == 0) x[i] -= acc;
+    }
+    __syncthreads();
+  }
+  seg_forward(S, rdiag, h, n, x, A);
+  seg_backward(S, rdiag, h, n, x, A);
+  if (h > 0) {
+    for (int i = threadIdx.x; i < h; i += NT) {   // segment rows -= L[tail][i]^T . x_tail
+      double acc = 0.0;
+      for (int k = h; k < n; ++k) {
+        const int fk = S.fc[k];
+        if (fk <= i) acc += S.L[S.ro[k] + i - fk] * x[k];
+      }
       x[i] -= acc;
     }
     __syncthreads();
   }
+  for (int q = gi; q < ns; q += ng) seg_backward(S, rdiag, sh.seg[q], sh.seg[q + 1], x, G);
+  __syncthreads();
 }
 
 extern __shared__ double dyn_smem[];
@@ -298,8 +503,8 @@ __device__ unsigned long long g_phase[16];
 #define PHASE(k) do {} while (0)
 #endif
 
-// Newton sweep 3/4 (direct): assembly + dense Cholesky solve of H_ff p = -g_f
-__global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, int smem_dofs) {
+// Newton sweep 3/4 (direct): assembly + skyline Cholesky solve of H_ff p = -g_f
+__global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* list, int env_cap) {
   __shared__ DirShared S;
   AsmShared& A = S.A;
   Red& sm = A.sm;
@@ -315,9 +520,15 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
   if (!asm_prologue(D, E, A, dt2, &Etot)) return;
   PHASE(0);
   const int n = 3 * E.nf;
+  const int nd = 3 * D.max_free;
+  double* rdiag = dyn_smem;
+  double* xv = rdiag + nd;
+  int* fcd = reinterpret_cast<int*>(xv + nd);
+  int* ro = fcd + nd;
+  int* fcn = ro + nd + 1;
+  double* Lsm = dyn_smem + dir_aux_bytes(nd, D.max_free) / sizeof(double);
   const size_t vb = (size_t)e * 3 * D.max_free;
-  double* L = (n <= smem_dofs) ? dyn_smem : D.dense_L + (size_t)e * D.dense_stride;
-  double* kbuf = dyn_smem + (size_t)smem_dofs * (smem_dofs + 1) / 2;   // NWARP x 576 element blocks
+  const int* perm = D.dense_perm + E.f0;
   double* X = D.pcg_x;
   double* Q = D.pcg_q;
   double* RHS = D.pcg_b;
@@ -330,6 +541,11 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
     for (int i = threadIdx.x; i < n; i += NT) X[vb + i] = 0.0;
     __syncthreads();
     solved = true;
+  }
+  Sky L{nullptr, ro, fcd};
+  if (!solved) {
+    const int tot = sky_build(D, E, fcn, fcd, ro, S);
+    L.L = tot <= env_cap ? Lsm : D.dense_L + (size_t)e * D.dense_stride;
   }
   for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
     if (attempt == 1) {
@@ -347,20 +563,17 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
       if (threadIdx.x == 0) D.regularized[e] = 1;
       __syncthreads();
     }
-    dense_assemble(D, E, dt2, 0.0, L, n, S, kbuf);   // sb_val already carries the shift
+    sky_assemble(D, E, dt2, L, n, S);
     PHASE(1);
-    if (!dense_cholesky(L, n, S)) continue;
+    if (!sky_cholesky(L, rdiag, n, S)) continue;
     PHASE(2);
-    {
-      const int* perm = D.dense_perm + E.f0;
-      for (int f = threadIdx.x; f < E.nf; f += NT)
-        for (int c = 0; c < 3; ++c) D.pcg_p[vb + 3 * perm[f] + c] = RHS[vb + 3 * f + c];
-      __syncthreads();
-      dense_solve(L, n, D.pcg_p + vb, D.pcg_z + vb);
-      for (int f = threadIdx.x; f < E.nf; f += NT)
-        for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] = D.pcg_z[vb + 3 * perm[f] + c];
-      __syncthreads();
-    }
+    for (int f = threadIdx.x; f < E.nf; f += NT)
+      for (int c = 0; c < 3; ++c) xv[3 * perm[f] + c] = RHS[vb + 3 * f + c];
+    __syncthreads();
+    sky_solve(L, rdiag, n, xv, S);
+    for (int f = threadIdx.x; f < E.nf; f += NT)
+      for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] = xv[3 * perm[f] + c];
+    __syncthreads();
     PHASE(3);
     // refinement on the true residual (solver.py:117-122)
     int fin = 1;
@@ -369,20 +582,17 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
     if (!fin) continue;
     spmv(D, E, dt2, X, Q, A);
     double r2 = 0.0;
-    for (int i = threadIdx.x; i < n; i += NT) {
-      const double r = RHS[vb + i] - Q[vb + i];
-      D.pcg_r[vb + i] = r;
-      r2 += r * r;
-    }
+    for (int f = threadIdx.x; f < E.nf; f += NT)
+      for (int c = 0; c < 3; ++c) {
+        const double r = RHS[vb + 3 * f + c] - Q[vb + 3 * f + c];
+        xv[3 * perm[f] + c] = r;
+        r2 += r * r;
+      }
     r2 = block_sum(r2, sm);
     if (r2 > 1e-20 * bn2) {
-      const int* perm = D.dense_perm + E.f0;
+      sky_solve(L, rdiag, n, xv, S);
       for (int f = threadIdx.x; f < E.nf; f += NT)
-        for (int c = 0; c < 3; ++c) D.pcg_p[vb + 3 * perm[f] + c] = D.pcg_r[vb + 3 * f + c];
-      __syncthreads();
-      dense_solve(L, n, D.pcg_p + vb, D.pcg_z + vb);
-      for (int f = threadIdx.x; f < E.nf; f += NT)
-        for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] += D.pcg_z[vb + 3 * perm[f] + c];
+        for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] += xv[3 * perm[f] + c];
       __syncthreads();
       spmv(D, E, dt2, X, Q, A);
       r2 = 0.0;
@@ -398,6 +608,14 @@ __global__ void __launch_bounds__(NT) k_assemble_direct(Dev D, const int* list, 
   if (!solved) { fail_env(D, e, GRIP_R_SOLVE); return; }
   asm_converge(D, E, X, Etot, sm);
   PHASE(5);
+#ifdef GRIP_PHASE_TIMING
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_phase[8], 1ull);
+    atomicAdd(&g_phase[9], (unsigned long long)n);
+    atomicAdd(&g_phase[10], (unsigned long long)(D.n_act[e] + D.n_anc[e]));
+    atomicAdd(&g_phase[11], (unsigned long long)(L.L == Lsm));
+  }
+#endif
 }
 
 }  // namespace grip

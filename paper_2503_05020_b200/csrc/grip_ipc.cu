@@ -58,7 +58,7 @@ struct GripBatch {
   bool prof = false;
   bool warp_elements = getenv("GRIP_THREAD_ELEMENTS") == nullptr;  // per-thread path kept for A/B
   bool direct = getenv("GRIP_SOLVER") == nullptr || std::string(getenv("GRIP_SOLVER")) != "pcg";
-  int smem_dofs = 0;      // direct solve: matrices up to this many dofs live in shared memory
+  int env_cap = 0;        // direct solve: skyline capacity (doubles) in shared memory
   size_t dyn_smem = 0;
   static constexpr int NK = 8;
   std::vector<cudaEvent_t> kev;   // pairs
@@ -118,6 +118,7 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   ok &= swap_alloc(D.el_idx, E * D.cap_el * 4);
   ok &= swap_alloc(D.c_r, E * 12 * (D.cap_act + D.cap_anc));
   ok &= swap_alloc(D.inc, E * 4 * (D.cap_act + D.cap_anc));
+  ok &= swap_alloc(D.emap, E * 4 * (D.cap_act + D.cap_anc));
   ok &= swap_alloc(D.bp_tmp, E * std::max(D.cap_pt, D.cap_ee));
   ok &= swap_alloc(D.cs_pt, E * 4 * D.cap_pt);
   ok &= swap_alloc(D.cs_ee, E * 4 * D.cap_ee);
@@ -263,10 +264,49 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
       if (partners[x] != partners[y]) return partners[x] < partners[y];
       return x > y;
     });
+    // within a soft body: reverse Cuthill-McKee on the tet graph of its free nodes (small
+    // envelope for the skyline Cholesky); affine bodies keep their [t, A rows] node order
+    const int n0 = b->node_off[e], nn = b->node_off[e + 1] - n0;
+    std::vector<std::vector<int>> nbr(nn);
+    for (int t = b->tet_off[e]; t < b->tet_off[e + 1]; ++t) {
+      const int* tn = d->tet_nodes + 4 * (size_t)t;
+      for (int a = 0; a < 4; ++a)
+        for (int c = 0; c < 4; ++c)
+          if (a != c && node_fidx[n0 + tn[a]] >= 0 && node_fidx[n0 + tn[c]] >= 0) nbr[tn[a]].push_back(tn[c]);
+    }
+    for (auto& v : nbr) {
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+    }
     int pos = 0;
-    for (int bi : order)
-      for (int n = b->node_off[e]; n < b->node_off[e + 1]; ++n)
-        if (node_fidx[n] >= 0 && d->node_body[n] == bi) dense_perm[free_off[e] + node_fidx[n]] = pos++;
+    for (int bi : order) {
+      std::vector<int> nodes;
+      for (int n = 0; n < nn; ++n)
+        if (node_fidx[n0 + n] >= 0 && d->node_body[n0 + n] == bi) nodes.push_back(n);
+      if (d->body_kind[b0 + bi] == 0) {
+        std::vector<int> cm, mark(nn, 0);
+        auto deg = [&](int n) { return (int)nbr[n].size(); };
+        for (;;) {
+          int start = -1;
+          for (int n : nodes)
+            if (!mark[n] && (start < 0 || deg(n) < deg(start))) start = n;
+          if (start < 0) break;
+          size_t head = cm.size();
+          cm.push_back(start);
+          mark[start] = 1;
+          while (head < cm.size()) {
+            const int u = cm[head++];
+            std::vector<int> nx;
+            for (int w : nbr[u])
+              if (!mark[w] && d->node_body[n0 + w] == bi) { mark[w] = 1; nx.push_back(w); }
+            std::stable_sort(nx.begin(), nx.end(), [&](int x, int y) { return deg(x) < deg(y); });
+            cm.insert(cm.end(), nx.begin(), nx.end());
+          }
+        }
+        nodes.assign(cm.rbegin(), cm.rend());
+      }
+      for (int n : nodes) dense_perm[free_off[e] + node_fidx[n0 + n]] = pos++;
+    }
   }
   std::vector<int> sb_rowptr(NF + 1, 0), sb_col, sb_diag(NF, -1), sbc_ptr(1, 0), sbc;
   std::vector<int> tinc_ptr(NN + 1, 0), tinc;
@@ -327,6 +367,39 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
     }
   }
   b->n_blk = (int)sb_col.size();
+  // skyline (envelope) data for the direct solve: block -> row, per dense position the lowest
+  // dense position it couples to statically; the shared-memory envelope capacity assumes the
+  // hub rows (last body) fill up through contact
+  std::vector<int> sb_row(std::max((int)sb_col.size(), 1), 0), dense_fc(std::max(NF, 1), 0), dense_tail(E, 0);
+  size_t env_need = 0;
+  for (int e = 0; e < E; ++e) {
+    const int f0 = free_off[e], nf = free_off[e + 1] - f0;
+    if (nf == 0) continue;
+    const int* pm = dense_perm.data() + f0;
+    int hub_pos = nf;   // first dense position of the last body
+    {
+      const int n0 = b->node_off[e];
+      int last = -1;
+      for (int f = 0; f < nf; ++f)
+        if (pm[f] == nf - 1) last = d->node_body[n0 + free_node[f0 + f]];
+      for (int f = 0; f < nf; ++f)
+        if (d->node_body[n0 + free_node[f0 + f]] == last) hub_pos = std::min(hub_pos, pm[f]);
+    }
+    std::vector<int> fcn(nf);
+    for (int f = 0; f < nf; ++f) {
+      int m = pm[f];
+      for (int q = sb_rowptr[f0 + f]; q < sb_rowptr[f0 + f + 1]; ++q) {
+        sb_row[q] = f0 + f;
+        m = std::min(m, pm[sb_col[q]]);
+      }
+      dense_fc[f0 + pm[f]] = m;
+    }
+    dense_tail[e] = hub_pos;
+    for (int p = 0; p < nf; ++p) fcn[p] = p >= hub_pos ? 0 : dense_fc[f0 + p];
+    size_t tot = 0;
+    for (int i = 0; i < 3 * nf; ++i) tot += i - ((3 * fcn[i / 3]) & ~7) + 1;
+    env_need = std::max(env_need, tot);
+  }
   // ---- uploads ----
   D.node_off = b->upload(b->node_off.data(), E + 1);
   D.sv_off = b->upload(b->sv_off.data(), E + 1);
@@ -344,6 +417,9 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.node_fidx = b->upload(node_fidx.data(), NN);
   D.free_node = b->upload(free_node.data(), std::max(NF, 1));
   D.dense_perm = b->upload(dense_perm.data(), std::max(NF, 1));
+  D.dense_fc = b->upload(dense_fc.data(), std::max(NF, 1));
+  D.dense_tail = b->upload(dense_tail.data(), E);
+  D.sb_row = b->upload(sb_row.data(), sb_row.size());
   D.sv_kind = b->upload(d->sv_kind, NS);
   D.sv_node = b->upload(d->sv_node, NS);
   D.sv_xi = b->upload(d->sv_xi, 3 * (size_t)NS);
@@ -450,24 +526,22 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.abd_pinv = b->alloc<double>(144 * (size_t)std::max(NA, 1));
   D.sb_val = b->alloc<double>(9 * (size_t)std::max(b->n_blk, 1));
   {
-    // direct solve storage: packed lower triangle in shared memory if it fits, else global
+    // direct solve storage: the skyline of H_ff in shared memory (capacity env_cap doubles, sized
+    // from the static envelope + 15%); an env whose envelope outgrows it this iteration uses its
+    // global slot (full packed triangle, so any envelope fits)
     const int nd = 3 * max_free;
     const size_t packed = (size_t)nd * (nd + 1) / 2;
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    const size_t kb = (size_t)NWARP * 576 * sizeof(double);   // per-chunk element blocks
-    const size_t avail = (size_t)dev_smem - sizeof(DirShared) - 1024;
-    if (packed * sizeof(double) + kb <= avail) {
-      b->smem_dofs = nd;
-      b->dyn_smem = packed * sizeof(double) + kb;
-      D.dense_stride = 1;
-      D.dense_L = b->alloc<double>(1);
-    } else {
-      b->smem_dofs = 0;
-      b->dyn_smem = kb;
-      D.dense_stride = packed;
-      D.dense_L = b->alloc<double>(packed * (size_t)E);
-    }
+    const size_t aux = dir_aux_bytes(nd, max_free);
+    const size_t avail = (size_t)dev_smem - sizeof(DirShared) - 1024 - aux;
+    size_t cap = std::min(packed, (env_need * 115 / 100 + 63) / 64 * 64);
+    if (getenv("GRIP_DENSE_GLOBAL")) cap = 0;
+    cap = std::min(cap, avail / sizeof(double));
+    b->env_cap = (int)cap;
+    b->dyn_smem = aux + cap * sizeof(double);
+    D.dense_stride = packed;
+    D.dense_L = b->alloc<double>(packed * (size_t)E);
     CK(cudaFuncSetAttribute(k_assemble_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b->dyn_smem));
   }
   D.c_u = b->alloc<double>((size_t)E * 3 * max_sv);
@@ -503,7 +577,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.emap};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -606,7 +680,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     kt_end(b, t);
     t = kt_begin(b, K_ASM);
     if (b->direct)
-      k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, b->d_list, b->smem_dofs);
+      k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, b->d_list, b->env_cap);
     else
       k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
     kt_end(b, t);

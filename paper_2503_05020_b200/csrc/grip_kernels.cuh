@@ -732,23 +732,22 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
   nonfinite = block_or(nonfinite, sm);
   if (nonfinite) { fail_env(D, e, GRIP_R_NONFINITE); return false; }
   // ---- static block values (mass + dt^2 * element blocks) ----
-  for (int f = threadIdx.x; f < E.nf; f += NT) {
-    const int fg = E.f0 + f;
-    const int nrow = D.free_node[fg];
-    for (int b = D.sb_rowptr[fg]; b < D.sb_rowptr[fg + 1]; ++b) {
-      double v[9];
-      for (int i = 0; i < 9; ++i) v[i] = 0.0;
-      for (int q = D.sbc_ptr[b]; q < D.sbc_ptr[b + 1]; ++q) {
-        const int code = D.sbc[q];
-        const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
-        const double* H = D.el_H + (elbase + sl) * 144;
-        for (int i = 0; i < 3; ++i)
-          for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
-      }
-      const bool diag = D.sb_col[b] == f;
-      const double* M = D.node_M + 9 * (size_t)(E.n0 + nrow);
-      for (int i = 0; i < 9; ++i) D.sb_val[9 * (size_t)b + i] = (diag ? M[i] : 0.0) + dt2 * v[i];
+  const int blk0 = D.sb_rowptr[E.f0], nblk = D.sb_rowptr[E.f0 + E.nf] - blk0;
+  for (int t = threadIdx.x; t < nblk; t += NT) {   // one block per thread
+    const int b = blk0 + t;
+    const int f = D.sb_row[b] - E.f0;
+    double v[9];
+    for (int i = 0; i < 9; ++i) v[i] = 0.0;
+    for (int q = D.sbc_ptr[b]; q < D.sbc_ptr[b + 1]; ++q) {
+      const int code = D.sbc[q];
+      const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
+      const double* H = D.el_H + (elbase + sl) * 144;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
     }
+    const bool diag = D.sb_col[b] == f;
+    const double* M = D.node_M + 9 * (size_t)(E.n0 + D.free_node[E.f0 + f]);
+    for (int i = 0; i < 9; ++i) D.sb_val[9 * (size_t)b + i] = (diag ? M[i] : 0.0) + dt2 * v[i];
   }
   __syncthreads();
   *Etot_out = Etot;

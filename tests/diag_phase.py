@@ -14,4 +14,5 @@ v = np.array(list(out), float)
 names = ["prologue", "dense_assemble", "cholesky", "solve", "refine", "converge"]
 tot = v[:6].sum()
 for k, nm in enumerate(names):
-    print(f"{nm:16s} {100 * v[k] / tot:5.1f}%")
+    print(f"{nm:16s} {100 * v[k] / tot:5.1f}%  {v[k] / v[8]:10.0f} cyc/CTA")
+print("CTAs", v[8], "mean n", v[9] / v[8], "mean contact elems", v[10] / v[8], "regularized", v[11])
