@@ -12,6 +12,14 @@
 
 namespace grip {
 
+#ifdef GRIP_PHASE_TIMING
+__device__ unsigned long long g_phase[64];   // diagnostic counters (grip_debug_phase)
+#define GSTAT(k, v) atomicAdd(&g_phase[k], (unsigned long long)(v))
+#else
+#define GSTAT(k, v) do {} while (0)
+#endif
+
+
 constexpr int NT = 256;           // threads per env CTA
 constexpr int NWARP = NT / 32;
 constexpr int MAXC = 4096;        // broad-phase grid cells per env
@@ -35,6 +43,7 @@ struct Dev {
   const int* dense_fc;       // per env-dense position (global free offset): lowest statically coupled position
   const int* dense_tail;     // per env: first dense position of the hub (last) body
   const int* sb_row;         // per block: global free row
+  const int* sv_code;        // per surface vertex: dense node position << 2 | kind (0 soft, 1 affine), -1 none
   const uint8_t* sv_kind;
   const int* sv_node;
   const double* sv_xi;
@@ -119,7 +128,10 @@ struct Dev {
   double *c_u, *c_w; // per env 3*max_sv
   double* c_r;       // per env 12*(cap_act+cap_anc)
   int *inc_ptr, *inc; // per env max_sv+1 ; 4*(cap_act+cap_anc)
-  int* emap;          // per env 4*(cap_act+cap_anc): contact slot -> (dense node position << 2 | kind), -1 none
+  double* el_K;       // direct solve, per contact slot (env (cap_act+cap_anc)): dt^2 J^T H J, lower triangle over
+                      // the element's DOFs in dense order (<= 24 DOFs -> 300 entries)
+  int* el_kn;         // per contact slot 9: node count, then the element's dense node positions (ascending)
+  int dense_k;        // 1: the element kernel writes el_K / el_kn (direct solver)
   double* sv_g;      // per env 3*max_sv
 };
 

@@ -20,10 +20,7 @@ constexpr int MAXSEG = 8;   // independent segments factored concurrently (2 war
 
 struct DirShared {
   AsmShared A;
-  double Hs[NWARP][144];   // per-warp element Hessian staging (contact scatter)
-  double xs[NWARP][12];    // per-warp affine-slot material coordinates
-  int nodes[NWARP][8];     // per-warp element node list (dense positions)
-  int nn[NWARP];
+  int turn;                // next contact element allowed to add into the skyline
   int ok[2];
   int nseg;                // independent row segments ahead of the tail (hub) rows
   int seg[MAXSEG + 1];     // segment starts, seg[nseg] = tail start (DOFs)
@@ -43,39 +40,20 @@ struct Sky {
 };
 
 // Per-iteration envelope: static first columns lowered by every contact element's node set
-// (min is order independent, so the shared-memory atomics are deterministic).  Also writes
-// each contact element's slot map (emap) for the scatter.  Returns the stored entry count.
+// (min is order independent, so the shared-memory atomics are deterministic).  Returns the
+// stored entry count.
 __device__ int sky_build(const Dev& D, const EnvIx& E, int* fcn, int* fcd, int* ro, DirShared& sh) {
   Red& sm = sh.A.sm;
   const int e = E.e, nf = E.nf, n = 3 * nf;
   const int* perm = D.dense_perm + E.f0;
   for (int p = threadIdx.x; p < nf; p += NT) fcn[p] = D.dense_fc[E.f0 + p];
   __syncthreads();
-  const size_t elbase = (size_t)e * D.cap_el;
-  const int nce = D.n_act[e] + D.n_anc[e];
-  int* em = D.emap + (size_t)e * 4 * (D.cap_act + D.cap_anc);
-  for (int k = threadIdx.x; k < nce; k += NT) {
-    const int* ix = D.el_idx + (elbase + ce_slot(D, e, k)) * 4;
-    int code[4], mn = 1 << 29;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      code[u] = -1;
-      const int g = E.s0 + ix[u];
-      const int kind = D.sv_kind[g];
-      if (kind == 2) continue;
-      const int f = D.node_fidx[E.n0 + D.sv_node[g]];
-      if (f < 0) continue;
-      const int P = perm[f];   // affine: translation node, A rows at P+1..P+3
-      code[u] = (P << 2) | kind;
-      mn = min(mn, P);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      em[4 * k + u] = code[u];
-      if (code[u] < 0) continue;
-      const int P = code[u] >> 2, cnt = (code[u] & 3) ? 4 : 1;
-      for (int q = 0; q < cnt; ++q) atomicMin(&fcn[P + q], mn);
-    }
+  const int na = D.n_act[e], nce = na + D.n_anc[e];
+  const size_t cs0 = (size_t)e * (D.cap_act + D.cap_anc);
+  for (int t = threadIdx.x; t < 8 * nce; t += NT) {   // (element, node) pairs
+    const int k = t >> 3, q = t & 7;
+    const int* kn = D.el_kn + (cs0 + (k < na ? k : D.cap_act + (k - na))) * 9;
+    if (q < kn[0]) atomicMin(&fcn[kn[1 + q]], kn[1]);   // nodes ascending: kn[1] is the lowest
   }
   __syncthreads();
   // independent segments of the rows ahead of the tail: a boundary at node p when no row
@@ -114,9 +92,9 @@ __device__ int sky_build(const Dev& D, const EnvIx& E, int* fcn, int* fcd, int* 
   return tot;
 }
 
-// H_ff (static blocks from sb_val, which carries mass, dt^2 element blocks and any shift)
-// plus dt^2 J^T H J of the contact / friction elements, into the skyline
-__device__ void sky_assemble(const Dev& D, const EnvIx& E, double dt2, const Sky& S, int n, DirShared& sh) {
+// H_ff into the skyline: the static blocks from sb_val (mass, dt^2 element blocks and any
+// shift), then dt^2 J^T H J of the contact / friction elements (sky_scatter_contacts)
+__device__ void sky_static(const Dev& D, const EnvIx& E, const Sky& S, int n) {
   const int e = E.e;
   const int* perm = D.dense_perm + E.f0;
   const int tot = S.ro[n];
@@ -131,86 +109,57 @@ __device__ void sky_assemble(const Dev& D, const EnvIx& E, double dt2, const Sky
     if (i >= j) S.at(i, j) = D.sb_val[9 * (size_t)b + q];
   }
   __syncthreads();
-  // contact / friction elements: row i is owned by warp i % NWARP; every warp walks the
-  // elements in order and adds its rows of K -> deterministic and barrier-free
-  const size_t elbase = (size_t)e * D.cap_el;
-  const int nce = D.n_act[e] + D.n_anc[e];
-  const int* em = D.emap + (size_t)e * 4 * (D.cap_act + D.cap_anc);
+}
+
+// The contact / friction elements' K (precomputed by the element kernel, w_store_K) into the
+// skyline.  Warp w takes elements k = w, w + NWARP, ...: it loads K and computes the skyline
+// offsets into registers (the warps overlap this), then adds them when the turn counter
+// reaches k -> every entry accumulates its elements in element order (deterministic), and
+// only the short add section is serialised.
+__device__ void sky_scatter_contacts(const Dev& D, const EnvIx& E, const Sky& S, DirShared& sh) {
+  const int e = E.e;
+  const int na = D.n_act[e];
+  const int nce = na + D.n_anc[e];
+  const size_t cs0 = (size_t)e * (D.cap_act + D.cap_anc);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* Hs = sh.Hs[warp];
-  double* xs = sh.xs[warp];
-  int* nodes = sh.nodes[warp];
-  for (int k = 0; k < nce; ++k) {
-    const size_t sl = elbase + ce_slot(D, e, k);
-    int code[4];
+  if (threadIdx.x == 0) sh.turn = 0;
+  __syncthreads();
+  for (int k = warp; k < nce; k += NWARP) {
+    const size_t cs = cs0 + (k < na ? k : D.cap_act + (k - na));
+    const int* kn = D.el_kn + cs * 9;
+    const double* K = D.el_K + cs * 300;
+    const int nn = kn[0];
+    const int node = lane < 8 ? kn[1 + lane] : 0;
+    const int nd = 3 * nn, ne = nd * (nd + 1) / 2;
+    double kv[10];
+    int ko[10];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) code[u] = em[4 * k + u];
-    const double* H = D.el_H + sl * 144;
-    for (int t = lane; t < 144; t += 32) Hs[t] = H[t];
-    if (lane < 12) {
-      const int u = lane / 3;
-      xs[lane] = (code[u] >= 0 && (code[u] & 3)) ? D.sv_xi[3 * (size_t)(E.s0 + D.el_idx[sl * 4 + u]) + lane % 3] : 0.0;
-    }
-    if (lane == 0) {
-      int m = 0;
-      for (int u = 0; u < 4; ++u) {
-        if (code[u] < 0) continue;
-        const int P = code[u] >> 2, cnt = (code[u] & 3) ? 4 : 1;
-        bool have = false;
-        for (int r = 0; r < m; ++r) have |= nodes[r] == P;
-        if (have) continue;   // second slot on the same affine body (or the same node)
-        for (int q = 0; q < cnt; ++q) nodes[m++] = P + q;
+    for (int mi = 0; mi < 10; ++mi) {
+      const int t = lane + 32 * mi;
+      const int tt = t < ne ? t : 0;
+      int r = (int)((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
+      while ((r + 1) * (r + 2) / 2 <= tt) ++r;
+      while (r * (r + 1) / 2 > tt) --r;
+      const int q = tt - r * (r + 1) / 2;
+      const int Nr = __shfl_sync(0xffffffffu, node, r / 3), Nq = __shfl_sync(0xffffffffu, node, q / 3);
+      ko[mi] = -1;
+      kv[mi] = 0.0;
+      if (t < ne) {
+        const int i = 3 * Nr + r % 3, j = 3 * Nq + q % 3;
+        kv[mi] = K[t];
+        ko[mi] = S.ro[i] + j - S.fc[i];
       }
-      sh.nn[warp] = m;
     }
+    if (lane == 0)
+      while (*(volatile int*)&sh.turn != k) {}
     __syncwarp();
-    const int nd = 3 * sh.nn[warp];
-    const int myrow = lane < nd ? 3 * nodes[lane / 3] + lane % 3 : -1;
-    const unsigned own = __ballot_sync(0xffffffffu, myrow >= 0 && myrow % NWARP == warp);
-    const int no = __popc(own);
-    for (int t = lane; t < no * nd; t += 32) {
-      const int ri = t / nd, q = t - ri * nd;
-      unsigned m = own;
-      for (int x = 0; x < ri; ++x) m &= m - 1;
-      const int r = __ffs(m) - 1;
-      const int Nr = nodes[r / 3], cr = r % 3, Nq = nodes[q / 3], cq = q % 3;
-      const int i = 3 * Nr + cr, j = 3 * Nq + cq;
-      if (j > i) continue;
-      double v = 0.0;
+    __threadfence_block();
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (code[u] < 0) continue;
-        const int Pu = code[u] >> 2, ou = Nr - Pu;
-        int au;
-        double cu = 1.0;
-        if ((code[u] & 3) == 0) {
-          if (ou != 0) continue;
-          au = cr;
-        } else {
-          if (ou < 0 || ou > 3) continue;
-          if (ou == 0) au = cr;
-          else { au = ou - 1; cu = xs[3 * u + cr]; }
-        }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          if (code[w] < 0) continue;
-          const int Pw = code[w] >> 2, ow = Nq - Pw;
-          int aw;
-          double cw = 1.0;
-          if ((code[w] & 3) == 0) {
-            if (ow != 0) continue;
-            aw = cq;
-          } else {
-            if (ow < 0 || ow > 3) continue;
-            if (ow == 0) aw = cq;
-            else { aw = ow - 1; cw = xs[3 * w + cq]; }
-          }
-          v += cu * cw * Hs[(3 * u + au) * 12 + 3 * w + aw];
-        }
-      }
-      S.at(i, j) += dt2 * v;
-    }
+    for (int mi = 0; mi < 10; ++mi)
+      if (ko[mi] >= 0) S.L[ko[mi]] += kv[mi];
+    __threadfence_block();
     __syncwarp();
+    if (lane == 0) *(volatile int*)&sh.turn = k + 1;
   }
   __syncthreads();
 }
@@ -486,18 +435,127 @@ __device__ void sky_solve(const Sky& S, const double* rdiag, int n, double* x, c
   __syncthreads();
 }
 
+// Per contact / friction element: K = dt^2 J^T H J over its free DOFs, J the surface-vertex ->
+// DOF map (soft vertex: identity on its node; ABD vertex: [I, xi0 I, xi1 I, xi2 I] on the
+// body's translation and A-row nodes), stored as the lower triangle in dense order with the
+// element's node list (el_K / el_kn), so the assembly only adds entries (solver.py:542-586).
+// CTA per env, warp per element: T = H J then K = J^T T from per-DOF slot tables.
+struct KWS {
+  double H[144];
+  double kx[12];   // affine-slot material coordinates
+  double kj[96];   // per DOF: the 4 slot coefficients of its J column
+  double kt[288];  // H J (12 x nd)
+  int kr[96];      // ... and the H rows they pick
+  int kc[4];       // slot codes (sv_code)
+  int kn[8];       // node list (dense positions, ascending)
+  int knn;
+};
+
+__global__ void __launch_bounds__(NT) k_contact_K(Dev D, const int* list) {
+  __shared__ KWS ws[NWARP];
+  const int e = list[blockIdx.x];
+  if (D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  KWS& w = ws[warp];
+  const int s0 = D.sv_off[e];
+  const size_t elbase = (size_t)e * D.cap_el;
+  const int na = D.n_act[e], nce = na + D.n_anc[e];
+  const double dt = P_(D, e)[GRIP_P_DT], dt2 = dt * dt;
+  for (int k = warp; k < nce; k += NWARP) {
+    const int kk = k < na ? k : D.cap_act + (k - na);
+    const size_t slot = elbase + D.max_tet + D.max_abd + kk;
+    const size_t cs = (size_t)e * (D.cap_act + D.cap_anc) + kk;
+    for (int t = lane; t < 144; t += 32) w.H[t] = D.el_H[slot * 144 + t];
+    const int src = lane < 12 ? lane / 3 : 0;
+    const int g = s0 + D.el_idx[slot * 4 + src];
+    const int cd = D.sv_code[g];   // affine: translation node, A rows follow
+    const double xv = lane < 12 ? D.sv_xi[3 * (size_t)g + lane % 3] : 0.0;
+    const int kcv = __shfl_sync(0xffffffffu, cd, lane < 4 ? 3 * lane : 0);
+    if (lane < 4) w.kc[lane] = kcv;
+    if (lane < 12) w.kx[lane] = (cd >= 0 && (cd & 3)) ? xv : 0.0;
+    __syncwarp();
+    if (lane == 0) {
+      int m = 0;
+      for (int u = 0; u < 4; ++u) {
+        const int c = w.kc[u];
+        if (c < 0) continue;
+        const int P = c >> 2, cnt = (c & 3) ? 4 : 1;
+        bool have = false;
+        for (int r = 0; r < m; ++r) have |= w.kn[r] == P;
+        if (have) continue;   // second slot on the same affine body (or the same node)
+        for (int q = 0; q < cnt; ++q) w.kn[m++] = P + q;
+      }
+      w.knn = m;
+    }
+    __syncwarp();
+    const int nn = w.knn;
+    {
+      const int my = lane < nn ? w.kn[lane] : 0;
+      int rank = 0;
+      for (int q = 0; q < nn; ++q) rank += w.kn[q] < my;
+      __syncwarp();
+      if (lane < nn) w.kn[rank] = my;
+      __syncwarp();
+    }
+    const int nd = 3 * nn, ne = nd * (nd + 1) / 2;
+    if (lane < nd) {   // J column of DOF lane: per slot the H row it picks and its coefficient
+      const int Nr = w.kn[lane / 3], cr = lane % 3;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = w.kc[u];
+        int row = 0;
+        double cf = 0.0;
+        if (c >= 0) {
+          const int o = Nr - (c >> 2);
+          if ((c & 3) == 0) {
+            if (o == 0) { row = 3 * u + cr; cf = 1.0; }
+          } else if (o == 0) {
+            row = 3 * u + cr; cf = 1.0;
+          } else if (o >= 1 && o <= 3) {
+            row = 3 * u + o - 1; cf = w.kx[3 * u + cr];
+          }
+        }
+        w.kj[4 * lane + u] = cf;
+        w.kr[4 * lane + u] = row;
+      }
+    }
+    __syncwarp();
+    double* kt = w.kt;
+    for (int t = lane; t < 12 * nd; t += 32) {   // T = H J
+      const int a = t / nd, d = t - a * nd;
+      double v = 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v += w.kj[4 * d + u] * w.H[12 * a + w.kr[4 * d + u]];
+      kt[t] = v;
+    }
+    __syncwarp();
+    double* Ko = D.el_K + cs * 300;
+    for (int t = lane; t < ne; t += 32) {        // K = J^T T, lower triangle
+      int r = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+      while ((r + 1) * (r + 2) / 2 <= t) ++r;
+      while (r * (r + 1) / 2 > t) --r;
+      const int q = t - r * (r + 1) / 2;
+      double v = 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v += w.kj[4 * r + u] * kt[w.kr[4 * r + u] * nd + q];
+      Ko[t] = dt2 * v;
+    }
+    if (lane < 9) D.el_kn[cs * 9 + lane] = lane == 0 ? nn : (lane - 1 < nn ? w.kn[lane - 1] : -1);
+    __syncwarp();
+  }
+}
+
 extern __shared__ double dyn_smem[];
 
 #ifdef GRIP_PHASE_TIMING
-__device__ unsigned long long g_phase[16];
-#define PHASE(k)                                                   \
-  do {                                                             \
-    __syncthreads();                                               \
-    if (threadIdx.x == 0) {                                        \
-      const long long t = clock64();                               \
-      atomicAdd(&g_phase[k], (unsigned long long)(t - t_last));    \
-      t_last = t;                                                  \
-    }                                                              \
+#define PHASE(k)                                  \
+  do {                                            \
+    __syncthreads();                              \
+    if (threadIdx.x == 0) {                       \
+      const long long t = clock64();              \
+      ph[k] += t - t_last;                        \
+      t_last = t;                                 \
+    }                                             \
   } while (0)
 #else
 #define PHASE(k) do {} while (0)
@@ -515,7 +573,7 @@ __global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* lis
   const double dt = P[GRIP_P_DT], dt2 = dt * dt;
   double Etot = 0.0;
 #ifdef GRIP_PHASE_TIMING
-  long long t_last = clock64();
+  long long t_last = clock64(), ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   if (!asm_prologue(D, E, A, dt2, &Etot)) return;
   PHASE(0);
@@ -563,10 +621,13 @@ __global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* lis
       if (threadIdx.x == 0) D.regularized[e] = 1;
       __syncthreads();
     }
-    sky_assemble(D, E, dt2, L, n, S);
+    sky_static(D, E, L, n);
     PHASE(1);
-    if (!sky_cholesky(L, rdiag, n, S)) continue;
+    sky_scatter_contacts(D, E, L, S);
     PHASE(2);
+    const bool chol_ok = sky_cholesky(L, rdiag, n, S);
+    PHASE(3);
+    if (!chol_ok) continue;
     for (int f = threadIdx.x; f < E.nf; f += NT)
       for (int c = 0; c < 3; ++c) xv[3 * perm[f] + c] = RHS[vb + 3 * f + c];
     __syncthreads();
@@ -574,7 +635,7 @@ __global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* lis
     for (int f = threadIdx.x; f < E.nf; f += NT)
       for (int c = 0; c < 3; ++c) X[vb + 3 * f + c] = xv[3 * perm[f] + c];
     __syncthreads();
-    PHASE(3);
+    PHASE(4);
     // refinement on the true residual (solver.py:117-122)
     int fin = 1;
     for (int i = threadIdx.x; i < n; i += NT) fin &= isfinite(X[vb + i]);
@@ -604,16 +665,29 @@ __global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* lis
     }
     solved = isfinite(r2) && r2 <= 1e-16 * bn2;
   }
-  PHASE(4);
+  PHASE(5);
   if (!solved) { fail_env(D, e, GRIP_R_SOLVE); return; }
   asm_converge(D, E, X, Etot, sm);
-  PHASE(5);
+  PHASE(6);
 #ifdef GRIP_PHASE_TIMING
   if (threadIdx.x == 0) {
-    atomicAdd(&g_phase[8], 1ull);
-    atomicAdd(&g_phase[9], (unsigned long long)n);
-    atomicAdd(&g_phase[10], (unsigned long long)(D.n_act[e] + D.n_anc[e]));
-    atomicAdd(&g_phase[11], (unsigned long long)(L.L == Lsm));
+    const int nce = D.n_act[e] + D.n_anc[e];
+    const bool heavy = nce > 128;
+    long long tot = 0;
+    for (int k = 0; k < 7; ++k) {
+      GSTAT(k, ph[k]);
+      if (heavy) GSTAT(16 + k, ph[k]);
+      tot += ph[k];
+    }
+    GSTAT(8, 1);
+    GSTAT(9, nce);
+    if (heavy) { GSTAT(24, 1); GSTAT(25, nce); }
+    atomicMax(&g_phase[40], (unsigned long long)tot);
+    atomicMax(&g_phase[41], (unsigned long long)nce);
+    GSTAT(42, L.L == Lsm);
+    GSTAT(43, S.nseg >= 2);
+    GSTAT(44, shift != 0.0);
+    if (S.nseg < 2) { GSTAT(45, ph[3]); GSTAT(46, 1); }
   }
 #endif
 }

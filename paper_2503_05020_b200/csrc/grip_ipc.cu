@@ -118,7 +118,13 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   ok &= swap_alloc(D.el_idx, E * D.cap_el * 4);
   ok &= swap_alloc(D.c_r, E * 12 * (D.cap_act + D.cap_anc));
   ok &= swap_alloc(D.inc, E * 4 * (D.cap_act + D.cap_anc));
-  ok &= swap_alloc(D.emap, E * 4 * (D.cap_act + D.cap_anc));
+  if (b->direct) {
+    ok &= swap_alloc(D.el_K, E * 300 * (D.cap_act + D.cap_anc));
+    ok &= swap_alloc(D.el_kn, E * 9 * (D.cap_act + D.cap_anc));
+  } else if (!D.el_K) {
+    ok &= swap_alloc(D.el_K, 1);
+    ok &= swap_alloc(D.el_kn, 1);
+  }
   ok &= swap_alloc(D.bp_tmp, E * std::max(D.cap_pt, D.cap_ee));
   ok &= swap_alloc(D.cs_pt, E * 4 * D.cap_pt);
   ok &= swap_alloc(D.cs_ee, E * 4 * D.cap_ee);
@@ -418,6 +424,17 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.free_node = b->upload(free_node.data(), std::max(NF, 1));
   D.dense_perm = b->upload(dense_perm.data(), std::max(NF, 1));
   D.dense_fc = b->upload(dense_fc.data(), std::max(NF, 1));
+  {   // per surface vertex: (dense node position << 2 | kind), -1 when it carries no free DOF
+    std::vector<int> sv_code(std::max(NS, 1), -1);
+    for (int e = 0; e < E; ++e)
+      for (int g = b->sv_off[e]; g < b->sv_off[e + 1]; ++g) {
+        const int kind = d->sv_kind[g];
+        if (kind == 2) continue;
+        const int f = node_fidx[b->node_off[e] + d->sv_node[g]];
+        if (f >= 0) sv_code[g] = (dense_perm[free_off[e] + f] << 2) | kind;
+      }
+    D.sv_code = b->upload(sv_code.data(), sv_code.size());
+  }
   D.dense_tail = b->upload(dense_tail.data(), E);
   D.sb_row = b->upload(sb_row.data(), sb_row.size());
   D.sv_kind = b->upload(d->sv_kind, NS);
@@ -548,6 +565,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.c_w = b->alloc<double>((size_t)E * 3 * max_sv);
   D.sv_g = b->alloc<double>((size_t)E * 3 * max_sv);
   D.inc_ptr = b->alloc<int>((size_t)E * (max_sv + 1));
+  D.dense_k = b->direct ? 1 : 0;
   if (alloc_dynamic(b, false, 0)) return -1;
   b->tet_env.resize(NTET);
   for (int e = 0; e < E; ++e)
@@ -577,7 +595,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.emap};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sv_code};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -679,8 +697,10 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
       k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
     kt_end(b, t);
     t = kt_begin(b, K_ASM);
-    if (b->direct)
+    if (b->direct) {
+      k_contact_K<<<n, NT, 0, b->stream>>>(D, b->d_list);
       k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, b->d_list, b->env_cap);
+    }
     else
       k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
     kt_end(b, t);
@@ -1055,7 +1075,7 @@ int grip_stream_timer(GripBatch* b, int start, double* ms) {
 
 #ifdef GRIP_PHASE_TIMING
 int grip_debug_phase(unsigned long long* out) {
-  CK(cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 16));
+  CK(cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * 64));
   return 0;
 }
 #endif

@@ -102,60 +102,85 @@ __device__ double w_power9(WarpWS& w, int lane) {
 
 // Jacobi eigendecomposition of the symmetric 9x9 w.S (-> diagonal), eigenvectors in w.V.
 // Round-robin ordering over 10 players (index 9 is a bye): every pair once per sweep.
+// Lane l owns entries l, l+32, l+64 of S and V (row/column indices precomputed).
+__device__ __constant__ signed char kRR[9][5][2] = {
+    {{0, 1}, {2, 9}, {3, 8}, {4, 7}, {5, 6}}, {{0, 2}, {3, 1}, {4, 9}, {5, 8}, {6, 7}},
+    {{0, 3}, {4, 2}, {5, 1}, {6, 9}, {7, 8}}, {{0, 4}, {5, 3}, {6, 2}, {7, 1}, {8, 9}},
+    {{0, 5}, {6, 4}, {7, 3}, {8, 2}, {9, 1}}, {{0, 6}, {7, 5}, {8, 4}, {9, 3}, {1, 2}},
+    {{0, 7}, {8, 6}, {9, 5}, {1, 4}, {2, 3}}, {{0, 8}, {9, 7}, {1, 6}, {2, 5}, {3, 4}},
+    {{0, 9}, {1, 8}, {2, 7}, {3, 6}, {4, 5}}};
+
 __device__ void w_jacobi9(WarpWS& w, int lane, bool init_identity = true) {
   if (init_identity) {
     for (int e = lane; e < 81; e += 32) w.V[e] = (e / 9 == e % 9) ? 1.0 : 0.0;
     __syncwarp();
   }
+  int ei[3], ej[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int e = lane + 32 * c;
+    ei[c] = e < 81 ? e / 9 : 0;
+    ej[c] = e < 81 ? e % 9 : 0;
+  }
+  const int nown = lane < 17 ? 3 : 2;   // 81 = 2*32 + 17
   for (int sweep = 0; sweep < 30; ++sweep) {
     double off = 0.0, tot = 0.0;
-    for (int e = lane; e < 81; e += 32) {
-      const double a2 = w.S[e] * w.S[e];
-      tot += a2;
-      if (e / 9 != e % 9) off += a2;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (c < nown) {
+        const double v = w.S[lane + 32 * c];
+        tot += v * v;
+        if (ei[c] != ej[c]) off += v * v;
+      }
     }
     off = wred_sum(off);
     tot = wred_sum(tot);
     if (off <= 1e-32 * tot || off == 0.0) break;
     for (int r = 0; r < 9; ++r) {
       if (lane < 5) {
-        int a = lane == 0 ? 0 : 1 + ((r + lane) % 9);
-        int b = lane == 0 ? 1 + (r % 9) : 1 + ((r + 9 - lane) % 9);
-        // map players 0..9 to indices; player 9 is the bye
+        const int a = kRR[r][lane][0], b = kRR[r][lane][1];
         const int p = min(a, b), q = max(a, b);
         if (q == 9) {
           w.al[p] = 1.0; w.be[p] = 0.0; w.pi[p] = p;
         } else {
           const double apq = w.S[p * 9 + q];
-          double c = 1.0, s = 0.0;
+          double c = 1.0, sn = 0.0;
           if (apq != 0.0) {
-            const double theta = (w.S[q * 9 + q] - w.S[p * 9 + p]) / (2.0 * apq);
-            const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-            c = 1.0 / sqrt(t * t + 1.0);
-            s = t * c;
+            // t = sgn(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (aqq - app) / (2 apq)
+            const double d = w.S[q * 9 + q] - w.S[p * 9 + p];
+            const double sg = ((d >= 0.0) == (apq > 0.0)) ? 1.0 : -1.0;
+            const double t = sg * 2.0 * fabs(apq) / (fabs(d) + sqrt(d * d + 4.0 * apq * apq));
+            c = rsqrt(t * t + 1.0);
+            sn = t * c;
           }
-          w.al[p] = c; w.be[p] = -s; w.pi[p] = q;
-          w.al[q] = c; w.be[q] = s; w.pi[q] = p;
+          w.al[p] = c; w.be[p] = -sn; w.pi[p] = q;
+          w.al[q] = c; w.be[q] = sn; w.pi[q] = p;
         }
       }
       __syncwarp();
       double ns[3], nv[3];
-      int cnt = 0;
-      for (int e = lane; e < 81; e += 32, ++cnt) {
-        const int i = e / 9, j = e % 9;
-        const double ai = w.al[i], bi = w.be[i], aj = w.al[j], bj = w.be[j];
-        const int pi_ = w.pi[i], pj = w.pi[j];
-        ns[cnt] = ai * aj * w.S[i * 9 + j] + ai * bj * w.S[i * 9 + pj] + bi * aj * w.S[pi_ * 9 + j] +
+      bool z[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (c < nown) {
+          const int i = ei[c], j = ej[c];
+          const double ai = w.al[i], bi = w.be[i], aj = w.al[j], bj = w.be[j];
+          const int pi_ = w.pi[i], pj = w.pi[j];
+          ns[c] = ai * aj * w.S[i * 9 + j] + ai * bj * w.S[i * 9 + pj] + bi * aj * w.S[pi_ * 9 + j] +
                   bi * bj * w.S[pi_ * 9 + pj];
-        nv[cnt] = aj * w.V[i * 9 + j] + bj * w.V[i * 9 + pj];
+          nv[c] = aj * w.V[i * 9 + j] + bj * w.V[i * 9 + pj];
+          // the rotated pair's off-diagonal is exactly zero after its rotation
+          z[c] = i != j && pi_ == j && bi != 0.0;
+        }
       }
       __syncwarp();
-      cnt = 0;
-      for (int e = lane; e < 81; e += 32, ++cnt) {
-        const int i = e / 9, j = e % 9;
-        // the rotated pair's off-diagonal is exactly zero after its rotation
-        w.S[e] = (i != j && w.pi[i] == j && w.be[i] != 0.0) ? 0.0 : ns[cnt];
-        w.V[e] = nv[cnt];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (c < nown) {
+          const int e = lane + 32 * c;
+          w.S[e] = z[c] ? 0.0 : ns[c];
+          w.V[e] = nv[c];
+        }
       }
       __syncwarp();
     }
@@ -210,10 +235,37 @@ __device__ void w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullp
   for (int e = lane; e < 81; e += 32) fro += w.S[e] * w.S[e];
   fro = sqrt(wred_sum(fro));
   double f;
+  bool pd = false;
   if (!Vwarm && w_chol_pd9(w, 1e-12 * fro, lane)) {
     f = 1e-12 * w_power9(w, lane);
-  } else {
-    if (Vwarm) w_rotate_into(w, Vwarm, lane);
+    pd = true;
+  } else if (Vwarm) {
+    // S~ = V0^T S V0 is near diagonal; when every Gershgorin disc of S~ lies above the clamp
+    // floor 1e-12 max|lambda|, no eigenvalue is clamped and H passes through unchanged
+    w_rotate_into(w, Vwarm, lane);
+    if (lane < 9) {
+      double rad = 0.0;
+      for (int j = 0; j < 9; ++j)
+        if (j != lane) rad += fabs(w.S[lane * 9 + j]);
+      const double dg = w.S[lane * 10];
+      w.sc[lane] = dg - rad;
+      w.sc[9 + lane] = dg + rad;
+      w.sc[18 + lane] = fabs(dg);
+    }
+    __syncwarp();
+    double lo = w.sc[0], hi = w.sc[9], dm = w.sc[18];
+    for (int k = 1; k < 9; ++k) {
+      lo = fmin(lo, w.sc[k]);
+      hi = fmax(hi, w.sc[9 + k]);
+      dm = fmax(dm, w.sc[18 + k]);
+    }
+    __syncwarp();
+    if (lo > 1e-12 * hi) {
+      f = 1e-12 * dm;
+      pd = true;
+    }
+  }
+  if (!pd) {
     w_jacobi9(w, lane, Vwarm == nullptr);
     if (Vout)
       for (int e = lane; e < 81; e += 32) Vout[e] = w.V[e];

@@ -8,11 +8,11 @@ import bench
 sys.argv = ["bench.py", "--no-cpu", "--steps", "100", "--warmup", "200"]
 bench.main()
 from paper_2503_05020_b200 import _native as nv
-out = (ctypes.c_ulonglong * 16)()
+out = (ctypes.c_ulonglong * 64)()
 assert nv._lib.grip_debug_phase(out) == 0
 v = np.array(list(out), float)
-names = ["prologue", "dense_assemble", "cholesky", "solve", "refine", "converge"]
-tot = v[:6].sum()
+names = ["prologue", "static", "scatter", "cholesky", "solve", "refine", "converge"]
+print(f"CTAs {v[8]:.0f} mean nce {v[9] / v[8]:.1f}  heavy(>128) CTAs {v[24]:.0f} mean nce {v[25] / max(v[24], 1):.1f}  max nce {v[41]:.0f}  max CTA cyc {v[40]:.0f}  smem {v[42]:.0f}")
 for k, nm in enumerate(names):
-    print(f"{nm:16s} {100 * v[k] / tot:5.1f}%  {v[k] / v[8]:10.0f} cyc/CTA")
-print("CTAs", v[8], "mean n", v[9] / v[8], "mean contact elems", v[10] / v[8], "regularized", v[11])
+    print(f"{nm:10s} all {v[k] / v[8]:10.0f}   heavy {v[16 + k] / max(v[24], 1):10.0f}")
+print("nseg>=2", v[43], "shifted", v[44], "chol cyc when nseg<2", v[45] / max(v[46], 1), v[46])
