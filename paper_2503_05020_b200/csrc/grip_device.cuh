@@ -295,6 +295,7 @@ __device__ __forceinline__ V3 sv_dir(const Dev& D, const EnvIx& E, int i, const 
 struct BPShared {
   int head[MAXC + 1];
   int cur[MAXC];
+  double bb[32][6];   // per-body surface AABB (culling: primitives far from every partner body)
 };
 
 struct Grid {
@@ -339,6 +340,7 @@ __device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells,
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += NT) {
     const double* b = aabb + 6 * i;
+    if (!(b[0] <= b[3])) continue;   // culled primitive
     int x0 = G.cx(b[0]), y0 = G.cy(b[1]), z0 = G.cz(b[2]);
     int x1 = G.cx(b[3]), y1 = G.cy(b[4]), z1 = G.cz(b[5]);
     for (int a = x0; a <= x1; ++a)
@@ -353,6 +355,7 @@ __device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells,
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += NT) {
     const double* b = aabb + 6 * i;
+    if (!(b[0] <= b[3])) continue;
     int x0 = G.cx(b[0]), y0 = G.cy(b[1]), z0 = G.cz(b[2]);
     int x1 = G.cx(b[3]), y1 = G.cy(b[4]), z1 = G.cz(b[5]);
     lc[3 * i] = x0; lc[3 * i + 1] = y0; lc[3 * i + 2] = z0;
@@ -409,6 +412,39 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
   }
   const uint32_t* pm = D.body_pairmask + E.b0;
   const int* vb = D.sv_body + E.s0;
+  // per-body AABBs: a primitive can only pair with bodies its pair mask allows, and every such
+  // pair needs the primitive's r-box to reach that body's AABB -> primitives (and query
+  // vertices) that reach no partner body are culled before the grid (membership unchanged)
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int b = warp; b < E.nb; b += NWARP) {
+      double l[3] = {INFINITY, INFINITY, INFINITY}, u[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int i = lane; i < E.ns; i += 32)
+        if (vb[i] == b)
+          for (int c = 0; c < 3; ++c) {
+            l[c] = fmin(l[c], X[3 * i + c]);
+            u[c] = fmax(u[c], X[3 * i + c]);
+          }
+      for (int c = 0; c < 3; ++c) {
+        l[c] = wmin(l[c]);
+        u[c] = wmax(u[c]);
+      }
+      if (lane == 0)
+        for (int c = 0; c < 3; ++c) { S.bb[b][c] = l[c]; S.bb[b][3 + c] = u[c]; }
+    }
+    __syncthreads();
+  }
+  // does box [l, u] inflated by rc reach a partner body of body bo (mask m)?
+  auto reaches = [&](const double* l, const double* u, uint32_t m, int bo, double rc) {
+    for (int b = 0; b < E.nb; ++b) {
+      if (!((m >> b) & 1u)) continue;
+      const double* q = S.bb[b];
+      if (l[0] - rc <= q[3] && l[1] - rc <= q[4] && l[2] - rc <= q[5] && u[0] + rc >= q[0] && u[1] + rc >= q[1] &&
+          u[2] + rc >= q[2])
+        return true;
+    }
+    return false;
+  };
   double h = fmax(r, D.cell_hint[E.e]);
   int npt = 0, nee = 0;
   bool ok = true;
@@ -434,6 +470,9 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
         V3 l = vmin(vmin(a, b), c), u = vmax(vmax(a, b), c);
         double* o = aabb + 6 * t;
         o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
+        const int bt = vb[tris[3 * t]];
+        const uint32_t m = pm[bt] & (((pm[bt] >> bt) & 1u) ? ~0u : ~(1u << bt));
+        if (!reaches(o, o + 3, m, bt, r + eps)) o[0] = INFINITY;   // culled
       }
       __syncthreads();
       if (!grid_build(G, aabb, E.nt, cells, lc, D.cap_cells, S, sm)) {
@@ -453,7 +492,9 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
             const int own_lo = selfc ? 0 : D.body_tri_lo[E.b0 + bv];
             const int own_hi = selfc ? 0 : D.body_tri_hi[E.b0 + bv];
             int count = 0;
-            for (int a = qx0; a <= qx1; ++a)
+            const double pv[3] = {p.x, p.y, p.z};
+            const bool live = reaches(pv, pv, okmask & (selfc ? ~0u : ~(1u << bv)), bv, r + eps);
+            for (int a = qx0; a <= (live ? qx1 : qx0 - 1); ++a)
               for (int bb = qy0; bb <= qy1; ++bb)
                 for (int c = qz0; c <= qz1; ++c) {
                   const int cell = (a * G.ny + bb) * G.nz + c;
@@ -512,12 +553,19 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
         V3 l = vmin(a, b), u = vmax(a, b);
         double* o = aabb + 6 * i;
         o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
+        const int be = vb[edges[2 * i]];
+        const uint32_t m = pm[be] & (((pm[be] >> be) & 1u) ? ~0u : ~(1u << be));
+        if (!reaches(o, o + 3, m, be, r + eps)) o[0] = INFINITY;   // culled
       }
       __syncthreads();
       if (!grid_build(G, aabb, E.ne, cells, lc, D.cap_cells, S, sm)) { h *= 2.0; continue; }
       for (int pass = 0; pass < 2; ++pass) {
         for (int i = threadIdx.x; i < E.ne; i += NT) {
           const double* bi = aabb + 6 * i;
+          if (!(bi[0] <= bi[3])) {   // culled: no partner body within reach
+            if (!pass) cnt[i] = 0;
+            continue;
+          }
           const double lx = bi[0] - r, ly = bi[1] - r, lz = bi[2] - r;
           const double ux = bi[3] + r, uy = bi[4] + r, uz = bi[5] + r;
           const int qx0 = G.cx(lx - eps), qy0 = G.cy(ly - eps), qz0 = G.cz(lz - eps);
