@@ -51,6 +51,22 @@ EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, 
             "anchors": 16 + 32 + 48 + 16 + 192 + EL_OUT}  # verts, gamma, T, lam/mu, x and x_prev
 
 
+def _ncu_traffic(kernel):
+    """dram read + write bytes per launch of `kernel` from the committed ncu --set full summary."""
+    p = ROOT / "profiles" / "r1_ncu_full_v2.json"
+    try:
+        for d in json.loads(p.read_text()):
+            if d["kernel"] == kernel:
+                tot = 0.0
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, unit = d[k].split()
+                    tot += float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+                return tot, f"{p.relative_to(ROOT)} (ncu --set full, one launch)"
+    except (OSError, KeyError, ValueError):
+        pass
+    return None, None
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -358,6 +374,8 @@ def main():
         u = ks["elements"]["units"]
         alg = sum(EL_BYTES[k] * u[k] for k in EL_BYTES)
         roof["achieved"] = alg / (ks["elements"]["ms"] / 1e3) / 1e9
+        roof["alg_bytes_per_launch"] = alg / max(ks["elements"]["launches"], 1)
+        roof["traffic"], roof["traffic_source"] = _ncu_traffic("k_elements_w")
     else:
         roof["achieved"] = None
     roof["frac"] = (roof["achieved"] / peak) if roof.get("achieved") else None
