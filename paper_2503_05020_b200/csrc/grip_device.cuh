@@ -43,6 +43,10 @@ struct Dev {
   const int* dense_fc;       // per env-dense position (global free offset): lowest statically coupled position
   const int* dense_tail;     // per env: first dense position of the hub (last) body
   const int* sb_row;         // per block: global free row
+  double* tet_S;             // per tet 45: warm-rotated S~ (upper) awaiting the batched eigensolve
+  double* tet_W;             // per tet 90: its eigenvalues (9) and rotation R (81, row-major)
+  int2* jac_list;            // (tet, element slot) of the tets whose clamp was deferred this sweep
+  int* jac_n;
   const int* sv_code;        // per surface vertex: dense node position << 2 | kind (0 soft, 1 affine), -1 none
   const uint8_t* sv_kind;
   const int* sv_node;

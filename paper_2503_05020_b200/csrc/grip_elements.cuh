@@ -283,7 +283,7 @@ GHD void edge_mollifier(double c, double eps_x, double* m, double* dm, double* d
 // contact elements (contact.py:178-344) -- energy, grad, SPD-projected Hessian
 // ---------------------------------------------------------------------------
 
-enum { EL_ACTIVE = 1, EL_BAD_D = 2, EL_INVERTED = 4 };
+enum { EL_ACTIVE = 1, EL_BAD_D = 2, EL_INVERTED = 4, EL_DEFERRED = 8 };
 
 // Point-triangle stencil x[0]=point, x[1..3]=triangle.  Returns EL_* flags.
 // Non-face regions keep only their gradient: the reference's _expand_rows writes

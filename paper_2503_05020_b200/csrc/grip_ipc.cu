@@ -13,6 +13,7 @@
 #include "grip_kernels.cuh"
 #include "grip_warp_elements.cuh"
 #include "grip_direct.cuh"
+#include "grip_tetclamp.cuh"
 
 using namespace grip;
 
@@ -454,6 +455,11 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
     for (int t = 0; t < std::max(NTET, 1); ++t)
       for (int k = 0; k < 9; ++k) eye[81 * (size_t)t + 10 * k] = 1.0;
     D.tet_eig = b->upload(eye.data(), eye.size());
+  D.tet_S = b->alloc<double>(45 * (size_t)std::max(NTET, 1));
+  D.tet_W = b->alloc<double>(90 * (size_t)std::max(NTET, 1));
+  D.jac_list = b->alloc<int2>((size_t)std::max(NTET, 1));
+  D.jac_n = b->alloc<int>(1);
+  CK(cudaFuncSetAttribute(k_tet_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 81 * TJ * (int)sizeof(double)));
   }
   D.abd_node = b->upload(d->abd_node, NA);
   D.abd_kV = b->upload(d->abd_kV, NA);
@@ -595,7 +601,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sv_code};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -691,8 +697,11 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     k_work_scan<<<1, NT, 0, b->stream>>>(D, b->d_list, n);
     kt_end(b, t);
     t = kt_begin(b, K_ELEM);
-    if (b->warp_elements)
+    if (b->warp_elements) {
       k_elements_w<<<148 * 4, EW * 32, 0, b->stream>>>(D, b->d_list, n);
+      k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D);
+      k_tet_finish<<<148 * 4, EW * 32, 0, b->stream>>>(D);
+    }
     else
       k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
     kt_end(b, t);

@@ -220,7 +220,10 @@ __device__ void w_rotate_into(WarpWS& w, const double* V0, int lane) {
 
 // reference clamp (materials.py:101-113) of a translation-invariant 4-point stencil Hessian in w.H
 // (Vwarm: previous eigenvectors of this element or null; Vout: where to keep the new ones)
-__device__ void w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullptr, double* Vout = nullptr) {
+// defer_S (tets, with Vwarm): when the eigensolve is needed, write the warm-rotated S~ (upper
+// triangle, 45) there and return true without clamping; k_tet_jacobi / k_tet_finish complete it
+__device__ bool w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullptr, double* Vout = nullptr,
+                                double* defer_S = nullptr) {
   for (int e = lane; e < 144; e += 32) {
     const int i = e / 12, j = e % 12;
     if (i < j) {
@@ -265,6 +268,15 @@ __device__ void w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullp
       pd = true;
     }
   }
+  if (!pd && Vwarm && defer_S) {
+    for (int q = lane; q < 45; q += 32) {
+      int i = 0, rem = q;
+      while (rem >= 9 - i) { rem -= 9 - i; ++i; }
+      defer_S[q] = w.S[i * 9 + i + rem];
+    }
+    __syncwarp();
+    return true;
+  }
   if (!pd) {
     w_jacobi9(w, lane, Vwarm == nullptr);
     if (Vout)
@@ -278,47 +290,34 @@ __device__ void w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullp
       w.sc[lane] = fmax(lk, f) - lk;
     }
     __syncwarp();
-    // C = V diag(d) V^T, written over S
-    for (int e = lane; e < 81; e += 32) {
-      const int i = e / 9, j = e % 9;
-      double s = 0.0;
+    // H += U diag(d) U^T with U = Q V (12x9): only the clamped eigenpairs (d_k != 0) contribute
+    for (int e = lane; e < 108; e += 32) {
+      const int r = e / 9, k = e - 9 * r, n = r / 3, a = r - 3 * n;
+      double u = 0.0;
+      if (w.sc[k] != 0.0)
+        for (int i = 0; i < 3; ++i) u += helmert(i, n) * w.V[(3 * i + a) * 9 + k];
+      w.T[e] = u;
+    }
+    __syncwarp();
+  }
+  // plus the reference's lifted translation modes (f/4 on equal components); both terms are
+  // symmetric and added to the mirrored entries identically, so H stays exactly symmetric
+  for (int t = lane; t < 78; t += 32) {
+    int i = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    while (i * (i + 1) / 2 > t) --i;
+    const int j = t - i * (i + 1) / 2;
+    double s = (i % 3 == j % 3) ? 0.25 * f : 0.0;
+    if (!pd)
       for (int k = 0; k < 9; ++k) {
         const double d = w.sc[k];
-        if (d != 0.0) s += d * w.V[i * 9 + k] * w.V[j * 9 + k];
+        if (d != 0.0) s += d * (w.T[i * 9 + k] * w.T[j * 9 + k]);
       }
-      w.S[e] = s;
-    }
-    __syncwarp();
-    // T = Q C (12x9)
-    for (int e = lane; e < 108; e += 32) {
-      const int ka = e / 9, c = e % 9, k = ka / 3, a = ka % 3;
-      double s = 0.0;
-      for (int i = 0; i < 3; ++i) s += helmert(i, k) * w.S[(3 * i + a) * 9 + c];
-      w.T[e] = s;
-    }
-    __syncwarp();
-    for (int e = lane; e < 144; e += 32) {
-      const int r = e / 12, lb = e % 12, l = lb / 3, b = lb % 3;
-      double s = 0.0;
-      for (int j = 0; j < 3; ++j) s += w.T[r * 9 + 3 * j + b] * helmert(j, l);
-      w.H[e] += s;
-    }
-    __syncwarp();
-  }
-  for (int e = lane; e < 144; e += 32) {
-    const int i = e / 12, j = e % 12;
-    if (i % 3 == j % 3) w.H[e] += 0.25 * f;
+    w.H[i * 12 + j] += s;
+    if (i != j) w.H[j * 12 + i] += s;
   }
   __syncwarp();
-  for (int e = lane; e < 144; e += 32) {
-    const int i = e / 12, j = e % 12;
-    if (i < j) {
-      const double v = 0.5 * (w.H[e] + w.H[j * 12 + i]);
-      w.H[e] = v;
-      w.H[j * 12 + i] = v;
-    }
-  }
-  __syncwarp();
+  return false;
 }
 
 // rank-one clamp: H = c g g^T + f (I - g g^T/|g|^2), f = 1e-12 c |g|^2 ; g in w.sc[0..11]

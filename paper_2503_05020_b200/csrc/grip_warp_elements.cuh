@@ -54,7 +54,7 @@ __device__ __constant__ double kEE_C[3][4] = {{-1, 0, 1, 0}, {-1, 1, 0, 0}, {0, 
 
 // ---- Neo-Hookean tet (materials.py:116-158); H[(m,c),(M,C)] = V0 [mu d_cC WW_mM + c2 WA_Mc WA_mC + c3 WA_mc WA_MC]
 __device__ int w_nh(WarpEl& W, const V3* x, const double* Dmi, double V0, double mu, double lam, double* E, int lane,
-                    double* Vtet = nullptr) {
+                    double* Vtet = nullptr, double* defer_S = nullptr) {
   double F[9];
   tet_F(x, Dmi, F);
   const double J = det3(F);
@@ -98,8 +98,7 @@ __device__ int w_nh(WarpEl& W, const V3* x, const double* Dmi, double V0, double
                    c3 * wa[3 * m + c] * wa[3 * M + C]);
   }
   __syncwarp();
-  w_clamp_stencil(ws_of(W), lane, Vtet, Vtet);
-  return 0;
+  return w_clamp_stencil(ws_of(W), lane, Vtet, Vtet, defer_S) ? EL_DEFERRED : 0;
 }
 
 // ---- point-triangle stencil (contact.py:178-211, 283-303)
@@ -365,7 +364,8 @@ __global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* lis
         x[j] = ld3(D.x + 3 * (size_t)(E.n0 + idx[j]));
       }
       const int fl = w_nh(W, x, D.tet_Dmi + 9 * (size_t)t, D.tet_V0[t], D.tet_mu[t], D.tet_lam[t], &Eel, lane,
-                          D.tet_eig + 81 * (size_t)t);
+                          D.tet_eig + 81 * (size_t)t, D.tet_S + 45 * (size_t)t);
+      if ((fl & EL_DEFERRED) && lane == 0) D.jac_list[atomicAdd(D.jac_n, 1)] = make_int2(t, (int)slot);
       if (fl & EL_INVERTED) {
         if (lane == 0) atomicOr(&D.flags[e], ERR_INVERTED);
         Eel = 0.0;
