@@ -47,6 +47,10 @@ struct Dev {
   double* tet_W;             // per tet 90: its eigenvalues (9) and rotation R (81, row-major)
   int2* jac_list;            // (tet, element slot) of the tets whose clamp was deferred this sweep
   int* jac_n;
+  double* cjac_S;            // contacts (cold clamps), per active slot env*cap_act + k: S (45)
+  double* cjac_W;            // ... eigenvalues + eigenvectors (90)
+  int2* cjac_list;           // (active slot, element slot)
+  int* cjac_n;
   const int* sv_code;        // per surface vertex: dense node position << 2 | kind (0 soft, 1 affine), -1 none
   const uint8_t* sv_kind;
   const int* sv_node;

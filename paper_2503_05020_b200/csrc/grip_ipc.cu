@@ -119,6 +119,10 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   ok &= swap_alloc(D.el_idx, E * D.cap_el * 4);
   ok &= swap_alloc(D.c_r, E * 12 * (D.cap_act + D.cap_anc));
   ok &= swap_alloc(D.inc, E * 4 * (D.cap_act + D.cap_anc));
+  ok &= swap_alloc(D.cjac_S, E * 45 * D.cap_act);
+  ok &= swap_alloc(D.cjac_W, E * 90 * D.cap_act);
+  ok &= swap_alloc(D.cjac_list, E * D.cap_act);
+  if (!D.cjac_n) ok &= swap_alloc(D.cjac_n, 1);
   if (b->direct) {
     ok &= swap_alloc(D.el_K, E * 300 * (D.cap_act + D.cap_anc));
     ok &= swap_alloc(D.el_kn, E * 9 * (D.cap_act + D.cap_anc));
@@ -601,7 +605,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -699,8 +703,10 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     t = kt_begin(b, K_ELEM);
     if (b->warp_elements) {
       k_elements_w<<<148 * 4, EW * 32, 0, b->stream>>>(D, b->d_list, n);
-      k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D);
-      k_tet_finish<<<148 * 4, EW * 32, 0, b->stream>>>(D);
+      k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+      k_tet_jacobi<<<148, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
+      k_tet_finish<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W, D.tet_eig);
+      k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
     }
     else
       k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);

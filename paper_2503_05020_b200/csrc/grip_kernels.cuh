@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
   ct = block_sum(ct, sm); ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
   if (threadIdx.x == 0) {
     D.work_off[n] = base;
-    *D.jac_n = 0;   // the element kernel appends deferred tet clamps
+    *D.jac_n = 0;   // the element kernel appends deferred tet / contact clamps
+    *D.cjac_n = 0;
     D.stats[0] += ct; D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;
   }
 }

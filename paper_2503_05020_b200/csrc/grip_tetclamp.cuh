@@ -68,13 +68,14 @@ __device__ __forceinline__ void jround(double* s, double* R, int tid) {
   if constexpr (A4 != 9 && B4 != 9) jrot<(A4 < B4 ? A4 : B4), (A4 < B4 ? B4 : A4)>(s, R, tid);
 }
 
-__global__ void __launch_bounds__(TJ) k_tet_jacobi(Dev D) {
+// list[i].x indexes the S (45) / W (90) scratch of the matrix
+__global__ void __launch_bounds__(TJ) k_tet_jacobi(const int2* list, const int* n_ptr, const double* Sbuf, double* Wbuf) {
   extern __shared__ double rsm[];   // R: [81][TJ]
-  const int n = *D.jac_n;
+  const int n = *n_ptr;
   const int tid = threadIdx.x;
   for (int idx = blockIdx.x * TJ + tid; idx < n; idx += gridDim.x * TJ) {
-    const int t = D.jac_list[idx].x;
-    const double* Sg = D.tet_S + 45 * (size_t)t;
+    const int t = list[idx].x;
+    const double* Sg = Sbuf + 45 * (size_t)t;
     double s[45];
 #pragma unroll
     for (int q = 0; q < 45; ++q) s[q] = Sg[q];
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(TJ) k_tet_jacobi(Dev D) {
       jround<3>(s, rsm, tid); jround<4>(s, rsm, tid); jround<5>(s, rsm, tid);
       jround<6>(s, rsm, tid); jround<7>(s, rsm, tid); jround<8>(s, rsm, tid);
     }
-    double* W = D.tet_W + 90 * (size_t)t;
+    double* W = Wbuf + 90 * (size_t)t;
 #pragma unroll
     for (int k = 0; k < 9; ++k) W[k] = s[up9(k, k)];
 #pragma unroll
@@ -104,21 +105,23 @@ __global__ void __launch_bounds__(TJ) k_tet_jacobi(Dev D) {
   }
 }
 
-__global__ void __launch_bounds__(EW * 32) k_tet_finish(Dev D) {
+// eig: the tets' warm-start eigenbases (V = V0 R is stored back), or null for cold matrices (V = R)
+__global__ void __launch_bounds__(EW * 32) k_tet_finish(Dev D, const int2* list, const int* n_ptr, const double* Wbuf,
+                                                        double* eig) {
   __shared__ WarpWS ws[EW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpWS& w = ws[warp];
-  const int n = *D.jac_n;
+  const int n = *n_ptr;
   for (int idx = blockIdx.x * EW + warp; idx < n; idx += gridDim.x * EW) {
-    const int2 it = D.jac_list[idx];
+    const int2 it = list[idx];
     const size_t t = it.x, slot = it.y;
     double* Hg = D.el_H + slot * 144;
-    const double* W = D.tet_W + 90 * t;
-    double* V0 = D.tet_eig + 81 * t;
+    const double* W = Wbuf + 90 * t;
+    double* V0 = eig ? eig + 81 * t : nullptr;
     for (int e = lane; e < 144; e += 32) w.H[e] = Hg[e];
     for (int e = lane; e < 81; e += 32) {
-      w.S[e] = V0[e];       // V0
-      w.T[e] = W[9 + e];    // R
+      w.S[e] = V0 ? V0[e] : ((e / 9 == e % 9) ? 1.0 : 0.0);   // V0
+      w.T[e] = W[9 + e];                                     // R
     }
     double amax = 0.0;
     for (int k = 0; k < 9; ++k) amax = fmax(amax, fabs(W[k]));
@@ -135,7 +138,8 @@ __global__ void __launch_bounds__(EW * 32) k_tet_finish(Dev D) {
       w.V[e] = a;
     }
     __syncwarp();
-    for (int e = lane; e < 81; e += 32) V0[e] = w.V[e];
+    if (V0)
+      for (int e = lane; e < 81; e += 32) V0[e] = w.V[e];
     for (int e = lane; e < 108; e += 32) {  // U = Q V, clamped columns only
       const int r = e / 9, k = e - 9 * r, nd = r / 3, a = r - 3 * nd;
       double u = 0.0;

@@ -102,7 +102,7 @@ __device__ int w_nh(WarpEl& W, const V3* x, const double* Dmi, double V0, double
 }
 
 // ---- point-triangle stencil (contact.py:178-211, 283-303)
-__device__ int w_pt(WarpEl& W, const V3* x, double kappa, double dhat, double* E, int lane) {
+__device__ int w_pt(WarpEl& W, const V3* x, double kappa, double dhat, double* E, int lane, double* defer_S = nullptr) {
   double bary[3];
   int reg;
   const double D = pt_closest(x[0], x[1], x[2], x[3], bary, &reg);
@@ -133,7 +133,7 @@ __device__ int w_pt(WarpEl& W, const V3* x, double kappa, double dhat, double* E
       W.H[e] = kappa * (f2 * W.sc[i] * W.sc[j] + f1 * W.H[e]);
     }
     __syncwarp();
-    w_clamp_stencil(ws_of(W), lane);
+    if (w_clamp_stencil(ws_of(W), lane, nullptr, nullptr, defer_S)) return EL_ACTIVE | EL_DEFERRED;
   } else {
     w_rank1(ws_of(W), kappa * f2, lane);
   }
@@ -141,7 +141,8 @@ __device__ int w_pt(WarpEl& W, const V3* x, double kappa, double dhat, double* E
 }
 
 // ---- edge-edge stencil with the parallel mollifier (contact.py:213-269, 305-340)
-__device__ int w_ee(WarpEl& W, const V3* x, double eps_x, double kappa, double dhat, double* E, int lane) {
+__device__ int w_ee(WarpEl& W, const V3* x, double eps_x, double kappa, double dhat, double* E, int lane,
+                    double* defer_S = nullptr) {
   double s, t;
   const double D = ee_closest(x[0], x[1], x[2], x[3], &s, &t);
   if (!(D > 0.0)) return EL_BAD_D;
@@ -204,7 +205,7 @@ __device__ int w_ee(WarpEl& W, const V3* x, double eps_x, double kappa, double d
     W.H[e] = kappa * (m * hb + b * hm + dm * ci * f1 * gj + f1 * gi * dm * cj);
   }
   __syncwarp();
-  w_clamp_stencil(ws_of(W), lane);
+  if (w_clamp_stencil(ws_of(W), lane, nullptr, nullptr, defer_S)) return EL_ACTIVE | EL_DEFERRED;
   return EL_ACTIVE;
 }
 
@@ -390,13 +391,17 @@ __global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* lis
         idx[j] = row[j];
         x[j] = ld3(D.sv_pos + 3 * (size_t)(E.s0 + idx[j]));
       }
+      const size_t cs = (size_t)e * D.cap_act + k;
+      double* dS = D.cjac_S + 45 * cs;
+      int fl;
       if (is_ee) {
         const int* eid = D.c1_eid + ((size_t)e * D.cap_ee + (code - D.cap_pt)) * 2;
         const double epsx = D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]];
-        w_ee(W, x, epsx, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, lane);
+        fl = w_ee(W, x, epsx, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, lane, dS);
       } else {
-        w_pt(W, x, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, lane);
+        fl = w_pt(W, x, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, lane, dS);
       }
+      if ((fl & EL_DEFERRED) && lane == 0) D.cjac_list[atomicAdd(D.cjac_n, 1)] = make_int2((int)cs, (int)slot);
     } else {
       k -= D.n_act[e];
       slot = elbase + D.max_tet + D.max_abd + D.cap_act + k;
