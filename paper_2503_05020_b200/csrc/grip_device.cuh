@@ -25,7 +25,7 @@ constexpr int NWARP = NT / 32;
 constexpr int MAXC = 4096;        // broad-phase grid cells per env
 
 // error / flag bits per env and Newton sweep
-enum { ERR_INVERTED = 1, ERR_CONTACT_D = 2, FLAG_OVERFLOW = 4 };
+enum { ERR_INVERTED = 1, ERR_CONTACT_D = 2, FLAG_OVERFLOW = 4, FLAG_OVF_BEGIN = 8, FLAG_OVF_FIN = 16 };  // OVF_*: stage
 
 struct Dev {
   int n_env;

@@ -52,6 +52,15 @@ struct GripBatch {
   int* d_list2 = nullptr;
   int* d_tet_env = nullptr;
   int* h_pin = nullptr;         // pinned small readbacks
+  int* h_lists = nullptr;       // pinned: round lists (begin | iterating), 2 n_env
+  // pinned per-round snapshot: everything the host reads after a round, one D2H batch
+  char* h_snap = nullptr;
+  int *s_flags = nullptr, *s_done = nullptr, *s_st = nullptr, *s_rs = nullptr, *s_it = nullptr, *s_kb = nullptr,
+      *s_rg = nullptr, *s_si = nullptr, *s_nc = nullptr, *s_pi = nullptr;
+  double *s_res = nullptr, *s_md = nullptr, *s_en = nullptr, *s_tm = nullptr, *s_alpha = nullptr, *s_force = nullptr,
+         *s_com = nullptr, *s_speed = nullptr;
+  uint32_t* s_cmask = nullptr;
+  bool snap_valid = false;      // snapshot equals device state (no state change since the round)
   int max_it = 100;
   double last_ms = 0.0;
   long long launches = 0, sweeps = 0;
@@ -584,6 +593,23 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   b->d_list = b->alloc<int>(E + 1);
   b->d_list2 = b->alloc<int>(E + 1);
   CK(cudaMallocHost(&b->h_pin, 64 * sizeof(int)));
+  CK(cudaMallocHost(&b->h_lists, 2 * sizeof(int) * std::max(b->n_env, 1)));
+  {
+    const size_t E = std::max(b->n_env, 1), NBd = std::max(b->n_body, 1), A = std::max(b->D.max_alpha, 1);
+    const size_t bytes = 10 * 4 * E + (8 * E + A * E + NBd + 3 * NBd) * 8 + 4 * NBd + 64;
+    CK(cudaMallocHost(&b->h_snap, bytes));
+    char* q = b->h_snap;
+    auto take = [&](auto*& ptr, size_t n) {
+      using T = std::remove_reference_t<decltype(*ptr)>;
+      q = (char*)(((uintptr_t)q + 7) & ~(uintptr_t)7);
+      ptr = reinterpret_cast<T*>(q);
+      q += n * sizeof(T);
+    };
+    take(b->s_res, E); take(b->s_md, E); take(b->s_en, E); take(b->s_tm, E); take(b->s_alpha, A * E);
+    take(b->s_force, NBd); take(b->s_com, 3 * NBd); take(b->s_speed, E);
+    take(b->s_flags, E); take(b->s_done, E); take(b->s_st, E); take(b->s_rs, E); take(b->s_it, E); take(b->s_kb, E);
+    take(b->s_rg, E); take(b->s_si, E); take(b->s_nc, E); take(b->s_pi, E); take(b->s_cmask, NBd);
+  }
   for (void* p : b->owned)
     if (!p) {
       g_err = "out of device memory";
@@ -626,6 +652,8 @@ int grip_destroy(GripBatch* b) {
   if (b->r0) cudaEventDestroy(b->r0);
   if (b->r1) cudaEventDestroy(b->r1);
   if (b->h_pin) cudaFreeHost(b->h_pin);
+  if (b->h_lists) cudaFreeHost(b->h_lists);
+  if (b->h_snap) cudaFreeHost(b->h_snap);
   cudaEventDestroy(b->ev0);
   cudaEventDestroy(b->ev1);
   cudaStreamDestroy(b->stream);
@@ -648,6 +676,7 @@ static std::vector<int> mask_to_list(const GripBatch* b, const uint8_t* m) {
 }
 
 int grip_begin_step(GripBatch* b, const uint8_t* active) {
+  b->snap_valid = false;
   std::vector<int> L = mask_to_list(b, active);
   if (L.empty()) return 0;
   if (upload_list(b, L, b->d_list)) return -1;
@@ -759,6 +788,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
 }
 
 int grip_newton_iteration(GripBatch* b, uint8_t* pending) {
+  b->snap_valid = false;
   std::vector<int> L = mask_to_list(b, pending);
   if (L.empty()) return 0;
   if (upload_list(b, L, b->d_list)) return -1;
@@ -813,6 +843,7 @@ static int read_reports(GripBatch* b, const std::vector<int>& L, GripStepReport*
 }
 
 int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas) {
+  b->snap_valid = false;
   std::vector<int> L = mask_to_list(b, active);
   if (L.empty()) return 0;
   if (upload_list(b, L, b->d_list)) return -1;
@@ -823,6 +854,7 @@ int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* repo
 }
 
 int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas) {
+  b->snap_valid = false;
   std::vector<int> L = mask_to_list(b, active);
   if (L.empty()) return 0;
   const long long l0 = b->launches;
@@ -868,56 +900,170 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
   return 0;
 }
 
+// the sweep kernels over a device list of n envs, no host synchronisation
+static void sweep_launch(GripBatch* b, int n, const int* list) {
+  Dev& D = b->D;
+  int t = kt_begin(b, K_CAND);
+  k_candidates<<<n, NT, 0, b->stream>>>(D, list);
+  kt_end(b, t);
+  t = kt_begin(b, K_SCAN);
+  k_work_scan<<<1, NT, 0, b->stream>>>(D, list, n);
+  kt_end(b, t);
+  t = kt_begin(b, K_ELEM);
+  if (b->warp_elements) {
+    k_elements_w<<<148 * 4, EW * 32, 0, b->stream>>>(D, list, n);
+    k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+    k_tet_jacobi<<<148, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
+    k_tet_finish<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W, D.tet_eig);
+    k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
+  } else {
+    k_elements<<<148 * 8, 128, 0, b->stream>>>(D, list, n);
+  }
+  kt_end(b, t);
+  t = kt_begin(b, K_ASM);
+  if (b->direct) {
+    k_contact_K<<<n, NT, 0, b->stream>>>(D, list);
+    k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
+  } else {
+    k_assemble_solve<<<n, NT, 0, b->stream>>>(D, list);
+  }
+  kt_end(b, t);
+  t = kt_begin(b, K_LS);
+  k_linesearch<<<n, NT, 0, b->stream>>>(D, list);
+  kt_end(b, t);
+  b->launches += 5;
+  b->sweeps += 1;
+}
+
+// queue the D2H copies of everything the host reads after a round into the pinned snapshot
+static int snapshot_async(GripBatch* b) {
+  Dev& D = b->D;
+  const size_t E = b->n_env, NBd = b->n_body;
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, b->stream);
+  };
+  CK(cp(b->s_flags, D.flags, 4 * E));
+  CK(cp(b->s_done, D.ns_done, 4 * E));
+  CK(cp(b->s_st, D.ns_status, 4 * E));
+  CK(cp(b->s_rs, D.reason, 4 * E));
+  CK(cp(b->s_it, D.iters, 4 * E));
+  CK(cp(b->s_kb, D.kin_blocked, 4 * E));
+  CK(cp(b->s_rg, D.regularized, 4 * E));
+  CK(cp(b->s_si, D.step_index, 4 * E));
+  CK(cp(b->s_nc, D.newton_calls, 4 * E));
+  CK(cp(b->s_pi, D.pcg_iters, 4 * E));
+  CK(cp(b->s_res, D.residual, 8 * E));
+  CK(cp(b->s_md, D.min_dist, 8 * E));
+  CK(cp(b->s_en, D.energy, 8 * E));
+  CK(cp(b->s_tm, D.time, 8 * E));
+  CK(cp(b->s_alpha, D.alphas, 8 * E * D.max_alpha));
+  CK(cp(b->s_force, D.body_force, 8 * NBd));
+  CK(cp(b->s_cmask, D.contact_mask, 4 * NBd));
+  CK(cp(b->s_com, D.body_com, 24 * NBd));
+  CK(cp(b->s_speed, D.max_speed, 8 * E));
+  return 0;
+}
+
 // One continuous-batching round: begin_step for envs in `begin` (their controls must be set),
 // one Newton sweep over every unfinished env in begin|iter, finalize for every env that finished
 // in this round.  finalized[e] is set for those envs and reports[e] filled.
+//
+// The round is one queue of launches over device lists and one synchronisation: the envs
+// that overflowed a buffer (flagged, state untouched) are redone after growth on the
+// synchronous per-stage path (rare: capacities only grow early in a run).
 int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t* finalized, GripStepReport* reports,
                double* alphas) {
   Dev& D = b->D;
-  std::vector<int> B, L;
-  for (int e = 0; e < b->n_env; ++e) {
-    if (begin && begin[e]) B.push_back(e);
-    if ((begin && begin[e]) || (iter && iter[e])) L.push_back(e);
+  b->snap_valid = false;
+  const int E = b->n_env;
+  int nb = 0, n = 0;
+  for (int e = 0; e < E; ++e) {
+    if (begin && begin[e]) b->h_lists[nb++] = e;
+    if ((begin && begin[e]) || (iter && iter[e])) b->h_lists[E + n++] = e;
   }
-  if (finalized) memset(finalized, 0, b->n_env);
-  if (L.empty()) return 0;
-  if (!B.empty()) {
-    if (upload_list(b, B, b->d_list)) return -1;
-    const int nb = (int)B.size();
-    if (run_with_growth(b, nb, [&] {
-          int t = kt_begin(b, K_BEGIN);
-          k_begin<<<nb, NT, 0, b->stream>>>(D, b->d_list);
-          kt_end(b, t);
-        }))
-      return -1;
-    kt_collect(b);
+  if (finalized) memset(finalized, 0, E);
+  if (n == 0) return 0;
+  if (nb) CK(cudaMemcpyAsync(b->d_list, b->h_lists, sizeof(int) * nb, cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(b->d_list2, b->h_lists + E, sizeof(int) * n, cudaMemcpyHostToDevice, b->stream));
+  if (nb) {
+    const int t = kt_begin(b, K_BEGIN);
+    k_begin<<<nb, NT, 0, b->stream>>>(D, b->d_list);
+    kt_end(b, t);
+    b->launches++;
   }
-  if (upload_list(b, L, b->d_list)) return -1;
-  int n2 = 0;
-  if (newton_sweep(b, (int)L.size(), &n2)) return -1;   // leaves still-pending envs in d_list
-  if (upload_list(b, L, b->d_list)) return -1;
-  const int n = (int)L.size();
-  if (run_with_growth(b, n, [&] {
-        int t = kt_begin(b, K_FIN);
-        k_finalize<<<n, NT, 0, b->stream>>>(D, b->d_list, 1);
-        kt_end(b, t);
-      }))
-    return -1;
-  kt_collect(b);
-  std::vector<int> done(b->n_env);
-  CK(cudaMemcpyAsync(done.data(), D.ns_done, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+  sweep_launch(b, n, b->d_list2);
+  {
+    const int t = kt_begin(b, K_FIN);
+    k_finalize<<<n, NT, 0, b->stream>>>(D, b->d_list2, 1);
+    kt_end(b, t);
+    b->launches++;
+  }
+  CK(cudaGetLastError());
+  if (snapshot_async(b)) return -1;
   CK(cudaStreamSynchronize(b->stream));
-  std::vector<int> F;
-  for (int e : L)
-    if (done[e]) F.push_back(e);
-  for (int e : F)
+  kt_collect(b, n);
+  const std::vector<int> L(b->h_lists + E, b->h_lists + E + n);
+  std::vector<int> ovB, ovS, ovF;
+  for (int e : L) {
+    const int fl = b->s_flags[e];
+    if (!(fl & FLAG_OVERFLOW)) continue;
+    if (fl & FLAG_OVF_BEGIN) ovB.push_back(e);
+    else if (fl & FLAG_OVF_FIN) ovF.push_back(e);
+    else ovS.push_back(e);
+  }
+  if (!ovB.empty() || !ovS.empty() || !ovF.empty()) {
+    if (grow(b)) return -1;
+    CK(cudaMemsetAsync(D.flags, 0, sizeof(int) * E, b->stream));
+    if (!ovB.empty()) {
+      if (upload_list(b, ovB, b->d_list)) return -1;
+      const int m = (int)ovB.size();
+      if (run_with_growth(b, m, [&] { k_begin<<<m, NT, 0, b->stream>>>(D, b->d_list); })) return -1;
+    }
+    std::vector<int> S2 = ovB;
+    S2.insert(S2.end(), ovS.begin(), ovS.end());
+    std::sort(S2.begin(), S2.end());
+    if (!S2.empty()) {
+      if (upload_list(b, S2, b->d_list)) return -1;
+      int n2 = 0;
+      if (newton_sweep(b, (int)S2.size(), &n2)) return -1;
+    }
+    std::vector<int> F2 = S2;
+    F2.insert(F2.end(), ovF.begin(), ovF.end());
+    std::sort(F2.begin(), F2.end());
+    if (upload_list(b, F2, b->d_list)) return -1;
+    const int m = (int)F2.size();
+    if (run_with_growth(b, m, [&] { k_finalize<<<m, NT, 0, b->stream>>>(D, b->d_list, 1); })) return -1;
+    kt_collect(b);
+    if (snapshot_async(b)) return -1;
+    CK(cudaStreamSynchronize(b->stream));
+  }
+  b->snap_valid = true;
+  for (int e : L) {
+    if (!b->s_done[e]) continue;
     if (finalized) finalized[e] = 1;
-  if (reports && !F.empty()) return read_reports(b, F, reports, alphas);
+    if (!reports) continue;
+    GripStepReport& r = reports[e];
+    r.status = b->s_st[e];
+    r.reason = b->s_rs[e];
+    r.iterations = b->s_it[e];
+    r.n_alphas = std::min(b->s_it[e], D.max_alpha);
+    r.residual = b->s_res[e];
+    r.min_distance = b->s_md[e];
+    r.energy = b->s_en[e];
+    r.step_index = b->s_si[e] - 1;
+    r.time = b->s_tm[e];
+    r.kinematic_blocked = b->s_kb[e];
+    r.regularized = b->s_rg[e];
+    r.newton_calls = b->s_nc[e];
+    r.pcg_iters = b->s_pi[e];
+  }
+  if (alphas) memcpy(alphas, b->s_alpha, sizeof(double) * (size_t)E * D.max_alpha);
   return 0;
 }
 
 int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
                     const double* tet_Dmi, const double* tet_V0) {
+  b->snap_valid = false;
   Dev& D = b->D;
   auto cp = [&](double* dst, const double* src, size_t off, size_t n) {
     return cudaMemcpyAsync(dst + off, src + off, n * sizeof(double), cudaMemcpyHostToDevice, b->stream);
@@ -978,6 +1124,7 @@ int grip_get_state(GripBatch* b, double* x, double* v, double* kin) {
 }
 
 int grip_set_state(GripBatch* b, const double* x, const double* v, const double* kin) {
+  b->snap_valid = false;
   CK(cudaMemsetAsync(b->D.cs_valid, 0, sizeof(int) * b->n_env, b->stream));
   if (x) CK(cudaMemcpyAsync(b->D.x, x, 3 * sizeof(double) * b->n_node, cudaMemcpyHostToDevice, b->stream));
   if (v) CK(cudaMemcpyAsync(b->D.v, v, 3 * sizeof(double) * b->n_node, cudaMemcpyHostToDevice, b->stream));
@@ -998,6 +1145,12 @@ int grip_get_surface(GripBatch* b, double* sv) {
 }
 
 int grip_get_contacts(GripBatch* b, double* body_force, uint32_t* contact_mask, double* min_distance) {
+  if (b->snap_valid) {   // unchanged since the round's snapshot
+    if (body_force) memcpy(body_force, b->s_force, sizeof(double) * b->n_body);
+    if (contact_mask) memcpy(contact_mask, b->s_cmask, sizeof(uint32_t) * b->n_body);
+    if (min_distance) memcpy(min_distance, b->s_md, sizeof(double) * b->n_env);
+    return 0;
+  }
   if (body_force) CK(cudaMemcpyAsync(body_force, b->D.body_force, sizeof(double) * b->n_body, cudaMemcpyDeviceToHost, b->stream));
   if (contact_mask)
     CK(cudaMemcpyAsync(contact_mask, b->D.contact_mask, sizeof(uint32_t) * b->n_body, cudaMemcpyDeviceToHost, b->stream));
@@ -1043,6 +1196,11 @@ int grip_stress(GripBatch* b, double* out) {
 }
 
 int grip_get_body_state(GripBatch* b, double* body_com, double* max_speed) {
+  if (b->snap_valid) {
+    if (body_com) memcpy(body_com, b->s_com, 3 * sizeof(double) * b->n_body);
+    if (max_speed) memcpy(max_speed, b->s_speed, sizeof(double) * b->n_env);
+    return 0;
+  }
   if (body_com) CK(cudaMemcpyAsync(body_com, b->D.body_com, 3 * sizeof(double) * b->n_body, cudaMemcpyDeviceToHost, b->stream));
   if (max_speed) CK(cudaMemcpyAsync(max_speed, b->D.max_speed, sizeof(double) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
                            D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, sm);
     } else if (!broad_phase_env(D, E, rk, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
                                 D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm)) {
-      if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+      if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_BEGIN;
       return;
     }
     if (cn[0] + cn[1] > 0) {
@@ -228,7 +228,11 @@ __global__ void __launch_bounds__(NT) k_candidates(Dev D, const int* list) {
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dhat = P[GRIP_P_DHAT];
-  if (D.ns_done[e]) return;  // finished (or failed in begin_step) envs of a round list
+  // finished (or failed in begin_step) envs of a round list; an env whose begin_step overflowed
+  // this round keeps its flag and is re-run by the host after growth
+  const bool skip = D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW);
+  __syncthreads();
+  if (skip) return;
   if (threadIdx.x == 0) {
     D.flags[e] = 0;
     D.newton_calls[e] += 1;
@@ -1220,10 +1224,11 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   __shared__ BPShared S;
   __shared__ unsigned int cmask[32];
   const int e = list[blockIdx.x];
-  if (only_done && (!D.ns_done[e] || D.fin_done[e])) return;
+  if (only_done && (!D.ns_done[e] || D.fin_done[e] || (D.flags[e] & FLAG_OVERFLOW))) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
+  __syncthreads();
   if (threadIdx.x == 0) D.flags[e] = 0;
   // a failed step keeps x, v and the anchors (solver.py:736-738); the contact readout the
   // protocol does after every step (protocol.py:179-180) is still produced
@@ -1239,7 +1244,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   int* cee = D.c1_ee + (size_t)e * 4 * D.cap_ee;
   int* ceid = D.c1_eid + (size_t)e * 2 * D.cap_ee;
   if (!ensure_superset(D, E, 1.05 * dhat, dhat, S, sm)) {
-    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_FIN;
     return;
   }
   filter_from_superset(D, E, dhat * 1.05, cpt, cee, ceid, cn, sm);
@@ -1332,7 +1337,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
     base += tot;
   }
   if (base > D.cap_anc && !failed) {
-    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_FIN;
     return;
   }
   dmin = block_min(dmin, sm);

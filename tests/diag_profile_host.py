@@ -1,0 +1,11 @@
+import cProfile, pstats, sys, io
+sys.path.insert(0, '.')
+import bench
+sys.argv = ["bench.py", "--no-cpu", "--steps", "200", "--warmup", "100"]
+pr = cProfile.Profile()
+pr.enable()
+bench.main()
+pr.disable()
+s = io.StringIO()
+pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25)
+print(s.getvalue()[:6000])
