@@ -550,6 +550,11 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.cap_act = 512;
   D.cap_anc = 512;
   D.cap_cells = 32 * std::max(max_tri, max_edge) + 4096;
+  if (getenv("GRIP_SMALL_CAPS")) {   // test hook: start tiny so every growth / redo path runs
+    D.cap_pt = D.cap_ee = 8;
+    D.cap_act = D.cap_anc = 4;
+    D.cap_cells = 64;
+  }
   D.bp_aabb = b->alloc<double>((size_t)E * 6 * std::max(max_tri, max_edge));
   D.bp_cnt = b->alloc<int>((size_t)E * (std::max(max_sv, max_edge) + 1));
   D.pcg_x = b->alloc<double>((size_t)E * 3 * max_free);

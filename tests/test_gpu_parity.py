@@ -138,11 +138,15 @@ def test_stress_matches_oracle(golden):
     assert oen is not None
 
 
-@pytest.mark.parametrize("lockstep", [True, False])
-def test_protocol_labels_match_reference(golden, lockstep):
+@pytest.mark.parametrize("lockstep,small_caps", [(True, False), (False, False), (False, True)])
+def test_protocol_labels_match_reference(golden, lockstep, small_caps, monkeypatch):
     """Grasp labels (stable / unstable / sim-failed), step counts, halts and phase markers of the
     full protocol (protocol.py:152-277) on the reference's own seeds, all envs batched, in
-    lockstep (Batch.step semantics) and with continuous batching (grip_round)."""
+    lockstep (Batch.step semantics) and with continuous batching (grip_round).  small_caps starts
+    every candidate / contact / anchor / grid buffer tiny, so the rounds overflow and the
+    per-stage growth-and-redo path runs many times; the labels must not change."""
+    if small_caps:
+        monkeypatch.setenv("GRIP_SMALL_CAPS", "1")
     from paper_2503_05020_b200 import scene as sc
     from paper_2503_05020_b200.multienv import DeviceEnvGroup
     from paper_2503_05020_b200.protocol import BatchedGraspTrials
