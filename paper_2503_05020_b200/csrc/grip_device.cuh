@@ -115,6 +115,7 @@ struct Dev {
   double *el_E, *el_g, *el_H;
   int* el_idx;
   int* work_off;     // per list position (n+1)
+  int* cwork_off;    // per list position (n+1): contact / friction elements only
   // anchors (persist across steps)
   int* anc_v;        // 4
   double *anc_gamma, *anc_T, *anc_lam, *anc_mu;   // 4, 6, 1, 1

@@ -451,17 +451,24 @@ struct KWS {
   int knn;
 };
 
-__global__ void __launch_bounds__(NT) k_contact_K(Dev D, const int* list) {
+__global__ void __launch_bounds__(NT) k_contact_K(Dev D, const int* list, int n) {
   __shared__ KWS ws[NWARP];
-  const int e = list[blockIdx.x];
-  if (D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   KWS& w = ws[warp];
-  const int s0 = D.sv_off[e];
-  const size_t elbase = (size_t)e * D.cap_el;
-  const int na = D.n_act[e], nce = na + D.n_anc[e];
-  const double dt = P_(D, e)[GRIP_P_DT], dt2 = dt * dt;
-  for (int k = warp; k < nce; k += NWARP) {
+  const int total = D.cwork_off[n];
+  // flat over the contact elements of all listed envs (cwork_off from k_work_scan), warp each
+  for (int item = blockIdx.x * NWARP + warp; item < total; item += gridDim.x * NWARP) {
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (D.cwork_off[mid] <= item) lo = mid;
+      else hi = mid;
+    }
+    const int e = list[lo], k = item - D.cwork_off[lo];
+    const int s0 = D.sv_off[e];
+    const size_t elbase = (size_t)e * D.cap_el;
+    const int na = D.n_act[e];
+    const double dt = P_(D, e)[GRIP_P_DT], dt2 = dt * dt;
     const int kk = k < na ? k : D.cap_act + (k - na);
     const size_t slot = elbase + D.max_tet + D.max_abd + kk;
     const size_t cs = (size_t)e * (D.cap_act + D.cap_anc) + kk;

@@ -543,6 +543,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.n_act = b->alloc<int>(E);
   D.n_anc = b->alloc<int>(E);
   D.work_off = b->alloc<int>(E + 1);
+  D.cwork_off = b->alloc<int>(E + 1);
   D.max_sv = max_sv; D.max_tri = max_tri; D.max_edge = max_edge; D.max_free = max_free;
   D.max_node = max_node; D.max_tet = max_tet; D.max_abd = max_abd;
   D.cap_pt = std::max(2048, 16 * max_sv);
@@ -631,7 +632,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.surf_prev, D.kin_pos, D.sv_disp, D.ell, D.tol, D.residual, D.energy, D.alphas, D.min_dist, D.time, D.iters,
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
-        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.anc_v,
+        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
@@ -747,7 +748,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     kt_end(b, t);
     t = kt_begin(b, K_ASM);
     if (b->direct) {
-      k_contact_K<<<n, NT, 0, b->stream>>>(D, b->d_list);
+      k_contact_K<<<148 * 2, NT, 0, b->stream>>>(D, b->d_list, n);
       k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, b->d_list, b->env_cap);
     }
     else
@@ -927,7 +928,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   kt_end(b, t);
   t = kt_begin(b, K_ASM);
   if (b->direct) {
-    k_contact_K<<<n, NT, 0, b->stream>>>(D, list);
+    k_contact_K<<<148 * 2, NT, 0, b->stream>>>(D, list, n);
     k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
   } else {
     k_assemble_solve<<<n, NT, 0, b->stream>>>(D, list);

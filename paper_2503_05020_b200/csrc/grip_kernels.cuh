@@ -280,14 +280,16 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
   __shared__ Red sm;
   int base = 0;
   double ct = 0.0, ca = 0.0, cc = 0.0, cf = 0.0;
+  int cbase = 0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
-    int w = 0;
+    int w = 0, wc = 0;
     if (i < n) {
       const int e = list[i];
       if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e]) {
         const int nt = D.tet_off[e + 1] - D.tet_off[e], na = D.abd_off[e + 1] - D.abd_off[e];
-        w = nt + na + D.n_act[e] + D.n_anc[e];
+        wc = D.n_act[e] + D.n_anc[e];
+        w = nt + na + wc;
         ct += nt; ca += na; cc += D.n_act[e]; cf += D.n_anc[e];
       }
     }
@@ -295,10 +297,14 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
     const int pre = block_scan(w, sm, &tot);
     if (i < n) D.work_off[i] = base + pre;
     base += tot;
+    const int cpre = block_scan(wc, sm, &tot);
+    if (i < n) D.cwork_off[i] = cbase + cpre;
+    cbase += tot;
   }
   ct = block_sum(ct, sm); ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
   if (threadIdx.x == 0) {
     D.work_off[n] = base;
+    D.cwork_off[n] = cbase;
     *D.jac_n = 0;   // the element kernel appends deferred tet / contact clamps
     *D.cjac_n = 0;
     D.stats[0] += ct; D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;

@@ -7,5 +7,5 @@ pr.enable()
 bench.main()
 pr.disable()
 s = io.StringIO()
-pstats.Stats(pr, stream=s).sort_stats("tottime").print_stats(25)
+pstats.Stats(pr, stream=s).sort_stats("cumtime").print_stats("protocol|_native|bench", 30)
 print(s.getvalue()[:6000])
