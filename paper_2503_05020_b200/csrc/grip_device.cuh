@@ -105,6 +105,7 @@ struct Dev {
   int *cs_pt, *cs_ee, *cs_eid, *cs_n;
   double* cs_R;
   int* cs_valid;
+  double ss_k;        // superset covers dhat + ss_k * (last Newton step's max displacement)
   double* md_prev;   // last Newton step's max surface displacement
   double* md_kin;    // this step's prescribed (kinematic) displacement bound
   // elements (uniform capacity per env): [tets | abd | contacts | anchors]

@@ -534,6 +534,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.stats = b->alloc<double>(8);
   D.cs_n = b->alloc<int>(2 * (size_t)E);
   D.cs_R = b->alloc<double>(E);
+  D.ss_k = getenv("GRIP_SS_K") ? atof(getenv("GRIP_SS_K")) : 0.0;
   D.cs_valid = b->alloc<int>(E);
   D.md_prev = b->alloc<double>(E);
   D.md_kin = b->alloc<double>(E);

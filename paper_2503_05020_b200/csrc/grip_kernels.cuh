@@ -23,11 +23,12 @@ __device__ __forceinline__ void fail_env(const Dev& D, int e, int reason) {
   }
 }
 
-// radius of the candidate superset: covers 1.05 dhat, the next line search's d^+2 max_disp
-// (predicted from the last step, x1.5) and the kinematic CCD radius; capped so a huge first
-// Newton step does not blow the set up (that line search then runs its own broad phase)
+// radius of the candidate superset: covers 1.05 dhat, optionally the next line search's
+// dhat + 2 max_disp predicted from the last step (ss_k * md_prev, GRIP_SS_K; default 0: measured,
+// the grid cost grows faster with R than the line search saves) and the kinematic CCD radius;
+// capped so a huge Newton step does not blow the set up (that line search runs its own)
 __device__ __forceinline__ double superset_radius(const Dev& D, int e, double dhat) {
-  double R = fmax(1.05 * dhat, dhat + 3.0 * D.md_prev[e]);
+  double R = fmax(1.05 * dhat, dhat + D.ss_k * D.md_prev[e]);
   R = fmax(R, dhat + 2.0 * D.md_kin[e]);
   return fmin(R, 12.0 * dhat);
 }
