@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
-LIB_PATH = LIB_DIR / "libgripipc.so"
+LIB_PATH = Path(os.environ["GRIP_LIB"]) if os.environ.get("GRIP_LIB") else LIB_DIR / "libgripipc.so"  # GRIP_LIB: A/B builds
 ABI_VERSION = 2
 NPARAM = 14
 (P_DT, P_KAPPA, P_DHAT, P_EPSV, P_RELTOL, P_MAXIT, P_ELLFLOOR, P_MAXLS, P_CCDSCALE, P_CCDIT, P_KINGUARD, P_MURULE,

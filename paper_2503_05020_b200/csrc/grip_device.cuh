@@ -124,6 +124,7 @@ struct Dev {
   // scratch
   int max_sv, max_tri, max_edge, max_free, max_node;
   int cap_cells;
+  int bp_mode;       // broad phase: 0 direct over culled primitives with grid fallback, 1 grid only (GRIP_BP)
   int* bp_cells;     // per env cap_cells
   double* bp_aabb;   // per env 6*max(max_tri, max_edge)
   int* bp_cnt;       // per env max(max_sv, max_edge) + 1
@@ -302,10 +303,21 @@ __device__ __forceinline__ V3 sv_dir(const Dev& D, const EnvIx& E, int i, const 
 // cell common to both boxes).  The grid only prunes; the predicate decides,
 // so the cell size cannot change the result.
 // ---------------------------------------------------------------------------
+constexpr int BP_TILE = 512;      // direct broad phase: partner primitives staged per tile
 struct BPShared {
-  int head[MAXC + 1];
-  int cur[MAXC];
+  union {
+    struct {
+      int head[MAXC + 1];
+      int cur[MAXC];
+    };
+    struct {                        // direct path: one tile of compacted partners
+      double pb[BP_TILE][6];        // tight AABB (lo, hi)
+      int pv[BP_TILE][3];           // vertices (edges: 2)
+      int pid[BP_TILE];             // primitive id
+    };
+  };
   double bb[32][6];   // per-body surface AABB (culling: primitives far from every partner body)
+  int rs[32], re[32]; // per-body range of the compacted primitive list (direct path)
 };
 
 struct Grid {
@@ -395,8 +407,8 @@ __device__ bool grid_build(const Grid& G, const double* aabb, int n, int* cells,
 // out_n[0] = n_pt, out_n[1] = n_ee (true counts, even past capacity).
 // Returns false if an output or scratch capacity was exceeded; the host then
 // grows the buffers and re-runs the whole sweep for that env.
-__device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
-                                int* out_n, BPShared& S, Red& sm) {
+__device__ bool broad_phase_grid(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
+                                 int* out_n, BPShared& S, Red& sm) {
   const double* X = D.sv_pos + 3 * (size_t)E.s0;
   const int* tris = D.tris + 3 * (size_t)E.t0;
   const int* edges = D.edges + 2 * (size_t)E.ed0;
@@ -638,6 +650,324 @@ __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out
   }
   __syncthreads();
   return ok;
+}
+
+// ---------------------------------------------------------------------------
+// Direct broad phase over the culled primitives (the default; the grid above is the fallback
+// for envs whose culled sets are large).  Same membership predicates and canonical order:
+//   1. per-body AABBs; a primitive (query vertex) survives iff its (r+eps)-box reaches the
+//      AABB of a body its pair mask allows -- every predicate-true pair survives (see above);
+//   2. survivors are compacted in ascending id order (ids ascend body by body, so each body
+//      is one contiguous range of the compacted list);
+//   3. one warp per query walks the allowed bodies' ranges 32 primitives at a time; the
+//      ballot of the exact predicate gives each hit its rank, so a query's candidates come
+//      out in ascending primitive id with no sort: (v, t) and (i, j) canonical order.
+// Two passes (count, block scan, fill).  Work is balanced across the warps of the CTA and
+// every load of a 32-chunk is contiguous.
+// ---------------------------------------------------------------------------
+constexpr long long BP_DIRECT_MAX = 1ll << 21;   // estimated pair tests above which the grid is used
+
+__device__ __forceinline__ bool reaches_body(const BPShared& S, int nb, V3 l, V3 u, uint32_t m, double rc) {
+  for (int b = 0; b < nb; ++b) {
+    if (!((m >> b) & 1u)) continue;
+    const double* q = S.bb[b];
+    if (l.x - rc <= q[3] && l.y - rc <= q[4] && l.z - rc <= q[5] && u.x + rc >= q[0] && u.y + rc >= q[1] &&
+        u.z + rc >= q[2])
+      return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ int lower_bound_int(const int* a, int n, int key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// compacts the K-vertex primitives (K = 3 triangles, 2 edges) that survive the body cull:
+// ids -> cid[c], vertices -> cv[K c + k], tight AABBs -> cb[6 c]; per-body compact ranges
+// -> S.rs / S.re.  Returns the survivor count.
+template <int K>
+__device__ int bp_compact(const Dev& D, const EnvIx& E, const double* X, const int* prim, int n, const int* blo,
+                          const int* bhi, double rc, int* cid, int* cv, double* cb, BPShared& S, Red& sm) {
+  const uint32_t* pm = D.body_pairmask + E.b0;
+  const int* vb = D.sv_body + E.s0;
+  int ns = 0;
+  for (int s0 = 0; s0 < n; s0 += NT) {
+    const int i = s0 + threadIdx.x;
+    int keep = 0;
+    int w[K];
+    V3 l = V3{0, 0, 0}, u = V3{0, 0, 0};
+    if (i < n) {
+      for (int k = 0; k < K; ++k) w[k] = prim[K * i + k];
+      const V3 a = ld3(X + 3 * w[0]), b = ld3(X + 3 * w[1]);
+      l = vmin(a, b);
+      u = vmax(a, b);
+      if (K == 3) {
+        const V3 c = ld3(X + 3 * w[K - 1]);
+        l = vmin(l, c);
+        u = vmax(u, c);
+      }
+      const int bt = vb[w[0]];
+      keep = reaches_body(S, E.nb, l, u, pm[bt], rc);
+    }
+    int tot;
+    const int pre = block_scan(keep, sm, &tot);
+    if (keep) {
+      const int c = ns + pre;
+      cid[c] = i;
+      for (int k = 0; k < K; ++k) cv[K * c + k] = w[k];
+      double* o = cb + 6 * c;
+      o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
+    }
+    ns += tot;
+  }
+  __syncthreads();
+  if (threadIdx.x < E.nb) {
+    S.rs[threadIdx.x] = lower_bound_int(cid, ns, blo[E.b0 + threadIdx.x]);
+    S.re[threadIdx.x] = lower_bound_int(cid, ns, bhi[E.b0 + threadIdx.x]);
+  }
+  __syncthreads();
+  return ns;
+}
+
+// One query against staged partner k (tile-local kt) -- the reference's exact predicates.
+//   PT (broadphase.py:177-183): v not in t, x_v in [tri_lo - r, tri_hi + r]
+//   EE (:195-210): no shared vertex, hi_j >= lo_i - r and lo_j <= hi_i + r
+template <int K>
+__device__ __forceinline__ bool bp_hit(const BPShared& S, int kt, const double* q, int q0, int q1, double r) {
+  const double* bx = S.pb[kt];
+  if (K == 3) {
+    const int t0 = S.pv[kt][0], t1 = S.pv[kt][1], t2 = S.pv[kt][2];
+    return t0 != q0 && t1 != q0 && t2 != q0 && (q[0] >= bx[0] - r && q[1] >= bx[1] - r && q[2] >= bx[2] - r) &&
+           (q[0] <= bx[3] + r && q[1] <= bx[4] + r && q[2] <= bx[5] + r);
+  } else {
+    const int b0 = S.pv[kt][0], b1 = S.pv[kt][1];
+    return !(q0 == b0 || q0 == b1 || q1 == b0 || q1 == b1) &&
+           (bx[3] >= q[0] - r && bx[4] >= q[1] - r && bx[5] >= q[2] - r) &&
+           (bx[0] <= q[3] + r && bx[1] <= q[4] + r && bx[2] <= q[5] + r);
+  }
+}
+
+// Pairs of the nq queries with the np compacted partners (tiles of BP_TILE in shared memory).
+// K = 3: PT, queries are sv ids qid[q]; K = 2: EE, queries are the compacted edges themselves
+// (partner index > query index, i.e. i < j).  Per 32-query group and tile the warp picks the
+// cheaper traversal: lane-per-query over the group's partner ranges (uniform loop, broadcast
+// shared reads) or query-by-query with lanes over 32 partners (ballot ranks).  Both emit each
+// query's hits in ascending partner order; cnt[q] carries the count (pass 0) or the write
+// cursor (pass 1) across tiles.  Returns the total (pass 0).
+template <int K>
+__device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, const int* qid, int np, const int* cid,
+                        const int* cv, const double* cb, double r, int* cnt, int* out, int* out_eid, int cap,
+                        BPShared& S, Red& sm) {
+  const uint32_t* pm = D.body_pairmask + E.b0;
+  const int* vb = D.sv_body + E.s0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int total = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 0)
+      for (int q = threadIdx.x; q < nq; q += NT) cnt[q] = 0;
+    for (int p0 = 0; p0 < np; p0 += BP_TILE) {
+      const int p1 = min(np, p0 + BP_TILE);
+      __syncthreads();
+      for (int k = p0 + threadIdx.x; k < p1; k += NT) {
+        const int kt = k - p0;
+        for (int c = 0; c < 6; ++c) S.pb[kt][c] = cb[6 * k + c];
+        for (int c = 0; c < K; ++c) S.pv[kt][c] = cv[K * k + c];
+        S.pid[kt] = cid[k];
+      }
+      __syncthreads();
+      for (int g0 = warp * 32; g0 < nq; g0 += NT) {
+        const int q = g0 + lane;
+        const bool valid = q < nq;
+        double qd[6] = {0, 0, 0, 0, 0, 0};
+        int q0 = -1, q1 = -1, qi = 0;   // PT: v; EE: a0, a1, compact index
+        uint32_t allow = 0;
+        if (valid) {
+          if (K == 3) {
+            q0 = qid[q];
+            const V3 pq = ld3(X + 3 * q0);
+            qd[0] = pq.x; qd[1] = pq.y; qd[2] = pq.z;
+            allow = pm[vb[q0]];
+          } else {
+            for (int c = 0; c < 6; ++c) qd[c] = cb[6 * q + c];
+            q0 = cv[2 * q];
+            q1 = cv[2 * q + 1];
+            qi = q;
+            allow = pm[vb[q0]];
+          }
+        }
+        int run = valid ? cnt[q] : 0;
+        const uint32_t uni = __reduce_or_sync(0xffffffffu, allow);
+        const int kmin = K == 2 ? __reduce_min_sync(0xffffffffu, valid ? qi + 1 : 0x7fffffff) : 0;
+        // cost of the two traversals over this tile
+        int wl = 0, ww = 0;
+        for (int b = 0; b < E.nb; ++b) {
+          const int lo = max(max(S.rs[b], p0), kmin), hi = min(S.re[b], p1);
+          if (((uni >> b) & 1u) && hi > lo) wl += hi - lo;
+          if (valid && ((allow >> b) & 1u)) {
+            const int lq = max(max(S.rs[b], p0), K == 2 ? qi + 1 : 0);
+            if (hi > lq) ww += (hi - lq + 31) >> 5;
+          }
+        }
+        ww = __reduce_add_sync(0xffffffffu, ww);
+        if (wl <= ww) {
+          // lane per query
+          for (int b = 0; b < E.nb; ++b) {
+            if (!((uni >> b) & 1u)) continue;
+            const int lo = max(max(S.rs[b], p0), kmin), hi = min(S.re[b], p1);
+            const bool mine = valid && ((allow >> b) & 1u);
+            for (int k = lo; k < hi; ++k) {
+              const int kt = k - p0;
+              if (mine && (K == 3 || k > qi) && bp_hit<K>(S, kt, qd, q0, q1, r)) {
+                if (pass) {
+                  if (K == 3) {
+                    int* row = out + 4 * run;
+                    row[0] = q0; row[1] = S.pv[kt][0]; row[2] = S.pv[kt][1]; row[3] = S.pv[kt][2];
+                  } else {
+                    int* row = out + 4 * run;
+                    row[0] = q0; row[1] = q1; row[2] = S.pv[kt][0]; row[3] = S.pv[kt][1];
+                    out_eid[2 * run] = cid[qi];
+                    out_eid[2 * run + 1] = S.pid[kt];
+                  }
+                }
+                ++run;
+              }
+            }
+          }
+        } else {
+          // query by query, lanes over partners
+          const int nvalid = min(32, nq - g0);
+          for (int j = 0; j < nvalid; ++j) {
+            double qj[6];
+            for (int c = 0; c < 6; ++c) qj[c] = __shfl_sync(0xffffffffu, qd[c], j);
+            const int j0 = __shfl_sync(0xffffffffu, q0, j), j1 = __shfl_sync(0xffffffffu, q1, j);
+            const int ji = __shfl_sync(0xffffffffu, qi, j);
+            const uint32_t aj = __shfl_sync(0xffffffffu, allow, j);
+            int rj = __shfl_sync(0xffffffffu, run, j);
+            for (int b = 0; b < E.nb; ++b) {
+              if (!((aj >> b) & 1u)) continue;
+              const int lo = max(max(S.rs[b], p0), K == 2 ? ji + 1 : 0), hi = min(S.re[b], p1);
+              for (int s = lo; s < hi; s += 32) {
+                const int k = s + lane;
+                const bool hit = k < hi && bp_hit<K>(S, k - p0, qj, j0, j1, r);
+                const unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (pass && hit) {
+                  const int pos = rj + __popc(m & lt);
+                  const int kt = k - p0;
+                  int* row = out + 4 * pos;
+                  if (K == 3) {
+                    row[0] = j0; row[1] = S.pv[kt][0]; row[2] = S.pv[kt][1]; row[3] = S.pv[kt][2];
+                  } else {
+                    row[0] = j0; row[1] = j1; row[2] = S.pv[kt][0]; row[3] = S.pv[kt][1];
+                    out_eid[2 * pos] = cid[ji];
+                    out_eid[2 * pos + 1] = S.pid[kt];
+                  }
+                }
+                rj += __popc(m);
+              }
+            }
+            if (lane == j) run = rj;
+          }
+        }
+        if (valid) cnt[q] = run;
+      }
+    }
+    __syncthreads();
+    if (pass == 0) {
+      total = block_scan_array(cnt, nq, sm);
+      if (total > cap) return total;
+    }
+  }
+  return total;
+}
+
+// returns false on output overflow (*too_big: the culled sets are too large for the direct
+// path; nothing was written and the caller runs the grid)
+__device__ bool broad_phase_direct(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
+                                   int* out_n, BPShared& S, Red& sm, bool* too_big) {
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  const int* tris = D.tris + 3 * (size_t)E.t0;
+  const int* edges = D.edges + 2 * (size_t)E.ed0;
+  const int Mx = max(D.max_tri, D.max_edge);
+  double* cb = D.bp_aabb + (size_t)E.e * 6 * Mx;
+  int* cid = D.bp_cells + (size_t)E.e * D.cap_cells;   // [0, Mx) ids, [Mx, 4 Mx) vertices, [4 Mx, ..) queries
+  int* cv = cid + Mx;
+  int* qid = cid + 4 * Mx;
+  int* cnt = D.bp_cnt + (size_t)E.e * (max(D.max_sv, D.max_edge) + 1);
+  const uint32_t* pm = D.body_pairmask + E.b0;
+  const int* vb = D.sv_body + E.s0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  *too_big = false;
+  // per-body AABBs
+  for (int b = warp; b < E.nb; b += NWARP) {
+    double l[3] = {INFINITY, INFINITY, INFINITY}, u[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int i = lane; i < E.ns; i += 32)
+      if (vb[i] == b)
+        for (int c = 0; c < 3; ++c) {
+          l[c] = fmin(l[c], X[3 * i + c]);
+          u[c] = fmax(u[c], X[3 * i + c]);
+        }
+    for (int c = 0; c < 3; ++c) {
+      l[c] = wmin(l[c]);
+      u[c] = wmax(u[c]);
+    }
+    if (lane == 0)
+      for (int c = 0; c < 3; ++c) { S.bb[b][c] = l[c]; S.bb[b][3 + c] = u[c]; }
+  }
+  __syncthreads();
+  const double rc = r + 1e-9 * fmax(r, D.cell_hint[E.e]);
+  // ---------------- point-triangle ----------------
+  const int nts = bp_compact<3>(D, E, X, tris, E.nt, D.body_tri_lo, D.body_tri_hi, rc, cid, cv, cb, S, sm);
+  int nq = 0;
+  for (int s0 = 0; s0 < E.ns; s0 += NT) {
+    const int v = s0 + threadIdx.x;
+    int keep = 0;
+    if (v < E.ns && nts) {
+      const V3 p = ld3(X + 3 * v);
+      keep = reaches_body(S, E.nb, p, p, pm[vb[v]], rc);
+    }
+    int tot;
+    const int pre = block_scan(keep, sm, &tot);
+    if (keep) qid[nq + pre] = v;
+    nq += tot;
+  }
+  __syncthreads();
+  if ((double)nq * nts + 0.5 * (1.5 * nts) * (1.5 * nts) > (double)BP_DIRECT_MAX) {
+    *too_big = true;
+    return false;
+  }
+  const int npt = bp_pairs<3>(D, E, X, nq, qid, nts, cid, cv, cb, r, cnt, out_pt, nullptr, D.cap_pt, S, sm);
+  int nee = 0;
+  bool ok = npt <= D.cap_pt;
+  // ---------------- edge-edge ----------------
+  if (ok) {
+    const int nes = bp_compact<2>(D, E, X, edges, E.ne, D.body_edge_lo, D.body_edge_hi, rc, cid, cv, cb, S, sm);
+    nee = bp_pairs<2>(D, E, X, nes, nullptr, nes, cid, cv, cb, r, cnt, out_ee, out_eid, D.cap_ee, S, sm);
+    ok = nee <= D.cap_ee;
+  }
+  if (threadIdx.x == 0) {
+    out_n[0] = npt;
+    out_n[1] = nee;
+  }
+  __syncthreads();
+  return ok;
+}
+
+// Candidate stencils of one env at radius r (see broad_phase_grid for the contract).
+__device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
+                                int* out_n, BPShared& S, Red& sm) {
+  if (D.bp_mode == 0 && E.ns > 0) {
+    bool too_big = false;
+    const bool ok = broad_phase_direct(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm, &too_big);
+    if (!too_big) return ok;
+  }
+  return broad_phase_grid(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm);
 }
 
 // Exact candidate set at radius r as an order-preserving filter of a superset computed at

@@ -535,6 +535,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.cs_n = b->alloc<int>(2 * (size_t)E);
   D.cs_R = b->alloc<double>(E);
   D.ss_k = getenv("GRIP_SS_K") ? atof(getenv("GRIP_SS_K")) : 0.0;
+  D.bp_mode = (getenv("GRIP_BP") && std::string(getenv("GRIP_BP")) == "grid") ? 1 : 0;
   D.cs_valid = b->alloc<int>(E);
   D.md_prev = b->alloc<double>(E);
   D.md_kin = b->alloc<double>(E);
@@ -758,7 +759,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     t = kt_begin(b, K_LS);
     k_linesearch<<<n, NT, 0, b->stream>>>(D, b->d_list);
     kt_end(b, t);
-    b->launches += 5;
+    b->launches += 3 + (b->warp_elements ? 5 : 1) + (b->direct ? 2 : 1);
     b->sweeps += 1;
     CK(cudaGetLastError());
     std::vector<int> fl(b->n_env);
@@ -938,7 +939,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   t = kt_begin(b, K_LS);
   k_linesearch<<<n, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
-  b->launches += 5;
+  b->launches += 3 + (b->warp_elements ? 5 : 1) + (b->direct ? 2 : 1);
   b->sweeps += 1;
 }
 

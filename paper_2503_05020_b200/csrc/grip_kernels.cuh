@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
 // Newton sweep 1/4: surface positions, candidate set at 1.05 dhat, active stencils
 // (solver.py:652-653, contact.py:283-309)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT) k_candidates(Dev D, const int* list) {
+__global__ void __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
   const int e = list[blockIdx.x];
