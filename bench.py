@@ -273,6 +273,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=150, help="CPU baseline: max protocol steps per env (full trial)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lockstep", action="store_true", help="lockstep Batch.step rounds instead of continuous batching")
+    ap.add_argument("--lanes", type=int, default=3,
+                    help="1: one device batch; 3k: k device batches (own stream + host thread) per object kind")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -294,69 +296,121 @@ def main():
 
     cands = sc.load_cfg2_candidates()
     ids = [rank * args.envs + i for i in range(args.envs)]       # weak scaling: 400 envs per GPU
-    scenes = [sc.cfg2_scene(i % 400, cands) for i in ids]
-    envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
-    group = DeviceEnvGroup(envs, device=local)
-    trials = BatchedGraspTrials(group, scenes)
-    dev = group.dev
-    # refill queues: candidates of each object kind, cycled (same topology per kind)
     kinds = np.asarray(cands["kind"])
-    queue = {k: [j for j in range(400) if kinds[j] == k] for k in range(3)}
-    qpos = {k: 0 for k in range(3)}
-    payloads = {}
-    done_trials = []
-
-    def payload(j):
-        if j not in payloads:
-            payloads[j] = BatchedGraspTrials.scene_payload(sc.cfg2_scene(j, cands))
-        return payloads[j]
-
-    for j in range(400):                                          # precompute outside timing
-        payload(j)
     slot_kind = np.array([kinds[i % 400] for i in ids])
+    # lanes: one device batch (own CUDA stream, own host thread) per object kind, so the light
+    # box / cylinder envs are not held at every kernel boundary by the heavy sphere envs; --lanes 1
+    # puts all envs of this rank in one batch
+    if args.lanes == 1:
+        lane_ids = [ids]
+    else:
+        per_kind = max(1, args.lanes // 3)
+        lane_ids = []
+        for kk in range(3):
+            of_kind = [i for i, k in zip(ids, slot_kind) if k == kk]
+            lane_ids += [of_kind[j::per_kind] for j in range(per_kind)]
+        lane_ids = [l for l in lane_ids if l]
+    payloads = {j: BatchedGraspTrials.scene_payload(sc.cfg2_scene(j, cands)) for j in range(400)}  # outside timing
+    queue = {k: [j for j in range(400) if kinds[j] == k] for k in range(3)}
+    qlock = threading.Lock()
+    qpos = {k: 0 for k in range(3)}
 
-    def refill():
-        fin = np.nonzero(trials.phase == 4)[0]
-        if len(fin) == 0:
-            return
-        pls = []
-        for e in fin:
-            done_trials.append(trials.records[e].verdict)
-            k = int(slot_kind[e])
-            j = queue[k][qpos[k] % len(queue[k])]
-            qpos[k] += 1
-            pls.append(payloads[j])
-        trials.refill(fin, pls)
+    class Lane:
+        def __init__(self, lids):
+            scenes = [sc.cfg2_scene(i % 400, cands) for i in lids]
+            envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+            self.group = DeviceEnvGroup(envs, device=local)
+            self.trials = BatchedGraspTrials(self.group, scenes)
+            self.dev = self.group.dev
+            self.kind = np.array([kinds[i % 400] for i in lids])
+            self.done_trials = []
+            self.advance = self.trials.advance if args.lockstep else self.trials.advance_round
+            self.env_steps = 0
+            self.rounds = 0
 
-    advance = trials.advance if args.lockstep else trials.advance_round
-    for _ in range(args.warmup):
-        advance()
-        refill()
-    dev.set_profiling(True)
-    _, l0, _ = dev.stats()
-    E, B = group.packed.n_env, group.packed.n_body_total
-    maxa = dev.max_alpha
-    h2d = 8 * 3 * E + 8 * 3 * B + 2 * E                                # gravity, body velocities, round masks
-    d2h = 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E + E  # reports, alphas, forces+masks+min_d, com, speed, finalized
+        def refill(self):
+            fin = np.nonzero(self.trials.phase == 4)[0]
+            if len(fin) == 0:
+                return
+            pls = []
+            with qlock:
+                for e in fin:
+                    self.done_trials.append(self.trials.records[e].verdict)
+                    k = int(self.kind[e])
+                    pls.append(payloads[queue[k][qpos[k] % len(queue[k])]])
+                    qpos[k] += 1
+            self.trials.refill(fin, pls)
+
+        def round(self):
+            n = self.advance()
+            self.refill()
+            self.env_steps += n
+            self.rounds += 1
+
+    lanes = [Lane(l) for l in lane_ids]
+
+    def run_lanes(n_rounds, timed):
+        """Every lane runs rounds on its own thread; the lane with the most envs runs exactly
+        n_rounds, the others keep going until it is done (their streams stay busy)."""
+        main_lane = max(range(len(lanes)), key=lambda i: len(lane_ids[i]))
+        stop = threading.Event()
+
+        def work(i):
+            ln = lanes[i]
+            if timed:
+                ln.dev.timer_start()
+            if i == main_lane:
+                for _ in range(n_rounds):
+                    ln.round()
+                stop.set()
+            else:
+                while not stop.is_set():
+                    ln.round()
+            if timed:
+                ln.ms = ln.dev.timer_stop()
+
+        th = [threading.Thread(target=work, args=(i,)) for i in range(len(lanes))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    run_lanes(args.warmup, False)
+    for ln in lanes:
+        ln.dev.set_profiling(True)
+        ln.l0 = ln.dev.stats()[1]
+        ln.sw0 = ln.dev.stats()[2]
+        ln.env_steps = 0
+        ln.rounds = 0
+        ln.nd0 = len(ln.done_trials)
+    h2d = d2h = 0
+    for ln in lanes:
+        E, B = ln.group.packed.n_env, ln.group.packed.n_body_total
+        maxa = ln.dev.max_alpha
+        h2d += 8 * 3 * E + 8 * 3 * B + 2 * E                                # gravity, body velocities, round masks
+        d2h += 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E + E  # reports, alphas, forces+masks+min_d, com, speed, finalized
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ndone0 = len(done_trials)
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
-        dev.timer_start()
-        env_steps = 0
-        sweeps0 = dev.stats()[2]
-        for _ in range(args.steps):
-            env_steps += advance()
-            refill()
-        ms = dev.timer_stop()
+        run_lanes(args.steps, True)
         wall = time.perf_counter() - t0
     torch.cuda.synchronize()
-    _, l1, sweeps1 = dev.stats()
-    ks = dev.kernel_stats()
+    ms = max(ln.ms for ln in lanes)
+    env_steps = sum(ln.env_steps for ln in lanes)
+    nsweeps = sum(ln.dev.stats()[2] - ln.sw0 for ln in lanes)
+    launches = sum(ln.dev.stats()[1] - ln.l0 for ln in lanes)
+    kss = [ln.dev.kernel_stats() for ln in lanes]
+    ks = {}
+    for name in kss[0]:
+        ks[name] = {"ms": sum(k[name]["ms"] for k in kss), "launches": sum(k[name]["launches"] for k in kss)}
+    ks["elements"]["units"] = {u: sum(k["elements"]["units"][u] for k in kss) for u in kss[0]["elements"]["units"]}
+    for f in ("pcg_iterations", "solves"):
+        ks["assemble_pcg"][f] = sum(k["assemble_pcg"][f] for k in kss)
+    ks["assemble_pcg"]["mean_unknowns"] = 0.0
     if world > 1:
-        t = torch.tensor([ms, wall, float(env_steps), float(sweeps1 - sweeps0)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, wall, float(env_steps), float(nsweeps)], dtype=torch.float64, device="cuda")
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         sm_ = t.clone()
@@ -385,7 +439,6 @@ def main():
     roof["pcg"] = {"iterations_per_solve": pk["pcg_iterations"] / max(pk["solves"], 1.0),
                    "mean_unknowns": pk["mean_unknowns"], "solves": pk["solves"]}
     roof["element_counts"] = ks["elements"]["units"]
-    nsweeps = sweeps1 - sweeps0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -397,17 +450,20 @@ def main():
                    "env_steps_timed": total_steps, "newton_sweeps": int(nsweeps),
                    "ms_per_newton_sweep": ms_max / max(nsweeps, 1),
                    "mode": "lockstep Batch.step" if args.lockstep else "continuous batching, steady-state refill",
-                   "trials_completed_timed": len(done_trials) - ndone0},
+                   "trials_completed_timed": sum(len(ln.done_trials) - ln.nd0 for ln in lanes),
+                   "lanes": [{"envs": len(l), "rounds": ln.rounds, "env_steps": ln.env_steps, "ms": round(ln.ms, 3)}
+                             for l, ln in zip(lane_ids, lanes)]},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": roof,
-        "gpu_launches": int(l1 - l0),
+        "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if world > 1:
         # the path's one collective: fixed-size per-env outcome records, gathered once at the end
         from paper_2503_05020_b200.distributed import gather_outcomes, pack_outcomes
         tg = time.perf_counter()
-        allr = gather_outcomes(pack_outcomes(trials.records, ids), args.envs * world, device="cuda")
+        recs = {i: r for l, ln in zip(lane_ids, lanes) for i, r in zip(l, ln.trials.records)}
+        allr = gather_outcomes(pack_outcomes([recs[i] for i in ids], ids), args.envs * world, device="cuda")
         line["outcome_gather"] = {"envs": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg), "backend": "nccl"}
     if rank == 0 and not args.no_cpu:
         cores = os.cpu_count() or 1
