@@ -117,6 +117,8 @@ struct Dev {
   int* el_idx;
   int* work_off;     // per list position (n+1)
   int* cwork_off;    // per list position (n+1): contact / friction elements only
+  int* twork_off;    // per list position (n+1): tets only (k_tet_front)
+  int* ework_off;    // per list position (n+1): abd + contacts + anchors (k_elements_w)
   // anchors (persist across steps)
   int* anc_v;        // 4
   double *anc_gamma, *anc_T, *anc_lam, *anc_mu;   // 4, 6, 1, 1

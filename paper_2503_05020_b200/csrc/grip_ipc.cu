@@ -12,6 +12,7 @@
 
 #include "grip_kernels.cuh"
 #include "grip_warp_elements.cuh"
+#include "grip_tet.cuh"
 #include "grip_direct.cuh"
 #include "grip_tetclamp.cuh"
 
@@ -546,6 +547,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.n_anc = b->alloc<int>(E);
   D.work_off = b->alloc<int>(E + 1);
   D.cwork_off = b->alloc<int>(E + 1);
+  D.twork_off = b->alloc<int>(E + 1);
+  D.ework_off = b->alloc<int>(E + 1);
   D.max_sv = max_sv; D.max_tri = max_tri; D.max_edge = max_edge; D.max_free = max_free;
   D.max_node = max_node; D.max_tet = max_tet; D.max_abd = max_abd;
   D.cap_pt = std::max(2048, 16 * max_sv);
@@ -634,7 +637,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.surf_prev, D.kin_pos, D.sv_disp, D.ell, D.tol, D.residual, D.energy, D.alphas, D.min_dist, D.time, D.iters,
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
-        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.anc_v,
+        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
@@ -739,10 +742,11 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     kt_end(b, t);
     t = kt_begin(b, K_ELEM);
     if (b->warp_elements) {
-      k_elements_w<<<148 * 4, EW * 32, 0, b->stream>>>(D, b->d_list, n);
+      k_tet_front<<<148 * 2, TF, 0, b->stream>>>(D, b->d_list, n);
+      k_elements_w<<<148 * 2, EW * 32, 0, b->stream>>>(D, b->d_list, n);
       k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
       k_tet_jacobi<<<148, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-      k_tet_finish<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W, D.tet_eig);
+      k_tet_back<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
       k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
     }
     else
@@ -759,7 +763,7 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     t = kt_begin(b, K_LS);
     k_linesearch<<<n, NT, 0, b->stream>>>(D, b->d_list);
     kt_end(b, t);
-    b->launches += 3 + (b->warp_elements ? 5 : 1) + (b->direct ? 2 : 1);
+    b->launches += 3 + (b->warp_elements ? 6 : 1) + (b->direct ? 2 : 1);
     b->sweeps += 1;
     CK(cudaGetLastError());
     std::vector<int> fl(b->n_env);
@@ -919,10 +923,11 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   kt_end(b, t);
   t = kt_begin(b, K_ELEM);
   if (b->warp_elements) {
-    k_elements_w<<<148 * 4, EW * 32, 0, b->stream>>>(D, list, n);
+    k_tet_front<<<148 * 2, TF, 0, b->stream>>>(D, list, n);
+    k_elements_w<<<148 * 2, EW * 32, 0, b->stream>>>(D, list, n);
     k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
     k_tet_jacobi<<<148, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-    k_tet_finish<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W, D.tet_eig);
+    k_tet_back<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
     k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
   } else {
     k_elements<<<148 * 8, 128, 0, b->stream>>>(D, list, n);
@@ -939,7 +944,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   t = kt_begin(b, K_LS);
   k_linesearch<<<n, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
-  b->launches += 3 + (b->warp_elements ? 5 : 1) + (b->direct ? 2 : 1);
+  b->launches += 3 + (b->warp_elements ? 6 : 1) + (b->direct ? 2 : 1);
   b->sweeps += 1;
 }
 

@@ -281,16 +281,18 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
   __shared__ Red sm;
   int base = 0;
   double ct = 0.0, ca = 0.0, cc = 0.0, cf = 0.0;
-  int cbase = 0;
+  int cbase = 0, tbase = 0, ebase = 0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
-    int w = 0, wc = 0;
+    int w = 0, wc = 0, wt = 0, we = 0;
     if (i < n) {
       const int e = list[i];
       if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e]) {
         const int nt = D.tet_off[e + 1] - D.tet_off[e], na = D.abd_off[e + 1] - D.abd_off[e];
         wc = D.n_act[e] + D.n_anc[e];
         w = nt + na + wc;
+        wt = nt;
+        we = na + wc;
         ct += nt; ca += na; cc += D.n_act[e]; cf += D.n_anc[e];
       }
     }
@@ -301,11 +303,19 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
     const int cpre = block_scan(wc, sm, &tot);
     if (i < n) D.cwork_off[i] = cbase + cpre;
     cbase += tot;
+    const int tpre = block_scan(wt, sm, &tot);
+    if (i < n) D.twork_off[i] = tbase + tpre;
+    tbase += tot;
+    const int epre = block_scan(we, sm, &tot);
+    if (i < n) D.ework_off[i] = ebase + epre;
+    ebase += tot;
   }
   ct = block_sum(ct, sm); ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
   if (threadIdx.x == 0) {
     D.work_off[n] = base;
     D.cwork_off[n] = cbase;
+    D.twork_off[n] = tbase;
+    D.ework_off[n] = ebase;
     *D.jac_n = 0;   // the element kernel appends deferred tet / contact clamps
     *D.cjac_n = 0;
     D.stats[0] += ct; D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;

@@ -340,41 +340,23 @@ __global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* lis
   __shared__ WarpEl ws[EW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpEl& W = ws[warp];
-  const int total = D.work_off[n];
+  const int total = D.ework_off[n];   // tets run thread-per-tet in k_tet_front
   for (int item = blockIdx.x * EW + warp; item < total; item += gridDim.x * EW) {
     int lo = 0, hi = n;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (D.work_off[mid] <= item) lo = mid;
+      if (D.ework_off[mid] <= item) lo = mid;
       else hi = mid;
     }
     const int e = list[lo];
     const EnvIx E = env_ix(D, e);
     const double* P = P_(D, e);
-    int k = item - D.work_off[lo];
+    int k = item - D.ework_off[lo];
     const size_t elbase = (size_t)e * D.cap_el;
     double Eel = 0.0;
     int idx[4];
     size_t slot;
-    if (k < E.ntet) {
-      const int t = E.te0 + k;
-      slot = elbase + k;
-      V3 x[4];
-      for (int j = 0; j < 4; ++j) {
-        idx[j] = D.tet_nodes[4 * (size_t)t + j];
-        x[j] = ld3(D.x + 3 * (size_t)(E.n0 + idx[j]));
-      }
-      const int fl = w_nh(W, x, D.tet_Dmi + 9 * (size_t)t, D.tet_V0[t], D.tet_mu[t], D.tet_lam[t], &Eel, lane,
-                          D.tet_eig + 81 * (size_t)t, D.tet_S + 45 * (size_t)t);
-      if ((fl & EL_DEFERRED) && lane == 0) D.jac_list[atomicAdd(D.jac_n, 1)] = make_int2(t, (int)slot);
-      if (fl & EL_INVERTED) {
-        if (lane == 0) atomicOr(&D.flags[e], ERR_INVERTED);
-        Eel = 0.0;
-        for (int i = lane; i < 144; i += 32) W.H[i] = 0.0;
-        if (lane < 12) W.g[lane] = 0.0;
-        __syncwarp();
-      }
-    } else if ((k -= E.ntet) < E.na) {
+    if (k < E.na) {
       const int a = E.a0 + k;
       slot = elbase + D.max_tet + k;
       const int pn = D.abd_node[a];
