@@ -126,6 +126,8 @@ struct Dev {
   // scratch
   int max_sv, max_tri, max_edge, max_free, max_node;
   int cap_cells;
+  int bp_qm_min;     // direct broad phase: groups with > bp_qm_min lane-mode iterations use query mode
+  float bp_qm_fac;   //   when that costs <= bp_qm_fac x the lane-mode iterations (GRIP_BP_QM=min,fac)
   int bp_mode;       // broad phase: 0 direct over culled primitives with grid fallback, 1 grid only (GRIP_BP)
   int* bp_cells;     // per env cap_cells
   double* bp_aabb;   // per env 6*max(max_tri, max_edge)
@@ -306,6 +308,7 @@ __device__ __forceinline__ V3 sv_dir(const Dev& D, const EnvIx& E, int i, const 
 // so the cell size cannot change the result.
 // ---------------------------------------------------------------------------
 constexpr int BP_TILE = 512;      // direct broad phase: partner primitives staged per tile
+constexpr int BP_MAXG = 512;      // direct broad phase: query groups with a recorded traversal mode
 struct BPShared {
   union {
     struct {
@@ -313,13 +316,14 @@ struct BPShared {
       int cur[MAXC];
     };
     struct {                        // direct path: one tile of compacted partners
-      double pb[BP_TILE][6];        // tight AABB (lo, hi)
-      int pv[BP_TILE][3];           // vertices (edges: 2)
+      double pb[6][BP_TILE];        // tight AABB (lo, hi), SoA: conflict-free across lanes
+      int pv[3][BP_TILE];           // vertices (edges: 2)
       int pid[BP_TILE];             // primitive id
     };
   };
   double bb[32][6];   // per-body surface AABB (culling: primitives far from every partner body)
   int rs[32], re[32]; // per-body range of the compacted primitive list (direct path)
+  unsigned char gmode[BP_MAXG];   // direct path: per 32-query group, 1 = queries one by one
 };
 
 struct Grid {
@@ -742,34 +746,83 @@ __device__ int bp_compact(const Dev& D, const EnvIx& E, const double* X, const i
 //   EE (:195-210): no shared vertex, hi_j >= lo_i - r and lo_j <= hi_i + r
 template <int K>
 __device__ __forceinline__ bool bp_hit(const BPShared& S, int kt, const double* q, int q0, int q1, double r) {
-  const double* bx = S.pb[kt];
+  const double b0x = S.pb[0][kt], b0y = S.pb[1][kt], b0z = S.pb[2][kt];
+  const double b1x = S.pb[3][kt], b1y = S.pb[4][kt], b1z = S.pb[5][kt];
   if (K == 3) {
-    const int t0 = S.pv[kt][0], t1 = S.pv[kt][1], t2 = S.pv[kt][2];
-    return t0 != q0 && t1 != q0 && t2 != q0 && (q[0] >= bx[0] - r && q[1] >= bx[1] - r && q[2] >= bx[2] - r) &&
-           (q[0] <= bx[3] + r && q[1] <= bx[4] + r && q[2] <= bx[5] + r);
+    const int t0 = S.pv[0][kt], t1 = S.pv[1][kt], t2 = S.pv[2][kt];
+    return t0 != q0 && t1 != q0 && t2 != q0 && (q[0] >= b0x - r && q[1] >= b0y - r && q[2] >= b0z - r) &&
+           (q[0] <= b1x + r && q[1] <= b1y + r && q[2] <= b1z + r);
   } else {
-    const int b0 = S.pv[kt][0], b1 = S.pv[kt][1];
+    const int b0 = S.pv[0][kt], b1 = S.pv[1][kt];
     return !(q0 == b0 || q0 == b1 || q1 == b0 || q1 == b1) &&
-           (bx[3] >= q[0] - r && bx[4] >= q[1] - r && bx[5] >= q[2] - r) &&
-           (bx[0] <= q[3] + r && bx[1] <= q[4] + r && bx[2] <= q[5] + r);
+           (b1x >= q[0] - r && b1y >= q[1] - r && b1z >= q[2] - r) &&
+           (b0x <= q[3] + r && b0y <= q[4] + r && b0z <= q[5] + r);
   }
 }
 
 // Pairs of the nq queries with the np compacted partners (tiles of BP_TILE in shared memory).
 // K = 3: PT, queries are sv ids qid[q]; K = 2: EE, queries are the compacted edges themselves
-// (partner index > query index, i.e. i < j).  Per 32-query group and tile the warp picks the
-// cheaper traversal: lane-per-query over the group's partner ranges (uniform loop, broadcast
-// shared reads) or query-by-query with lanes over 32 partners (ballot ranks).  Both emit each
-// query's hits in ascending partner order; cnt[q] carries the count (pass 0) or the write
-// cursor (pass 1) across tiles.  Returns the total (pass 0).
+// (partner index > query index, i.e. i < j).  Per 32-query group and tile the cheaper of two
+// traversals is used:
+//   lane mode : lane per query, a uniform loop over the group's partner ranges (broadcast
+//               shared reads);
+//   query mode: one query at a time, lanes over 32 partners (ballot ranks).  These queries
+//               are dealt out to the warps one by one, so a few heavy groups (e.g. the pad
+//               vertices against a sphere's triangles) are spread over the whole CTA.
+// Both emit each query's hits in ascending partner order; cnt[q] carries the count (pass 0)
+// or the write cursor (pass 1) across tiles.  Returns the total (pass 0).
+template <int K>
+struct BPQuery {
+  double qd[6];
+  int q0, q1, qi;
+  uint32_t allow;
+};
+
+template <int K>
+__device__ __forceinline__ BPQuery<K> bp_load_query(const Dev& D, const EnvIx& E, const double* X, int q,
+                                                    const int* qid, const int* cv, const double* cb) {
+  BPQuery<K> Q;
+  const uint32_t* pm = D.body_pairmask + E.b0;
+  const int* vb = D.sv_body + E.s0;
+  if (K == 3) {
+    Q.q0 = qid[q];
+    Q.q1 = -1;
+    Q.qi = 0;
+    const V3 pq = ld3(X + 3 * Q.q0);
+    Q.qd[0] = pq.x; Q.qd[1] = pq.y; Q.qd[2] = pq.z;
+    Q.qd[3] = Q.qd[4] = Q.qd[5] = 0.0;
+  } else {
+    for (int c = 0; c < 6; ++c) Q.qd[c] = cb[6 * q + c];
+    Q.q0 = cv[2 * q];
+    Q.q1 = cv[2 * q + 1];
+    Q.qi = q;
+  }
+  Q.allow = pm[vb[Q.q0]];
+  return Q;
+}
+
+template <int K>
+__device__ __forceinline__ void bp_emit(const BPShared& S, int kt, int q0, int q1, int qid_global, int pos, int* out,
+                                        int* out_eid) {
+  int* row = out + 4 * pos;
+  row[0] = q0;
+  if (K == 3) {
+    row[1] = S.pv[0][kt]; row[2] = S.pv[1][kt]; row[3] = S.pv[2][kt];
+  } else {
+    row[1] = q1; row[2] = S.pv[0][kt]; row[3] = S.pv[1][kt];
+    out_eid[2 * pos] = qid_global;
+    out_eid[2 * pos + 1] = S.pid[kt];
+  }
+}
+
 template <int K>
 __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, const int* qid, int np, const int* cid,
                         const int* cv, const double* cb, double r, int* cnt, int* out, int* out_eid, int cap,
                         BPShared& S, Red& sm) {
-  const uint32_t* pm = D.body_pairmask + E.b0;
-  const int* vb = D.sv_body + E.s0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
+  const int ngroups = (nq + 31) >> 5;
+  const bool modes = ngroups <= BP_MAXG;   // else every group runs in lane mode
   int total = 0;
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 0)
@@ -777,108 +830,95 @@ __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, c
     for (int p0 = 0; p0 < np; p0 += BP_TILE) {
       const int p1 = min(np, p0 + BP_TILE);
       __syncthreads();
-      for (int k = p0 + threadIdx.x; k < p1; k += NT) {
-        const int kt = k - p0;
-        for (int c = 0; c < 6; ++c) S.pb[kt][c] = cb[6 * k + c];
-        for (int c = 0; c < K; ++c) S.pv[kt][c] = cv[K * k + c];
-        S.pid[kt] = cid[k];
-      }
-      __syncthreads();
-      for (int g0 = warp * 32; g0 < nq; g0 += NT) {
-        const int q = g0 + lane;
-        const bool valid = q < nq;
-        double qd[6] = {0, 0, 0, 0, 0, 0};
-        int q0 = -1, q1 = -1, qi = 0;   // PT: v; EE: a0, a1, compact index
-        uint32_t allow = 0;
-        if (valid) {
-          if (K == 3) {
-            q0 = qid[q];
-            const V3 pq = ld3(X + 3 * q0);
-            qd[0] = pq.x; qd[1] = pq.y; qd[2] = pq.z;
-            allow = pm[vb[q0]];
-          } else {
-            for (int c = 0; c < 6; ++c) qd[c] = cb[6 * q + c];
-            q0 = cv[2 * q];
-            q1 = cv[2 * q + 1];
-            qi = q;
-            allow = pm[vb[q0]];
-          }
+      if (pass == 0 || np > BP_TILE) {   // a single tile stays staged for the second pass
+        for (int k = p0 + threadIdx.x; k < p1; k += NT) {
+          const int kt = k - p0;
+          for (int c = 0; c < 6; ++c) S.pb[c][kt] = cb[6 * k + c];
+          for (int c = 0; c < K; ++c) S.pv[c][kt] = cv[K * k + c];
+          S.pid[kt] = cid[k];
         }
-        int run = valid ? cnt[q] : 0;
-        const uint32_t uni = __reduce_or_sync(0xffffffffu, allow);
-        const int kmin = K == 2 ? __reduce_min_sync(0xffffffffu, valid ? qi + 1 : 0x7fffffff) : 0;
-        // cost of the two traversals over this tile
+        __syncthreads();
+      }
+      // phase 1: each warp takes whole groups, decides their mode, runs the lane-mode ones
+      for (int g = warp; g < ngroups; g += NWARP) {
+        const int q = 32 * g + lane;
+        const bool valid = q < nq;
+        BPQuery<K> Q;
+        if (valid) Q = bp_load_query<K>(D, E, X, q, qid, cv, cb);
+        else { Q.allow = 0; Q.q0 = Q.q1 = -1; Q.qi = 0; for (int c = 0; c < 6; ++c) Q.qd[c] = 0.0; }
+        const uint32_t uni = __reduce_or_sync(0xffffffffu, Q.allow);
+        const int kmin = K == 2 ? __reduce_min_sync(0xffffffffu, valid ? Q.qi + 1 : 0x7fffffff) : 0;
         int wl = 0, ww = 0;
         for (int b = 0; b < E.nb; ++b) {
-          const int lo = max(max(S.rs[b], p0), kmin), hi = min(S.re[b], p1);
+          const int hi = min(S.re[b], p1);
+          const int lo = max(max(S.rs[b], p0), kmin);
           if (((uni >> b) & 1u) && hi > lo) wl += hi - lo;
-          if (valid && ((allow >> b) & 1u)) {
-            const int lq = max(max(S.rs[b], p0), K == 2 ? qi + 1 : 0);
+          if (valid && ((Q.allow >> b) & 1u)) {
+            const int lq = max(max(S.rs[b], p0), K == 2 ? Q.qi + 1 : 0);
             if (hi > lq) ww += (hi - lq + 31) >> 5;
           }
         }
         ww = __reduce_add_sync(0xffffffffu, ww);
-        if (wl <= ww) {
-          // lane per query
-          for (int b = 0; b < E.nb; ++b) {
-            if (!((uni >> b) & 1u)) continue;
-            const int lo = max(max(S.rs[b], p0), kmin), hi = min(S.re[b], p1);
-            const bool mine = valid && ((allow >> b) & 1u);
-            for (int k = lo; k < hi; ++k) {
-              const int kt = k - p0;
-              if (mine && (K == 3 || k > qi) && bp_hit<K>(S, kt, qd, q0, q1, r)) {
-                if (pass) {
-                  if (K == 3) {
-                    int* row = out + 4 * run;
-                    row[0] = q0; row[1] = S.pv[kt][0]; row[2] = S.pv[kt][1]; row[3] = S.pv[kt][2];
-                  } else {
-                    int* row = out + 4 * run;
-                    row[0] = q0; row[1] = q1; row[2] = S.pv[kt][0]; row[3] = S.pv[kt][1];
-                    out_eid[2 * run] = cid[qi];
-                    out_eid[2 * run + 1] = S.pid[kt];
-                  }
-                }
-                ++run;
-              }
+        const bool qmode = modes && (ww <= wl || (wl > D.bp_qm_min && ww <= D.bp_qm_fac * wl));
+        if (modes && lane == 0) S.gmode[g] = qmode;
+        if (qmode) continue;
+        int run = valid ? cnt[q] : 0;
+        for (int b = 0; b < E.nb; ++b) {
+          if (!((uni >> b) & 1u)) continue;
+          const int lo = max(max(S.rs[b], p0), kmin), hi = min(S.re[b], p1);
+          const bool mine = valid && ((Q.allow >> b) & 1u);
+          for (int k = lo; k < hi; ++k) {
+            const int kt = k - p0;
+            if (mine && (K == 3 || k > Q.qi) && bp_hit<K>(S, kt, Q.qd, Q.q0, Q.q1, r)) {
+              if (pass) bp_emit<K>(S, kt, Q.q0, Q.q1, K == 2 ? cid[Q.qi] : 0, run, out, out_eid);
+              ++run;
             }
           }
-        } else {
-          // query by query, lanes over partners
-          const int nvalid = min(32, nq - g0);
-          for (int j = 0; j < nvalid; ++j) {
+        }
+        if (valid) cnt[q] = run;
+      }
+      __syncthreads();
+      // phase 2: query-mode queries, dealt out one by one: warp w takes queries base + w + 8 l
+      // (l = lane), loads their data in one go and walks them with broadcasts
+      if (modes)
+        for (int base = 0; base < nq; base += 32 * NWARP) {
+          const int q = base + warp + NWARP * lane;
+          const bool mine = q < nq && S.gmode[q >> 5];
+          const unsigned todo = __ballot_sync(0xffffffffu, mine);
+          if (!todo) continue;
+          BPQuery<K> Q;
+          int run = 0;
+          if (mine) {
+            Q = bp_load_query<K>(D, E, X, q, qid, cv, cb);
+            run = cnt[q];
+          } else {
+            Q.allow = 0; Q.q0 = Q.q1 = -1; Q.qi = 0;
+            for (int c = 0; c < 6; ++c) Q.qd[c] = 0.0;
+          }
+          for (unsigned left = todo; left; left &= left - 1) {
+            const int j = __ffs(left) - 1;
             double qj[6];
-            for (int c = 0; c < 6; ++c) qj[c] = __shfl_sync(0xffffffffu, qd[c], j);
-            const int j0 = __shfl_sync(0xffffffffu, q0, j), j1 = __shfl_sync(0xffffffffu, q1, j);
-            const int ji = __shfl_sync(0xffffffffu, qi, j);
-            const uint32_t aj = __shfl_sync(0xffffffffu, allow, j);
+            for (int c = 0; c < 6; ++c) qj[c] = __shfl_sync(0xffffffffu, Q.qd[c], j);
+            const int j0 = __shfl_sync(0xffffffffu, Q.q0, j), j1 = __shfl_sync(0xffffffffu, Q.q1, j);
+            const int ji = __shfl_sync(0xffffffffu, Q.qi, j);
+            const uint32_t aj = __shfl_sync(0xffffffffu, Q.allow, j);
             int rj = __shfl_sync(0xffffffffu, run, j);
+            const int gid = K == 2 ? cid[ji] : 0;
             for (int b = 0; b < E.nb; ++b) {
               if (!((aj >> b) & 1u)) continue;
               const int lo = max(max(S.rs[b], p0), K == 2 ? ji + 1 : 0), hi = min(S.re[b], p1);
-              for (int s = lo; s < hi; s += 32) {
-                const int k = s + lane;
+              for (int s0 = lo; s0 < hi; s0 += 32) {
+                const int k = s0 + lane;
                 const bool hit = k < hi && bp_hit<K>(S, k - p0, qj, j0, j1, r);
                 const unsigned m = __ballot_sync(0xffffffffu, hit);
-                if (pass && hit) {
-                  const int pos = rj + __popc(m & lt);
-                  const int kt = k - p0;
-                  int* row = out + 4 * pos;
-                  if (K == 3) {
-                    row[0] = j0; row[1] = S.pv[kt][0]; row[2] = S.pv[kt][1]; row[3] = S.pv[kt][2];
-                  } else {
-                    row[0] = j0; row[1] = j1; row[2] = S.pv[kt][0]; row[3] = S.pv[kt][1];
-                    out_eid[2 * pos] = cid[ji];
-                    out_eid[2 * pos + 1] = S.pid[kt];
-                  }
-                }
+                if (pass && hit) bp_emit<K>(S, k - p0, j0, j1, gid, rj + __popc(m & lt), out, out_eid);
                 rj += __popc(m);
               }
             }
             if (lane == j) run = rj;
           }
+          if (mine) cnt[q] = run;
         }
-        if (valid) cnt[q] = run;
-      }
     }
     __syncthreads();
     if (pass == 0) {

@@ -537,6 +537,9 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.cs_R = b->alloc<double>(E);
   D.ss_k = getenv("GRIP_SS_K") ? atof(getenv("GRIP_SS_K")) : 0.0;
   D.bp_mode = (getenv("GRIP_BP") && std::string(getenv("GRIP_BP")) == "grid") ? 1 : 0;
+  D.bp_qm_min = 1 << 30;   // measured: plain cost comparison is best (GRIP_BP_QM to experiment)
+  D.bp_qm_fac = 1.0f;
+  if (getenv("GRIP_BP_QM")) sscanf(getenv("GRIP_BP_QM"), "%d,%f", &D.bp_qm_min, &D.bp_qm_fac);
   D.cs_valid = b->alloc<int>(E);
   D.md_prev = b->alloc<double>(E);
   D.md_kin = b->alloc<double>(E);
