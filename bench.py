@@ -273,6 +273,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=150, help="CPU baseline: max protocol steps per env (full trial)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lockstep", action="store_true", help="lockstep Batch.step rounds instead of continuous batching")
+    ap.add_argument("--only-kind", type=int, default=-1, help="diagnostic: run only the lanes of this object kind")
     ap.add_argument("--lanes", type=int, default=3,
                     help="1: one device batch; 3k: k device batches (own stream + host thread) per object kind")
     args = ap.parse_args()
@@ -310,6 +311,8 @@ def main():
             of_kind = [i for i, k in zip(ids, slot_kind) if k == kk]
             lane_ids += [of_kind[j::per_kind] for j in range(per_kind)]
         lane_ids = [l for l in lane_ids if l]
+        if args.only_kind >= 0:   # diagnostic: one kind's lane(s) alone
+            lane_ids = [l for l in lane_ids if slot_kind[ids.index(l[0])] == args.only_kind]
     payloads = {j: BatchedGraspTrials.scene_payload(sc.cfg2_scene(j, cands)) for j in range(400)}  # outside timing
     queue = {k: [j for j in range(400) if kinds[j] == k] for k in range(3)}
     qlock = threading.Lock()

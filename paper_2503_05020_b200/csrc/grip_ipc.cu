@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -658,8 +659,18 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   return 0;
 }
 
+// host-side time split of grip_round (GRIP_TRACE_HOST=1 prints it at grip_destroy)
+static double g_host_enq = 0.0, g_host_wait = 0.0, g_host_post = 0.0;
+static long long g_host_rounds = 0;
+static double host_now() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int grip_destroy(GripBatch* b) {
   if (!b) return 0;
+  if (getenv("GRIP_TRACE_HOST") && g_host_rounds)
+    fprintf(stderr, "GRIP_TRACE_HOST rounds %lld enqueue %.3f ms wait %.3f ms post %.3f ms (per round)\n", g_host_rounds,
+            g_host_enq / g_host_rounds, g_host_wait / g_host_rounds, g_host_post / g_host_rounds);
   cudaStreamSynchronize(b->stream);
   for (void* p : b->owned) cudaFree(p);
   for (auto ev : b->kev) cudaEventDestroy(ev);
@@ -991,6 +1002,7 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
                double* alphas) {
   Dev& D = b->D;
   b->snap_valid = false;
+  const double h0 = host_now();
   const int E = b->n_env;
   int nb = 0, n = 0;
   for (int e = 0; e < E; ++e) {
@@ -1016,7 +1028,12 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
   }
   CK(cudaGetLastError());
   if (snapshot_async(b)) return -1;
+  const double h1 = host_now();
   CK(cudaStreamSynchronize(b->stream));
+  const double h2 = host_now();
+  g_host_enq += h1 - h0;
+  g_host_wait += h2 - h1;
+  g_host_rounds += 1;
   kt_collect(b, n);
   const std::vector<int> L(b->h_lists + E, b->h_lists + E + n);
   std::vector<int> ovB, ovS, ovF;
@@ -1074,6 +1091,7 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
     r.pcg_iters = b->s_pi[e];
   }
   if (alphas) memcpy(alphas, b->s_alpha, sizeof(double) * (size_t)E * D.max_alpha);
+  g_host_post += host_now() - h0;
   return 0;
 }
 

@@ -5,7 +5,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 import bench
-sys.argv = ["bench.py", "--no-cpu", "--steps", "100", "--warmup", "200"]
+sys.argv = ["bench.py", "--no-cpu", "--steps", "100", "--warmup", "200"] + sys.argv[1:]
 bench.main()
 from paper_2503_05020_b200 import _native as nv
 out = (ctypes.c_ulonglong * 64)()
