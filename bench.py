@@ -51,20 +51,51 @@ EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, 
             "anchors": 16 + 32 + 48 + 16 + 192 + EL_OUT}  # verts, gamma, T, lam/mu, x and x_prev
 
 
-def _ncu_traffic(kernel):
-    """dram read + write bytes per launch of `kernel` from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "r1_ncu_full_v2.json"
+# kernel groups as timed live (grip_kernel_stats) -> the kernels of the committed ncu capture
+KGROUPS = {"elements": ["k_tet_front", "k_elements_w", "k_tet_jacobi", "k_tet_back", "k_tet_finish"],
+           "assemble_pcg": ["k_contact_K", "k_assemble_direct"], "candidates": ["k_candidates"],
+           "line_search": ["k_linesearch"], "begin": ["k_begin"], "finalize": ["k_finalize"]}
+NCU_FULL = ROOT / "profiles" / "r1_ncu_full_v3.json"
+
+
+def _ncu_group(group):
+    """dram read + write bytes and fp64 FLOPs per launch of a kernel group, from the committed
+    ncu --set full capture (one round: each kernel of the group once)."""
     try:
-        for d in json.loads(p.read_text()):
-            if d["kernel"] == kernel:
-                tot = 0.0
-                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                    v, unit = d[k].split()
-                    tot += float(v) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-                return tot, f"{p.relative_to(ROOT)} (ncu --set full, one launch)"
-    except (OSError, KeyError, ValueError):
-        pass
-    return None, None
+        rows = json.loads(NCU_FULL.read_text())
+    except (OSError, ValueError):
+        return None, None, None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    want = {k: 2 if k == "k_tet_jacobi" else 1 for k in KGROUPS.get(group, [])}   # launches per round
+    seen, traffic, flop = {}, 0.0, 0.0
+    for d in rows:
+        k = d["kernel"].split("::")[-1]
+        if seen.get(k, 0) >= want.get(k, 0):
+            continue
+        seen[k] = seen.get(k, 0) + 1
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v, unit = d[m].split()
+            traffic += float(v.replace(",", "")) * scale[unit]
+        flop += d.get("fp64_flop", 0.0)
+    if not seen:
+        return None, None, None
+    return traffic, flop, f"{NCU_FULL.relative_to(ROOT)} (ncu --set full, one round)"
+
+
+def _fp64_peak():
+    """fp64 DFMA peak: the microbenchmark (tools/fp64_peak.cu) run live, else its committed B200 run."""
+    exe = ROOT / "build" / "fp64_peak"
+    if exe.exists():
+        try:
+            out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60).stdout
+            return float(json.loads(out)["fp64_tflops"]), "measured live (tools/fp64_peak.cu)"
+        except Exception:
+            pass
+    try:
+        d = json.loads((ROOT / "profiles" / "fp64_peak_b200.json").read_text())
+        return float(d["fp64_tflops"]), "profiles/fp64_peak_b200.json (tools/fp64_peak.cu on B200)"
+    except (OSError, ValueError, KeyError):
+        return None, None
 
 
 def _peaks():
@@ -423,19 +454,38 @@ def main():
         ms_max, wall_max, total_steps = ms, wall, float(env_steps)
     value = total_steps / (ms_max / 1e3)
     e2e = total_steps / wall_max
-    # roofline of the dominant kernel (live CUDA events per launch, this rank)
+    # roofline of the dominant kernel group (live CUDA events per launch, this rank)
     dom = max((k for k in ks if k != "work_scan"), key=lambda k: ks[k]["ms"])
     peak, peak_kind = _peaks()
-    roof = {"kernel": dom, "bound": "hbm", "peak": peak, "unit": "GB/s", "peak_source": peak_kind, "traffic": None}
+    roof = {"kernel": dom, "kernels": KGROUPS.get(dom, []), "bound": "hbm", "peak": peak, "unit": "GB/s",
+            "peak_source": peak_kind, "traffic": None}
+    u = ks["elements"]["units"]
+    nlaunch = max(ks[dom]["launches"], 1)
+    sec_per_launch = ks[dom]["ms"] / 1e3 / nlaunch
     if dom == "elements":
-        u = ks["elements"]["units"]
-        alg = sum(EL_BYTES[k] * u[k] for k in EL_BYTES)
-        roof["achieved"] = alg / (ks["elements"]["ms"] / 1e3) / 1e9
-        roof["alg_bytes_per_launch"] = alg / max(ks["elements"]["launches"], 1)
-        roof["traffic"], roof["traffic_source"] = _ncu_traffic("k_elements_w")
+        alg = sum(EL_BYTES[k] * u[k] for k in EL_BYTES) / nlaunch
+    elif dom == "assemble_pcg":
+        # every element's Hessian, gradient and energy read once (1152 + 96 + 8 B)
+        alg = 1256.0 * sum(u.values()) / nlaunch
     else:
-        roof["achieved"] = None
-    roof["frac"] = (roof["achieved"] / peak) if roof.get("achieved") else None
+        alg = None
+    if alg is not None:
+        roof["alg_bytes_per_launch"] = alg
+        roof["achieved"] = alg / sec_per_launch / 1e9
+        roof["frac"] = roof["achieved"] / peak
+    else:
+        roof["achieved"] = roof["frac"] = None
+    traffic, flop, src = _ncu_group(dom)
+    if traffic is not None:
+        roof["traffic"] = traffic
+        roof["traffic_source"] = src
+        roof["traffic_note"] = ("ncu capture = one launch over a single 400-env batch (--lanes 1); "
+                                f"the bench's launches cover {args.envs / len(lanes):.0f} envs each")
+    fpk, fpk_src = _fp64_peak()
+    if flop and fpk:
+        roof["fp64"] = {"flop_per_launch": flop, "achieved_tflops": flop / sec_per_launch / 1e12, "peak_tflops": fpk,
+                        "frac": flop / sec_per_launch / 1e12 / fpk, "peak_source": fpk_src,
+                        "flop_source": "ncu (2 dfma + dadd + dmul thread instructions), " + (src or "")}
     roof["kernel_ms"] = {k: round(v["ms"], 3) for k, v in ks.items()}
     roof["kernel_launches"] = {k: v["launches"] for k, v in ks.items()}
     pk = ks["assemble_pcg"]

@@ -15,7 +15,15 @@ KEYS = [
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+    "sm__cycles_active.sum", "sm__warps_active.avg.per_cycle_active", "smsp__cycles_elapsed.avg",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed",
+    "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed",
 ]
+
+
+def _num(v):
+    return float(v.split()[0].replace(",", ""))
 
 
 def main(rep, out):
@@ -29,12 +37,20 @@ def main(rep, out):
             if k in hdr:
                 i = hdr.index(k)
                 d[k] = f"{r[i]} {units[i]}".strip()
+        try:   # fp64 FLOPs of the launch: (2 dfma + dadd + dmul) thread instructions
+            cyc = _num(d["smsp__cycles_elapsed.avg"])
+            d["fp64_flop"] = cyc * (2 * _num(d["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum.per_cycle_elapsed"])
+                                    + _num(d["smsp__sass_thread_inst_executed_op_dadd_pred_on.sum.per_cycle_elapsed"])
+                                    + _num(d["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum.per_cycle_elapsed"]))
+        except (KeyError, ValueError):
+            pass
         res.append(d)
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     for d in res:
         print(d["kernel"], d.get("gpu__time_duration.sum"), "issue", d.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-              "dram", d.get("dram__bytes_read.sum"), d.get("dram__bytes_write.sum"))
+              "dram", d.get("dram__bytes_read.sum"), d.get("dram__bytes_write.sum"), "fp64 GFLOP",
+              round(d.get("fp64_flop", 0) / 1e9, 3))
 
 
 if __name__ == "__main__":
