@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GRIP_ABI_VERSION 2
+#define GRIP_ABI_VERSION 3
 
 /* Flattened description of N environments (all arrays host, row-major).
  * Index spaces are ENV-LOCAL (node / surface-vertex / body ids restart at 0 in
@@ -159,6 +159,15 @@ int grip_get_contacts(GripBatch* b, double* body_force /* n_body */, uint32_t* c
 int grip_query_candidates(GripBatch* b, int env, double radius, int32_t* pt, int32_t cap_pt, int32_t* n_pt,
                           int32_t* ee, int32_t cap_ee, int32_t* n_ee);
 int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
+/* Contact-event recording (protocol.py:72-75 contact_events_now, contact.py:348-372
+ * ContactSet.stencil_forces): while on, every finalize_step also stores the env's active
+ * stencils of the fresh 1.05*dhat candidate set, PT then EE in canonical order.
+ * grip_get_events copies them for the envs with mask[e]=1, packed in env order:
+ * counts[e] (n_env) = events of env e (> the copied number if the capacity truncated them),
+ * ev_i (7 per event: kind 0 PT / 1 EE, body a, body b, 4 env-local sv ids), ev_d (2 per event:
+ * d, lambda = kappa m |b'(d)|).  cap = rows available in ev_i / ev_d. */
+int grip_set_recording(GripBatch* b, int on);
+int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t* ev_i, double* ev_d, int64_t cap);
 /* per-body centre of mass (n_body*3) and per-env max point speed after the last finalize
  * (solver.py:384-428; read by the protocol's steady / COM tests, protocol.py:231-249) */
 int grip_get_body_state(GripBatch* b, double* body_com, double* max_speed);

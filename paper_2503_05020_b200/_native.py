@@ -15,7 +15,7 @@ import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = Path(os.environ["GRIP_LIB"]) if os.environ.get("GRIP_LIB") else LIB_DIR / "libgripipc.so"  # GRIP_LIB: A/B builds
-ABI_VERSION = 2
+ABI_VERSION = 3
 NPARAM = 14
 (P_DT, P_KAPPA, P_DHAT, P_EPSV, P_RELTOL, P_MAXIT, P_ELLFLOOR, P_MAXLS, P_CCDSCALE, P_CCDIT, P_KINGUARD, P_MURULE,
  P_PCGRTOL, P_SPARE) = range(NPARAM)
@@ -93,7 +93,8 @@ def load():
         ("grip_kernel_stats", [vp, i32, vp, vp, vp]), ("grip_stream_timer", [vp, i32, vp]),
         ("grip_round", [vp, vp, vp, vp, vp, vp]),
         ("grip_debug_elements", [i32, i32, vp, i32, vp, vp, vp, vp]),
-        ("grip_reset_envs", [vp, vp, vp, vp, vp, vp])):
+        ("grip_reset_envs", [vp, vp, vp, vp, vp, vp]), ("grip_set_recording", [vp, i32]),
+        ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64])):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = i32
@@ -244,6 +245,38 @@ class DeviceBatch:
         sp = np.empty(self.n_env)
         check(self.lib.grip_get_body_state(self.h, ptr(com), ptr(sp)))
         return com, sp
+
+    def set_recording(self, on=True):
+        """Contact-event recording in every finalize (grip_set_recording)."""
+        check(self.lib.grip_set_recording(self.h, int(on)))
+
+    EVENT_KINDS = ("point-triangle", "edge-edge")
+
+    def events(self, mask):
+        """Contact events of the last finalize for envs with mask[e] (protocol.py:72-75): a dict
+        env -> list of {kind, bodies, verts, d, lambda} in the reference's order."""
+        m = np.ascontiguousarray(mask, np.uint8)
+        counts = np.zeros(self.n_env, np.int32)
+        cap = int(max(1, m.sum()) * 64)
+        while True:
+            ei = np.zeros((cap, 7), np.int32)
+            ed = np.zeros((cap, 2))
+            rc = self.lib.grip_get_events(self.h, ptr(m), ptr(counts), ptr(ei), ptr(ed), cap)
+            if rc == 0:
+                break
+            if b"capacity" not in self.lib.grip_last_error():
+                check(rc)
+            cap *= 2
+        out, off = {}, 0
+        for e in np.nonzero(m)[0]:
+            n = int(counts[e])
+            rows = []
+            for k in range(off, off + n):
+                rows.append({"kind": self.EVENT_KINDS[ei[k, 0]], "bodies": (int(ei[k, 1]), int(ei[k, 2])),
+                             "verts": [int(v) for v in ei[k, 3:7]], "d": float(ed[k, 0]), "lambda": float(ed[k, 1])})
+            out[int(e)] = rows
+            off += n
+        return out
 
     def set_profiling(self, on=True):
         check(self.lib.grip_set_profiling(self.h, int(on)))

@@ -123,6 +123,12 @@ struct Dev {
   int* anc_v;        // 4
   double *anc_gamma, *anc_T, *anc_lam, *anc_mu;   // 4, 6, 1, 1
   int* anc_b;        // 2
+  // contact events of the last finalize (protocol.py:72-75 contact_events_now; recorded when ev_on):
+  // per env cap_anc slots, active stencils in candidate order (PT then EE)
+  int ev_on;
+  int* ev_i;         // 7 per event: kind (0 PT, 1 EE), body a, body b, 4 vertices
+  double* ev_d;      // 2 per event: d, lambda
+  int* ev_n;         // per env: event count (may exceed cap_anc: truncated)
   // scratch
   int max_sv, max_tri, max_edge, max_free, max_node;
   int cap_cells;

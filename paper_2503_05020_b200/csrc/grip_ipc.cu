@@ -165,6 +165,8 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   ok &= grow_anc(D.anc_lam, 1);
   ok &= grow_anc(D.anc_mu, 1);
   ok &= grow_anc(D.anc_b, 2);
+  ok &= swap_alloc(D.ev_i, E * 7 * D.cap_anc);   // events: per step, not preserved across growth
+  ok &= swap_alloc(D.ev_d, E * 2 * D.cap_anc);
   if (!ok) {
     g_err = "out of device memory growing candidate/element buffers";
     return -1;
@@ -552,6 +554,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.work_off = b->alloc<int>(E + 1);
   D.cwork_off = b->alloc<int>(E + 1);
   D.twork_off = b->alloc<int>(E + 1);
+  D.ev_n = b->alloc<int>(E);
+  D.ev_on = 0;
   D.ework_off = b->alloc<int>(E + 1);
   D.max_sv = max_sv; D.max_tri = max_tri; D.max_edge = max_edge; D.max_free = max_free;
   D.max_node = max_node; D.max_tet = max_tet; D.max_abd = max_abd;
@@ -642,7 +646,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
-        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
+        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
@@ -1092,6 +1096,39 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
   }
   if (alphas) memcpy(alphas, b->s_alpha, sizeof(double) * (size_t)E * D.max_alpha);
   g_host_post += host_now() - h0;
+  return 0;
+}
+
+int grip_set_recording(GripBatch* b, int on) {
+  b->D.ev_on = on ? 1 : 0;
+  return 0;
+}
+
+int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t* ev_i, double* ev_d, int64_t cap) {
+  Dev& D = b->D;
+  if (!D.ev_on) {
+    g_err = "grip_get_events: recording is off (grip_set_recording)";
+    return -1;
+  }
+  const int E = b->n_env;
+  CK(cudaMemcpyAsync(counts, D.ev_n, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  int64_t off = 0;
+  for (int e = 0; e < E; ++e) {
+    if (!mask[e]) continue;
+    const int n = std::min(counts[e], D.cap_anc);
+    if (off + n > cap) {
+      g_err = "grip_get_events: output capacity too small";
+      return -1;
+    }
+    if (n) {
+      const size_t s = (size_t)e * D.cap_anc;
+      CK(cudaMemcpyAsync(ev_i + 7 * off, D.ev_i + 7 * s, sizeof(int) * 7 * n, cudaMemcpyDeviceToHost, b->stream));
+      CK(cudaMemcpyAsync(ev_d + 2 * off, D.ev_d + 2 * s, sizeof(double) * 2 * n, cudaMemcpyDeviceToHost, b->stream));
+    }
+    off += n;
+  }
+  CK(cudaStreamSynchronize(b->stream));
   return 0;
 }
 

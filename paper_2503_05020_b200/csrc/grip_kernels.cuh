@@ -1278,7 +1278,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   for (int s = 0; s < npt + nee; s += NT) {
     const int k = s + threadIdx.x;
     int act = 0;
-    double lam = 0.0, gam[4], Tm[6], mu = 0.0;
+    double lam = 0.0, gam[4], Tm[6], mu = 0.0, dmin_k = 0.0;
     int rowv[4], bb[2];
     if (k < npt + nee) {
       const bool is_ee = k >= npt;
@@ -1291,6 +1291,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
       double Dq, bary[3], sp = 0.0, tp = 0.0;
       Dq = is_ee ? ee_closest(x[0], x[1], x[2], x[3], &sp, &tp) : pt_closest(x[0], x[1], x[2], x[3], bary, nullptr);
       dmin = fmin(dmin, Dq);
+      dmin_k = Dq;
       if (Dq < dhat * dhat) {
         act = 1;
         const double d = sqrt(Dq);
@@ -1339,6 +1340,16 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
     }
     int tot;
     const int pre = block_scan(act, sm, &tot);
+    if (act && D.ev_on && base + pre < D.cap_anc) {
+      const size_t vi = (size_t)e * D.cap_anc + base + pre;
+      int* ei = D.ev_i + 7 * vi;
+      ei[0] = k >= npt;
+      ei[1] = bb[0];
+      ei[2] = bb[1];
+      for (int j = 0; j < 4; ++j) ei[3 + j] = rowv[j];
+      D.ev_d[2 * vi] = sqrt(dmin_k);
+      D.ev_d[2 * vi + 1] = lam;
+    }
     if (act && !failed && base + pre < D.cap_anc) {
       const size_t ai = (size_t)e * D.cap_anc + base + pre;
       for (int j = 0; j < 4; ++j) {
@@ -1414,6 +1425,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   if (threadIdx.x < nbl) D.contact_mask[E.b0 + threadIdx.x] = cmask[threadIdx.x];
   if (threadIdx.x == 0) {
     D.fin_done[e] = 1;
+    if (D.ev_on) D.ev_n[e] = base;
     if (!failed) D.n_anc[e] = base;
     D.min_dist[e] = (!failed && (npt + nee) > 0) ? sqrt(dmin) : INFINITY;
     D.time[e] += dt;

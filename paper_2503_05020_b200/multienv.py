@@ -149,6 +149,16 @@ class DeviceEnvGroup:
         a, b = self.packed.body_off[slot], self.packed.body_off[slot + 1]
         return f[a:b], m[a:b], float(md[slot])
 
+    def _events(self, slot):
+        """Device contact events of the slot's last finalize (recording switched on here)."""
+        if not getattr(self, "_recording", False):
+            raise RuntimeError("contact-event recording is off for this device group")
+        return self.dev.events(self._mask([slot]))[slot]
+
+    def set_recording(self, on=True):
+        self.dev.set_recording(on)
+        self._recording = bool(on)
+
     def _stress(self, slot):
         s = self.dev.stress()
         a, b = self.packed.tet_off[slot], self.packed.tet_off[slot + 1]

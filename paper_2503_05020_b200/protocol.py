@@ -50,6 +50,7 @@ class TrialRecord:
     times: np.ndarray = None
     stress: np.ndarray = None
     step_reports: list = field(default_factory=list)
+    contacts: list = field(default_factory=list)      # per step: list of contact events
     com_displacement: dict = field(default_factory=dict)
     halt_forces: dict = field(default_factory=dict)
     finger_forces: list = field(default_factory=list)
@@ -183,7 +184,23 @@ def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closi
     rec = TrialRecord(object_body=object_body,
                       gripper_bodies=tuple(sorted({b for ids in finger_links.values() for b in ids})))
     markers, halt_forces, positions, reps, times, forces_log, stress = {}, {}, [], [], [], [], []
+    velocities, contacts_log = [], []
     n_done = [0]
+    group = env._owner()
+    if record:
+        group.set_recording(True)   # contact events straight from the device finalize
+    kin_recs = [r for r in env.records if r["kind"] == "kinematic"]
+
+    def snapshot(events, report, forces):
+        """protocol.py:113-146 (_Recorder.snapshot)."""
+        kp = [r["positions"] for r in kin_recs]
+        kv = [np.tile(np.asarray(r["body"].velocity, np.float64), (r["n_sv"], 1)) for r in kin_recs]
+        positions.append(np.concatenate([env.node_positions()] + kp) if kp else env.node_positions().copy())
+        velocities.append(np.concatenate([env.v.reshape(-1, 3)] + kv) if kv else env.v.reshape(-1, 3).copy())
+        stress.append(env.stress_rows())
+        contacts_log.append(events)
+        reps.append(report.to_dict())
+        forces_log.append(forces)
 
     def fail(phase, report):
         rec.verdict = "sim-failed"
@@ -195,15 +212,13 @@ def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closi
         start = n_done[0]
         for _ in range(n_steps):
             report = env.step()
-            events = contact_events_now(env)
+            events = group._events(env._slot) if record else contact_events_now(env)
             last_events[0] = events
             forces = {f: finger_contact_force(env, ids, events) for f, ids in finger_links.items()}
             n_done[0] += 1
             times.append(env.time)
             if record:
-                positions.append(env.node_positions().copy())
-                reps.append(report.to_dict())
-                forces_log.append(forces)
+                snapshot(events, report, forces)
             if per_step is not None:
                 per_step(forces)
             if report.status == "failed":
@@ -272,7 +287,11 @@ def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closi
     rec.n_steps = n_done[0]
     if record:
         rec.positions = np.array(positions)
+        rec.velocities = np.array(velocities)
         rec.times = np.array(times)
+        n_tets = env.layout.n_tet
+        rec.stress = np.array(stress) if n_tets else np.zeros((len(times), 0, 7))
+        rec.contacts = contacts_log
         rec.step_reports = reps
         rec.finger_forces = forces_log
     return rec

@@ -444,6 +444,28 @@ def _verdict_job(args):
             "positions": r.positions.tolist() if (seed == 0 and kind == "box" and not soft_object) else None}
 
 
+def gen_dataset(out):
+    """One config-1 trial (box, seed 0) under a shortened protocol, emitted by the reference's own
+    dataset writer (pipeline/dataset.py:121-167): the byte-level and value-level fixture of §8f-3."""
+    import shutil
+    from gripsim.pipeline import dataset as ds
+    sc = scene_for("box")
+    c = candidate("box", 0)
+    env, ob, fl = cfg.build_trial_env(sc, c)
+    prot = proto.TrialProtocol(settle_duration=0.02, steady_max_duration=0.05, gravity_phase_duration=0.02)
+    rec = proto.run_grasp_trial(env, prot, ob, fl)
+    rec.candidate = {"R": np.asarray(c.rotation).tolist(), "T": np.asarray(c.translation).tolist(),
+                     "opening": float(c.joints[0])}
+    dest = out / "dataset_cfg1"
+    if dest.exists():
+        shutil.rmtree(dest)
+    manifest = ds.emit_dataset([rec], dest, params={"protocol": "short", "seed": 0})
+    (out / "dataset_cfg1_protocol.json").write_text(json.dumps(
+        {"settle_duration": 0.02, "steady_max_duration": 0.05, "gravity_phase_duration": 0.02,
+         "R": rec.candidate["R"], "T": rec.candidate["T"], "opening": rec.candidate["opening"]}))
+    print("dataset", rec.verdict, rec.n_steps, manifest["trials"][0]["files"])
+
+
 def _cand_job(i):
     kind = KINDS[i % 3]
     c = candidate(kind, i)
@@ -471,7 +493,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*")
     args = ap.parse_args()
-    want = set(args.only or ["kernels", "meshes", "traj", "bimanual", "verdicts", "candidates"])
+    want = set(args.only or ["kernels", "meshes", "traj", "bimanual", "verdicts", "candidates", "dataset"])
     out = HERE
     ctx = mp.get_context("fork")
     scene_for("cylinder")  # write the cylinder OBJ once, before forking
@@ -480,6 +502,8 @@ def main():
         gen_kernels(out); print("kernels", time.time() - t0)
     if "meshes" in want:
         gen_meshes(out); print("meshes", time.time() - t0)
+    if "dataset" in want:
+        gen_dataset(out); print("dataset", time.time() - t0)
     with ctx.Pool(os.cpu_count()) as pool:
         if "traj" in want:
             jobs = [

@@ -1,0 +1,115 @@
+"""Dataset emission: byte compatibility with the reference's writer and, on the
+GPU, a recorded trial against the trial the reference recorded (tests/golden/dataset_cfg1,
+written by gripsim.pipeline.dataset.emit_dataset in tests/golden/make_golden.py)."""
+
+import hashlib
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2503_05020_b200 import dataset as ds
+from paper_2503_05020_b200.protocol import TrialRecord
+
+GOLD = Path(__file__).resolve().parent / "golden" / "dataset_cfg1"
+
+
+def _sha(p):
+    return hashlib.sha256(Path(p).read_bytes()).hexdigest()
+
+
+def _record_from_golden(tr):
+    meta = tr["meta"]
+    steps = [json.loads(line) for line in (GOLD / "trial_0000" / "steps.jsonl").read_text().splitlines()]
+    rec = TrialRecord(candidate=meta["candidate"], verdict=meta["verdict"], failure=meta["failure"],
+                      phase_markers=meta["phase_markers"], positions=tr["positions"], velocities=tr["velocities"],
+                      times=tr["times"], stress=tr["stress"], step_reports=steps,
+                      com_displacement=meta["com_displacement"], halt_forces=meta["halt_forces"],
+                      finger_forces=meta["finger_forces"], metrics=meta["metrics"], object_body=meta["object_body"],
+                      gripper_bodies=tuple(meta["gripper_bodies"]), n_steps=meta["n_steps"])
+    rec.contacts = [c["events"] for c in tr["contacts"]]
+    return rec, meta["params"]
+
+
+def test_loaders_read_reference_files():
+    man = ds.load_manifest(GOLD)
+    assert man["format"] == "gripsim-dataset-v1" and man["n_trials"] == 1
+    tr = ds.load_trial(GOLD / "trial_0000")
+    n = tr["meta"]["n_steps"]
+    assert tr["positions"].shape == (n, tr["positions"].shape[1], 3) and tr["velocities"].shape == tr["positions"].shape
+    assert tr["stress"].shape[0] == n and tr["stress"].shape[2] == 7
+    assert len(tr["contacts"]) == n and [c["step"] for c in tr["contacts"]] == list(range(n))
+    for f, h in man["trials"][0]["files"].items():
+        assert _sha(GOLD / "trial_0000" / f) == h
+
+
+def test_writer_reproduces_reference_bytes(tmp_path):
+    tr = ds.load_trial(GOLD / "trial_0000")
+    rec, params = _record_from_golden(tr)
+    man = ds.emit_dataset([rec], tmp_path, params=params)
+    gold = ds.load_manifest(GOLD)
+    assert man == gold
+    assert (tmp_path / "manifest.json").read_bytes() == (GOLD / "manifest.json").read_bytes()
+
+
+def test_traj_loader_rejects_bad_files(tmp_path):
+    p = tmp_path / "t.bin"
+    ds.write_traj(p, np.arange(3) * 0.01, np.zeros((3, 2, 3)), np.zeros((3, 2, 3)))
+    raw = bytearray(p.read_bytes())
+    raw[24] = 7  # frame 0 index
+    p.write_bytes(bytes(raw))
+    with pytest.raises(ValueError, match="index"):
+        ds.load_traj(p)
+    p.write_bytes(b"NOTATRAJ" + bytes(16))
+    with pytest.raises(ValueError, match="magic"):
+        ds.load_traj(p)
+    q = tmp_path / "s.bin"
+    ds.write_stress(q, np.zeros((0, 0, 7)))
+    assert ds.load_stress(q).shape == (0, 0, 7)
+
+
+@pytest.mark.gpu
+def test_recorded_trial_matches_reference(tmp_path):
+    """Our run_grasp_trial (device step, device contact events, device stress) under the same
+    shortened protocol as the golden trial, emitted by our writer: same verdict, markers, step
+    count, Newton iterations and contact stencils; positions within 1e-6 ell."""
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.protocol import TrialProtocol, run_grasp_trial
+    from paper_2503_05020_b200.solver import Environment
+
+    pj = json.loads((GOLD.parent / "dataset_cfg1_protocol.json").read_text())
+    s = sc.build_trial_scene(sc.ObjectSpec(kind="box"), sc.GripperSpec(soft_fingers=True), np.array(pj["R"]),
+                             np.array(pj["T"]), float(pj["opening"]))
+    env = Environment(s.bodies, collide_pairs_off=s.collide_pairs_off)
+    prot = TrialProtocol(settle_duration=pj["settle_duration"], steady_max_duration=pj["steady_max_duration"],
+                         gravity_phase_duration=pj["gravity_phase_duration"])
+    ell = max(env.bbox_diagonal(), 0.05)
+    rec = run_grasp_trial(env, prot, s.object_body, s.finger_links, record=True, closing_dirs=s.closing_dirs)
+    rec.candidate = {"R": pj["R"], "T": pj["T"], "opening": pj["opening"]}
+    ds.emit_dataset([rec], tmp_path, params={"protocol": "short", "seed": 0})
+    ours = ds.load_trial(tmp_path / "trial_0000")
+    ref = ds.load_trial(GOLD / "trial_0000")
+    mo, mr = ours["meta"], ref["meta"]
+    for k in ("verdict", "failure", "phase_markers", "n_steps", "object_body", "gripper_bodies"):
+        assert mo[k] == mr[k], k
+    assert set(mo["halt_forces"]) == set(mr["halt_forces"])
+    for f in mr["halt_forces"]:
+        assert mo["halt_forces"][f]["step"] == mr["halt_forces"][f]["step"]
+        assert np.isclose(mo["halt_forces"][f]["force"], mr["halt_forces"][f]["force"], rtol=1e-6)
+    assert ours["positions"].shape == ref["positions"].shape
+    assert np.abs(ours["positions"] - ref["positions"]).max() <= 1e-6 * ell
+    assert np.abs(ours["velocities"] - ref["velocities"]).max() <= 1e-6 * ell / 0.01
+    np.testing.assert_allclose(ours["times"], ref["times"], rtol=0, atol=1e-12)
+    sr = np.abs(ref["stress"]).max()
+    assert np.abs(ours["stress"] - ref["stress"]).max() <= 1e-6 * sr
+    for co, cr in zip(ours["contacts"], ref["contacts"]):
+        assert [(e["kind"], e["bodies"], e["verts"]) for e in co["events"]] == \
+               [(e["kind"], e["bodies"], e["verts"]) for e in cr["events"]]
+        for eo, er in zip(co["events"], cr["events"]):
+            assert abs(eo["d"] - er["d"]) <= 1e-6 * ell
+            assert np.isclose(eo["lambda"], er["lambda"], rtol=1e-5, atol=1e-9)
+    so = [json.loads(x) for x in (tmp_path / "trial_0000" / "steps.jsonl").read_text().splitlines()]
+    sref = [json.loads(x) for x in (GOLD / "trial_0000" / "steps.jsonl").read_text().splitlines()]
+    assert [(r["step"], r["status"], r["iterations"], r["reason"]) for r in so] == \
+           [(r["step"], r["status"], r["iterations"], r["reason"]) for r in sref]

@@ -25,7 +25,8 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     lib.grip_abi_version.restype = ctypes.c_int
-    assert lib.grip_abi_version() == 2
+    from paper_2503_05020_b200 import _native as nv
+    assert lib.grip_abi_version() == nv.ABI_VERSION == 3
 
 
 def test_struct_layouts_match_header():
