@@ -316,9 +316,19 @@ class BatchedGraspTrials:
     sequence of controls and decisions; envs are only batched, never coupled.
     """
 
-    def __init__(self, group, scenes, protocol=None):
+    def __init__(self, group, scenes, protocol=None, record=False):
         self.group = group
         self.dev = group.dev
+        self.record = record
+        if record:   # per-step frames for dataset emission (protocol.py:113-146, dataset.py)
+            group.set_recording(True)
+            p0 = group.packed
+            self._kin_sl = []
+            for i, env in enumerate(group.envs):
+                sl = [(int(p0.sv_off[i]) + r.surf0, int(p0.sv_off[i]) + r.surf0 + r.n_sv, r.id)
+                      for r in env.layout.records if r.kind == "kinematic"]
+                self._kin_sl.append(sl)
+            self._frames = [self._empty_frames() for _ in group.envs]
         self.protocol = pr = protocol or TrialProtocol()
         p = group.packed
         E = p.n_env
@@ -360,6 +370,48 @@ class BatchedGraspTrials:
                         for s in scenes]
         self.env_steps = 0
         self.reports = []
+
+    @staticmethod
+    def _empty_frames():
+        return {"x": [], "v": [], "t": [], "stress": [], "events": [], "reports": [], "forces": []}
+
+    def _snapshot(self, ids, rep, alphas, events, ff):
+        """Record one frame for every env in ids (the reference's _Recorder.snapshot)."""
+        from paper_2503_05020_b200.solver import report_from_row
+        p = self.group.packed
+        x, v, kin = self.dev.get_state(True)
+        st = self.dev.stress()
+        boff = p.body_off
+        for k, e in enumerate(ids):
+            n0, n1 = p.node_off[e], p.node_off[e + 1]
+            kp = [kin[a:b] for a, b, _ in self._kin_sl[e]]
+            kv = [np.tile(self.vel[boff[e] + bid], (b - a, 1)) for a, b, bid in self._kin_sl[e]]
+            fr = self._frames[e]
+            fr["x"].append(np.concatenate([x[n0:n1]] + kp))
+            fr["v"].append(np.concatenate([v[n0:n1]] + kv))
+            env = self.group.envs[e]
+            fr["t"].append(env._time + env.solver_params.dt)   # env.time after the step, accumulated
+            fr["stress"].append(st[p.tet_off[e]:p.tet_off[e + 1]].copy())
+            fr["events"].append(events[e])
+            r = report_from_row(rep[e], alphas[e], self.group.envs[e].env_id)
+            r.time = env._time
+            r.step_index = env._step
+            fr["reports"].append(r.to_dict())
+            fr["forces"].append({self.fnames[e][j]: ff[k][j] for j in range(len(ff[k]))})
+
+    def _close_record(self, e):
+        """Move env e's frames into its TrialRecord (trial finished)."""
+        fr = self._frames[e]
+        r = self.records[e]
+        r.positions = np.array(fr["x"])
+        r.velocities = np.array(fr["v"])
+        r.times = np.array(fr["t"])
+        nt = self.group.packed.tet_off[e + 1] - self.group.packed.tet_off[e]
+        r.stress = np.array(fr["stress"]) if nt else np.zeros((len(fr["t"]), 0, 7))
+        r.contacts = fr["events"]
+        r.step_reports = fr["reports"]
+        r.finger_forces = fr["forces"]
+        self._frames[e] = self._empty_frames()
 
     @property
     def done(self):
@@ -406,6 +458,8 @@ class BatchedGraspTrials:
             self.halted[e] = False
             self.com_disp[e] = np.nan
             self.records[e] = TrialRecord(object_body=sc.object_body, gripper_bodies=self.records[e].gripper_bodies)
+            if self.record:
+                self._frames[e] = self._empty_frames()
             env = self.group.envs[e]
             env._time, env._step, env.status = 0.0, 0, "active"
             mask[e] = 1
@@ -423,7 +477,7 @@ class BatchedGraspTrials:
         mask[ids] = 1
         self.dev.set_controls(self.grav, self.vel)
         rep, alphas = self.dev.step(mask)
-        self._after_step(ids, rep, keep_reports)
+        self._after_step(ids, rep, keep_reports, alphas)
         return len(ids)
 
     def advance_round(self, keep_reports=False):
@@ -444,16 +498,25 @@ class BatchedGraspTrials:
         self._need = np.zeros(self.E, bool)
         ids = np.nonzero(fin)[0]
         if len(ids):
-            self._after_step(ids, rep, keep_reports)
+            self._after_step(ids, rep, keep_reports, alphas)
             self._need[ids] = self.phase[ids] != _DONE
         return len(ids)
 
-    def _after_step(self, ids, rep, keep_reports=False):
+    def _after_step(self, ids, rep, keep_reports=False, alphas=None):
         """Protocol bookkeeping after envs `ids` completed a time step (protocol.py:176-188)."""
         pr = self.protocol
         force, cmask, _ = self.dev.contacts()
         com, speed = self.dev.body_state()
         self.group.invalidate()
+        if self.record:
+            m = np.zeros(self.E, np.uint8)
+            m[ids] = 1
+            events = self.dev.events(m)
+            # finger forces from the recorded events, as the reference sums them (protocol.py:78-86)
+            fsum = [[sum(ev["lambda"] for ev in events[e] if (self.fb[e, j] - self.group.packed.body_off[e])
+                         in ev["bodies"]) for j in range(self.fb.shape[1])] for e in ids]
+            ffr = np.array(fsum, np.float64).reshape(len(ids), self.fb.shape[1])
+            self._snapshot(ids, rep, alphas, events, fsum)
         for e in ids:
             env = self.group.envs[e]
             env._time += env.solver_params.dt
@@ -465,6 +528,8 @@ class BatchedGraspTrials:
         self.pstep[ids] += 1
         ph = self.phase[ids]
         ff = force[self.fb[ids]]                       # (n, fingers)
+        if self.record:
+            ff = ffr   # the recorded events' sums, exactly as the single-env recorder halts on
         # close-phase halting happens before the failure check (protocol.py:181-186)
         closing = ph == _CLOSE
         newly = closing[:, None] & ~self.halted[ids] & (ff > pr.force_halt)
@@ -532,6 +597,8 @@ class BatchedGraspTrials:
                     self.com0[e] = com[self.obj[e]]
         for e in ids:
             self.records[e].n_steps = int(self.nsteps[e])
+            if self.record and self.phase[e] == _DONE:
+                self._close_record(e)
 
     def run(self, max_steps=None, lockstep=False):
         n = 0
@@ -541,6 +608,7 @@ class BatchedGraspTrials:
         return self.records
 
 
-def run_grasp_trials(group, scenes, protocol=None, max_steps=None, lockstep=False):
-    """Protocol for all envs of a group; returns TrialRecords (labels, markers, COM, halts)."""
-    return BatchedGraspTrials(group, scenes, protocol).run(max_steps, lockstep=lockstep)
+def run_grasp_trials(group, scenes, protocol=None, max_steps=None, lockstep=False, record=False):
+    """Protocol for all envs of a group; returns TrialRecords (labels, markers, COM, halts; with
+    record=True also the per-step frames the reference's recorder keeps, for dataset emission)."""
+    return BatchedGraspTrials(group, scenes, protocol, record=record).run(max_steps, lockstep=lockstep)

@@ -113,3 +113,36 @@ def test_recorded_trial_matches_reference(tmp_path):
     sref = [json.loads(x) for x in (GOLD / "trial_0000" / "steps.jsonl").read_text().splitlines()]
     assert [(r["step"], r["status"], r["iterations"], r["reason"]) for r in so] == \
            [(r["step"], r["status"], r["iterations"], r["reason"]) for r in sref]
+
+
+@pytest.mark.gpu
+def test_batched_recording_matches_single_env(tmp_path):
+    """BatchedGraspTrials(record=True): the golden trial recorded inside a batch of 3 (continuous
+    batching) gives the same emitted trial as the single-env recorder, byte for byte."""
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.multienv import DeviceEnvGroup
+    from paper_2503_05020_b200.protocol import BatchedGraspTrials, TrialProtocol, run_grasp_trial
+    from paper_2503_05020_b200.solver import Environment
+
+    pj = json.loads((GOLD.parent / "dataset_cfg1_protocol.json").read_text())
+    prot = TrialProtocol(settle_duration=pj["settle_duration"], steady_max_duration=pj["steady_max_duration"],
+                         gravity_phase_duration=pj["gravity_phase_duration"])
+    cands = sc.load_cfg2_candidates()
+    scenes = [sc.build_trial_scene(sc.ObjectSpec(kind="box"), sc.GripperSpec(soft_fingers=True), np.array(pj["R"]),
+                                   np.array(pj["T"]), float(pj["opening"]))] + [sc.cfg2_scene(i, cands) for i in (3, 6)]
+    envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+    trials = BatchedGraspTrials(DeviceEnvGroup(envs), scenes, prot, record=True)
+    recs = trials.run()
+    one = sc.build_trial_scene(sc.ObjectSpec(kind="box"), sc.GripperSpec(soft_fingers=True), np.array(pj["R"]),
+                               np.array(pj["T"]), float(pj["opening"]))
+    env1 = Environment(one.bodies, collide_pairs_off=one.collide_pairs_off)
+    r1 = run_grasp_trial(env1, prot, one.object_body, one.finger_links, record=True, closing_dirs=one.closing_dirs)
+    for r in (recs[0], r1):
+        r.candidate = {"R": pj["R"], "T": pj["T"], "opening": pj["opening"]}
+    ma = ds.emit_dataset([recs[0]], tmp_path / "batched")
+    mb = ds.emit_dataset([r1], tmp_path / "single")
+    a = json.loads((tmp_path / "batched" / "trial_0000" / "meta.json").read_text())
+    b = json.loads((tmp_path / "single" / "trial_0000" / "meta.json").read_text())
+    assert [k for k in a if a[k] != b[k]] == []
+    assert ma["trials"][0]["files"] == mb["trials"][0]["files"]
+    assert recs[1].positions is not None and len(recs[1].contacts) == recs[1].n_steps
