@@ -304,6 +304,8 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=150, help="CPU baseline: max protocol steps per env (full trial)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lockstep", action="store_true", help="lockstep Batch.step rounds instead of continuous batching")
+    ap.add_argument("--record", default=None, help="record every trial (frames, stress, contact events) and "
+                                                   "emit it to this directory in the reference's dataset format")
     ap.add_argument("--only-kind", type=int, default=-1, help="diagnostic: run only the lanes of this object kind")
     ap.add_argument("--lanes", type=int, default=3,
                     help="1: one device batch; 3k: k device batches (own stream + host thread) per object kind")
@@ -354,7 +356,7 @@ def main():
             scenes = [sc.cfg2_scene(i % 400, cands) for i in lids]
             envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
             self.group = DeviceEnvGroup(envs, device=local)
-            self.trials = BatchedGraspTrials(self.group, scenes)
+            self.trials = BatchedGraspTrials(self.group, scenes, record=args.record is not None)
             self.dev = self.group.dev
             self.kind = np.array([kinds[i % 400] for i in lids])
             self.done_trials = []
@@ -370,6 +372,8 @@ def main():
             with qlock:
                 for e in fin:
                     self.done_trials.append(self.trials.records[e].verdict)
+                    if writer is not None:
+                        writer.put(self.trials.records[e])
                     k = int(self.kind[e])
                     pls.append(payloads[queue[k][qpos[k] % len(queue[k])]])
                     qpos[k] += 1
@@ -381,6 +385,25 @@ def main():
             self.env_steps += n
             self.rounds += 1
 
+    writer = None
+    if args.record is not None:
+        # dataset emission: finished trials go to a writer thread (dataset.py)
+        import queue as queue_mod
+        from paper_2503_05020_b200 import dataset as ds
+        writer = queue_mod.Queue()
+        out_dir = Path(args.record)
+        n_written = [0]
+
+        def write_loop():
+            while True:
+                rec = writer.get()
+                if rec is None:
+                    return
+                ds.emit_trial(rec, out_dir / f"trial_{n_written[0]:05d}")
+                n_written[0] += 1
+
+        wthread = threading.Thread(target=write_loop, daemon=True)
+        wthread.start()
     lanes = [Lane(l) for l in lane_ids]
 
     def run_lanes(n_rounds, timed):
@@ -389,7 +412,16 @@ def main():
         main_lane = max(range(len(lanes)), key=lambda i: len(lane_ids[i]))
         stop = threading.Event()
 
+        errors = []
+
         def work(i):
+            try:
+                work_lane(i)
+            except BaseException as exc:   # surface a lane's failure in the main thread
+                errors.append(exc)
+                stop.set()
+
+        def work_lane(i):
             ln = lanes[i]
             if timed:
                 ln.dev.timer_start()
@@ -408,6 +440,8 @@ def main():
             t.start()
         for t in th:
             t.join()
+        if errors:
+            raise errors[0]
 
     run_lanes(args.warmup, False)
     for ln in lanes:
@@ -509,6 +543,8 @@ def main():
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": roof,
         "gpu_launches": int(launches),
+        "recording": None if writer is None else {"dir": str(args.record), "trials_written": n_written[0],
+                                                  "format": "gripsim-dataset-v1 (traj.bin, stress.bin, jsonl, meta)"},
         "clocks": clk.summary(),
     }
     if world > 1:

@@ -163,7 +163,7 @@ int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
  * ContactSet.stencil_forces): while on, every finalize_step also stores the env's active
  * stencils of the fresh 1.05*dhat candidate set, PT then EE in canonical order.
  * grip_get_events copies them for the envs with mask[e]=1, packed in env order:
- * counts[e] (n_env) = events of env e (> the copied number if the capacity truncated them),
+ * counts[e] (n_env) = events of env e copied (bounded by the anchor capacity),
  * ev_i (7 per event: kind 0 PT / 1 EE, body a, body b, 4 env-local sv ids), ev_d (2 per event:
  * d, lambda = kappa m |b'(d)|).  cap = rows available in ev_i / ev_d. */
 int grip_set_recording(GripBatch* b, int on);

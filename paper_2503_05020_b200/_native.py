@@ -123,6 +123,28 @@ def debug_elements(etype, inputs):
     return E, g, H.reshape(n, 12, 12), fl
 
 
+class EventBlock:
+    """One step's contact events of one env, as arrays (contact.py:348-372 stencil_forces rows)."""
+
+    __slots__ = ("i", "d")
+    KINDS = ("point-triangle", "edge-edge")
+
+    def __init__(self, i, d):
+        self.i, self.d = i, d
+
+    def __len__(self):
+        return len(self.i)
+
+    def as_dicts(self):
+        return [{"kind": self.KINDS[r[0]], "bodies": (int(r[1]), int(r[2])), "verts": [int(v) for v in r[3:7]],
+                 "d": float(dd[0]), "lambda": float(dd[1])} for r, dd in zip(self.i.tolist(), self.d)]
+
+    def force_on(self, body):
+        """Summed lambda of the events touching `body` (protocol.py:78-86); 0 (int) when none."""
+        sel = (self.i[:, 1] == body) | (self.i[:, 2] == body)
+        return sum(self.d[sel, 1].tolist()) if sel.any() else 0
+
+
 class DeviceBatch:
     """Owns one GripBatch handle (device memory + stream) built from a packed scene."""
 
@@ -252,9 +274,9 @@ class DeviceBatch:
 
     EVENT_KINDS = ("point-triangle", "edge-edge")
 
-    def events(self, mask):
-        """Contact events of the last finalize for envs with mask[e] (protocol.py:72-75): a dict
-        env -> list of {kind, bodies, verts, d, lambda} in the reference's order."""
+    def event_blocks(self, mask):
+        """Contact events of the last finalize for envs with mask[e] (protocol.py:72-75):
+        env -> EventBlock (int rows kind, body a, body b, 4 verts; float rows d, lambda)."""
         m = np.ascontiguousarray(mask, np.uint8)
         counts = np.zeros(self.n_env, np.int32)
         cap = int(max(1, m.sum()) * 64)
@@ -270,13 +292,13 @@ class DeviceBatch:
         out, off = {}, 0
         for e in np.nonzero(m)[0]:
             n = int(counts[e])
-            rows = []
-            for k in range(off, off + n):
-                rows.append({"kind": self.EVENT_KINDS[ei[k, 0]], "bodies": (int(ei[k, 1]), int(ei[k, 2])),
-                             "verts": [int(v) for v in ei[k, 3:7]], "d": float(ed[k, 0]), "lambda": float(ed[k, 1])})
-            out[int(e)] = rows
+            out[int(e)] = EventBlock(ei[off:off + n], ed[off:off + n])
             off += n
         return out
+
+    def events(self, mask):
+        """As event_blocks, as the reference's lists of {kind, bodies, verts, d, lambda} dicts."""
+        return {e: b.as_dicts() for e, b in self.event_blocks(mask).items()}
 
     def set_profiling(self, on=True):
         check(self.lib.grip_set_profiling(self.h, int(on)))

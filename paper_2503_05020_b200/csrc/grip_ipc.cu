@@ -1117,6 +1117,7 @@ int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t*
   for (int e = 0; e < E; ++e) {
     if (!mask[e]) continue;
     const int n = std::min(counts[e], D.cap_anc);
+    counts[e] = n;   // rows copied (a step with more active stencils than cap_anc is truncated)
     if (off + n > cap) {
       g_err = "grip_get_events: output capacity too small";
       return -1;

@@ -511,10 +511,10 @@ class BatchedGraspTrials:
         if self.record:
             m = np.zeros(self.E, np.uint8)
             m[ids] = 1
-            events = self.dev.events(m)
+            events = self.dev.event_blocks(m)
             # finger forces from the recorded events, as the reference sums them (protocol.py:78-86)
-            fsum = [[sum(ev["lambda"] for ev in events[e] if (self.fb[e, j] - self.group.packed.body_off[e])
-                         in ev["bodies"]) for j in range(self.fb.shape[1])] for e in ids]
+            boff = self.group.packed.body_off
+            fsum = [[events[e].force_on(self.fb[e, j] - boff[e]) for j in range(self.fb.shape[1])] for e in ids]
             ffr = np.array(fsum, np.float64).reshape(len(ids), self.fb.shape[1])
             self._snapshot(ids, rep, alphas, events, fsum)
         for e in ids:

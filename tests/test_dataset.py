@@ -146,3 +146,17 @@ def test_batched_recording_matches_single_env(tmp_path):
     assert [k for k in a if a[k] != b[k]] == []
     assert ma["trials"][0]["files"] == mb["trials"][0]["files"]
     assert recs[1].positions is not None and len(recs[1].contacts) == recs[1].n_steps
+
+
+def test_event_block_lines_match_reference_json():
+    """The array fast path of contacts.jsonl writes exactly the reference's json.dumps text."""
+    from paper_2503_05020_b200._native import EventBlock
+    for line in (GOLD / "trial_0000" / "contacts.jsonl").read_text().splitlines():
+        o = json.loads(line)
+        ev = o["events"]
+        i = np.array([[0 if e["kind"] == "point-triangle" else 1, *e["bodies"], *e["verts"]] for e in ev],
+                     np.int32).reshape(-1, 7)
+        d = np.array([[e["d"], e["lambda"]] for e in ev]).reshape(-1, 2)
+        blk = EventBlock(i, d)
+        assert ds._events_line(o["step"], blk) == line + "\n"
+        assert blk.as_dicts() == [dict(e, bodies=tuple(e["bodies"])) for e in ev]
