@@ -167,6 +167,19 @@ int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
  * ev_i (7 per event: kind 0 PT / 1 EE, body a, body b, 4 env-local sv ids), ev_d (2 per event:
  * d, lambda = kappa m |b'(d)|).  cap = rows available in ev_i / ev_d. */
 int grip_set_recording(GripBatch* b, int on);
+/* SDFs for the D1/D2 grasp-quality metrics (gripsim/geometry/sdf.py, pipeline/metrics.py).
+ * grip_sdf_exact replaces the narrow-band loop of build_sdf (sdf.py:168-241): for every point
+ * the exact distance to the closest of the n_tris triangles, signed by the angle-weighted
+ * pseudonormal of the closest feature (face_n: n_tris*3; edge_n: n_tris*9, edges (0,1),
+ * (1,2), (2,0); vert_n: n_verts*3).  grip_sdf_query evaluates metrics.py:58-75 on n samples:
+ * d_o = -(trilinear SDF) inside the grid box (in the frame body = (p - trans) rot, rot
+ * row-major 3x3 or NULL for identity) and -|gap to [world_lo, world_hi]| outside; it returns
+ * max d_o in *d_max and, if d_o is not NULL, every value. */
+int grip_sdf_exact(const double* pts, int64_t n, const double* verts, int32_t n_verts, const int32_t* tris,
+                   int32_t n_tris, const double* face_n, const double* edge_n, const double* vert_n, double* out);
+int grip_sdf_query(const double* values, const int32_t* dims, const double* origin, const double* spacing,
+                   const double* rot, const double* trans, const double* world_lo, const double* world_hi,
+                   const double* pts, int64_t n, double* d_o, double* d_max);
 int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t* ev_i, double* ev_d, int64_t cap);
 /* per-body centre of mass (n_body*3) and per-env max point speed after the last finalize
  * (solver.py:384-428; read by the protocol's steady / COM tests, protocol.py:231-249) */

@@ -94,7 +94,9 @@ def load():
         ("grip_round", [vp, vp, vp, vp, vp, vp]),
         ("grip_debug_elements", [i32, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_reset_envs", [vp, vp, vp, vp, vp, vp]), ("grip_set_recording", [vp, i32]),
-        ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64])):
+        ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64]),
+        ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
+        ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = i32
@@ -121,6 +123,32 @@ def debug_elements(etype, inputs):
     E, g, H, fl = np.zeros(n), np.zeros((n, 12)), np.zeros((n, 144)), np.zeros(n, np.int32)
     check(lib.grip_debug_elements(int(etype), n, ptr(a), stride, ptr(E), ptr(g), ptr(H), ptr(fl)))
     return E, g, H.reshape(n, 12, 12), fl
+
+
+def sdf_exact(pts, verts, tris, face_n, edge_n, vert_n):
+    """Signed exact distances of pts to a triangle surface (grip_sdf_exact)."""
+    lib = load()
+    f = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+    pts, verts, face_n, edge_n, vert_n = f(pts), f(verts), f(face_n), f(edge_n), f(vert_n)
+    tris = np.ascontiguousarray(tris, np.int32)
+    out = np.empty(len(pts))
+    check(lib.grip_sdf_exact(ptr(pts), len(pts), ptr(verts), len(verts), ptr(tris), len(tris), ptr(face_n),
+                             ptr(edge_n), ptr(vert_n), ptr(out)))
+    return out
+
+
+def sdf_query(values, origin, spacing, pts, rot=None, trans=None, world_lo=None, world_hi=None, want_values=False):
+    """max d_o over pts (and every d_o if want_values) of a grid SDF (grip_sdf_query)."""
+    lib = load()
+    f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)  # noqa: E731
+    values, pts = f(values), f(pts).reshape(-1, 3)
+    dims = np.asarray(values.shape, np.int32)
+    origin, spacing, rot, trans, world_lo, world_hi = map(f, (origin, spacing, rot, trans, world_lo, world_hi))
+    d_o = np.empty(len(pts)) if want_values else None
+    dmax = ctypes.c_double()
+    check(lib.grip_sdf_query(ptr(values), ptr(dims), ptr(origin), ptr(spacing), ptr(rot), ptr(trans), ptr(world_lo),
+                             ptr(world_hi), ptr(pts), len(pts), ptr(d_o), ctypes.byref(dmax)))
+    return dmax.value, d_o
 
 
 class EventBlock:

@@ -16,6 +16,7 @@
 #include "grip_tet.cuh"
 #include "grip_direct.cuh"
 #include "grip_tetclamp.cuh"
+#include "grip_sdf.cuh"
 
 using namespace grip;
 
@@ -1333,3 +1334,74 @@ int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// SDF kernels for the D1/D2 metrics; stateless, default stream, device 0
+// of the calling thread's current device
+// ---------------------------------------------------------------------------
+namespace {
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  bool put(const T* h, size_t n) {
+    if (cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)) != cudaSuccess) return false;
+    return !n || cudaMemcpy(p, h, sizeof(T) * n, cudaMemcpyHostToDevice) == cudaSuccess;
+  }
+  bool alloc(size_t n) { return cudaMalloc(&p, sizeof(T) * std::max<size_t>(n, 1)) == cudaSuccess; }
+};
+}  // namespace
+
+int grip_sdf_exact(const double* pts, int64_t n, const double* verts, int32_t n_verts, const int32_t* tris,
+                   int32_t n_tris, const double* face_n, const double* edge_n, const double* vert_n, double* out) {
+  if (n <= 0) return 0;
+  DevBuf<double> dp, dv, dfn, den, dvn, dout;
+  DevBuf<int> dt;
+  if (!dp.put(pts, 3 * (size_t)n) || !dv.put(verts, 3 * (size_t)n_verts) || !dt.put(tris, 3 * (size_t)n_tris) ||
+      !dfn.put(face_n, 3 * (size_t)n_tris) || !den.put(edge_n, 9 * (size_t)n_tris) ||
+      !dvn.put(vert_n, 3 * (size_t)n_verts) || !dout.alloc(n)) {
+    g_err = "grip_sdf_exact: device allocation / copy failed";
+    return -1;
+  }
+  const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+  k_sdf_exact<<<blocks, 128>>>(dp.p, n, dv.p, dt.p, n_tris, dfn.p, den.p, dvn.p, dout.p);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int grip_sdf_query(const double* values, const int32_t* dims, const double* origin, const double* spacing,
+                   const double* rot, const double* trans, const double* world_lo, const double* world_hi,
+                   const double* pts, int64_t n, double* d_o, double* d_max) {
+  const size_t nv = (size_t)dims[0] * dims[1] * dims[2];
+  DevBuf<double> dvals, dp, dR, dout;
+  DevBuf<unsigned long long> dm;
+  if (!dvals.put(values, nv) || !dp.put(pts, 3 * (size_t)std::max<int64_t>(n, 0)) || !dm.alloc(1) ||
+      (rot && !dR.put(rot, 9)) || (d_o && !dout.alloc(std::max<int64_t>(n, 1)))) {
+    g_err = "grip_sdf_query: device allocation / copy failed";
+    return -1;
+  }
+  CK(cudaMemset(dm.p, 0, sizeof(unsigned long long)));
+  SdfGridDev G{dvals.p, dims[0], dims[1], dims[2], origin[0], origin[1], origin[2], spacing[0], spacing[1], spacing[2]};
+  const V3 lo{origin[0], origin[1], origin[2]};
+  const V3 hi{origin[0] + spacing[0] * (dims[0] - 1), origin[1] + spacing[1] * (dims[1] - 1),
+              origin[2] + spacing[2] * (dims[2] - 1)};
+  const V3 T = trans ? V3{trans[0], trans[1], trans[2]} : V3{0, 0, 0};
+  const V3 wlo = world_lo ? V3{world_lo[0], world_lo[1], world_lo[2]} : lo;
+  const V3 whi = world_hi ? V3{world_hi[0], world_hi[1], world_hi[2]} : hi;
+  if (n > 0) {
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    k_sdf_query<<<blocks, 256>>>(G, rot ? dR.p : nullptr, T, lo, hi, wlo, whi, dp.p, n, d_o ? dout.p : nullptr, dm.p);
+    CK(cudaGetLastError());
+  }
+  unsigned long long u = 0;
+  CK(cudaMemcpy(&u, dm.p, sizeof(u), cudaMemcpyDeviceToHost));
+  if (d_o && n > 0) CK(cudaMemcpy(d_o, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  if (n <= 0) {
+    *d_max = -INFINITY;
+  } else {
+    u = (u & 0x8000000000000000ull) ? (u & 0x7fffffffffffffffull) : ~u;
+    memcpy(d_max, &u, sizeof(double));
+  }
+  return 0;
+}

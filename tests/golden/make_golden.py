@@ -464,6 +464,42 @@ def gen_dataset(out):
         {"settle_duration": 0.02, "steady_max_duration": 0.05, "gravity_phase_duration": 0.02,
          "R": rec.candidate["R"], "T": rec.candidate["T"], "opening": rec.candidate["opening"]}))
     print("dataset", rec.verdict, rec.n_steps, manifest["trials"][0]["files"])
+    gen_metrics(out, env, ob, rec)
+
+
+def gen_metrics(out, env, ob, rec):
+    """D1/D2 grasp-quality metrics (pipeline/metrics.py:99-164) of the dataset trial's final state,
+    plus the SDF build (geometry/sdf.py:117-178) and the surface sampler they rest on."""
+    from gripsim.geometry.mesh import TriSurface
+    from gripsim.pipeline import metrics as qm
+    res = {"x": env.x.tolist(), "object_body": ob, "gripper_bodies": list(rec.gripper_bodies)}
+    for resolution in (32, 128):
+        t0 = time.time()
+        d1, d2, h = qm.trial_quality_metrics(env, ob, rec.gripper_bodies, resolution=resolution)
+        res[f"res{resolution}"] = {"D1": d1, "D2": d2, "spacing": h, "wall_s": time.time() - t0}
+    grips = qm.gripper_surfaces_from_env(env, rec.gripper_bodies)
+    pts = qm._sample_surfaces(grips, 50_000, 0)
+    # per-sample d_o (positive inside) at resolution 32: the interior (trilinear) and far-field
+    # branches value by value -- D1 / D2 alone are 0.0 here (samples inside the posed grid's
+    # world AABB but outside the rotated grid get -|0| = -0.0, metrics.py:58-75)
+    sdf32 = qm.object_sdf_from_env(env, ob, resolution=32)
+    res["d_o_res32"] = qm._object_signed_inside(sdf32, pts).tolist()
+    res["samples_head"] = pts[:32].tolist()
+    res["samples_sum"] = pts.sum(axis=0).tolist()
+    r = env.records[ob]
+    rest = TriSurface(r["xi"], r["body"].surface.triangles)
+    sdf = build_sdf(rest, resolution=32)
+    q = env.x[r["dof0"]:r["dof0"] + 12]
+    res["polar_R"] = qm._polar_rotation(q[3:].reshape(3, 3)).tolist()
+    np.savez_compressed(out / "sdf_box32.npz", values=sdf.values, origin=sdf.origin, spacing=sdf.spacing)
+    soft = {}
+    for name, mesh in (("cube", gm.box_tet_lattice((0.04, 0.04, 0.04), resolution=3)),):
+        surf, _ = mesh.boundary_surface()
+        s2 = build_sdf(surf, resolution=24)
+        np.savez_compressed(out / f"sdf_soft_{name}24.npz", values=s2.values, origin=s2.origin, spacing=s2.spacing,
+                            vertices=surf.vertices, triangles=surf.triangles)
+    (out / "metrics.json").write_text(json.dumps(res))
+    print("metrics", {k: v for k, v in res.items() if k.startswith("res")})
 
 
 def _cand_job(i):
