@@ -763,8 +763,8 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     if (b->warp_elements) {
       k_tet_front<<<148 * 2, TF, 0, b->stream>>>(D, b->d_list, n);
       k_elements_w<<<148 * 2, EW * 32, 0, b->stream>>>(D, b->d_list, n);
-      k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
-      k_tet_jacobi<<<148, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
+      k_tet_jacobi2<<<148 * 2, TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+      k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
       k_tet_back<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
       k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
     }
@@ -944,8 +944,8 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   if (b->warp_elements) {
     k_tet_front<<<148 * 2, TF, 0, b->stream>>>(D, list, n);
     k_elements_w<<<148 * 2, EW * 32, 0, b->stream>>>(D, list, n);
-    k_tet_jacobi<<<148 * 2, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
-    k_tet_jacobi<<<148, TJ, 81 * TJ * sizeof(double), b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
+    k_tet_jacobi2<<<148 * 2, TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+    k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
     k_tet_back<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
     k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
   } else {

@@ -105,6 +105,96 @@ __global__ void __launch_bounds__(TJ) k_tet_jacobi(const int2* list, const int* 
   }
 }
 
+// ---- register-only variant: two threads per matrix ----
+// Both threads of a pair hold the whole S (identical instruction streams, the rotation
+// parameters computed redundantly, no communication) and half of the rotation R: thread h
+// owns rows 5h .. 5h+4 (thread 1's fifth row is padding).  No shared memory, so the kernel
+// co-resides with the CTA-per-env kernels of other lanes.
+template <int P, int Q>
+__device__ __forceinline__ void jrot2(double* s, double (&Rr)[5][9]) {
+  const double apq = s[up9(P, Q)];
+  const double d = s[up9(Q, Q)] - s[up9(P, P)];
+  const double sg = ((d >= 0.0) == (apq > 0.0)) ? 1.0 : -1.0;
+  const double den = fabs(d) + sqrt(d * d + 4.0 * apq * apq);
+  const double t = apq != 0.0 ? sg * 2.0 * fabs(apq) / den : 0.0;
+  const double c = rsqrt(t * t + 1.0), sn = t * c;
+  s[up9(P, P)] -= t * apq;
+  s[up9(Q, Q)] += t * apq;
+  s[up9(P, Q)] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 9; ++r) {
+    if (r == P || r == Q) continue;
+    const int rp = r < P ? up9(r, P) : up9(P, r);
+    const int rq = r < Q ? up9(r, Q) : up9(Q, r);
+    const double a = s[rp], b = s[rq];
+    s[rp] = c * a - sn * b;
+    s[rq] = sn * a + c * b;
+  }
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const double a = Rr[r][P], b = Rr[r][Q];
+    Rr[r][P] = c * a - sn * b;
+    Rr[r][Q] = sn * a + c * b;
+  }
+}
+
+template <int RND>
+__device__ __forceinline__ void jround2(double* s, double (&Rr)[5][9]) {
+  constexpr int A1 = 1 + (RND + 1) % 9, B1 = 1 + (RND + 8) % 9;
+  constexpr int A2 = 1 + (RND + 2) % 9, B2 = 1 + (RND + 7) % 9;
+  constexpr int A3 = 1 + (RND + 3) % 9, B3 = 1 + (RND + 6) % 9;
+  constexpr int A4 = 1 + (RND + 4) % 9, B4 = 1 + (RND + 5) % 9;
+  constexpr int A0 = 0, B0 = 1 + RND % 9;
+  if constexpr (B0 != 9) jrot2<(A0 < B0 ? A0 : B0), (A0 < B0 ? B0 : A0)>(s, Rr);
+  if constexpr (A1 != 9 && B1 != 9) jrot2<(A1 < B1 ? A1 : B1), (A1 < B1 ? B1 : A1)>(s, Rr);
+  if constexpr (A2 != 9 && B2 != 9) jrot2<(A2 < B2 ? A2 : B2), (A2 < B2 ? B2 : A2)>(s, Rr);
+  if constexpr (A3 != 9 && B3 != 9) jrot2<(A3 < B3 ? A3 : B3), (A3 < B3 ? B3 : A3)>(s, Rr);
+  if constexpr (A4 != 9 && B4 != 9) jrot2<(A4 < B4 ? A4 : B4), (A4 < B4 ? B4 : A4)>(s, Rr);
+}
+
+__global__ void __launch_bounds__(TJ) k_tet_jacobi2(const int2* list, const int* n_ptr, const double* Sbuf, double* Wbuf) {
+  const int n = *n_ptr;
+  const int h = threadIdx.x & 1;
+  for (int idx = (blockIdx.x * TJ + threadIdx.x) >> 1; idx < n; idx += (gridDim.x * TJ) >> 1) {
+    const int t = list[idx].x;
+    const double* Sg = Sbuf + 45 * (size_t)t;
+    double s[45];
+#pragma unroll
+    for (int q = 0; q < 45; ++q) s[q] = Sg[q];
+    double Rr[5][9];
+#pragma unroll
+    for (int r = 0; r < 5; ++r)
+#pragma unroll
+      for (int c = 0; c < 9; ++c) Rr[r][c] = (5 * h + r == c) ? 1.0 : 0.0;
+    for (int sweep = 0; sweep < 30; ++sweep) {
+      double off = 0.0, dg = 0.0;
+#pragma unroll
+      for (int i = 0; i < 9; ++i)
+#pragma unroll
+        for (int j = i; j < 9; ++j) {
+          const double v = s[up9(i, j)];
+          if (i == j) dg += v * v;
+          else off += v * v;
+        }
+      off *= 2.0;
+      if (off <= 1e-32 * (dg + off) || off == 0.0) break;
+      jround2<0>(s, Rr); jround2<1>(s, Rr); jround2<2>(s, Rr);
+      jround2<3>(s, Rr); jround2<4>(s, Rr); jround2<5>(s, Rr);
+      jround2<6>(s, Rr); jround2<7>(s, Rr); jround2<8>(s, Rr);
+    }
+    double* W = Wbuf + 90 * (size_t)t;
+    if (h == 0) {
+#pragma unroll
+      for (int k = 0; k < 9; ++k) W[k] = s[up9(k, k)];
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r)
+      if (5 * h + r < 9)
+#pragma unroll
+        for (int c = 0; c < 9; ++c) W[9 + (5 * h + r) * 9 + c] = Rr[r][c];
+  }
+}
+
 // eig: the tets' warm-start eigenbases (V = V0 R is stored back), or null for cold matrices (V = R)
 __global__ void __launch_bounds__(EW * 32) k_tet_finish(Dev D, const int2* list, const int* n_ptr, const double* Wbuf,
                                                         double* eig) {
