@@ -635,26 +635,35 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
   const size_t elbase = (size_t)e * D.cap_el;
   const int nce = D.n_act[e] + D.n_anc[e];
   // ---- contact incidence per sv (element order), used by gradient and SpMV ----
+  // counting sort over the 4 nce (element, vertex) items: counts, scan, scatter, then each
+  // sv's short list sorted by code = (k << 2) | j, i.e. element order
   int* ip = D.inc_ptr + (size_t)e * (D.max_sv + 1);
   int* inc = D.inc + (size_t)e * 4 * (D.cap_act + D.cap_anc);
-  for (int i = threadIdx.x; i < E.ns; i += NT) {
-    int c = 0;
-    for (int k = 0; k < nce; ++k) {
-      const int* ix = D.el_idx + (elbase + ce_slot(D, e, k)) * 4;
-      c += (ix[0] == i) + (ix[1] == i) + (ix[2] == i) + (ix[3] == i);
-    }
-    ip[i] = c;
-  }
+  int* cur = D.bp_cnt + (size_t)e * (max(D.max_sv, D.max_edge) + 1);   // broad-phase scratch, free here
+  for (int i = threadIdx.x; i < E.ns; i += NT) ip[i] = 0;
+  __syncthreads();
+  for (int it = threadIdx.x; it < 4 * nce; it += NT)
+    atomicAdd(&ip[D.el_idx[(elbase + ce_slot(D, e, it >> 2)) * 4 + (it & 3)]], 1);
   __syncthreads();
   const int tot_inc = block_scan_array(ip, E.ns, sm);
   if (threadIdx.x == 0) ip[E.ns] = tot_inc;
+  for (int i = threadIdx.x; i < E.ns; i += NT) cur[i] = ip[i];
+  __syncthreads();
+  for (int it = threadIdx.x; it < 4 * nce; it += NT) {
+    const int v = D.el_idx[(elbase + ce_slot(D, e, it >> 2)) * 4 + (it & 3)];
+    inc[atomicAdd(&cur[v], 1)] = it;   // it == (k << 2) | j
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < E.ns; i += NT) {
-    int q = ip[i];
-    for (int k = 0; k < nce; ++k) {
-      const int* ix = D.el_idx + (elbase + ce_slot(D, e, k)) * 4;
-      for (int j = 0; j < 4; ++j)
-        if (ix[j] == i) inc[q++] = (k << 2) | j;
+    const int lo = ip[i], hi = ip[i + 1];
+    for (int a = lo + 1; a < hi; ++a) {
+      const int t = inc[a];
+      int b = a - 1;
+      while (b >= lo && inc[b] > t) {
+        inc[b + 1] = inc[b];
+        --b;
+      }
+      inc[b + 1] = t;
     }
   }
   __syncthreads();
