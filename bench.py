@@ -52,7 +52,7 @@ EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, 
 
 
 # kernel groups as timed live (grip_kernel_stats) -> the kernels of the committed ncu capture
-KGROUPS = {"elements": ["k_tet_front", "k_elements_w", "k_tet_jacobi", "k_tet_back", "k_tet_finish"],
+KGROUPS = {"elements": ["k_tet_front", "k_elements_w", "k_tet_jacobi2", "k_tet_back", "k_tet_finish"],
            "assemble_pcg": ["k_contact_K", "k_assemble_direct"], "candidates": ["k_candidates"],
            "line_search": ["k_linesearch"], "begin": ["k_begin"], "finalize": ["k_finalize"]}
 NCU_FULL = ROOT / "profiles" / "r1_ncu_full_v3.json"
@@ -66,7 +66,7 @@ def _ncu_group(group):
     except (OSError, ValueError):
         return None, None, None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    want = {k: 2 if k == "k_tet_jacobi" else 1 for k in KGROUPS.get(group, [])}   # launches per round
+    want = {k: 2 if k == "k_tet_jacobi2" else 1 for k in KGROUPS.get(group, [])}   # launches per round
     seen, traffic, flop = {}, 0.0, 0.0
     for d in rows:
         k = d["kernel"].split("::")[-1]
