@@ -70,6 +70,9 @@ struct GripBatch {
   // optional per-kernel timing on the library stream (grip_set_profiling)
   bool prof = false;
   bool warp_elements = getenv("GRIP_THREAD_ELEMENTS") == nullptr;  // per-thread path kept for A/B
+  // grids of the flat element kernels (k_tet_front, k_elements_w, k_tet_jacobi2, k_tet_back), in
+  // blocks; GRIP_EGRID="f,w,j,b" (blocks per SM) overrides
+  int eg[4] = {148 * 2, 148 * 2, 148 * 2, 148 * 4};
   bool direct = getenv("GRIP_SOLVER") == nullptr || std::string(getenv("GRIP_SOLVER")) != "pcg";
   int env_cap = 0;        // direct solve: skyline capacity (doubles) in shared memory
   size_t dyn_smem = 0;
@@ -540,6 +543,11 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.cs_n = b->alloc<int>(2 * (size_t)E);
   D.cs_R = b->alloc<double>(E);
   D.ss_k = getenv("GRIP_SS_K") ? atof(getenv("GRIP_SS_K")) : 0.0;
+  if (getenv("GRIP_EGRID")) {
+    float m[4] = {2, 2, 2, 4};
+    sscanf(getenv("GRIP_EGRID"), "%f,%f,%f,%f", &m[0], &m[1], &m[2], &m[3]);
+    for (int k = 0; k < 4; ++k) b->eg[k] = std::max(1, (int)(148 * m[k] + 0.5f));
+  }
   D.bp_mode = (getenv("GRIP_BP") && std::string(getenv("GRIP_BP")) == "grid") ? 1 : 0;
   D.bp_qm_min = 1 << 30;   // measured: plain cost comparison is best (GRIP_BP_QM to experiment)
   D.bp_qm_fac = 1.0f;
@@ -761,11 +769,11 @@ static int newton_sweep(GripBatch* b, int n, int* n_out) {
     kt_end(b, t);
     t = kt_begin(b, K_ELEM);
     if (b->warp_elements) {
-      k_tet_front<<<148 * 2, TF, 0, b->stream>>>(D, b->d_list, n);
-      k_elements_w<<<148 * 2, EW * 32, 0, b->stream>>>(D, b->d_list, n);
-      k_tet_jacobi2<<<148 * 2, TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+      k_tet_front<<<b->eg[0], TF, 0, b->stream>>>(D, b->d_list, n);
+      k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, b->d_list, n);
+      k_tet_jacobi2<<<b->eg[2], TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
       k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-      k_tet_back<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
+      k_tet_back<<<b->eg[3], EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
       k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
     }
     else
@@ -942,11 +950,11 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   kt_end(b, t);
   t = kt_begin(b, K_ELEM);
   if (b->warp_elements) {
-    k_tet_front<<<148 * 2, TF, 0, b->stream>>>(D, list, n);
-    k_elements_w<<<148 * 2, EW * 32, 0, b->stream>>>(D, list, n);
-    k_tet_jacobi2<<<148 * 2, TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+    k_tet_front<<<b->eg[0], TF, 0, b->stream>>>(D, list, n);
+    k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, list, n);
+    k_tet_jacobi2<<<b->eg[2], TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
     k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-    k_tet_back<<<148 * 4, EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
+    k_tet_back<<<b->eg[3], EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
     k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
   } else {
     k_elements<<<148 * 8, 128, 0, b->stream>>>(D, list, n);
