@@ -167,6 +167,10 @@ int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
  * ev_i (7 per event: kind 0 PT / 1 EE, body a, body b, 4 env-local sv ids), ev_d (2 per event:
  * d, lambda = kappa m |b'(d)|).  cap = rows available in ev_i / ev_d. */
 int grip_set_recording(GripBatch* b, int on);
+/* One recorder frame (protocol.py:113-146) of the envs with mask[e]=1, packed in env order:
+ * x, v (their nodes * 3), kin (their surface vertices * 3: kinematic positions, zeros for
+ * the others) and stress (their tets * 7, materials.py:191-205).  Any output may be NULL. */
+int grip_get_frames(GripBatch* b, const uint8_t* mask, double* x, double* v, double* kin, double* stress);
 /* SDFs for the D1/D2 grasp-quality metrics (gripsim/geometry/sdf.py, pipeline/metrics.py).
  * grip_sdf_exact replaces the narrow-band loop of build_sdf (sdf.py:168-241): for every point
  * the exact distance to the closest of the n_tris triangles, signed by the angle-weighted

@@ -96,6 +96,7 @@ def load():
         ("grip_reset_envs", [vp, vp, vp, vp, vp, vp]), ("grip_set_recording", [vp, i32]),
         ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64]),
         ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
+        ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -289,6 +290,19 @@ class DeviceBatch:
         out = np.empty((max(self.packed.n_tet_total, 1), 7))
         check(self.lib.grip_stress(self.h, ptr(out)))
         return out[:self.packed.n_tet_total]
+
+    def frames(self, mask):
+        """Packed recorder frame of the masked envs (grip_get_frames): x, v (nodes x 3),
+        kin (surface vertices x 3), stress (tets x 7), each in env order."""
+        p = self.packed
+        m = np.ascontiguousarray(mask, np.uint8)
+        sel = np.nonzero(m)[0]
+        nn = int(sum(p.node_off[e + 1] - p.node_off[e] for e in sel))
+        ns = int(sum(p.sv_off[e + 1] - p.sv_off[e] for e in sel))
+        nt = int(sum(p.tet_off[e + 1] - p.tet_off[e] for e in sel))
+        x, v, kin, st = np.empty((nn, 3)), np.empty((nn, 3)), np.empty((ns, 3)), np.empty((nt, 7))
+        check(self.lib.grip_get_frames(self.h, ptr(m), ptr(x), ptr(v), ptr(kin), ptr(st)))
+        return x, v, kin, st
 
     def body_state(self):
         com = np.empty((self.packed.n_body_total, 3))

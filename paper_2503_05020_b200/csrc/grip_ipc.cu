@@ -54,6 +54,11 @@ struct GripBatch {
   int* d_list = nullptr;        // active / pending lists
   int* d_list2 = nullptr;
   int* d_tet_env = nullptr;
+  double* d_stress = nullptr;   // persistent: stress rows (n_tet * 7)
+  double* d_frame = nullptr;    // persistent: packed frame of the masked envs (grip_get_frames)
+  double* h_frame = nullptr;    // pinned staging of the same
+  int* d_fmask = nullptr;       // per env: packed offsets (node, sv, tet) or -1
+  int* h_fmask = nullptr;
   int* h_pin = nullptr;         // pinned small readbacks
   int* h_lists = nullptr;       // pinned: round lists (begin | iterating), 2 n_env
   // pinned per-round snapshot: everything the host reads after a round, one D2H batch
@@ -692,6 +697,8 @@ int grip_destroy(GripBatch* b) {
   if (b->h_pin) cudaFreeHost(b->h_pin);
   if (b->h_lists) cudaFreeHost(b->h_lists);
   if (b->h_snap) cudaFreeHost(b->h_snap);
+  if (b->h_frame) cudaFreeHost(b->h_frame);
+  if (b->h_fmask) cudaFreeHost(b->h_fmask);
   cudaEventDestroy(b->ev0);
   cudaEventDestroy(b->ev1);
   cudaStreamDestroy(b->stream);
@@ -1262,17 +1269,65 @@ int grip_query_candidates(GripBatch* b, int env, double radius, int32_t* pt, int
 
 int grip_stress(GripBatch* b, double* out) {
   if (b->n_tet == 0) return 0;
-  double* d_out = b->alloc<double>(7 * (size_t)b->n_tet);
-  if (!d_out) {
+  if (!b->d_stress && !(b->d_stress = b->alloc<double>(7 * (size_t)b->n_tet))) {
     g_err = "out of device memory";
     return -1;
   }
-  k_stress<<<std::min(148 * 8, (b->n_tet + 127) / 128), 128, 0, b->stream>>>(b->D, b->n_tet, b->d_tet_env, d_out);
+  k_stress<<<std::min(148 * 8, (b->n_tet + 127) / 128), 128, 0, b->stream>>>(b->D, b->n_tet, b->d_tet_env, b->d_stress);
   b->launches++;
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, d_out, 7 * sizeof(double) * b->n_tet, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(out, b->d_stress, 7 * sizeof(double) * b->n_tet, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
-  b->release(d_out);
+  return 0;
+}
+
+// One recorded frame of every masked env (protocol.py:113-146 _Recorder.snapshot), packed in
+// env order: node positions and velocities (nn*3 each), surface-vertex kinematic positions
+// (ns*3) and stress rows (n_tet*7).  One kernel gathers them on the device, one D2H moves
+// them through a pinned buffer.
+int grip_get_frames(GripBatch* b, const uint8_t* mask, double* x, double* v, double* kin, double* stress) {
+  const int E = b->n_env;
+  const size_t cap = 6 * (size_t)b->n_node + 3 * (size_t)b->n_sv + 7 * (size_t)b->n_tet;
+  if (!b->d_frame) {
+    b->d_frame = b->alloc<double>(cap);
+    b->d_fmask = b->alloc<int>(4 * (size_t)E);
+    if (!b->d_stress) b->d_stress = b->alloc<double>(7 * (size_t)std::max(b->n_tet, 1));
+    if (cudaMallocHost(&b->h_frame, sizeof(double) * std::max<size_t>(cap, 1)) != cudaSuccess ||
+        cudaMallocHost(&b->h_fmask, sizeof(int) * 4 * E) != cudaSuccess || !b->d_frame || !b->d_fmask) {
+      g_err = "out of memory (frame buffers)";
+      return -1;
+    }
+  }
+  size_t on = 0, os = 0, ot = 0;
+  for (int e = 0; e < E; ++e) {
+    int* m = b->h_fmask + 4 * e;
+    m[0] = mask[e] ? (int)on : -1;
+    m[1] = (int)os;
+    m[2] = (int)ot;
+    m[3] = 0;
+    if (mask[e]) {
+      on += b->node_off[e + 1] - b->node_off[e];
+      os += b->sv_off[e + 1] - b->sv_off[e];
+      ot += b->tet_off[e + 1] - b->tet_off[e];
+    }
+  }
+  if (on + os + ot == 0) return 0;
+  CK(cudaMemcpyAsync(b->d_fmask, b->h_fmask, sizeof(int) * 4 * E, cudaMemcpyHostToDevice, b->stream));
+  double* fx = b->d_frame;
+  double* fv = fx + 3 * on;
+  double* fk = fv + 3 * on;
+  double* fs = fk + 3 * os;
+  k_frames<<<E, 128, 0, b->stream>>>(b->D, b->d_fmask, fx, fv, fk, fs);
+  b->launches++;
+  CK(cudaGetLastError());
+  const size_t tot = 6 * on + 3 * os + 7 * ot;
+  CK(cudaMemcpyAsync(b->h_frame, b->d_frame, sizeof(double) * tot, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  const double* h = b->h_frame;
+  if (x) memcpy(x, h, sizeof(double) * 3 * on);
+  if (v) memcpy(v, h + 3 * on, sizeof(double) * 3 * on);
+  if (kin) memcpy(kin, h + 6 * on, sizeof(double) * 3 * os);
+  if (stress) memcpy(stress, h + 6 * on + 3 * os, sizeof(double) * 7 * ot);
   return 0;
 }
 

@@ -1446,6 +1446,30 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   }
 }
 
+// packed recorder frame of the envs with m[4e] >= 0 (grip_get_frames): CTA per env
+__global__ void k_frames(Dev D, const int* m, double* fx, double* fv, double* fk, double* fs) {
+  const int e = blockIdx.x;
+  const int on = m[4 * e], os = m[4 * e + 1], ot = m[4 * e + 2];
+  if (on < 0) return;
+  const int n0 = D.node_off[e], nn = D.node_off[e + 1] - n0;
+  const int s0 = D.sv_off[e], ns = D.sv_off[e + 1] - s0;
+  const int t0 = D.tet_off[e], nt = D.tet_off[e + 1] - t0;
+  for (int i = threadIdx.x; i < 3 * nn; i += blockDim.x) {
+    fx[3 * (size_t)on + i] = D.x[3 * (size_t)n0 + i];
+    fv[3 * (size_t)on + i] = D.v[3 * (size_t)n0 + i];
+  }
+  for (int i = threadIdx.x; i < 3 * ns; i += blockDim.x) fk[3 * (size_t)os + i] = D.kin_pos[3 * (size_t)s0 + i];
+  for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+    const int t = t0 + k;
+    V3 x[4];
+    for (int j = 0; j < 4; ++j) x[j] = ld3(D.x + 3 * (size_t)(n0 + D.tet_nodes[4 * (size_t)t + j]));
+    double row[7];
+    if (!nh_stress(x, D.tet_Dmi + 9 * (size_t)t, D.tet_mu[t], D.tet_lam[t], row))
+      for (int c = 0; c < 7; ++c) row[c] = NAN;
+    for (int c = 0; c < 7; ++c) fs[7 * ((size_t)ot + k) + c] = row[c];
+  }
+}
+
 // per-tet stress rows (materials.py:191-205), flat over all tets
 __global__ void k_stress(Dev D, int n_tet_total, const int* tet_env, double* out) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tet_total; t += gridDim.x * blockDim.x) {

@@ -379,19 +379,24 @@ class BatchedGraspTrials:
         """Record one frame for every env in ids (the reference's _Recorder.snapshot)."""
         from paper_2503_05020_b200.solver import report_from_row
         p = self.group.packed
-        x, v, kin = self.dev.get_state(True)
-        st = self.dev.stress()
+        m = np.zeros(self.E, np.uint8)
+        m[ids] = 1
+        x, v, kin, st = self.dev.frames(m)   # the finalized envs only, packed in env order
         boff = p.body_off
+        on = os_ = ot = 0
+        assert np.all(np.diff(ids) > 0)   # frames come packed in env order
         for k, e in enumerate(ids):
-            n0, n1 = p.node_off[e], p.node_off[e + 1]
-            kp = [kin[a:b] for a, b, _ in self._kin_sl[e]]
+            nn, ns, nt = p.node_off[e + 1] - p.node_off[e], p.sv_off[e + 1] - p.sv_off[e], p.tet_off[e + 1] - p.tet_off[e]
+            s0 = p.sv_off[e]
+            kp = [kin[os_ + a - s0:os_ + b - s0] for a, b, _ in self._kin_sl[e]]
             kv = [np.tile(self.vel[boff[e] + bid], (b - a, 1)) for a, b, bid in self._kin_sl[e]]
             fr = self._frames[e]
-            fr["x"].append(np.concatenate([x[n0:n1]] + kp))
-            fr["v"].append(np.concatenate([v[n0:n1]] + kv))
+            fr["x"].append(np.concatenate([x[on:on + nn]] + kp))
+            fr["v"].append(np.concatenate([v[on:on + nn]] + kv))
             env = self.group.envs[e]
             fr["t"].append(env._time + env.solver_params.dt)   # env.time after the step, accumulated
-            fr["stress"].append(st[p.tet_off[e]:p.tet_off[e + 1]].copy())
+            fr["stress"].append(st[ot:ot + nt])
+            on, os_, ot = on + nn, os_ + ns, ot + nt
             fr["events"].append(events[e])
             r = report_from_row(rep[e], alphas[e], self.group.envs[e].env_id)
             r.time = env._time
