@@ -152,6 +152,8 @@ struct Dev {
   double* el_K;       // direct solve, per contact slot (env (cap_act+cap_anc)): dt^2 J^T H J, lower triangle over
                       // the element's DOFs in dense order (<= 24 DOFs -> 300 entries)
   int* el_kn;         // per contact slot 9: node count, then the element's dense node positions (ascending)
+  int* sc_lst;        // direct solve scratch, per env 8*(cap_act+cap_anc): contact (element, node slot) items by node
+  int* sc_off;        // ... per env 2*(max_free+1): per dense node item offsets, fill cursors
   int dense_k;        // 1: the element kernel writes el_K / el_kn (direct solver)
   double* sv_g;      // per env 3*max_sv
 };

@@ -164,6 +164,116 @@ __device__ void sky_scatter_contacts(const Dev& D, const EnvIx& E, const Sky& S,
   __syncthreads();
 }
 
+// The contact / friction elements' K into the skyline, row node by row node: every entry of
+// the lower triangle belongs to the rows of exactly one dense node I, so the warp that owns I
+// adds, for each element containing I in ascending element order, that element's entries of
+// I's rows (columns of its nodes at or before I).  Rows of different nodes never share an
+// entry, so the warps run without synchronisation, and each entry still accumulates its
+// elements in element order (bitwise the same sums as the former turn-ordered scatter).
+// Node lists: counting sort of the (element, node slot) items by node; short lists are then
+// sorted by element, long ones (the hub nodes every object contact touches) are walked by
+// scanning all elements in order instead.
+constexpr int SC_LONG = 48;
+__device__ void sky_scatter_rows(const Dev& D, const EnvIx& E, const Sky& S, DirShared& sh) {
+  Red& sm = sh.A.sm;
+  const int e = E.e, nf = E.nf;
+  const int na = D.n_act[e];
+  const int nce = na + D.n_anc[e];
+  const size_t cs0 = (size_t)e * (D.cap_act + D.cap_anc);
+  int* off = D.sc_off + (size_t)e * 2 * (D.max_free + 1);
+  int* cur = off + (D.max_free + 1);
+  int* lst = D.sc_lst + (size_t)e * 8 * (D.cap_act + D.cap_anc);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto slot_of = [&](int k) { return cs0 + (k < na ? k : D.cap_act + (k - na)); };
+  for (int p = threadIdx.x; p < nf; p += NT) off[p] = 0;
+  __syncthreads();
+  for (int t = threadIdx.x; t < 8 * nce; t += NT) {
+    const int* kn = D.el_kn + slot_of(t >> 3) * 9;
+    if ((t & 7) < kn[0]) atomicAdd(&off[kn[1 + (t & 7)]], 1);
+  }
+  __syncthreads();
+  const int tot = block_scan_array(off, nf, sm);
+  if (threadIdx.x == 0) off[nf] = tot;
+  for (int p = threadIdx.x; p < nf; p += NT) cur[p] = off[p];
+  __syncthreads();
+  for (int t = threadIdx.x; t < 8 * nce; t += NT) {
+    const int* kn = D.el_kn + slot_of(t >> 3) * 9;
+    if ((t & 7) < kn[0]) lst[atomicAdd(&cur[kn[1 + (t & 7)]], 1)] = t;   // t == (k << 3) | slot
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < nf; p += NT) {
+    const int lo = off[p], hi = off[p + 1];
+    if (hi - lo > SC_LONG) continue;
+    for (int a = lo + 1; a < hi; ++a) {
+      const int t = lst[a];
+      int b = a - 1;
+      while (b >= lo && lst[b] > t) {
+        lst[b + 1] = lst[b];
+        --b;
+      }
+      lst[b + 1] = t;
+    }
+  }
+  __syncthreads();
+  // element u of node I's walk: its element index and I's slot in it (-1: not a member)
+  for (int I = warp; I < nf; I += NWARP) {
+    const int lo = off[I], hi = off[I + 1];
+    if (hi == lo) continue;
+    const bool scan_all = hi - lo > SC_LONG;
+    const int cnt = scan_all ? nce : hi - lo;
+    // chunks of SCH elements: every lane gathers its (address, value) pairs of all of them
+    // first (the loads overlap), then they are added element by element, in order
+    constexpr int SCH = 4;
+    for (int u0 = 0; u0 < cnt; u0 += SCH) {
+      int addr[SCH][3];
+      double val[SCH][3];
+#pragma unroll
+      for (int c = 0; c < SCH; ++c) {
+        const int u = u0 + c;
+        int k = -1, a = -1;
+        if (u < cnt) {
+          if (scan_all) {
+            const int* kn = D.el_kn + slot_of(u) * 9;
+            const int nn = kn[0];
+            for (int q = 0; q < nn; ++q)
+              if (kn[1 + q] == I) a = q;
+            k = a >= 0 ? u : -1;
+          } else {
+            const int t = lst[lo + u];
+            k = t >> 3;
+            a = t & 7;
+          }
+        }
+        const int* kn = k >= 0 ? D.el_kn + slot_of(k) * 9 : nullptr;
+        const double* K = k >= 0 ? D.el_K + slot_of(k) * 300 : nullptr;
+        const int nent = k >= 0 ? 9 * a + 6 : 0;   // rows 3a..3a+2, columns 0..row
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          const int t = lane + 32 * m;
+          addr[c][m] = -1;
+          val[c][m] = 0.0;
+          if (t < nent) {
+            const int ri = t < 3 * a + 1 ? 0 : (t < 6 * a + 3 ? 1 : 2);
+            const int q = t - (ri == 0 ? 0 : (ri == 1 ? 3 * a + 1 : 6 * a + 3));
+            const int r = 3 * a + ri;
+            const int i = 3 * I + ri, j = 3 * kn[1 + q / 3] + q % 3;
+            addr[c][m] = S.ro[i] + j - S.fc[i];
+            val[c][m] = K[r * (r + 1) / 2 + q];
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < SCH; ++c) {   // one element at a time: an address shared by two
+#pragma unroll                          // elements may sit in different lanes
+        for (int m = 0; m < 3; ++m)
+          if (addr[c][m] >= 0) S.L[addr[c][m]] += val[c][m];
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // A warp group: the whole CTA (barrier 0) or half of it (named barriers 1, 2)
 struct Grp {
   int t, nt, w, nw, id;
@@ -630,7 +740,7 @@ __global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* lis
     }
     sky_static(D, E, L, n);
     PHASE(1);
-    sky_scatter_contacts(D, E, L, S);
+    sky_scatter_rows(D, E, L, S);
     PHASE(2);
     const bool chol_ok = sky_cholesky(L, rdiag, n, S);
     PHASE(3);

@@ -146,9 +146,13 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   if (b->direct) {
     ok &= swap_alloc(D.el_K, E * 300 * (D.cap_act + D.cap_anc));
     ok &= swap_alloc(D.el_kn, E * 9 * (D.cap_act + D.cap_anc));
+    ok &= swap_alloc(D.sc_lst, E * 8 * (D.cap_act + D.cap_anc));
+    ok &= swap_alloc(D.sc_off, E * 2 * ((size_t)D.max_free + 1));
   } else if (!D.el_K) {
     ok &= swap_alloc(D.el_K, 1);
     ok &= swap_alloc(D.el_kn, 1);
+    ok &= swap_alloc(D.sc_lst, 1);
+    ok &= swap_alloc(D.sc_off, 1);
   }
   ok &= swap_alloc(D.bp_tmp, E * std::max(D.cap_pt, D.cap_ee));
   ok &= swap_alloc(D.cs_pt, E * 4 * D.cap_pt);
@@ -664,7 +668,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
