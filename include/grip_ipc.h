@@ -167,6 +167,38 @@ int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
  * ev_i (7 per event: kind 0 PT / 1 EE, body a, body b, 4 env-local sv ids), ev_d (2 per event:
  * d, lambda = kappa m |b'(d)|).  cap = rows available in ev_i / ev_d. */
 int grip_set_recording(GripBatch* b, int on);
+/* Device-resident grasp protocol (protocol.py:152-277): the phase state machine
+ * runs on the device after every finalize (k_protocol), sets the fingers' velocities and the
+ * gravity of the next step itself, and keeps the trial record, so many rounds run back to back
+ * with no host decision.  Setup (per env, n_env entries each): finger_body[2] (env-local body
+ * ids of finger 0 / 1), closing_dir[2*3], object_body, gripper_bits (bit b = body b is a finger
+ * link), max_close (close-phase step cap); cfg[8] = {settle steps, hold steps, gravity-phase
+ * steps, closing speed, force halt, gravity magnitude, steady speed steps, stability constant}.
+ * Every env starts a trial (settle, fingers still, gravity off). */
+typedef struct GripTrialOut {
+  double halt_force[2];
+  double com_disp[6];     /* gravity+x, -x, +y, -y, +z, -z */
+  double final_disp, threshold;
+  int32_t phase;          /* 0 settle 1 close 2 hold 3 gravity 4 done */
+  int32_t verdict;        /* 0 running 1 stable 2 unstable 3 sim-failed */
+  int32_t n_steps;
+  int32_t fail_phase;     /* 0 settle 1 close 2 hold 3+g gravity phase g */
+  int32_t fail_reason;    /* GRIP_R_* */
+  int32_t fail_step;
+  int32_t halted;         /* bit j: finger j halted */
+  int32_t final_contact;
+  int32_t halt_step[2];
+  int32_t markers[18];    /* [start, end) per phase 0..8, -1 = phase not completed */
+} GripTrialOut;
+int grip_protocol_setup(GripBatch* b, const int32_t* finger_body, const double* closing_dir, const int32_t* object_body,
+                        const int32_t* gripper_bits, const int32_t* max_close, const double* cfg);
+/* restart the protocol of the masked envs (after grip_reset_envs gave them a new candidate) */
+int grip_protocol_reset(GripBatch* b, const uint8_t* mask, const double* closing_dir, const int32_t* max_close);
+/* run `rounds` continuous-batching rounds on the device (begin / sweep / finalize / protocol)
+ * with one synchronisation at the end; capacity overflows are grown there and the affected
+ * envs simply resume.  *env_steps = time steps completed. */
+int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps);
+int grip_protocol_read(GripBatch* b, GripTrialOut* out /* n_env */);
 /* One recorder frame (protocol.py:113-146) of the envs with mask[e]=1, packed in env order:
  * x, v (their nodes * 3), kin (their surface vertices * 3: kinematic positions, zeros for
  * the others) and stress (their tets * 7, materials.py:191-205).  Any output may be NULL. */

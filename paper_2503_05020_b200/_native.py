@@ -97,6 +97,8 @@ def load():
         ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64]),
         ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
+        ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
+        ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -124,6 +126,15 @@ def debug_elements(etype, inputs):
     E, g, H, fl = np.zeros(n), np.zeros((n, 12)), np.zeros((n, 144)), np.zeros(n, np.int32)
     check(lib.grip_debug_elements(int(etype), n, ptr(a), stride, ptr(E), ptr(g), ptr(H), ptr(fl)))
     return E, g, H.reshape(n, 12, 12), fl
+
+
+class GripTrialOut(ctypes.Structure):
+    """include/grip_ipc.h GripTrialOut (device protocol record of one env)."""
+    _fields_ = [("halt_force", ctypes.c_double * 2), ("com_disp", ctypes.c_double * 6),
+                ("final_disp", ctypes.c_double), ("threshold", ctypes.c_double), ("phase", ctypes.c_int32),
+                ("verdict", ctypes.c_int32), ("n_steps", ctypes.c_int32), ("fail_phase", ctypes.c_int32),
+                ("fail_reason", ctypes.c_int32), ("fail_step", ctypes.c_int32), ("halted", ctypes.c_int32),
+                ("final_contact", ctypes.c_int32), ("halt_step", ctypes.c_int32 * 2), ("markers", ctypes.c_int32 * 18)]
 
 
 def sdf_exact(pts, verts, tris, face_n, edge_n, vert_n):
@@ -341,6 +352,29 @@ class DeviceBatch:
     def events(self, mask):
         """As event_blocks, as the reference's lists of {kind, bodies, verts, d, lambda} dicts."""
         return {e: b.as_dicts() for e, b in self.event_blocks(mask).items()}
+
+    # -- device-resident protocol (grip_protocol_*, grip_run_rounds) --------------------------
+    def protocol_setup(self, finger_body, closing_dir, object_body, gripper_bits, max_close, cfg):
+        i32a = lambda a: np.ascontiguousarray(a, np.int32)  # noqa: E731
+        self._pr_keep = [i32a(finger_body), np.ascontiguousarray(closing_dir, np.float64), i32a(object_body),
+                         i32a(gripper_bits), i32a(max_close), np.ascontiguousarray(cfg, np.float64)]
+        check(self.lib.grip_protocol_setup(self.h, *[ptr(a) for a in self._pr_keep]))
+
+    def protocol_reset(self, mask, closing_dir, max_close):
+        m = np.ascontiguousarray(mask, np.uint8)
+        cd = np.ascontiguousarray(closing_dir, np.float64)
+        mc = np.ascontiguousarray(max_close, np.int32)
+        check(self.lib.grip_protocol_reset(self.h, ptr(m), ptr(cd), ptr(mc)))
+
+    def run_rounds(self, rounds):
+        n = ctypes.c_int64()
+        check(self.lib.grip_run_rounds(self.h, int(rounds), ctypes.byref(n)))
+        return n.value
+
+    def protocol_read(self):
+        out = (GripTrialOut * self.n_env)()
+        check(self.lib.grip_protocol_read(self.h, out))
+        return out
 
     def set_profiling(self, on=True):
         check(self.lib.grip_set_profiling(self.h, int(on)))

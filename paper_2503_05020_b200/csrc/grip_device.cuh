@@ -27,6 +27,14 @@ constexpr int MAXC = 4096;        // broad-phase grid cells per env
 // error / flag bits per env and Newton sweep
 enum { ERR_INVERTED = 1, ERR_CONTACT_D = 2, FLAG_OVERFLOW = 4, FLAG_OVF_BEGIN = 8, FLAG_OVF_FIN = 16 };  // OVF_*: stage
 
+// device protocol state layout (per env)
+enum {
+  PI_PHASE = 0, PI_PSTEP, PI_GPHASE, PI_QUIET, PI_NSTEPS, PI_PSTART, PI_HALTED, PI_MAXCLOSE, PI_INSTEP,
+  PI_NEEDBEGIN, PI_VERDICT, PI_FPHASE, PI_FREASON, PI_FSTEP, PI_FCONTACT, PI_FB0, PI_FB1, PI_OBJ, PI_GBITS,
+  PI_HSTEP0, PI_HSTEP1, PI_MARK, PI_N = PI_MARK + 18
+};
+enum { PD_CD = 0, PD_COM0 = 6, PD_HF = 9, PD_CDISP = 11, PD_FDISP = 17, PD_THR = 18, PD_N = 19 };
+
 struct Dev {
   int n_env;
   // env slices
@@ -125,6 +133,12 @@ struct Dev {
   int* anc_b;        // 2
   // contact events of the last finalize (protocol.py:72-75 contact_events_now; recorded when ev_on):
   // per env cap_anc slots, active stencils in candidate order (PT then EE)
+  // device-resident protocol (k_protocol, grip_run_rounds): per env PI_N ints, PD_N doubles
+  int round_mode;
+  int* pr_i;
+  double* pr_d;
+  double* pr_cfg;          // 8 (grip_protocol_setup)
+  unsigned long long* pr_steps;  // env-steps completed (counter)
   int ev_on;
   int* ev_i;         // 7 per event: kind (0 PT, 1 EE), body a, body b, 4 vertices
   double* ev_d;      // 2 per event: d, lambda

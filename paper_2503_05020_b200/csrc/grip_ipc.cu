@@ -54,6 +54,7 @@ struct GripBatch {
   int* d_list = nullptr;        // active / pending lists
   int* d_list2 = nullptr;
   int* d_tet_env = nullptr;
+  int* d_ident = nullptr;       // 0..n_env-1 (device protocol rounds run over every env)
   double* d_stress = nullptr;   // persistent: stress rows (n_tet * 7)
   double* d_frame = nullptr;    // persistent: packed frame of the masked envs (grip_get_frames)
   double* h_frame = nullptr;    // pinned staging of the same
@@ -1116,6 +1117,155 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
   }
   if (alphas) memcpy(alphas, b->s_alpha, sizeof(double) * (size_t)E * D.max_alpha);
   g_host_post += host_now() - h0;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident protocol (k_protocol): setup, restart, rounds, readout
+// ---------------------------------------------------------------------------
+static int protocol_init_envs(GripBatch* b, const uint8_t* mask, const double* closing_dir, const int32_t* max_close,
+                              const int32_t* finger_body, const int32_t* object_body, const int32_t* gripper_bits) {
+  Dev& D = b->D;
+  const int E = b->n_env;
+  std::vector<int> hi((size_t)E * PI_N);
+  std::vector<double> hd((size_t)E * PD_N);
+  CK(cudaMemcpyAsync(hi.data(), D.pr_i, sizeof(int) * hi.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(hd.data(), D.pr_d, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, b->stream));
+  std::vector<double> vel((size_t)b->n_body * 3), grav((size_t)E * 3);
+  CK(cudaMemcpyAsync(vel.data(), D.body_vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(grav.data(), D.gravity, sizeof(double) * grav.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  for (int e = 0; e < E; ++e) {
+    if (mask && !mask[e]) continue;
+    int* I = hi.data() + (size_t)e * PI_N;
+    double* R = hd.data() + (size_t)e * PD_N;
+    const int fb0 = finger_body ? finger_body[2 * e] : I[PI_FB0], fb1 = finger_body ? finger_body[2 * e + 1] : I[PI_FB1];
+    const int obj = object_body ? object_body[e] : I[PI_OBJ], gb = gripper_bits ? gripper_bits[e] : I[PI_GBITS];
+    for (int k = 0; k < PI_N; ++k) I[k] = 0;
+    for (int k = 0; k < PD_N; ++k) R[k] = 0.0;
+    I[PI_FB0] = fb0; I[PI_FB1] = fb1; I[PI_OBJ] = obj; I[PI_GBITS] = gb;
+    I[PI_MAXCLOSE] = max_close[e];
+    I[PI_NEEDBEGIN] = 1;
+    for (int k = 0; k < 18; ++k) I[PI_MARK + k] = -1;
+    I[PI_HSTEP0] = I[PI_HSTEP1] = -1;
+    for (int k = 0; k < 6; ++k) R[PD_CD + k] = closing_dir[6 * e + k];
+    // settle: fingers still, gravity off (protocol.py:193-198)
+    for (int c = 0; c < 3; ++c) {
+      vel[3 * (size_t)(b->body_off[e] + fb0) + c] = 0.0;
+      vel[3 * (size_t)(b->body_off[e] + fb1) + c] = 0.0;
+      grav[3 * (size_t)e + c] = 0.0;
+    }
+  }
+  CK(cudaMemcpyAsync(D.pr_i, hi.data(), sizeof(int) * hi.size(), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(D.pr_d, hd.data(), sizeof(double) * hd.size(), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(D.body_vel, vel.data(), sizeof(double) * vel.size(), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaMemcpyAsync(D.gravity, grav.data(), sizeof(double) * grav.size(), cudaMemcpyHostToDevice, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  b->snap_valid = false;
+  return 0;
+}
+
+int grip_protocol_setup(GripBatch* b, const int32_t* finger_body, const double* closing_dir, const int32_t* object_body,
+                        const int32_t* gripper_bits, const int32_t* max_close, const double* cfg) {
+  Dev& D = b->D;
+  const int E = b->n_env;
+  if (!D.pr_i) {
+    D.pr_i = b->alloc<int>((size_t)E * PI_N);
+    D.pr_d = b->alloc<double>((size_t)E * PD_N);
+    D.pr_cfg = b->alloc<double>(8);
+    D.pr_steps = b->alloc<unsigned long long>(1);
+    b->d_ident = b->alloc<int>(E);
+    if (!D.pr_i || !D.pr_d || !D.pr_cfg || !D.pr_steps || !b->d_ident) {
+      g_err = "out of device memory (protocol state)";
+      return -1;
+    }
+    std::vector<int> id(E);
+    for (int e = 0; e < E; ++e) id[e] = e;
+    CK(cudaMemcpyAsync(b->d_ident, id.data(), sizeof(int) * E, cudaMemcpyHostToDevice, b->stream));
+  }
+  CK(cudaMemcpyAsync(D.pr_cfg, cfg, sizeof(double) * 8, cudaMemcpyHostToDevice, b->stream));
+  return protocol_init_envs(b, nullptr, closing_dir, max_close, finger_body, object_body, gripper_bits);
+}
+
+int grip_protocol_reset(GripBatch* b, const uint8_t* mask, const double* closing_dir, const int32_t* max_close) {
+  if (!b->D.pr_i) {
+    g_err = "grip_protocol_reset before grip_protocol_setup";
+    return -1;
+  }
+  return protocol_init_envs(b, mask, closing_dir, max_close, nullptr, nullptr, nullptr);
+}
+
+int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
+  Dev& D = b->D;
+  if (!D.pr_i) {
+    g_err = "grip_run_rounds before grip_protocol_setup";
+    return -1;
+  }
+  const int E = b->n_env;
+  b->snap_valid = false;
+  D.round_mode = 1;
+  CK(cudaMemsetAsync(D.pr_steps, 0, sizeof(unsigned long long), b->stream));
+  for (int r = 0; r < rounds; ++r) {
+    int t = kt_begin(b, K_BEGIN);
+    k_begin<<<E, NT, 0, b->stream>>>(D, b->d_ident);
+    kt_end(b, t);
+    sweep_launch(b, E, b->d_ident);
+    t = kt_begin(b, K_FIN);
+    k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
+    kt_end(b, t);
+    k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
+    b->launches += 3;
+  }
+  CK(cudaGetLastError());
+  unsigned long long steps = 0;
+  std::vector<int> fl(E);
+  CK(cudaMemcpyAsync(&steps, D.pr_steps, sizeof(steps), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(fl.data(), D.flags, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  kt_collect(b);
+  D.round_mode = 0;
+  bool ovf = false;
+  for (int e = 0; e < E; ++e) ovf |= (fl[e] & FLAG_OVERFLOW) != 0;
+  if (ovf) {   // grow; the overflowed envs' state is untouched and they resume next call
+    if (grow(b)) return -1;
+    CK(cudaMemsetAsync(D.flags, 0, sizeof(int) * E, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+  }
+  if (env_steps) *env_steps = (int64_t)steps;
+  return 0;
+}
+
+int grip_protocol_read(GripBatch* b, GripTrialOut* out) {
+  Dev& D = b->D;
+  if (!D.pr_i) {
+    g_err = "grip_protocol_read before grip_protocol_setup";
+    return -1;
+  }
+  const int E = b->n_env;
+  std::vector<int> hi((size_t)E * PI_N);
+  std::vector<double> hd((size_t)E * PD_N);
+  CK(cudaMemcpyAsync(hi.data(), D.pr_i, sizeof(int) * hi.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(hd.data(), D.pr_d, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  for (int e = 0; e < E; ++e) {
+    const int* I = hi.data() + (size_t)e * PI_N;
+    const double* R = hd.data() + (size_t)e * PD_N;
+    GripTrialOut& o = out[e];
+    o.halt_force[0] = R[PD_HF]; o.halt_force[1] = R[PD_HF + 1];
+    for (int k = 0; k < 6; ++k) o.com_disp[k] = R[PD_CDISP + k];
+    o.final_disp = R[PD_FDISP];
+    o.threshold = R[PD_THR];
+    o.phase = I[PI_PHASE];
+    o.verdict = I[PI_VERDICT];
+    o.n_steps = I[PI_NSTEPS];
+    o.fail_phase = I[PI_FPHASE];
+    o.fail_reason = I[PI_FREASON];
+    o.fail_step = I[PI_FSTEP];
+    o.halted = I[PI_HALTED];
+    o.final_contact = I[PI_FCONTACT];
+    o.halt_step[0] = I[PI_HSTEP0]; o.halt_step[1] = I[PI_HSTEP1];
+    for (int k = 0; k < 18; ++k) o.markers[k] = I[PI_MARK + k];
+  }
   return 0;
 }
 

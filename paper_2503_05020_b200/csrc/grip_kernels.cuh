@@ -91,10 +91,25 @@ __device__ double env_ccd(const Dev& D, const EnvIx& E, const int* pt, int npt, 
 // ---------------------------------------------------------------------------
 // begin_step (solver.py:590-645)
 // ---------------------------------------------------------------------------
+__device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S);
+
 __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
   const int e = list[blockIdx.x];
+  // device protocol: only envs whose protocol asked for a new step
+  if (D.round_mode && !D.pr_i[(size_t)e * PI_N + PI_NEEDBEGIN]) return;
+  begin_env(D, e, sm, S);
+  if (D.round_mode) {
+    __syncthreads();
+    if (threadIdx.x == 0 && !(D.flags[e] & FLAG_OVERFLOW)) {   // an overflowed begin is redone later
+      D.pr_i[(size_t)e * PI_N + PI_NEEDBEGIN] = 0;
+      D.pr_i[(size_t)e * PI_N + PI_INSTEP] = 1;
+    }
+  }
+}
+
+__device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], dhat = P[GRIP_P_DHAT];
@@ -1444,6 +1459,103 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
       D.reason[e] = GRIP_R_NONFINITE_STATE;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident grasp protocol (protocol.py:152-277), one thread per env, after k_finalize:
+// the same decisions as BatchedGraspTrials._after_step, in the same order (close-phase halting
+// before the failure check, phase ends, the verdict of the last gravity phase).
+// ---------------------------------------------------------------------------
+__constant__ double kGravDir[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
+
+__global__ void k_protocol(Dev D) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= D.n_env) return;
+  int* I = D.pr_i + (size_t)e * PI_N;
+  double* R = D.pr_d + (size_t)e * PD_N;
+  if (!I[PI_INSTEP] || !D.fin_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
+  I[PI_INSTEP] = 0;
+  atomicAdd(D.pr_steps, 1ull);
+  const double* C = D.pr_cfg;   // settle, hold, grav steps, speed, halt, g, steady, stability
+  const int b0 = D.body_off[e];
+  const double dt = D.params[(size_t)e * GRIP_NPARAM + GRIP_P_DT];
+  const double eps_v = D.params[(size_t)e * GRIP_NPARAM + GRIP_P_EPSV];
+  const int fb[2] = {I[PI_FB0], I[PI_FB1]};
+  const int obj = I[PI_OBJ];
+  I[PI_NSTEPS] += 1;
+  I[PI_PSTEP] += 1;
+  const int ph = I[PI_PHASE];
+  if (ph == 1)
+    for (int j = 0; j < 2; ++j) {
+      const double f = D.body_force[b0 + fb[j]];
+      if (!((I[PI_HALTED] >> j) & 1) && f > C[4]) {
+        I[PI_HALTED] |= 1 << j;
+        R[PD_HF + j] = f;
+        I[PI_HSTEP0 + j] = I[PI_NSTEPS] - 1;
+        for (int c = 0; c < 3; ++c) D.body_vel[3 * (size_t)(b0 + fb[j]) + c] = 0.0;
+      }
+    }
+  const double* com = D.body_com + 3 * (size_t)(b0 + obj);
+  auto disp = [&]() {
+    const double dx = com[0] - R[PD_COM0], dy = com[1] - R[PD_COM0 + 1], dz = com[2] - R[PD_COM0 + 2];
+    return sqrt(dx * dx + dy * dy + dz * dz);
+  };
+  if (D.ns_status[e] == GRIP_NS_FAILED) {
+    I[PI_VERDICT] = 3;
+    I[PI_FPHASE] = ph == 3 ? 3 + I[PI_GPHASE] : ph;
+    I[PI_FREASON] = D.reason[e];
+    I[PI_FSTEP] = I[PI_NSTEPS];
+    if (ph == 3) R[PD_CDISP + I[PI_GPHASE]] = disp();
+    I[PI_PHASE] = 4;
+    return;
+  }
+  bool ended = false;
+  if (ph == 0) ended = I[PI_PSTEP] >= (int)C[0];
+  else if (ph == 1) ended = I[PI_HALTED] == 3 || I[PI_PSTEP] >= I[PI_MAXCLOSE];
+  else if (ph == 2) {
+    I[PI_QUIET] = D.max_speed[e] < eps_v ? I[PI_QUIET] + 1 : 0;
+    ended = I[PI_QUIET] >= (int)C[6] || I[PI_PSTEP] >= (int)C[1];
+  } else if (ph == 3) ended = I[PI_PSTEP] >= (int)C[2];
+  if (ended) {
+    const int mk = ph == 3 ? 3 + I[PI_GPHASE] : ph;
+    I[PI_MARK + 2 * mk] = I[PI_PSTART];
+    I[PI_MARK + 2 * mk + 1] = I[PI_NSTEPS];
+    I[PI_PSTART] = I[PI_NSTEPS];
+    I[PI_PSTEP] = 0;
+    double* gr = D.gravity + 3 * (size_t)e;
+    if (ph == 0) {
+      I[PI_PHASE] = 1;
+      for (int j = 0; j < 2; ++j)
+        for (int c = 0; c < 3; ++c) D.body_vel[3 * (size_t)(b0 + fb[j]) + c] = R[PD_CD + 3 * j + c] * C[3];
+    } else if (ph == 1) {
+      for (int j = 0; j < 2; ++j)
+        for (int c = 0; c < 3; ++c) D.body_vel[3 * (size_t)(b0 + fb[j]) + c] = 0.0;
+      I[PI_PHASE] = 2;
+    } else if (ph == 2) {
+      I[PI_PHASE] = 3;
+      I[PI_GPHASE] = 0;
+      for (int c = 0; c < 3; ++c) gr[c] = C[5] * kGravDir[0][c];
+      for (int c = 0; c < 3; ++c) R[PD_COM0 + c] = com[c];
+    } else {
+      const int g = I[PI_GPHASE];
+      const double d = disp();
+      R[PD_CDISP + g] = d;
+      I[PI_GPHASE] = g + 1;
+      if (g + 1 >= 6) {
+        I[PI_PHASE] = 4;
+        const double thr = C[7] * (int)C[2] * eps_v * dt;
+        const bool in_contact = (D.contact_mask[b0 + obj] & (unsigned)I[PI_GBITS]) != 0u;
+        I[PI_VERDICT] = (in_contact && d < thr) ? 1 : 2;
+        R[PD_FDISP] = d;
+        R[PD_THR] = thr;
+        I[PI_FCONTACT] = in_contact;
+      } else {
+        for (int c = 0; c < 3; ++c) gr[c] = C[5] * kGravDir[g + 1][c];
+        for (int c = 0; c < 3; ++c) R[PD_COM0 + c] = com[c];
+      }
+    }
+  }
+  if (I[PI_PHASE] != 4) I[PI_NEEDBEGIN] = 1;
 }
 
 // packed recorder frame of the envs with m[4e] >= 0 (grip_get_frames): CTA per env

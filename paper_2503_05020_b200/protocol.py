@@ -617,3 +617,106 @@ def run_grasp_trials(group, scenes, protocol=None, max_steps=None, lockstep=Fals
     """Protocol for all envs of a group; returns TrialRecords (labels, markers, COM, halts; with
     record=True also the per-step frames the reference's recorder keeps, for dataset emission)."""
     return BatchedGraspTrials(group, scenes, protocol, record=record).run(max_steps, lockstep=lockstep)
+
+
+# ---------------------------------------------------------------------------
+# device-resident protocol: the state machine above as a kernel (grip_run_rounds)
+# ---------------------------------------------------------------------------
+_MARK_NAMES = ["settle", "close", "hold"] + PHASES
+_VERDICTS = {1: "stable", 2: "unstable", 3: "sim-failed"}
+
+
+class DeviceProtocolTrials:
+    """The grasp protocol (protocol.py:152-277) run on the device (k_protocol): after every
+    finalize the kernel makes BatchedGraspTrials' decisions itself -- finger halts, phase ends,
+    controls of the next step, the verdict -- so ``advance(R)`` runs R continuous-batching
+    rounds with one synchronisation.  Records are read back when trials end."""
+
+    def __init__(self, group, scenes, protocol=None):
+        from paper_2503_05020_b200._native import REASONS
+        self._reasons = REASONS
+        self.group = group
+        self.dev = group.dev
+        self.protocol = pr = protocol or TrialProtocol()
+        E = group.packed.n_env
+        self.E = E
+        env0 = group.envs[0]
+        self.dt = dt = env0.solver_params.dt
+        self.fnames = [list(s.finger_links) for s in scenes]
+        fb = np.zeros((E, 2), np.int32)
+        cd = np.zeros((E, 2, 3))
+        for i, s in enumerate(scenes):
+            if len(self.fnames[i]) != 2:
+                raise ValueError("device protocol expects two finger links")
+            for j, f in enumerate(self.fnames[i]):
+                ids = s.finger_links[f]
+                if len(ids) != 1:
+                    raise ValueError("device protocol expects one body per finger link")
+                fb[i, j] = ids[0]
+                cd[i, j] = np.asarray(s.closing_dirs[f], np.float64)
+        obj = np.array([s.object_body for s in scenes], np.int32)
+        gbits = np.array([sum(1 << b for ids in s.finger_links.values() for b in ids) for s in scenes], np.int32)
+        self.max_close = np.array([int(np.ceil((s.opening / 2.0) / (pr.closing_speed * dt))) + 5 for s in scenes],
+                                  np.int32)
+        self.cd = cd
+        cfg = [int(np.ceil(pr.settle_duration / dt)), int(np.ceil(pr.steady_max_duration / dt)),
+               int(np.ceil(pr.gravity_phase_duration / dt)), pr.closing_speed, pr.force_halt, pr.gravity_magnitude,
+               pr.steady_speed_steps, pr.stability_constant]
+        self.gripper_bodies = [tuple(sorted({b for ids in s.finger_links.values() for b in ids})) for s in scenes]
+        self.object_body = [s.object_body for s in scenes]
+        self.dev.protocol_setup(fb, cd, obj, gbits, self.max_close, cfg)
+        self.finished = np.zeros(E, bool)
+        self.env_steps = 0
+
+    def advance(self, rounds=1):
+        """R device rounds; returns the env-steps completed."""
+        n = self.dev.run_rounds(rounds)
+        self.group.invalidate()
+        self.env_steps += n
+        return n
+
+    def record(self, e, out=None):
+        """TrialRecord of env e from the device protocol state."""
+        o = (out if out is not None else self.dev.protocol_read())[e]
+        r = TrialRecord(object_body=self.object_body[e], gripper_bodies=self.gripper_bodies[e])
+        r.n_steps = int(o.n_steps)
+        r.verdict = _VERDICTS.get(int(o.verdict), "running")
+        r.phase_markers = {_MARK_NAMES[k]: [int(o.markers[2 * k]), int(o.markers[2 * k + 1])]
+                           for k in range(9) if o.markers[2 * k] >= 0}
+        for j, f in enumerate(self.fnames[e]):
+            if (o.halted >> j) & 1:
+                r.halt_forces[f] = {"force": float(o.halt_force[j]), "step": int(o.halt_step[j])}
+        ng = min(6, len([k for k in range(3, 9) if o.markers[2 * k] >= 0]) + (1 if o.verdict == 3 and o.fail_phase >= 3 else 0))
+        for g in range(ng):
+            r.com_displacement[PHASES[g]] = float(o.com_disp[g])
+        if o.verdict == 3:
+            r.failure = {"phase": _MARK_NAMES[int(o.fail_phase)], "reason": self._reasons.get(int(o.fail_reason), "unknown"),
+                         "step": int(o.fail_step)}
+        elif o.verdict in (1, 2):
+            r.metrics.update(final_phase_com_disp=float(o.final_disp), stability_threshold=float(o.threshold),
+                             final_contact=bool(o.final_contact))
+        return r
+
+    def done_envs(self, out=None):
+        o = out if out is not None else self.dev.protocol_read()
+        return np.array([o[e].phase == 4 for e in range(self.E)])
+
+    def restart(self, slots, closing_dirs, max_close):
+        """New trials in `slots` (after grip_reset_envs gave them new candidates)."""
+        m = np.zeros(self.E, np.uint8)
+        m[list(slots)] = 1
+        for e, c, mc in zip(slots, closing_dirs, max_close):
+            self.cd[e] = c
+            self.max_close[e] = mc
+        self.dev.protocol_reset(m, self.cd, self.max_close)
+
+    def run(self, rounds_per_call=8, max_rounds=100000):
+        n = 0
+        while n < max_rounds:
+            self.advance(rounds_per_call)
+            n += rounds_per_call
+            out = self.dev.protocol_read()
+            if self.done_envs(out).all():
+                break
+        out = self.dev.protocol_read()
+        return [self.record(e, out) for e in range(self.E)]
