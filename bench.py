@@ -306,6 +306,9 @@ def main():
     ap.add_argument("--lockstep", action="store_true", help="lockstep Batch.step rounds instead of continuous batching")
     ap.add_argument("--record", default=None, help="record every trial (frames, stress, contact events) and "
                                                    "emit it to this directory in the reference's dataset format")
+    ap.add_argument("--protocol", default="device", choices=["host", "device"],
+                    help="grasp-protocol state machine on the host (per round) or on the device (k_protocol)")
+    ap.add_argument("--rounds-per-call", type=int, default=4, help="device protocol: rounds per host call")
     ap.add_argument("--only-kind", type=int, default=-1, help="diagnostic: run only the lanes of this object kind")
     ap.add_argument("--lanes", type=int, default=3,
                     help="1: one device batch; 3k: k device batches (own stream + host thread) per object kind")
@@ -356,15 +359,46 @@ def main():
             scenes = [sc.cfg2_scene(i % 400, cands) for i in lids]
             envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
             self.group = DeviceEnvGroup(envs, device=local)
-            self.trials = BatchedGraspTrials(self.group, scenes, record=args.record is not None)
+            self.device = args.protocol == "device"
+            if self.device:
+                from paper_2503_05020_b200.protocol import DeviceProtocolTrials
+                self.trials = DeviceProtocolTrials(self.group, scenes)
+            else:
+                self.trials = BatchedGraspTrials(self.group, scenes, record=args.record is not None)
             self.dev = self.group.dev
             self.kind = np.array([kinds[i % 400] for i in lids])
             self.done_trials = []
-            self.advance = self.trials.advance if args.lockstep else self.trials.advance_round
+            self.advance = None if self.device else (self.trials.advance if args.lockstep else self.trials.advance_round)
             self.env_steps = 0
             self.rounds = 0
+            self.h2d = self.d2h = 0
+
+        def refill_device(self):
+            out = self.trials.dev.protocol_read()
+            E, B = self.group.packed.n_env, self.group.packed.n_body_total
+            rec = 4 * 39 + 8 * 19                                  # per-env protocol state (GripTrialOut source)
+            self.d2h += rec * E
+            fin = [e for e in range(len(out)) if out[e].phase == 4]
+            if not fin:
+                return
+            p = self.group.packed
+            for e in fin:                                        # grip_reset_envs slices of the new candidate
+                self.h2d += 8 * (3 * (p.node_off[e + 1] - p.node_off[e]) + 3 * (p.sv_off[e + 1] - p.sv_off[e])
+                                 + 10 * (p.tet_off[e + 1] - p.tet_off[e]))
+            self.h2d += (rec + 24) * E + 24 * B                    # grip_protocol_reset round trip
+            self.d2h += (rec + 24) * E + 24 * B
+            pls = []
+            with qlock:
+                for e in fin:
+                    self.done_trials.append(self.trials.record(e, out).verdict)
+                    k = int(self.kind[e])
+                    pls.append(payloads[queue[k][qpos[k] % len(queue[k])]])
+                    qpos[k] += 1
+            self.trials.refill(fin, pls)
 
         def refill(self):
+            if self.device:
+                return self.refill_device()
             fin = np.nonzero(self.trials.phase == 4)[0]
             if len(fin) == 0:
                 return
@@ -380,10 +414,15 @@ def main():
             self.trials.refill(fin, pls)
 
         def round(self):
-            n = self.advance()
+            if self.device:   # R device rounds per host call, protocol decisions on the device
+                n = self.trials.advance(args.rounds_per_call)
+                self.rounds += args.rounds_per_call
+                self.d2h += 8 + 4 * self.group.packed.n_env       # env-step counter, overflow flags
+            else:
+                n = self.advance()
+                self.rounds += 1
             self.refill()
             self.env_steps += n
-            self.rounds += 1
 
     writer = None
     if args.record is not None:
@@ -426,7 +465,8 @@ def main():
             if timed:
                 ln.dev.timer_start()
             if i == main_lane:
-                for _ in range(n_rounds):
+                r0 = ln.rounds
+                while ln.rounds - r0 < n_rounds:
                     ln.round()
                 stop.set()
             else:
@@ -452,11 +492,14 @@ def main():
         ln.rounds = 0
         ln.nd0 = len(ln.done_trials)
     h2d = d2h = 0
+    if args.protocol == "host":
+        for ln in lanes:
+            E, B = ln.group.packed.n_env, ln.group.packed.n_body_total
+            maxa = ln.dev.max_alpha
+            h2d += 8 * 3 * E + 8 * 3 * B + 2 * E                                # gravity, body velocities, round masks
+            d2h += 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E + E  # reports, alphas, forces+masks+min_d, com, speed, finalized
     for ln in lanes:
-        E, B = ln.group.packed.n_env, ln.group.packed.n_body_total
-        maxa = ln.dev.max_alpha
-        h2d += 8 * 3 * E + 8 * 3 * B + 2 * E                                # gravity, body velocities, round masks
-        d2h += 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E + E  # reports, alphas, forces+masks+min_d, com, speed, finalized
+        ln.h2d = ln.d2h = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -466,6 +509,9 @@ def main():
         wall = time.perf_counter() - t0
     torch.cuda.synchronize()
     ms = max(ln.ms for ln in lanes)
+    if args.protocol == "device":   # counted: per bench step (round of the largest lane)
+        h2d = sum(ln.h2d for ln in lanes) / max(args.steps, 1)
+        d2h = sum(ln.d2h for ln in lanes) / max(args.steps, 1)
     env_steps = sum(ln.env_steps for ln in lanes)
     nsweeps = sum(ln.dev.stats()[2] - ln.sw0 for ln in lanes)
     launches = sum(ln.dev.stats()[1] - ln.l0 for ln in lanes)
@@ -536,11 +582,13 @@ def main():
                    "l2": "working set > L2 (element Hessians alone ~0.5 GB per GPU)",
                    "env_steps_timed": total_steps, "newton_sweeps": int(nsweeps),
                    "ms_per_newton_sweep": ms_max / max(nsweeps, 1),
-                   "mode": "lockstep Batch.step" if args.lockstep else "continuous batching, steady-state refill",
+                   "mode": ("lockstep Batch.step" if args.lockstep else "continuous batching, steady-state refill")
+                           + (f", protocol on the device ({args.rounds_per_call} rounds per host call)"
+                              if args.protocol == "device" else ", protocol on the host"),
                    "trials_completed_timed": sum(len(ln.done_trials) - ln.nd0 for ln in lanes),
                    "lanes": [{"envs": len(l), "rounds": ln.rounds, "env_steps": ln.env_steps, "ms": round(ln.ms, 3)}
                              for l, ln in zip(lane_ids, lanes)]},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
         "gpu_launches": int(launches),
         "recording": None if writer is None else {"dir": str(args.record), "trials_written": n_written[0],

@@ -20,7 +20,6 @@ constexpr int MAXSEG = 8;   // independent segments factored concurrently (2 war
 
 struct DirShared {
   AsmShared A;
-  int turn;                // next contact element allowed to add into the skyline
   int ok[2];
   int nseg;                // independent row segments ahead of the tail (hub) rows
   int seg[MAXSEG + 1];     // segment starts, seg[nseg] = tail start (DOFs)
@@ -107,59 +106,6 @@ __device__ void sky_static(const Dev& D, const EnvIx& E, const Sky& S, int n) {
     if (pf2 > pf) continue;   // the mirrored block lands in the lower triangle
     const int i = 3 * pf + q / 3, j = 3 * pf2 + q % 3;
     if (i >= j) S.at(i, j) = D.sb_val[9 * (size_t)b + q];
-  }
-  __syncthreads();
-}
-
-// The contact / friction elements' K (precomputed by the element kernel, w_store_K) into the
-// skyline.  Warp w takes elements k = w, w + NWARP, ...: it loads K and computes the skyline
-// offsets into registers (the warps overlap this), then adds them when the turn counter
-// reaches k -> every entry accumulates its elements in element order (deterministic), and
-// only the short add section is serialised.
-__device__ void sky_scatter_contacts(const Dev& D, const EnvIx& E, const Sky& S, DirShared& sh) {
-  const int e = E.e;
-  const int na = D.n_act[e];
-  const int nce = na + D.n_anc[e];
-  const size_t cs0 = (size_t)e * (D.cap_act + D.cap_anc);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) sh.turn = 0;
-  __syncthreads();
-  for (int k = warp; k < nce; k += NWARP) {
-    const size_t cs = cs0 + (k < na ? k : D.cap_act + (k - na));
-    const int* kn = D.el_kn + cs * 9;
-    const double* K = D.el_K + cs * 300;
-    const int nn = kn[0];
-    const int node = lane < 8 ? kn[1 + lane] : 0;
-    const int nd = 3 * nn, ne = nd * (nd + 1) / 2;
-    double kv[10];
-    int ko[10];
-#pragma unroll
-    for (int mi = 0; mi < 10; ++mi) {
-      const int t = lane + 32 * mi;
-      const int tt = t < ne ? t : 0;
-      int r = (int)((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
-      while ((r + 1) * (r + 2) / 2 <= tt) ++r;
-      while (r * (r + 1) / 2 > tt) --r;
-      const int q = tt - r * (r + 1) / 2;
-      const int Nr = __shfl_sync(0xffffffffu, node, r / 3), Nq = __shfl_sync(0xffffffffu, node, q / 3);
-      ko[mi] = -1;
-      kv[mi] = 0.0;
-      if (t < ne) {
-        const int i = 3 * Nr + r % 3, j = 3 * Nq + q % 3;
-        kv[mi] = K[t];
-        ko[mi] = S.ro[i] + j - S.fc[i];
-      }
-    }
-    if (lane == 0)
-      while (*(volatile int*)&sh.turn != k) {}
-    __syncwarp();
-    __threadfence_block();
-#pragma unroll
-    for (int mi = 0; mi < 10; ++mi)
-      if (ko[mi] >= 0) S.L[ko[mi]] += kv[mi];
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) *(volatile int*)&sh.turn = k + 1;
   }
   __syncthreads();
 }

@@ -701,6 +701,35 @@ class DeviceProtocolTrials:
         o = out if out is not None else self.dev.protocol_read()
         return np.array([o[e].phase == 4 for e in range(self.E)])
 
+    def refill(self, slots, payloads):
+        """New trials in `slots` with new candidates of the same topology (BatchedGraspTrials.refill)."""
+        p = self.group.packed
+        if not hasattr(self, "_host"):
+            self._host = {"x0": p.node_x0.copy(), "kin0": p.sv_kin0.copy(), "Dmi": p.tet_Dmi.copy(),
+                          "V0": p.tet_V0.copy()}
+        h = self._host
+        mask = np.zeros(self.E, np.uint8)
+        pr = self.protocol
+        cds, mcs = [], []
+        for e, pl in zip(slots, payloads):
+            n0, n1 = p.node_off[e], p.node_off[e + 1]
+            s0, s1 = p.sv_off[e], p.sv_off[e + 1]
+            t0, t1 = p.tet_off[e], p.tet_off[e + 1]
+            if pl["sizes"] != (n1 - n0, s1 - s0, t1 - t0):
+                raise ValueError("refill needs the same topology as the slot's current scene")
+            h["x0"][3 * n0:3 * n1] = pl["x0"]
+            h["kin0"][3 * s0:3 * s1] = pl["kin0"]
+            h["Dmi"][9 * t0:9 * t1] = pl["Dmi"]
+            h["V0"][t0:t1] = pl["V0"]
+            sc = pl["scene"]
+            cds.append(np.array([np.asarray(sc.closing_dirs[f], np.float64) for f in self.fnames[e]]))
+            mcs.append(int(np.ceil((sc.opening / 2.0) / (pr.closing_speed * self.dt))) + 5)
+            env = self.group.envs[e]
+            env._time, env._step, env.status = 0.0, 0, "active"
+            mask[e] = 1
+        self.dev.reset_envs(mask, h["x0"], h["kin0"], h["Dmi"], h["V0"])
+        self.restart(slots, cds, mcs)
+
     def restart(self, slots, closing_dirs, max_close):
         """New trials in `slots` (after grip_reset_envs gave them new candidates)."""
         m = np.zeros(self.E, np.uint8)
