@@ -414,6 +414,12 @@ def main():
             self.trials.refill(fin, pls)
 
         def round(self):
+            t0 = time.perf_counter()
+            self._round()
+            self.call_ms_max = max(getattr(self, "call_ms_max", 0.0), 1e3 * (time.perf_counter() - t0))
+
+        def _round(self):
+            t0 = time.perf_counter()
             if self.device:   # R device rounds per host call, protocol decisions on the device
                 n = self.trials.advance(args.rounds_per_call)
                 self.rounds += args.rounds_per_call
@@ -421,7 +427,10 @@ def main():
             else:
                 n = self.advance()
                 self.rounds += 1
+            t1 = time.perf_counter()
             self.refill()
+            self.t_step = getattr(self, "t_step", 0.0) + t1 - t0
+            self.t_refill = getattr(self, "t_refill", 0.0) + time.perf_counter() - t1
             self.env_steps += n
 
     writer = None
@@ -500,6 +509,8 @@ def main():
             d2h += 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E + E  # reports, alphas, forces+masks+min_d, com, speed, finalized
     for ln in lanes:
         ln.h2d = ln.d2h = 0
+        ln.call_ms_max = 0.0
+        ln.t_step = ln.t_refill = 0.0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -586,7 +597,10 @@ def main():
                            + (f", protocol on the device ({args.rounds_per_call} rounds per host call)"
                               if args.protocol == "device" else ", protocol on the host"),
                    "trials_completed_timed": sum(len(ln.done_trials) - ln.nd0 for ln in lanes),
-                   "lanes": [{"envs": len(l), "rounds": ln.rounds, "env_steps": ln.env_steps, "ms": round(ln.ms, 3)}
+                   "lanes": [{"envs": len(l), "rounds": ln.rounds, "env_steps": ln.env_steps, "ms": round(ln.ms, 3),
+                              "max_call_ms": round(getattr(ln, "call_ms_max", 0.0), 2),
+                              "host_refill_ms": round(1e3 * getattr(ln, "t_refill", 0.0), 1),
+                              "step_call_ms": round(1e3 * getattr(ln, "t_step", 0.0), 1)}
                              for l, ln in zip(lane_ids, lanes)]},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "roofline": roof,
