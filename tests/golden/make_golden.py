@@ -559,6 +559,12 @@ def main():
             res = [r for r in pool.map(_verdict_job, jobs) if r is not None]
             (out / "verdicts.json").write_text(json.dumps(res))
             print("verdicts", [(r["seed"], r["verdict"], r["n_steps"]) for r in res], time.time() - t0)
+        if "verdicts_cfg2" in want:
+            # full-protocol labels of bench (config 2) envs: cylinder / sphere candidates i % 3 = 1, 2
+            jobs = [(("box", "cylinder", "sphere")[i % 3], i, False) for i in (1, 2, 4, 5, 7, 8, 10, 11)]
+            res = [r for r in pool.map(_verdict_job, jobs) if r is not None]
+            (out / "verdicts_cfg2.json").write_text(json.dumps(res))
+            print("verdicts_cfg2", [(r["kind"], r["seed"], r["verdict"], r["n_steps"]) for r in res], time.time() - t0)
         if "candidates" in want:
             gen_candidates(pool); print("candidates", time.time() - t0)
 

@@ -218,3 +218,38 @@ def test_device_element_kernels_vs_reference(golden):
     np.testing.assert_allclose(E, K["abd_E"], rtol=1e-12)
     for n in range(len(inp)):
         assert np.abs(H[n] - K["abd_H"][n]).max() <= 1e-9 * np.abs(K["abd_H"][n]).max()
+
+
+@pytest.mark.parametrize("mode", ["device", "host"])
+def test_protocol_labels_match_reference_cfg2(golden, mode):
+    """Full-protocol labels of bench (config 2) envs with cylinder and sphere objects, the
+    reference's own trials on the bench's candidates (verdicts_cfg2.json), batched together,
+    with the device-resident protocol (the bench default) and the host state machine."""
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.multienv import DeviceEnvGroup
+    from paper_2503_05020_b200.protocol import BatchedGraspTrials, DeviceProtocolTrials
+    from paper_2503_05020_b200.solver import Environment
+    path = golden / "verdicts_cfg2.json"
+    if not path.exists():
+        pytest.skip("verdicts_cfg2.json not generated")
+    ref = json.loads(path.read_text())
+    cands = sc.load_cfg2_candidates()
+    scenes = [sc.cfg2_scene(r["seed"], cands) for r in ref]
+    for s, r in zip(scenes, ref):
+        np.testing.assert_allclose(cands["R"][r["seed"]], r["R"])
+    envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+    grp = DeviceEnvGroup(envs)
+    recs = DeviceProtocolTrials(grp, scenes).run(rounds_per_call=4) if mode == "device" else \
+        BatchedGraspTrials(grp, scenes).run()
+    for r, g in zip(recs, ref):
+        key = (g["kind"], g["seed"])
+        assert r.verdict == g["verdict"], (key, r.verdict, g["verdict"])
+        assert r.n_steps == g["n_steps"], (key, r.n_steps, g["n_steps"])
+        assert r.phase_markers == g["phase_markers"], (key, r.phase_markers, g["phase_markers"])
+        if g["failure"]:
+            assert r.failure["reason"] == g["failure"]["reason"] and r.failure["phase"] == g["failure"]["phase"]
+        for f, h in g["halt_forces"].items():
+            assert r.halt_forces[f]["step"] == h["step"], key
+            assert abs(r.halt_forces[f]["force"] - h["force"]) <= 1e-5 * h["force"], key
+        for k, v in g["com_displacement"].items():
+            assert abs(r.com_displacement[k] - v) <= 1e-6 * 0.1 + 1e-9, (key, k, r.com_displacement[k], v)
