@@ -613,7 +613,13 @@ def main():
         # the path's one collective: fixed-size per-env outcome records, gathered once at the end
         from paper_2503_05020_b200.distributed import gather_outcomes, pack_outcomes
         tg = time.perf_counter()
-        recs = {i: r for l, ln in zip(lane_ids, lanes) for i, r in zip(l, ln.trials.records)}
+        recs = {}
+        for l, ln in zip(lane_ids, lanes):
+            if ln.device:   # the device protocol's current trial records
+                out = ln.trials.dev.protocol_read()
+                recs.update({i: ln.trials.record(k, out) for k, i in enumerate(l)})
+            else:
+                recs.update({i: r for i, r in zip(l, ln.trials.records)})
         allr = gather_outcomes(pack_outcomes([recs[i] for i in ids], ids), args.envs * world, device="cuda")
         line["outcome_gather"] = {"envs": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg), "backend": "nccl"}
     if rank == 0 and not args.no_cpu:

@@ -31,7 +31,7 @@ def pack_outcomes(records, env_ids, finger_names=("finger0", "finger1")):
     out = np.full((len(records), len(OUTCOME_FIELDS)), np.nan)
     for k, (r, e) in enumerate(zip(records, env_ids)):
         out[k, 0] = e
-        out[k, 1] = VERDICTS.index(r.verdict)
+        out[k, 1] = VERDICTS.index(r.verdict) if r.verdict in VERDICTS else -1   # -1: trial still running
         out[k, 2] = r.n_steps
         out[k, 3] = r.metrics.get("final_phase_com_disp", np.nan)
         for j, f in enumerate(finger_names[:2]):

@@ -69,3 +69,11 @@ def test_gather_outcomes_world2_gloo(n_envs):
         np.testing.assert_array_equal(a[:, 2], 70 + np.arange(n_envs))
         np.testing.assert_allclose(a[:, 6], 50.0 + np.arange(n_envs))
     np.testing.assert_array_equal(res[0], res[1])
+
+
+def test_pack_outcomes_running_trial():
+    """A trial still running when the outcomes are gathered (the device protocol's records mid
+    trial) packs as verdict -1 instead of failing."""
+    r = TrialRecord(verdict="running", n_steps=12)
+    a = pack_outcomes([r], [5])
+    assert a[0, 0] == 5 and a[0, 1] == -1 and a[0, 2] == 12
