@@ -213,6 +213,12 @@ int grip_get_frames(GripBatch* b, const uint8_t* mask, double* x, double* v, dou
  * max d_o in *d_max and, if d_o is not NULL, every value. */
 int grip_sdf_exact(const double* pts, int64_t n, const double* verts, int32_t n_verts, const int32_t* tris,
                    int32_t n_tris, const double* face_n, const double* edge_n, const double* vert_n, double* out);
+/* Exact nearest-neighbour distance of n points to a cloud of m points (the SDF far field,
+ * sdf.py:150-151): cloud sorted by the caller into leaves of 8 under an implicit complete
+ * binary tree of `levels` levels of boxes (heap order, 2^(levels+1)-1 nodes, box_lo / box_hi
+ * 3 per node, empty leaves as inverted boxes). */
+int grip_sdf_nn(const double* pts, int64_t n, const double* cloud, int64_t m, const double* box_lo, const double* box_hi,
+                int32_t levels, double* out);
 int grip_sdf_query(const double* values, const int32_t* dims, const double* origin, const double* spacing,
                    const double* rot, const double* trans, const double* world_lo, const double* world_hi,
                    const double* pts, int64_t n, double* d_o, double* d_max);

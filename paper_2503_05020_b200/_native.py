@@ -97,6 +97,7 @@ def load():
         ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64]),
         ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
+        ("grip_sdf_nn", [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp, i32, vp]),
         ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
         ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
@@ -146,6 +147,38 @@ def sdf_exact(pts, verts, tris, face_n, edge_n, vert_n):
     out = np.empty(len(pts))
     check(lib.grip_sdf_exact(ptr(pts), len(pts), ptr(verts), len(verts), ptr(tris), len(tris), ptr(face_n),
                              ptr(edge_n), ptr(vert_n), ptr(out)))
+    return out
+
+
+def sdf_nn(pts, cloud):
+    """Exact nearest-neighbour distances of pts to cloud (grip_sdf_nn): the cloud is Morton-sorted
+    into leaves of 8 under an implicit complete binary tree of boxes built here."""
+    lib = load()
+    pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+    cloud = np.asarray(cloud, np.float64).reshape(-1, 3)
+    lo, hi = cloud.min(axis=0), cloud.max(axis=0)
+    g = np.clip(((cloud - lo) / np.maximum(hi - lo, 1e-300) * 1023.0).astype(np.int64), 0, 1023)
+    code = np.zeros(len(cloud), np.int64)
+    for b in range(10):   # 30-bit Morton code
+        for a in range(3):
+            code |= ((g[:, a] >> b) & 1) << (3 * b + a)
+    cloud = np.ascontiguousarray(cloud[np.argsort(code, kind="stable")])
+    m = len(cloud)
+    n_leaf = max(1, -(-m // 8))
+    levels = int(np.ceil(np.log2(n_leaf))) if n_leaf > 1 else 0
+    L = 1 << levels
+    # padding slots: +inf for the minima, -inf for the maxima (empty leaves: inverted boxes)
+    llo = np.concatenate([cloud, np.full((L * 8 - m, 3), np.inf)]).reshape(L, 8, 3).min(axis=1)
+    lhi = np.concatenate([cloud, np.full((L * 8 - m, 3), -np.inf)]).reshape(L, 8, 3).max(axis=1)
+    lv_lo, lv_hi = [llo], [lhi]
+    while len(lv_lo[-1]) > 1:
+        a, b = lv_lo[-1], lv_hi[-1]
+        lv_lo.append(np.minimum(a[0::2], a[1::2]))
+        lv_hi.append(np.maximum(b[0::2], b[1::2]))
+    box_lo = np.ascontiguousarray(np.concatenate(lv_lo[::-1]))
+    box_hi = np.ascontiguousarray(np.concatenate(lv_hi[::-1]))
+    out = np.empty(len(pts))
+    check(lib.grip_sdf_nn(ptr(pts), len(pts), ptr(cloud), m, ptr(box_lo), ptr(box_hi), levels, ptr(out)))
     return out
 
 

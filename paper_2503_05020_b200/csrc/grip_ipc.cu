@@ -1622,3 +1622,20 @@ int grip_sdf_query(const double* values, const int32_t* dims, const double* orig
   }
   return 0;
 }
+
+int grip_sdf_nn(const double* pts, int64_t n, const double* cloud, int64_t m, const double* box_lo, const double* box_hi,
+                int32_t levels, double* out) {
+  if (n <= 0) return 0;
+  const size_t nodes = ((size_t)2 << levels) - 1;
+  DevBuf<double> dp, dc, dl, dh, dout;
+  if (!dp.put(pts, 3 * (size_t)n) || !dc.put(cloud, 3 * (size_t)m) || !dl.put(box_lo, 3 * nodes) ||
+      !dh.put(box_hi, 3 * nodes) || !dout.alloc(n)) {
+    g_err = "grip_sdf_nn: device allocation / copy failed";
+    return -1;
+  }
+  const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 32);
+  k_sdf_nn<<<blocks, 128>>>(dp.p, n, dc.p, m, dl.p, dh.p, levels, dout.p);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dout.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return 0;
+}

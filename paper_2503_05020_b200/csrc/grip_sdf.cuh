@@ -100,3 +100,65 @@ __global__ void k_sdf_query(SdfGridDev G, const double* R, V3 Tr, V3 lo, V3 hi, 
 }
 
 }  // namespace grip
+
+namespace grip {
+
+// Exact nearest-neighbour distance from every query to a point cloud (the far field of
+// build_sdf, sdf.py:150-151, there a scipy cKDTree).  The cloud is sorted by Morton code on
+// the host and grouped into leaves of SDF_LEAF points under an implicit complete binary tree
+// of boxes (heap order, node k -> children 2k+1, 2k+2); one thread per query walks it depth
+// first, nearer child first, pruning boxes farther than the best distance so far.  Squared
+// distances are summed without FMA contraction, in x, y, z order, as cKDTree does, so the
+// minimum is the same double.
+constexpr int SDF_LEAF = 8;
+
+__device__ __forceinline__ double d2_rn(V3 a, V3 b) {
+  const double dx = __dsub_rn(a.x, b.x), dy = __dsub_rn(a.y, b.y), dz = __dsub_rn(a.z, b.z);
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+__device__ __forceinline__ double box_d2(V3 q, const double* lo, const double* hi) {
+  const double gx = fmax(fmax(lo[0] - q.x, q.x - hi[0]), 0.0);
+  const double gy = fmax(fmax(lo[1] - q.y, q.y - hi[1]), 0.0);
+  const double gz = fmax(fmax(lo[2] - q.z, q.z - hi[2]), 0.0);
+  return gx * gx + gy * gy + gz * gz;
+}
+
+__global__ void k_sdf_nn(const double* pts, long long n, const double* cloud, long long m, const double* blo,
+                         const double* bhi, int levels, double* out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const V3 q = ld3(pts + 3 * i);
+    double best = INFINITY;
+    int stack[64];
+    int sp = 0;
+    stack[sp++] = 0;
+    const int first_leaf = (1 << levels) - 1;
+    while (sp) {
+      const int k = stack[--sp];
+      // the box test is a strict prune with a small relative margin: it only skips work,
+      // the exact distances below decide
+      if (box_d2(q, blo + 3 * (size_t)k, bhi + 3 * (size_t)k) * (1.0 - 1e-12) > best) continue;
+      if (k >= first_leaf) {
+        const long long p0 = (long long)(k - first_leaf) * SDF_LEAF;
+        const long long p1 = p0 + SDF_LEAF < m ? p0 + SDF_LEAF : m;
+        for (long long p = p0; p < p1; ++p) best = fmin(best, d2_rn(q, ld3(cloud + 3 * p)));
+        continue;
+      }
+      const int c0 = 2 * k + 1, c1 = 2 * k + 2;
+      const double d0 = box_d2(q, blo + 3 * (size_t)c0, bhi + 3 * (size_t)c0);
+      const double d1 = box_d2(q, blo + 3 * (size_t)c1, bhi + 3 * (size_t)c1);
+      // push the farther child first so the nearer one is visited next
+      const double m0 = d0 * (1.0 - 1e-12), m1 = d1 * (1.0 - 1e-12);
+      if (d0 <= d1) {
+        if (m1 <= best) stack[sp++] = c1;
+        if (m0 <= best) stack[sp++] = c0;
+      } else {
+        if (m0 <= best) stack[sp++] = c0;
+        if (m1 <= best) stack[sp++] = c1;
+      }
+    }
+    out[i] = sqrt(best);
+  }
+}
+
+}  // namespace grip

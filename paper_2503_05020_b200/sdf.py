@@ -7,11 +7,12 @@ band (cloud distance <= band_cells * h, or a cut cell) is the exact point-triang
 signed by the angle-weighted pseudonormal of the closest feature.
 
 What runs where: the grid, the seeded cloud (numpy's generator, the reference's call
-sequence), the cloud nearest-neighbour distances (scipy cKDTree, exact) and the flood fill
-(scipy.ndimage.label) are host preprocessing; the narrow band -- the reference's costly
-part, a Python loop over kd-tree candidates with certificates (sdf.py:181-241) -- is one
-CUDA kernel over all band points against all triangles (grip_sdf_exact).  Queries
-(trilinear, posed) run on the GPU too (metrics.py, grip_sdf_query).
+sequence) and the flood fill (scipy.ndimage.label) are host preprocessing.  On the GPU:
+the far field -- the exact nearest cloud point of every grid node (the reference's cKDTree;
+here a Morton-ordered box tree walked per node, grip_sdf_nn) -- and the narrow band -- the
+reference's costly part, a Python loop over kd-tree candidates with certificates
+(sdf.py:181-241), here one kernel over all band points against all triangles
+(grip_sdf_exact).  Queries (trilinear, posed) run on the GPU too (metrics.py, grip_sdf_query).
 """
 
 from __future__ import annotations
@@ -115,7 +116,6 @@ def build_sdf(vertices, triangles, resolution=128, padding_cells=4, band_cells=4
     import time
 
     from scipy import ndimage
-    from scipy.spatial import cKDTree
 
     clock = [time.perf_counter()]
 
@@ -142,7 +142,7 @@ def build_sdf(vertices, triangles, resolution=128, padding_cells=4, band_cells=4
     n_cloud = int(min(400_000, max(20_000, 4.0 * triangle_areas(v, t).sum() / (h * h))))
     cloud = np.concatenate([sample_surface(v, t, n_cloud, rng), v])
     lap("cloud")
-    d_cloud, _ = cKDTree(cloud).query(pts, k=1, workers=-1)
+    d_cloud = nv.sdf_nn(pts, cloud)   # exact nearest cloud point on the GPU (the reference: cKDTree)
     lap("cloud_nn")
 
     occupied = np.zeros(tuple(dims), dtype=bool)
