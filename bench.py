@@ -309,6 +309,8 @@ def main():
     ap.add_argument("--protocol", default="device", choices=["host", "device"],
                     help="grasp-protocol state machine on the host (per round) or on the device (k_protocol)")
     ap.add_argument("--rounds-per-call", type=int, default=4, help="device protocol: rounds per host call")
+    ap.add_argument("--lane-priority", default="0,1,2",
+                    help="stream priority per object kind (box, cylinder, sphere): the heavier envs first")
     ap.add_argument("--only-kind", type=int, default=-1, help="diagnostic: run only the lanes of this object kind")
     ap.add_argument("--lanes", type=int, default=3,
                     help="1: one device batch; 3k: k device batches (own stream + host thread) per object kind")
@@ -453,6 +455,10 @@ def main():
         wthread = threading.Thread(target=write_loop, daemon=True)
         wthread.start()
     lanes = [Lane(l) for l in lane_ids]
+    if args.lane_priority:   # e.g. "0,1,2": box, cylinder, sphere lanes
+        pr = [int(v) for v in args.lane_priority.split(",")]
+        for ln in lanes:
+            ln.dev.set_priority(pr[int(ln.kind[0])] if len(pr) > int(ln.kind[0]) else 0)
 
     def run_lanes(n_rounds, timed):
         """Every lane runs rounds on its own thread; the lane with the most envs runs exactly

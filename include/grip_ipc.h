@@ -167,6 +167,8 @@ int grip_stress(GripBatch* b, double* out /* n_tet*7 */);
  * ev_i (7 per event: kind 0 PT / 1 EE, body a, body b, 4 env-local sv ids), ev_d (2 per event:
  * d, lambda = kappa m |b'(d)|).  cap = rows available in ev_i / ev_d. */
 int grip_set_recording(GripBatch* b, int on);
+/* stream priority of the batch (0 default, larger = scheduled first among concurrent batches) */
+int grip_set_priority(GripBatch* b, int priority);
 /* Device-resident grasp protocol (protocol.py:152-277): the phase state machine
  * runs on the device after every finalize (k_protocol), sets the fingers' velocities and the
  * gravity of the next step itself, and keeps the trial record, so many rounds run back to back

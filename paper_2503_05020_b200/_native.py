@@ -98,6 +98,7 @@ def load():
         ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
         ("grip_sdf_nn", [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp, i32, vp]),
+        ("grip_set_priority", [vp, i32]),
         ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
         ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
@@ -353,6 +354,10 @@ class DeviceBatch:
         sp = np.empty(self.n_env)
         check(self.lib.grip_get_body_state(self.h, ptr(com), ptr(sp)))
         return com, sp
+
+    def set_priority(self, priority):
+        """Stream priority among concurrent batches (grip_set_priority)."""
+        check(self.lib.grip_set_priority(self.h, int(priority)))
 
     def set_recording(self, on=True):
         """Contact-event recording in every finalize (grip_set_recording)."""

@@ -1269,6 +1269,20 @@ int grip_protocol_read(GripBatch* b, GripTrialOut* out) {
   return 0;
 }
 
+// Scheduling priority of the batch's stream (0 = default, larger = more urgent, clamped to the
+// device's range): lanes sharing a GPU can favour the batch with the longest per-env chains.
+int grip_set_priority(GripBatch* b, int priority) {
+  int lo = 0, hi = 0;   // CUDA: numerically lower = higher priority (hi <= lo)
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  const int p = std::max(hi, std::min(lo, lo - priority));
+  CK(cudaStreamSynchronize(b->stream));
+  cudaStream_t s = nullptr;
+  CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, p));
+  CK(cudaStreamDestroy(b->stream));
+  b->stream = s;
+  return 0;
+}
+
 int grip_set_recording(GripBatch* b, int on) {
   b->D.ev_on = on ? 1 : 0;
   return 0;
