@@ -317,6 +317,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.record is not None or args.lockstep:
+        args.protocol = "host"   # recording and lockstep rounds drive the host state machine
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
