@@ -490,7 +490,6 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.tet_W = b->alloc<double>(90 * (size_t)std::max(NTET, 1));
   D.jac_list = b->alloc<int2>((size_t)std::max(NTET, 1));
   D.jac_n = b->alloc<int>(1);
-  CK(cudaFuncSetAttribute(k_tet_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 81 * TJ * (int)sizeof(double)));
   }
   D.abd_node = b->upload(d->abd_node, NA);
   D.abd_kV = b->upload(d->abd_kV, NA);

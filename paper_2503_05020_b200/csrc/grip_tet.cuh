@@ -12,7 +12,7 @@
 //   tet's eigenbasis Y of its previous Newton iteration, Gershgorin test of S~.  When every
 //   disc lies above the clamp floor nothing is clamped: H (direct formula) + the lifted
 //   translations is written.  Otherwise S~ goes to tet_S and the tet to jac_list.
-// k_tet_jacobi (grip_tetclamp.cuh): eigenvalues + rotation R of S~, thread per tet.
+// k_tet_jacobi2 (grip_tetclamp.cuh): eigenvalues + rotation R of S~, two threads per tet.
 // k_tet_back (one warp per deferred tet): V = Y R (the next warm start), S_proj =
 //   V diag(max(l, f)) V^T, H = Q S_proj Q^T + f/4 on equal components (translations lifted to
 //   f = 1e-12 max|l|, exactly the reference's clamp of the 12x12 matrix).
@@ -22,6 +22,19 @@
 namespace grip {
 
 constexpr int TF = 128;   // threads per k_tet_front block
+
+// Helmert basis (q1 = (1,-1,0,0)/sqrt2, q2 = (1,1,-2,0)/sqrt6, q3 = (1,1,1,-3)/sqrt12) and the
+// lower-triangle (row << 4 | column) list of a 12x12 matrix, for k_tet_back
+__constant__ double kHelm[3][4] = {{0.70710678118654752440, -0.70710678118654752440, 0.0, 0.0},
+                                   {0.40824829046386301637, 0.40824829046386301637, -2.0 * 0.40824829046386301637, 0.0},
+                                   {0.28867513459481288225, 0.28867513459481288225, 0.28867513459481288225,
+                                    -3.0 * 0.28867513459481288225}};   // the same doubles as helmert()
+__constant__ unsigned char kTri78[78] = {
+    0x00, 0x10, 0x11, 0x20, 0x21, 0x22, 0x30, 0x31, 0x32, 0x33, 0x40, 0x41, 0x42, 0x43, 0x44, 0x50, 0x51, 0x52, 0x53, 0x54,
+    0x55, 0x60, 0x61, 0x62, 0x63, 0x64, 0x65, 0x66, 0x70, 0x71, 0x72, 0x73, 0x74, 0x75, 0x76, 0x77, 0x80, 0x81, 0x82, 0x83,
+    0x84, 0x85, 0x86, 0x87, 0x88, 0x90, 0x91, 0x92, 0x93, 0x94, 0x95, 0x96, 0x97, 0x98, 0x99, 0xa0, 0xa1, 0xa2, 0xa3, 0xa4,
+    0xa5, 0xa6, 0xa7, 0xa8, 0xa9, 0xaa, 0xb0, 0xb1, 0xb2, 0xb3, 0xb4, 0xb5, 0xb6, 0xb7, 0xb8, 0xb9, 0xba, 0xbb};
+
 
 __device__ __forceinline__ double helm_c(int i, int k) {   // compile-time foldable Helmert entry
   const double r2 = 0.70710678118654752440, r6 = 0.40824829046386301637, r12 = 0.28867513459481288225;
@@ -253,24 +266,26 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
       w.S[e] = a;
     }
     __syncwarp();
-    double* Hg = D.el_H + slot * 144;
-    for (int q = lane; q < 78; q += 32) {   // H = Q S_proj Q^T + f/4 on equal components
-      int r = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
-      while ((r + 1) * (r + 2) / 2 <= q) ++r;
-      while (r * (r + 1) / 2 > q) --r;
-      const int c12 = q - r * (r + 1) / 2;   // column <= row
-      const int m = r / 3, c = r % 3, M = c12 / 3, C = c12 % 3;
-      double s = (c == C) ? 0.25 * f : 0.0;
-      for (int i = 0; i < 3; ++i) {
-        const double hi = helmert(i, m);
-        if (hi == 0.0) continue;
-        for (int j = 0; j < 3; ++j) {
-          const double hj = helmert(j, M);
-          if (hj == 0.0) continue;
-          const int p = 3 * i + c, pq = 3 * j + C;
-          s += hi * hj * (p <= pq ? w.S[p * 9 + pq] : w.S[pq * 9 + p]);
-        }
+    // H = Q S_proj Q^T + f/4 on equal components, as two 3-term contractions:
+    // T[(i,c)][(M,C)] = sum_j S[(i,c),(j,C)] h(j,M), then H[(m,c),(M,C)] = sum_i h(i,m) T[(i,c)][(M,C)]
+    for (int e = lane; e < 108; e += 32) {
+      const int pr = e / 12, q = e - 12 * pr, M = q / 3, C = q - 3 * M;
+      double a = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int pc = 3 * j + C;
+        a += (pr <= pc ? w.S[pr * 9 + pc] : w.S[pc * 9 + pr]) * kHelm[j][M];
       }
+      w.T[e] = a;
+    }
+    __syncwarp();
+    double* Hg = D.el_H + slot * 144;
+    for (int q = lane; q < 78; q += 32) {
+      const int rc = kTri78[q], r = rc >> 4, c12 = rc & 15;   // column <= row
+      const int m = r / 3, c = r - 3 * m;
+      double s = (c == c12 % 3) ? 0.25 * f : 0.0;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s += kHelm[i][m] * w.T[(3 * i + c) * 12 + c12];
       Hg[r * 12 + c12] = s;
       if (c12 != r) Hg[c12 * 12 + r] = s;
     }

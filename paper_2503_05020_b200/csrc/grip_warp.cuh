@@ -221,7 +221,7 @@ __device__ void w_rotate_into(WarpWS& w, const double* V0, int lane) {
 // reference clamp (materials.py:101-113) of a translation-invariant 4-point stencil Hessian in w.H
 // (Vwarm: previous eigenvectors of this element or null; Vout: where to keep the new ones)
 // defer_S: when the eigensolve is needed, write S (warm-rotated S~ for tets; upper triangle, 45)
-// there and return true without clamping; k_tet_jacobi / k_tet_finish complete the clamp
+// there and return true without clamping; k_tet_jacobi2 / k_tet_finish complete the clamp
 __device__ bool w_clamp_stencil(WarpWS& w, int lane, const double* Vwarm = nullptr, double* Vout = nullptr,
                                 double* defer_S = nullptr) {
   for (int e = lane; e < 144; e += 32) {
