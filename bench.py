@@ -539,6 +539,7 @@ def main():
     for name in kss[0]:
         ks[name] = {"ms": sum(k[name]["ms"] for k in kss), "launches": sum(k[name]["launches"] for k in kss)}
     ks["elements"]["units"] = {u: sum(k["elements"]["units"][u] for k in kss) for u in kss[0]["elements"]["units"]}
+    env_iters = sum(k["elements"].get("env_iterations", 0.0) for k in kss)
     for f in ("pcg_iterations", "solves"):
         ks["assemble_pcg"][f] = sum(k["assemble_pcg"][f] for k in kss)
     ks["assemble_pcg"]["mean_unknowns"] = 0.0
@@ -601,6 +602,12 @@ def main():
                    "l2": "working set > L2 (element Hessians alone ~0.5 GB per GPU)",
                    "env_steps_timed": total_steps, "newton_sweeps": int(nsweeps),
                    "ms_per_newton_sweep": ms_max / max(nsweeps, 1),
+                   # the metric's second half: one batched Newton iteration = one round of
+                   # a lane over its active envs; env_iterations = newton_iteration calls of all envs
+                   "newton": {"env_iterations_per_s": env_iters / (ms_max / 1e3),
+                              "ms_per_batched_iteration": ms_max / max(args.steps, 1),
+                              "envs_per_batched_iteration": env_iters / max(sum(ln.rounds for ln in lanes), 1),
+                              "note": "profiling on: env_iterations counted in k_work_scan since set_profiling"},
                    "mode": ("lockstep Batch.step" if args.lockstep else "continuous batching, steady-state refill")
                            + (f", protocol on the device ({args.rounds_per_call} rounds per host call)"
                               if args.protocol == "device" else ", protocol on the host"),

@@ -431,6 +431,7 @@ class DeviceBatch:
         out["assemble_pcg"]["pcg_iterations"] = units[4]
         out["assemble_pcg"]["solves"] = units[5]
         out["assemble_pcg"]["mean_unknowns"] = units[6] / max(units[5], 1.0)
+        out["elements"]["env_iterations"] = units[7]   # newton_iteration calls (env sweeps)
         return out
 
     def timer_start(self):

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
 __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n) {
   __shared__ Red sm;
   int base = 0;
-  double ct = 0.0, ca = 0.0, cc = 0.0, cf = 0.0;
+  double ct = 0.0, ca = 0.0, cc = 0.0, cf = 0.0, cn = 0.0;   // cn: envs iterating (newton_iteration calls)
   int cbase = 0, tbase = 0, ebase = 0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
         w = nt + na + wc;
         wt = nt;
         we = na + wc;
-        ct += nt; ca += na; cc += D.n_act[e]; cf += D.n_anc[e];
+        ct += nt; ca += na; cc += D.n_act[e]; cf += D.n_anc[e]; cn += 1.0;
       }
     }
     int tot;
@@ -326,6 +326,7 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
     ebase += tot;
   }
   ct = block_sum(ct, sm); ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
+  cn = block_sum(cn, sm);
   if (threadIdx.x == 0) {
     D.work_off[n] = base;
     D.cwork_off[n] = cbase;
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
     *D.jac_n = 0;   // the element kernel appends deferred tet / contact clamps
     *D.cjac_n = 0;
     D.stats[0] += ct; D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;
+    D.stats[7] += cn;
   }
 }
 
