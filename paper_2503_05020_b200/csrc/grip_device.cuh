@@ -113,6 +113,8 @@ struct Dev {
   int *cs_pt, *cs_ee, *cs_eid, *cs_n;
   double* cs_R;
   int* cs_valid;
+  double* cs_drift;  // summed max surface displacement since the superset was built (Verlet skin)
+  double ss_skin;    // extra radius (units of dhat) a superset is built with, GRIP_SKIN
   double ss_k;        // superset covers dhat + ss_k * (last Newton step's max displacement)
   double* md_prev;   // last Newton step's max surface displacement
   double* md_kin;    // this step's prescribed (kinematic) displacement bound

@@ -181,8 +181,11 @@ __device__ void sky_scatter_rows(const Dev& D, const EnvIx& E, const Sky& S, Dir
           if (scan_all) {
             const int* kn = D.el_kn + slot_of(u) * 9;
             const int nn = kn[0];
-            for (int q = 0; q < nn; ++q)
-              if (kn[1 + q] == I) a = q;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {   // all nine loads issued at once (no nn-dependent loop)
+              const int v = kn[1 + q];
+              if (q < nn && v == I) a = q;
+            }
             k = a >= 0 ? u : -1;
           } else {
             const int t = lst[lo + u];

@@ -33,17 +33,39 @@ __device__ __forceinline__ double superset_radius(const Dev& D, int e, double dh
   return fmin(R, 12.0 * dhat);
 }
 
-// make D.cs_* a superset at radius >= need for the current positions (D.sv_pos)
+// Verlet skin: a superset built at radius R from positions X0 is still a superset at radius
+// R - 2 drift for positions X, if no surface vertex moved more than drift (any norm >= the max
+// norm) between X0 and X: both reference predicates are per-axis box tests (broadphase.py:
+// 177-183, 195-210), and a vertex coordinate and an AABB face each move by at most drift.  The
+// relative / absolute margins cover the rounding of the drift sums and of the predicates.
+// With drift == 0 (positions unchanged since the build) the superset covers exactly R.
+__device__ __forceinline__ bool cs_covers(const Dev& D, int e, double need) {
+  if (!D.cs_valid[e]) return false;
+  const double dr = D.cs_drift[e];
+  return dr == 0.0 ? D.cs_R[e] >= need : D.cs_R[e] - 2.0 * dr * (1.0 + 1e-9) - 1e-12 >= need;
+}
+
+// surfaces of env e moved by at most dmax since the last call (thread 0)
+__device__ __forceinline__ void cs_moved(const Dev& D, int e, double dmax) {
+  if (threadIdx.x == 0) {
+    if (D.ss_skin > 0.0) D.cs_drift[e] += dmax;
+    else D.cs_valid[e] = 0;
+  }
+}
+
+// make D.cs_* a superset at radius >= need for the current positions (D.sv_pos); built with
+// the skin GRIP_SKIN * dhat on top, so that it survives the next small moves
 __device__ bool ensure_superset(const Dev& D, const EnvIx& E, double need, double dhat, BPShared& S, Red& sm) {
   const int e = E.e;
-  const bool valid = D.cs_valid[e] && D.cs_R[e] >= need;
+  const bool valid = cs_covers(D, e, need);
   __syncthreads();
   if (valid) return true;
-  const double R = fmax(need, superset_radius(D, e, dhat));
+  const double R = fmax(need, superset_radius(D, e, dhat)) + D.ss_skin * dhat;
   const bool ok = broad_phase_env(D, E, R, D.cs_pt + (size_t)e * 4 * D.cap_pt, D.cs_ee + (size_t)e * 4 * D.cap_ee,
                                   D.cs_eid + (size_t)e * 2 * D.cap_ee, D.cs_n + 2 * e, S, sm);
   if (threadIdx.x == 0) {
     D.cs_R[e] = R;
+    D.cs_drift[e] = 0.0;
     D.cs_valid[e] = ok ? 1 : 0;
   }
   __syncthreads();
@@ -147,7 +169,7 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
     if (threadIdx.x == 0) D.md_kin[e] = md;
     int* cn = D.c2_n + 2 * e;
     const double rk = dhat + 2.0 * md;
-    const bool reuse = D.cs_valid[e] && rk <= D.cs_R[e];
+    const bool reuse = cs_covers(D, e, rk);
     __syncthreads();
     if (reuse) {
       filter_from_superset(D, E, rk, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
@@ -182,7 +204,7 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
         for (int c = 0; c < 3; ++c) D.kin_pos[3 * (size_t)g + c] += alpha * vb[c] * dt;
       }
     }
-    if (threadIdx.x == 0) D.cs_valid[e] = 0;  // surfaces moved
+    cs_moved(D, e, alpha * md);  // surfaces moved
     __syncthreads();
   } else {
     if (threadIdx.x == 0) D.md_kin[e] = 0.0;
@@ -1103,7 +1125,7 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
   int* cee = D.c2_ee + (size_t)e * 4 * D.cap_ee;
   int* ceid = D.c2_eid + (size_t)e * 2 * D.cap_ee;
   const double r2 = dhat + 2.0 * md;
-  const bool reuse = D.cs_valid[e] && r2 <= D.cs_R[e];
+  const bool reuse = cs_covers(D, e, r2);
   __syncthreads();
   if (threadIdx.x == 0) D.md_prev[e] = md;
   if (reuse) {
@@ -1225,8 +1247,8 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
     const size_t g = 3 * (size_t)E.n0 + i;
     D.x[g] = D.x[g] + alpha * D.pdir[g];
   }
+  cs_moved(D, e, alpha * md);  // x moved
   if (threadIdx.x == 0) {
-    D.cs_valid[e] = 0;  // x moved
     const int it = D.iters[e];
     if (it < D.max_alpha) D.alphas[(size_t)e * D.max_alpha + it] = alpha;
     D.iters[e] = it + 1;
