@@ -55,7 +55,7 @@ EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, 
 KGROUPS = {"elements": ["k_tet_front", "k_elements_w", "k_tet_jacobi2", "k_tet_back", "k_tet_finish"],
            "assemble_pcg": ["k_contact_K", "k_assemble_direct"], "candidates": ["k_candidates"],
            "line_search": ["k_linesearch"], "begin": ["k_begin"], "finalize": ["k_finalize"]}
-NCU_FULL = ROOT / "profiles" / "r1_ncu_full_v4.json"
+NCU_FULL = ROOT / "profiles" / "r1_ncu_full_v5.json"
 
 
 def _ncu_group(group):
