@@ -407,16 +407,19 @@ __device__ void seg_forward(const Sky& S, const double* rdiag, int c0, int c1, d
   const int lane = G.t & 31;
   for (int kb = c0; kb < c1; kb += 32) {
     const int kend = min(kb + 32, c1);
-    if (G.w == 0) {
+    if (G.w == 0) {   // diagonal block in registers: lane i holds x[i], y_k by shuffle
       const int i = kb + lane;
-      const int fi = i < kend ? S.fc[i] : c1;
+      const bool in = i < kend;
+      const int fi = in ? S.fc[i] : c1;
+      const double* row = S.L + (in ? S.ro[i] - fi : 0);
+      double xi = in ? x[i] : 0.0;
+      const double rd = in ? rdiag[i] : 0.0;
       for (int k = kb; k < kend; ++k) {
-        const double yk = x[k] * rdiag[k];
-        __syncwarp();
-        if (lane == 0) x[k] = yk;
-        if (i > k && i < kend && fi <= k) x[i] -= S.at(i, k) * yk;
-        __syncwarp();
+        const double yk = __shfl_sync(0xffffffffu, xi * rd, k - kb);
+        if (i == k) xi = yk;
+        if (i > k && in && fi <= k) xi -= row[k] * yk;
       }
+      if (in) x[i] = xi;
     }
     G.sync();
     for (int i = kend + G.t; i < c1; i += G.nt) {
@@ -435,15 +438,18 @@ __device__ void seg_backward(const Sky& S, const double* rdiag, int c0, int c1, 
   const int lane = G.t & 31;
   for (int kb = c0 + ((c1 - 1 - c0) / 32) * 32; kb >= c0; kb -= 32) {
     const int kend = min(kb + 32, c1);
-    if (G.w == 0) {
+    if (G.w == 0) {   // diagonal block in registers: lane i holds x[i], x_k by shuffle
       const int i = kb + lane;
+      const bool in = i < kend;
+      double xi = in ? x[i] : 0.0;
+      const double rd = in ? rdiag[i] : 0.0;
       for (int k = kend - 1; k >= kb; --k) {
-        const double xk = x[k] * rdiag[k];
-        __syncwarp();
-        if (lane == 0) x[k] = xk;
-        if (i < k && i >= S.fc[k]) x[i] -= S.at(k, i) * xk;
-        __syncwarp();
+        const double xk = __shfl_sync(0xffffffffu, xi * rd, k - kb);
+        if (i == k) xi = xk;
+        const int fk = S.fc[k];
+        if (i < k && i >= fk) xi -= S.L[S.ro[k] + i - fk] * xk;
       }
+      if (in) x[i] = xi;
     }
     G.sync();
     for (int i = c0 + G.t; i < kb; i += G.nt) {

@@ -728,7 +728,6 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
   double* SG = D.sv_g + (size_t)e * 3 * D.max_sv;
   for (int i = threadIdx.x; i < E.ns; i += NT) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll 4
     for (int q = ip[i]; q < ip[i + 1]; ++q) {
       const int code = inc[q];
       const double* gg = D.el_g + (elbase + ce_slot(D, e, code >> 2)) * 12 + 3 * (code & 3);
@@ -747,7 +746,6 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     for (int c = 0; c < 3; ++c) d[c] = D.x[3 * g + c] - D.xhat[3 * g + c];
     for (int r = 0; r < 3; ++r) gr[r] = M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2];
     double ge[3] = {0.0, 0.0, 0.0};
-#pragma unroll 4
     for (int q = D.tinc_ptr[g]; q < D.tinc_ptr[g + 1]; ++q) {
       const int code = D.tinc[q];
       const double* gg = D.el_g + (elbase + (code >> 2)) * 12 + 3 * (code & 3);
@@ -811,7 +809,6 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     const int f = D.sb_row[b] - E.f0;
     double v[9];
     for (int i = 0; i < 9; ++i) v[i] = 0.0;
-#pragma unroll 4
     for (int q = D.sbc_ptr[b]; q < D.sbc_ptr[b + 1]; ++q) {
       const int code = D.sbc[q];
       const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
