@@ -276,17 +276,47 @@ __device__ __forceinline__ bool diag_factor(const Sky& S, double* rdiag, int kb,
 // Right-looking panels over columns [c0, c1): the diagonal blocks, the panel solve and the
 // rank-PW update of rows [j0, c1) and of the extra rows [x0, n) (the tail, whose updates are
 // limited to columns < c1).  Rows / columns whose envelope starts after a panel are
-// structurally zero in it and skipped.  Returns false on a non-positive pivot.
+// structurally zero in it and skipped.  Look-ahead: the group's first warp updates the next
+// panel's diagonal block (rows [j0, j0 + PW) of the trailing update) and factors it while the
+// other warps update the remaining rows, so a panel costs two barriers and the serial diagonal
+// factorisation overlaps the trailing update.  Returns false on a non-positive pivot.
+__device__ __forceinline__ void trail_row(const Sky& S, int i, int kb, int wb, int j0, int c1, int lane) {
+  if (S.fc[i] > kb) return;   // L[i][j] -= L[i][panel] . L[j][panel]
+  const double* pi = &S.at(i, kb);
+  double li[PW];
+  bool nz = false;
+#pragma unroll
+  for (int c = 0; c < PW; ++c) {
+    li[c] = c < wb ? pi[c] : 0.0;
+    nz |= li[c] != 0.0;
+  }
+  if (!nz) return;
+  double* row = S.L + S.ro[i] - S.fc[i];
+  const int jend = min(i, c1 - 1);
+  for (int j = j0 + lane; j <= jend; j += 32) {
+    const int fj = S.fc[j];
+    if (fj > kb) continue;
+    const double* pj = S.L + S.ro[j] + kb - fj;
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < PW; ++c)
+      if (c < wb) acc += li[c] * pj[c];
+    row[j] -= acc;
+  }
+}
+
 __device__ bool sky_panels(const Sky& S, double* rdiag, int c0, int c1, int x0, int n, const Grp& G, int* okf) {
+  static_assert(NT / 64 >= 2, "look-ahead needs two warps per group");
   const int lane = G.t & 31;
+  if (c0 >= c1) return true;
+  if (G.w == 0) {
+    const bool ok = diag_factor(S, rdiag, c0, min(PW, c1 - c0), lane);
+    if (lane == 0) *okf = ok;
+  }
+  G.sync();
   for (int kb = c0; kb < c1; kb += PW) {
-    const int wb = min(PW, c1 - kb);
-    if (G.w == 0) {
-      const bool ok = diag_factor(S, rdiag, kb, wb, lane);
-      if (lane == 0) *okf = ok;
-    }
-    G.sync();
     if (!*okf) return false;
+    const int wb = min(PW, c1 - kb);
     const int j0 = kb + wb;
     const int nrow = (c1 - j0) + (n - x0);
     for (int t = G.t; t < nrow; t += G.nt) {   // panel rows: r * L_kk^T = row
@@ -316,35 +346,24 @@ __device__ bool sky_panels(const Sky& S, double* rdiag, int c0, int c1, int x0, 
         if (c < wb) pi[c] = r[c];
     }
     G.sync();
-    for (int t = G.w; t < nrow; t += G.nw) {   // trailing: L[i][j] -= L[i][panel] . L[j][panel]
-      const int i = t < c1 - j0 ? j0 + t : x0 + t - (c1 - j0);
-      if (S.fc[i] > kb) continue;
-      const double* pi = &S.at(i, kb);
-      double li[PW];
-      bool nz = false;
-#pragma unroll
-      for (int c = 0; c < PW; ++c) {
-        li[c] = c < wb ? pi[c] : 0.0;
-        nz |= li[c] != 0.0;
+    const int nb = min(PW, c1 - j0);   // rows of the next diagonal block
+    if (G.w == 0) {
+      for (int t = 0; t < nb; ++t) trail_row(S, j0 + t, kb, wb, j0, c1, lane);
+      if (nb > 0) {
+        __syncwarp();
+        const bool ok = diag_factor(S, rdiag, j0, nb, lane);
+        if (lane == 0) *okf = ok;
       }
-      if (!nz) continue;
-      double* row = S.L + S.ro[i] - S.fc[i];
-      const int jend = min(i, c1 - 1);
-      for (int j = j0 + lane; j <= jend; j += 32) {
-        const int fj = S.fc[j];
-        if (fj > kb) continue;
-        const double* pj = S.L + S.ro[j] + kb - fj;
-        double acc = 0.0;
-#pragma unroll
-        for (int c = 0; c < PW; ++c)
-          if (c < wb) acc += li[c] * pj[c];
-        row[j] -= acc;
+    } else {
+      for (int t = nb + G.w - 1; t < nrow; t += G.nw - 1) {
+        const int i = t < c1 - j0 ? j0 + t : x0 + t - (c1 - j0);
+        trail_row(S, i, kb, wb, j0, c1, lane);
       }
     }
     G.sync();
   }
-  return true;
-}
+  return true;   // the last panel has no next block: *okf was checked at its top (and is not
+}                // re-read here, the caller's next segment may already be writing it)
 
 __device__ __forceinline__ Grp seg_group(int nseg) {
   const int G2 = nseg >= 2;
