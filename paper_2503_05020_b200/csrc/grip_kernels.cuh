@@ -666,6 +666,20 @@ __device__ void asm_converge(const Dev& D, const EnvIx& E, const double* X, doub
 // (-g over free dofs in pcg_b) and the static block values (mass + dt^2 element blocks).
 // Returns false if the env failed (element error or non-finite assembly).
 __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double dt2, double* Etot_out) {
+#ifdef GRIP_PHASE_TIMING   // sub-phases of the prologue (tests/diag_phase.py)
+  long long tl = clock64();
+#define PPH(k)                                 \
+  do {                                         \
+    __syncthreads();                           \
+    if (threadIdx.x == 0) {                    \
+      const long long t = clock64();           \
+      GSTAT(48 + (k), t - tl);                 \
+      tl = t;                                  \
+    }                                          \
+  } while (0)
+#else
+#define PPH(k) do {} while (0)
+#endif
   Red& sm = A.sm;
   const int e = E.e;
   // element-level failures, in the reference's raise order (_elastic before contact)
@@ -706,6 +720,7 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     }
   }
   __syncthreads();
+  PPH(0);
   // ---- energy (solver.py:543-562) ----
   double ein = 0.0;
   for (int n = threadIdx.x; n < E.nn; n += NT) {
@@ -724,6 +739,7 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
   for (int k = threadIdx.x; k < nce; k += NT) ecf += D.el_E[elbase + ce_slot(D, e, k)];
   ecf = block_sum(ecf, sm);
   const double Etot = ein + dt2 * eel + dt2 * ecf;
+  PPH(1);
   // ---- gradient: g = M dx + dt^2 (g_el + G^T g_sv) ----
   double* SG = D.sv_g + (size_t)e * 3 * D.max_sv;
   for (int i = threadIdx.x; i < E.ns; i += NT) {
@@ -736,6 +752,7 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     SG[3 * i] = s0; SG[3 * i + 1] = s1; SG[3 * i + 2] = s2;
   }
   __syncthreads();
+  PPH(2);
   const size_t vb = (size_t)e * 3 * D.max_free;
   double* RHS = D.pcg_b;  // -g over free dofs
   int nonfinite = !isfinite(Etot);
@@ -799,9 +816,11 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     }
     __syncthreads();
   }
+  PPH(3);
   for (int i = threadIdx.x; i < 3 * E.nf; i += NT) nonfinite |= !isfinite(RHS[vb + i]);
   nonfinite = block_or(nonfinite, sm);
   if (nonfinite) { fail_env(D, e, GRIP_R_NONFINITE); return false; }
+  PPH(4);
   // ---- static block values (mass + dt^2 * element blocks) ----
   const int blk0 = D.sb_rowptr[E.f0], nblk = D.sb_rowptr[E.f0 + E.nf] - blk0;
   for (int t = threadIdx.x; t < nblk; t += NT) {   // one block per thread
@@ -821,6 +840,8 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     for (int i = 0; i < 9; ++i) D.sb_val[9 * (size_t)b + i] = (diag ? M[i] : 0.0) + dt2 * v[i];
   }
   __syncthreads();
+  PPH(5);
+#undef PPH
   *Etot_out = Etot;
   return true;
 }

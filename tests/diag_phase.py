@@ -16,3 +16,6 @@ print(f"CTAs {v[8]:.0f} mean nce {v[9] / v[8]:.1f}  heavy(>128) CTAs {v[24]:.0f}
 for k, nm in enumerate(names):
     print(f"{nm:10s} all {v[k] / v[8]:10.0f}   heavy {v[16 + k] / max(v[24], 1):10.0f}")
 print("nseg>=2", v[43], "shifted", v[44], "chol cyc when nseg<2", v[45] / max(v[46], 1), v[46])
+pn = ["incidence", "energy", "grad_sv", "grad_nodes+abd", "nonfinite", "static_blocks"]
+for k, nm in enumerate(pn):
+    print(f"  prologue.{nm:15s} {v[48 + k] / v[8]:10.0f}")
