@@ -22,6 +22,7 @@ struct DirShared {
   AsmShared A;
   int ok[2];
   int nseg;                // independent row segments ahead of the tail (hub) rows
+  int sc_next;             // sky_scatter_rows: next node (dynamic schedule)
   int seg[MAXSEG + 1];     // segment starts, seg[nseg] = tail start (DOFs)
 };
 
@@ -160,9 +161,17 @@ __device__ void sky_scatter_rows(const Dev& D, const EnvIx& E, const Sky& S, Dir
       lst[b + 1] = t;
     }
   }
+  if (threadIdx.x == 0) sh.sc_next = 0;
   __syncthreads();
-  // element u of node I's walk: its element index and I's slot in it (-1: not a member)
-  for (int I = warp; I < nf; I += NWARP) {
+  // nodes are dealt out to the warps one at a time, last node first: the hub nodes (last in
+  // the dense order, with the long element walks) start at once and the other warps share the
+  // short lists, instead of a hub walk queued behind a warp's share of short ones
+  for (;;) {
+    int R = 0;
+    if (lane == 0) R = atomicAdd(&sh.sc_next, 1);
+    R = __shfl_sync(0xffffffffu, R, 0);
+    if (R >= nf) break;
+    const int I = nf - 1 - R;
     const int lo = off[I], hi = off[I + 1];
     if (hi == lo) continue;
     const bool scan_all = hi - lo > SC_LONG;
