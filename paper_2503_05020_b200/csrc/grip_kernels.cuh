@@ -707,8 +707,12 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
     inc[atomicAdd(&cur[v], 1)] = it;   // it == (k << 2) | j
   }
   __syncthreads();
+  // short lists: insertion sort by one thread; long ones (vertices of the grasped body that
+  // many contacts share): rank sort by a warp, every lane ranks its items against the list
+  constexpr int INC_SHORT = 12, INC_RANK = 4;   // warp rank sort up to 32 * INC_RANK items
   for (int i = threadIdx.x; i < E.ns; i += NT) {
     const int lo = ip[i], hi = ip[i + 1];
+    if (hi - lo > INC_SHORT && hi - lo <= 32 * INC_RANK) continue;
     for (int a = lo + 1; a < hi; ++a) {
       const int t = inc[a];
       int b = a - 1;
@@ -717,6 +721,37 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
         --b;
       }
       inc[b + 1] = t;
+    }
+  }
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int seen = 0;   // long lists are dealt out to warps in sv order (ballot over 32 svs)
+    for (int c0 = 0; c0 < E.ns; c0 += 32) {
+      const int len = c0 + lane < E.ns ? ip[c0 + lane + 1] - ip[c0 + lane] : 0;
+      unsigned m = __ballot_sync(0xffffffffu, len > INC_SHORT && len <= 32 * INC_RANK);
+      while (m) {
+        const int i = c0 + __ffs(m) - 1;
+        m &= m - 1;
+        if (seen++ % NWARP != warp) continue;
+        const int lo = ip[i], hi = ip[i + 1];
+        int t[INC_RANK], r[INC_RANK];
+#pragma unroll
+        for (int u = 0; u < INC_RANK; ++u) {
+          const int a = lo + lane + 32 * u;
+          t[u] = a < hi ? inc[a] : 0;
+          r[u] = 0;
+        }
+        for (int b = lo; b < hi; ++b) {   // codes (k << 2) | j are distinct
+          const int v = inc[b];
+#pragma unroll
+          for (int u = 0; u < INC_RANK; ++u) r[u] += v < t[u];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < INC_RANK; ++u)
+          if (lo + lane + 32 * u < hi) inc[lo + r[u]] = t[u];
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
