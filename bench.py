@@ -1,24 +1,33 @@
-"""Benchmark: env-steps/s of the batched grasp protocol (BASELINE config 2) on B200.
+"""Benchmark: env-steps/s of batched grasp trials (BASELINE configs 2-5) on B200.
 
-Workload (BASELINE.json configs[1]): 400 environments per GPU, each a soft UMI-style
-two-pad gripper grasping a rigid (ABD) box / cylinder / sphere (slot s: kind s % 3,
-reference-sampled antipodal candidates), stepped through the reference's validation
-protocol (settle, force-halted closing, hold, six gravity phases; protocol.py:152-277).
-Slots are kept full the way a dataset-generation run keeps them full: when a trial ends,
-its slot restarts with the next candidate of the same object kind.  A bench "step" is one
-device round: one Newton sweep of every unfinished env plus begin/finalize for envs at a
-time-step boundary.  W warm-up rounds bring the slots to steady state, then K timed
-rounds; value counts the env time steps (solver.py:764-771 newton_step calls) that
-completed in the timed rounds.
+Workload (BASELINE.json configs[1], the default): 400 environments per GPU, each a soft
+UMI-style two-pad gripper grasping a rigid (ABD) box / cylinder / sphere (env i: kind i % 3,
+the reference-sampled antipodal candidate of seed i), run through the reference's validation
+protocol (settle, force-halted closing, hold, six gravity phases; protocol.py:152-277) by
+``runner.TrialRunner``: one device batch ("lane") per object kind, each with its own CUDA stream
+and host thread, the protocol state machine on the device, and every finished trial's slot
+refilled in place with the rank's next candidate (dataset-generation steady state).
+``--config 3`` runs 400 soft Neo-Hookean objects with kinematic fingers and the reference's
+randomized material; ``--config 4`` 200 bimanual envs (two soft grippers, one soft object) with
+the recorder's stress field output every step; ``--sweep`` the config-5 env-count sweep.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+A bench "step" is ``--rounds-per-step`` (16) continuous-batching rounds of the lane with the most
+envs (one round = one Newton sweep of every unfinished env plus begin / finalize / protocol for
+the envs at a time-step boundary); the other lanes keep running until it is done.  Before the
+W timed-out warm-up steps end, every slot must also have finished one trial (steady phase mix,
+all buffers grown), whatever W says.  value = env time steps (solver.py:764-771 newton_step
+calls) completed in the K timed steps / device time (CUDA events on each lane's stream, max over
+lanes, max over ranks).
 
-Reports (one JSON line on rank 0): value = env-steps/s from CUDA events on the
-library stream (max over ranks), e2e = the same through the public Python API
-with host buffers (controls H2D, reports/forces D2H every step, wall clock),
-roofline of the dominant kernel from live per-launch CUDA events, and a CPU
-baseline: the oracle port (oracle/, the reference's algorithm restated in numpy)
-timed on this host's cores on a bounded sample of the same workload.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3|4]
+
+Also reported (one JSON line on rank 0): e2e (the same through the public runner API, host wall
+clock, with every refill's candidate payload H2D and every trial readout D2H inside the timed
+region), the north star's safety report (intersections, inverted elements, min distance, min J,
+label / failure mix of the timed trials), the roofline of the dominant kernel group and a
+whole-round byte model, and the CPU baseline: the UNMODIFIED reference (baseline/_ref gripsim)
+timed on this host's cores on a bounded sample of the same workload (the oracle port if the
+reference is not installed).
 """
 
 from __future__ import annotations
@@ -40,46 +49,73 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "env-steps/sec at 400 envs (1/2/4/8 B200) vs CPU ref; ms per Newton iteration"
 UNIT = "env-steps/s"
-ENVS_PER_GPU = 400
+REF_DIR = ROOT / "baseline" / "_ref"
 
-# Algorithmic bytes per element of the element kernel (fp64 8 B, index 4 B; each input
-# read once, each output written once): inputs + (E 8 + grad 96 + 12x12 Hessian 1152 + idx 16).
+WORKLOADS = {
+    2: dict(envs=400, mode="device", workload="cfg2: soft 2-pad UMI-style gripper on rigid (ABD) box/cylinder/sphere, "
+                                              "full grasp protocol, antipodal candidate seed i (kind i % 3)"),
+    3: dict(envs=400, mode="device", workload="cfg3: soft Neo-Hookean box/sphere (kind i % 2) with kinematic fingers, "
+                                              "randomized material (E log-uniform 1e4-1e7, mu 0.1-1), friction, full "
+                                              "grasp protocol"),
+    4: dict(envs=200, mode="host", workload="cfg4: bimanual, two soft 2-pad grippers on one soft cube (yaw i), full "
+                                            "grasp protocol with 4 halting pads, recorder frames incl. stress field "
+                                            "every step"),
+}
+
+# Algorithmic bytes per element of the element kernels (fp64 8 B, index 4 B; each input read once,
+# each output written once): inputs + (E 8 + grad 96 + 12x12 Hessian 1152 + idx 16).
 EL_OUT = 8 + 96 + 1152 + 16
 EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, Dm^-1, V0/mu/lam
             "affine": 96 + 8 + EL_OUT,                  # q, kappa*V
             "contacts": 16 + 4 + 96 + 8 + 8 + EL_OUT,   # row, code, 4 positions, rest lengths
             "anchors": 16 + 32 + 48 + 16 + 192 + EL_OUT}  # verts, gamma, T, lam/mu, x and x_prev
+ASM_BYTES = 1256.0   # per element: its Hessian, gradient and energy read once by the assembly
+
+# kernel groups as timed live (grip_kernel_stats) -> the kernels of the ncu capture; launches per round
+KGROUPS = {"elements": {"k_tet_front": 1, "k_elements_w": 1, "k_tet_jacobi2": 2, "k_tet_back": 1, "k_tet_finish": 1},
+           "assemble_pcg": {"k_contact_K": 1, "k_assemble_direct": 1}, "candidates": {"k_candidates": 1},
+           "line_search": {"k_linesearch": 1}, "begin": {"k_begin": 1}, "finalize": {"k_finalize": 1}}
+NCU_FULL = [ROOT / "profiles" / "r2_ncu_full.json", ROOT / "profiles" / "r1_ncu_full_v5.json"]
 
 
-# kernel groups as timed live (grip_kernel_stats) -> the kernels of the committed ncu capture
-KGROUPS = {"elements": ["k_tet_front", "k_elements_w", "k_tet_jacobi2", "k_tet_back", "k_tet_finish"],
-           "assemble_pcg": ["k_contact_K", "k_assemble_direct"], "candidates": ["k_candidates"],
-           "line_search": ["k_linesearch"], "begin": ["k_begin"], "finalize": ["k_finalize"]}
-NCU_FULL = ROOT / "profiles" / "r1_ncu_full_v5.json"
+# ---------------------------------------------------------------------------
+# helpers: peaks, ncu capture, clocks
+# ---------------------------------------------------------------------------
 
 
 def _ncu_group(group):
-    """dram read + write bytes and fp64 FLOPs per launch of a kernel group, from the committed
-    ncu --set full capture (one round: each kernel of the group once)."""
-    try:
-        rows = json.loads(NCU_FULL.read_text())
-    except (OSError, ValueError):
-        return None, None, None
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    want = {k: 2 if k == "k_tet_jacobi2" else 1 for k in KGROUPS.get(group, [])}   # launches per round
-    seen, traffic, flop = {}, 0.0, 0.0
-    for d in rows:
-        k = d["kernel"].split("::")[-1]
-        if seen.get(k, 0) >= want.get(k, 0):
+    """DRAM read + write bytes and fp64 FLOPs per round of a kernel group (each kernel's average
+    per launch in the committed ncu --set full capture x its launches per round), the capture's
+    element units per round (for rescaling to the timed launches) and its source."""
+    for path in NCU_FULL:
+        try:
+            doc = json.loads(path.read_text())
+        except (OSError, ValueError):
             continue
-        seen[k] = seen.get(k, 0) + 1
-        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            v, unit = d[m].split()
-            traffic += float(v.replace(",", "")) * scale[unit]
-        flop += d.get("fp64_flop", 0.0)
-    if not seen:
-        return None, None, None
-    return traffic, flop, f"{NCU_FULL.relative_to(ROOT)} (ncu --set full, one round)"
+        rows = doc["rows"] if isinstance(doc, dict) else doc
+        meta = doc.get("meta", {}) if isinstance(doc, dict) else {"units_per_round": {"tets": 76800.0},
+                                                                  "note": "one --lanes 1 round, 400 envs per launch"}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        acc = {}
+        for d in rows:
+            k = d["kernel"].split("::")[-1].split("(")[0]
+            if k not in KGROUPS.get(group, {}):
+                continue
+            b = 0.0
+            for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v, unit = d[m].split()
+                b += float(v.replace(",", "")) * scale[unit]
+            a = acc.setdefault(k, [0, 0.0, 0.0])
+            a[0] += 1
+            a[1] += b
+            a[2] += d.get("fp64_flop", 0.0)
+        if not acc:
+            continue
+        w = KGROUPS[group]
+        traffic = sum(w[k] * a[1] / a[0] for k, a in acc.items())
+        flop = sum(w[k] * a[2] / a[0] for k, a in acc.items())
+        return traffic, flop, meta, str(path.relative_to(ROOT))
+    return None, None, None, None
 
 
 def _fp64_peak():
@@ -102,8 +138,8 @@ def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -149,32 +185,128 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU side (oracle port): bounded sample of the same workload on the host cores
+# workloads: jobs (candidate indices), scenes, lane keys
 # ---------------------------------------------------------------------------
 
 
-def _cpu_worker(args):
-    """One env through W untimed + K timed protocol steps with the oracle; returns timings."""
-    i, warmup, steps = args
+def workload(cfg):
+    """(candidate pool size, scene_of(job), key_of(job), lane priority per key)."""
+    from paper_2503_05020_b200 import scene as sc
+    if cfg == 2:
+        c = sc.load_cfg2_candidates()
+        kinds = np.asarray(c["kind"])
+        return len(kinds), (lambda j: sc.cfg2_scene(j, c)), (lambda j: int(kinds[j])), {0: 0, 1: 1, 2: 2}
+    if cfg == 3:
+        c = sc.load_cfg3_candidates()
+        kinds = np.asarray(c["kind"])
+        return len(kinds), (lambda j: sc.cfg3_scene(j, c)), (lambda j: int(kinds[j])), {0: 0, 1: 1}
+    if cfg == 4:
+        return 1 << 30, (lambda j: sc.bimanual_scene(yaw=2.0 * np.pi * ((j * 0.6180339887498949) % 1.0))), \
+            (lambda j: 0), {0: 0}
+    raise ValueError(f"unknown config {cfg}")
+
+
+def rank_jobs(pool, envs, world, rank, global_envs=None):
+    """Jobs (candidate ids) of this rank.  Weak scaling: `envs` per rank, rank r takes candidates
+    [r*envs, (r+1)*envs) of the pool (distinct across ranks while the pool lasts).  Strong
+    scaling (global_envs): the contiguous shard of range(global_envs)."""
+    from paper_2503_05020_b200.distributed import shard
+    if global_envs:
+        lo, hi = shard(global_envs, world, rank)
+        return [j % pool for j in range(lo, hi)]
+    return [(rank * envs + i) % pool for i in range(envs)]
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference (baseline/_ref) or the oracle port, on the host cores
+# ---------------------------------------------------------------------------
+
+_CPU_COUNTER = None
+
+
+def _ref_available():
+    try:
+        sys.path.insert(0, str(REF_DIR))
+        import gripsim.pipeline.protocol  # noqa: F401
+        return True
+    except Exception:
+        return False
+    finally:
+        if sys.path and sys.path[0] == str(REF_DIR):
+            sys.path.pop(0)
+
+
+def _ref_trial(args):
+    """One full reference trial (pipeline/__init__.py:25-49 _validation_worker minus metrics): the
+    reference's own build_trial_env + run_grasp_trial, unmodified; env.step is wrapped on the
+    instance only to count completed env-steps into a shared counter."""
+    cfg, j = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    sys.path.insert(0, str(REF_DIR))
+    from gripsim.geometry import mesh as gm
+    from gripsim.pipeline import config as rcfg
+    from gripsim.pipeline import protocol as rproto
+    from gripsim.synth import GraspCandidate
+    from paper_2503_05020_b200 import scene as sc
+    sc_ = rcfg.SceneConfig()
+    override = None
+    if cfg == 2:
+        c = sc.load_cfg2_candidates()
+        kind = [str(k) for k in c["kinds"]][int(c["kind"][j])]
+        sc_.gripper.soft_fingers = True
+        if kind == "cylinder":
+            r, h, seg = c["cyl"]
+            path = Path(f"/tmp/grip_bench_cyl_{os.getpid()}.obj")
+            if not path.exists():
+                gm.save_obj(gm.revolved_surface([(0.0, 0.0), (r, 0.0), (r, h), (0.0, h)], segments=int(seg),
+                                                center=(0.0, 0.0, -0.5 * h)), path)
+            sc_.object.kind, sc_.object.mesh_path = "mesh", str(path)
+        else:
+            sc_.object.kind = kind
+    else:
+        c = sc.load_cfg3_candidates()
+        kind = [str(k) for k in c["kinds"]][int(c["kind"][j])]
+        sc_.object.kind, sc_.object.soft = kind, True
+        sc_.gripper.soft_fingers = False
+        from gripsim.materials import MaterialParams
+        override = MaterialParams(young_modulus=float(c["E"][j]), poisson_ratio=float(c["nu"][j]),
+                                  density=float(c["rho"][j]), friction_coefficient=float(c["mu"][j]))
+    cand = GraspCandidate("parallel", c["R"][j], c["T"][j], [c["opening"][j]], [])
+    env, ob, fl = rcfg.build_trial_env(sc_, cand, env_id=j, material_override=override)
+    step = env.step
+
+    def counted():
+        rep = step()
+        with _CPU_COUNTER.get_lock():
+            _CPU_COUNTER.value += 1
+        return rep
+
+    env.step = counted
+    rec = rproto.run_grasp_trial(env, sc_.protocol, ob, fl)
+    return rec.n_steps
+
+
+def _port_trial(args):
+    """The same trial through the oracle port (oracle/, the reference's algorithm restated)."""
+    cfg, j = args
     os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import solver as osv   # CPU baseline leg only
     from paper_2503_05020_b200 import scene as sc
-    s = sc.cfg2_scene(i % 400)
+    s = sc.cfg2_scene(j) if cfg == 2 else sc.cfg3_scene(j)
     env = osv.OracleEnv(s.bodies, collide_pairs_off=s.collide_pairs_off)
+    step = env.step
+
+    def counted():
+        rep = step()
+        with _CPU_COUNTER.get_lock():
+            _CPU_COUNTER.value += 1
+        return rep
+
+    env.step = counted
     sm = _OracleProtocol(env, s)
-    for _ in range(warmup):
-        if not sm.advance():
-            break
-    t0 = time.perf_counter()
-    n = 0
-    calls = 0
-    for _ in range(steps):
-        c0 = getattr(env, "n_calls", 0)
-        if not sm.advance():
-            break
-        calls += getattr(env, "n_calls", 0) - c0
-        n += 1
-    return n, time.perf_counter() - t0, calls
+    while sm.advance():
+        pass
+    return sm.k
 
 
 class _OracleProtocol:
@@ -192,9 +324,7 @@ class _OracleProtocol:
     def advance(self):
         from oracle import solver as osv
         env, s = self.env, self.s
-        if self.phase >= 4:
-            return False
-        if env.status != "active":
+        if self.phase >= 4 or env.status != "active":
             return False
         rep = env.step()
         ev = env.events_now()
@@ -245,43 +375,59 @@ class _OracleProtocol:
         return True
 
 
-def cpu_measure(n_envs, warmup, steps, cores):
+def _init_counter(counter):
+    global _CPU_COUNTER
+    _CPU_COUNTER = counter
+
+
+def cpu_measure(cfg, jobs, seconds, cores, warm=5.0):
+    """Steady-state CPU throughput: `cores` worker processes (fork, OMP_NUM_THREADS=1) run full
+    trials of `jobs` back to back (more jobs than cores, so no core idles); every completed
+    env-step bumps a shared counter.  After `warm` s the counter is read over `seconds` of wall
+    time: env-steps / s on all cores, partial trials included, no tail effect."""
+    use_ref = cfg in (2, 3) and _ref_available()
+    fn = _ref_trial if use_ref else _port_trial
     ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_cpu_worker, [(i, warmup, steps) for i in range(n_envs)], chunksize=1)
-    wall = time.perf_counter() - t0
-    n = sum(r[0] for r in res)
-    busy = sum(r[1] for r in res)
-    calls = sum(r[2] for r in res)
-    # each worker is single threaded: aggregate rate = env-steps / (busy core-seconds / cores)
-    rate = n / (busy / min(cores, n_envs)) if busy > 0 else 0.0
-    return {"value": rate, "env_steps": n, "core_seconds": busy, "wall_s": wall, "newton_calls": calls,
-            "ms_per_newton_iteration": 1e3 * busy / max(calls, 1)}
+    counter = ctx.Value("q", 0)
+    pool = ctx.Pool(cores, initializer=_init_counter, initargs=(counter,))
+    res = pool.imap_unordered(fn, [(cfg, j) for j in jobs], chunksize=1)
+    time.sleep(warm)
+    c0, t0 = counter.value, time.perf_counter()
+    time.sleep(seconds)
+    c1, t1 = counter.value, time.perf_counter()
+    pool.terminate()
+    pool.join()
+    del res
+    return {"value": (c1 - c0) / (t1 - t0), "env_steps": int(c1 - c0), "wall_s": t1 - t0, "cores": cores,
+            "kind": "reference" if use_ref else "port",
+            "impl": "baseline/_ref gripsim 0.1.0 (unmodified): build_trial_env + run_grasp_trial" if use_ref
+            else "oracle/ numpy port of the reference path"}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle port of the reference path on all host cores."""
+    """--impl reference: the reference's own CPU path on all host cores, same config / metric."""
     if rank != 0:
         return
+    cfg = 2 if args.config in (2, 5) else args.config
     cores = os.cpu_count() or 1
-    n_envs = cores
+    seconds = float(min(120.0, max(20.0, 3.0 * args.steps)))
+    pool, _, _, _ = workload(cfg) if cfg != 4 else (0, None, None, None)
+    if cfg == 4:
+        print(json.dumps({"impl": "reference", "unavailable": "config 4 (bimanual) has no reference trial driver"}))
+        return
+    jobs = rank_jobs(pool, WORKLOADS[cfg]["envs"], 1, 0)[:8 * cores]
     t_all = time.perf_counter()
-    # each worker runs one env's full protocol trial (capped at 150 steps): the same phase mix
-    # as the GPU's steady state; W / K are reported but the sample is the bounded trial set
-    r = cpu_measure(n_envs, 0, min(args.steps, 150), cores)
-    steps_done = r["env_steps"]
+    r = cpu_measure(cfg, jobs, seconds, cores)
     value = r["value"]
+    sample = (f"{r['impl']}; {cores} worker processes, full protocol trials of bench candidates "
+              f"{jobs[0]}..{jobs[-1]} back to back; env-steps counted over {r['wall_s']:.0f} s of wall time "
+              f"after 5 s warm-up: {r['env_steps']} env-steps")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * r["core_seconds"] / max(args.steps, 1) / max(min(cores, n_envs), 1),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["wall_s"] / max(args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: soft 2-pad gripper on rigid box/cylinder/sphere, full grasp protocol",
-                   "envs": n_envs, "sample": f"{n_envs} envs, full protocol trials (<= {min(args.steps, 150)} steps)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, n_envs), "kind": "port",
-                         "sample": f"oracle/ numpy port, {n_envs} envs, {steps_done} env-steps, "
-                                   f"{r['ms_per_newton_iteration']:.1f} ms per newton_iteration"},
+        "config": {"workload": WORKLOADS[cfg]["workload"], "envs": len(jobs), "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": r["kind"], "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t_all,
     }
@@ -293,32 +439,231 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 
 
+def build_runner(args, cfg, envs, rank, world, writer=None):
+    from paper_2503_05020_b200.runner import TrialRunner
+    pool, scene_of, key_of, prio = workload(cfg)
+    jobs = rank_jobs(pool, envs, world, rank, args.global_envs)
+    mode = WORKLOADS[cfg]["mode"] if args.protocol == "auto" else args.protocol
+    record = cfg == 4 or args.record is not None
+    if record:
+        mode = "host"
+    on_record = None if writer is None else (lambda j, r: writer.put(j, r))
+    runner = TrialRunner(jobs, scene_of, key_of, slots=None, lanes_per_key=args.lanes_per_kind,
+                         rounds_per_call=args.rounds_per_call, priority=prio if args.lane_priority else None,
+                         cycle=True, device=None, mode=mode, record=record, on_record=on_record)
+    distinct = len(set(jobs)) == len(jobs) and (args.global_envs or (world * envs <= pool))
+    return runner, jobs, mode, bool(distinct)
+
+
+def safety_report(trials, reasons):
+    """The north star's report over the trials finished in the timed region: intersections
+    (CCD / determinant / non-positive-distance failures, or a completed step at distance <= 0),
+    inverted elements (inversion failures, or a completed step with J <= 0), min distance, min J,
+    label and failure-reason mix (ccd.py:19, materials.py:125, solver.py:727-731)."""
+    inter_reasons = {reasons[7], reasons[8], reasons[4]}
+    inv_reasons = {reasons[3]}
+    mix, fails = {}, {}
+    inter = inv = 0
+    md, mj = np.inf, np.inf
+    for _, r in trials:
+        mix[r.verdict] = mix.get(r.verdict, 0) + 1
+        reason = r.failure.get("reason") if r.failure else None
+        if reason:
+            fails[reason] = fails.get(reason, 0) + 1
+        inter += int(reason in inter_reasons or r.min_distance <= 0.0)
+        inv += int(reason in inv_reasons or r.min_J <= 0.0)
+        md, mj = min(md, r.min_distance), min(mj, r.min_J)
+    return {"trials": len(trials), "intersections": inter, "inverted_elements": inv,
+            "min_distance_m": None if not np.isfinite(md) else md, "min_J": None if not np.isfinite(mj) else mj,
+            "verdicts": mix, "failure_reasons": fails,
+            "source": "device protocol records (k_finalize: min stencil distance, min det F / det A per step)"}
+
+
+def kernel_report(runner, env_steps_s, ms_max, peak):
+    """Per-group device time, the roofline of the dominant group and a whole-round byte model."""
+    lanes = runner.lanes
+    kss = [ln.dev.kernel_stats() for ln in lanes]
+    ks = {}
+    for name in kss[0]:
+        ks[name] = {"ms": sum(k[name]["ms"] for k in kss), "launches": sum(k[name]["launches"] for k in kss)}
+    units = {u: sum(k["elements"]["units"][u] for k in kss) for u in kss[0]["elements"]["units"]}
+    env_iters = sum(k["elements"].get("env_iterations", 0.0) for k in kss)
+    dom = max((k for k in ks if k != "work_scan"), key=lambda k: ks[k]["ms"])
+    roof = {"kernel": dom, "kernels": list(KGROUPS.get(dom, {})), "bound": "hbm", "peak": peak[0], "unit": "GB/s",
+            "peak_source": peak[1], "traffic": None}
+    nl = max(ks[dom]["launches"], 1)
+    sec_per_launch = ks[dom]["ms"] / 1e3 / nl
+    el_alg = sum(EL_BYTES[k] * units[k] for k in EL_BYTES)
+    alg = {"elements": el_alg, "assemble_pcg": ASM_BYTES * sum(units.values())}.get(dom)
+    if alg is not None:
+        roof["alg_bytes_per_launch"] = alg / nl
+        roof["achieved"] = alg / nl / sec_per_launch / 1e9
+        roof["frac"] = roof["achieved"] / peak[0]
+    else:
+        roof["achieved"] = roof["frac"] = None
+    traffic, flop, meta, src = _ncu_group(dom)
+    if traffic is not None:
+        # the capture's per-round figures rescaled to the timed launches by element units per launch
+        cap_units = sum((meta or {}).get("units_per_round", {}).values()) or None
+        timed_units = sum(units.values()) / nl if dom == "elements" or dom == "assemble_pcg" else None
+        s = (timed_units / cap_units) if (cap_units and timed_units) else 1.0
+        roof["traffic"] = traffic * s
+        roof["traffic_source"] = src
+        roof["traffic_scale"] = {"capture_units_per_launch": cap_units, "timed_units_per_launch": timed_units,
+                                 "factor": s, "note": (meta or {}).get("note")}
+        fpk, fpk_src = _fp64_peak()
+        if flop and fpk:
+            f = flop * s
+            roof["fp64"] = {"flop_per_launch": f, "achieved_tflops": f / sec_per_launch / 1e12, "peak_tflops": fpk,
+                            "frac": f / sec_per_launch / 1e12 / fpk, "peak_source": fpk_src,
+                            "flop_source": "ncu (2 dfma + dadd + dmul thread instructions), " + src}
+    roof["kernel_ms"] = {k: round(v["ms"], 3) for k, v in ks.items()}
+    roof["kernel_launches"] = {k: v["launches"] for k, v in ks.items()}
+    roof["element_counts"] = units
+    # whole-round algorithmic bytes (SURVEY §8d's per-kernel figures with the counts this run has):
+    # elements + assembly exact from the element counters; broad phase 2 x (24 N_sv + 12 N_tri +
+    # 8 N_e) and line search / begin / finalize 200 N_t + 72 N_n (one energy pass) + 48 B per node,
+    # per env-iteration, from each lane's mean env sizes
+    other = 0.0
+    for ln, k in zip(lanes, kss):
+        p = ln.group.packed
+        E = max(p.n_env, 1)
+        nsv, ntri, ne = p.n_sv_total / E, float(p.tri_off[-1]) / E, float(p.edge_off[-1]) / E
+        nt, nn = p.n_tet_total / E, p.n_node_total / E
+        it = k["elements"].get("env_iterations", 0.0)
+        other += it * (2 * (24 * nsv + 12 * ntri + 8 * ne) + 200 * nt + 72 * nn + 48 * nn)
+    total = el_alg + ASM_BYTES * sum(units.values()) + other
+    roof["round_model"] = {"alg_bytes": total, "device_ms": ms_max, "achieved_gbs": total / (ms_max / 1e3) / 1e9,
+                           "frac": total / (ms_max / 1e3) / 1e9 / peak[0], "env_iterations": env_iters,
+                           "parts_bytes": {"elements": el_alg, "assembly": ASM_BYTES * sum(units.values()),
+                                           "broad_phase+line_search+begin/finalize": other}}
+    return roof, ks, env_iters
+
+
+def run_gpu(args, rank, world, local, cfg, envs, dist=None, quiet=False):
+    import torch
+    from paper_2503_05020_b200._native import REASONS
+    writer = None
+    if args.record is not None:
+        from paper_2503_05020_b200 import dataset as ds
+        from paper_2503_05020_b200.distributed import rank_dir
+        writer = ds.ShardWriter(rank_dir(args.record, rank), params={"config": cfg})
+    t_build = time.perf_counter()
+    runner, jobs, mode, distinct = build_runner(args, cfg, envs, rank, world, writer)
+    build_s = time.perf_counter() - t_build
+    rps = args.rounds_per_step
+    cps = max(1, rps // args.rounds_per_call) if mode == "device" else rps
+    # warm-up: W steps, and at least every slot through one trial (steady phase mix, buffers grown)
+    t_w = time.perf_counter()
+    runner.run(main_calls=args.warmup * cps, min_trials=runner.n_slots)
+    warm_s = time.perf_counter() - t_w
+    warm_trials = len(runner.finished_order)
+    runner.reset_stats()
+    runner.set_profiling(True)
+    l0 = [ln.dev.stats()[1] for ln in runner.lanes]
+    n0 = len(runner.finished)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        runner.run(main_calls=args.steps * cps, timed=True)
+        wall = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    st = [ln.stats for ln in runner.lanes]
+    ms = max(s.device_ms for s in st)
+    env_steps = sum(s.env_steps for s in st)
+    launches = sum(ln.dev.stats()[1] - a for ln, a in zip(runner.lanes, l0))
+    if dist is not None:
+        t = torch.tensor([ms, wall, float(env_steps)], dtype=torch.float64, device="cuda")
+        mx, sm_ = t.clone(), t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
+        ms_max, wall_max, total_steps = float(mx[0]), float(mx[1]), float(sm_[2])
+    else:
+        ms_max, wall_max, total_steps = ms, wall, float(env_steps)
+    value = total_steps / (ms_max / 1e3)
+    e2e = total_steps / wall_max
+    roof, ks, env_iters = kernel_report(runner, env_steps, ms, _peaks())
+    timed = runner.finished[n0:]
+    h2d = sum(s.h2d_bytes for s in st) / max(args.steps, 1)
+    d2h = sum(s.d2h_bytes for s in st) / max(args.steps, 1)
+    main = runner.main_lane
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.global_envs else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg]["workload"], "config": cfg, "envs_per_gpu": runner.n_slots,
+                   "global_envs": args.global_envs or envs * world, "parallelism": f"env-shard x{world}",
+                   "distinct_candidates_across_ranks": distinct,
+                   "l2": "inputs > L2: working set ~1.3 GB per 400 envs (element Hessians alone ~0.5 GB)",
+                   "step": f"{rps} continuous-batching rounds of the largest lane",
+                   "protocol": "device (k_protocol), %d rounds per host call" % args.rounds_per_call
+                               if mode == "device" else "host (BatchedGraspTrials), one round per host call",
+                   "lanes": [{"key": int(ln.key), "slots": s.slots, "calls": s.calls, "rounds": s.rounds,
+                              "env_steps": s.env_steps, "trials_done": s.trials_done, "device_ms": round(s.device_ms, 2),
+                              "max_call_ms": round(s.max_call_ms, 2), "host_refill_ms": round(1e3 * s.refill_s, 1),
+                              "host_step_ms": round(1e3 * s.step_s, 1)} for ln, s in zip(runner.lanes, st)],
+                   "env_steps_timed": total_steps, "trials_completed_timed": len(timed),
+                   "warmup": {"trials": warm_trials, "s": round(warm_s, 2), "build_s": round(build_s, 2)},
+                   # the metric's second half (SURVEY §8d): one batched Newton iteration = one round of
+                   # the largest lane over its active envs; env_iterations = newton_iteration calls
+                   "newton": {"env_iterations_per_s": env_iters / (ms / 1e3),
+                              "ms_per_batched_iteration": ms / max(st[main].rounds, 1),
+                              "envs_per_batched_iteration": env_iters / max(sum(s.rounds for s in st), 1)}},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "what": "TrialRunner.run (public API) wall clock: every refill's candidate payload H2D (pinned "
+                        "staging) and every call's trial-record readout D2H inside the timed region"},
+        "safety": safety_report(timed, REASONS),
+        "roofline": roof,
+        "gpu_launches": int(launches),
+        "recording": None,
+        "clocks": clk.summary(),
+    }
+    if writer is not None:
+        man = writer.close()
+        line["recording"] = {"dir": str(args.record), "rank_trials": man["n_trials"],
+                             "format": "gripsim-dataset-v1 (traj.bin, stress.bin, jsonl, meta), per-rank shards"}
+    if dist is not None:
+        # the path's one collective: every finished trial's fixed-size outcome record
+        from paper_2503_05020_b200.distributed import gather_outcomes, merge_manifests, pack_outcomes
+        tg = time.perf_counter()
+        allr = gather_outcomes(pack_outcomes([r for _, r in timed], [j for j, _ in timed], rank=rank,
+                                             reasons=REASONS), device="cuda")
+        line["outcome_gather"] = {"trials": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg), "backend": "nccl",
+                                  "ranks": sorted({int(x) for x in allr[:, 12]}) if len(allr) else []}
+        if writer is not None:
+            dist.barrier()
+            if rank == 0:
+                from paper_2503_05020_b200 import dataset as ds
+                m = merge_manifests(args.record, world, ds.FORMAT)
+                line["recording"]["merged_trials"] = m["n_trials"]
+    return line, jobs
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
-    ap.add_argument("--warmup", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--envs", type=int, default=ENVS_PER_GPU, help="envs per GPU")
-    ap.add_argument("--cpu-envs", type=int, default=0, help="CPU baseline sample envs (0 = host cores)")
-    ap.add_argument("--cpu-steps", type=int, default=150, help="CPU baseline: max protocol steps per env (full trial)")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--lockstep", action="store_true", help="lockstep Batch.step rounds instead of continuous batching")
-    ap.add_argument("--record", default=None, help="record every trial (frames, stress, contact events) and "
-                                                   "emit it to this directory in the reference's dataset format")
-    ap.add_argument("--protocol", default="device", choices=["host", "device"],
-                    help="grasp-protocol state machine on the host (per round) or on the device (k_protocol)")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE configs[config-1]; 5 = the env-count sweep of config 2 (see --sweep)")
+    ap.add_argument("--envs", type=int, default=0, help="envs per GPU (default: the config's)")
+    ap.add_argument("--global-envs", type=int, default=0, help="strong scaling: total envs split over the ranks")
+    ap.add_argument("--sweep", default="", help="config 5: comma-separated env counts, one JSON line each")
+    ap.add_argument("--rounds-per-step", type=int, default=16)
     ap.add_argument("--rounds-per-call", type=int, default=4, help="device protocol: rounds per host call")
-    ap.add_argument("--lane-priority", default="0,1,2",
-                    help="stream priority per object kind (box, cylinder, sphere): the heavier envs first")
-    ap.add_argument("--only-kind", type=int, default=-1, help="diagnostic: run only the lanes of this object kind")
-    ap.add_argument("--lanes", type=int, default=3,
-                    help="1: one device batch; 3k: k device batches (own stream + host thread) per object kind")
+    ap.add_argument("--lanes-per-kind", type=int, default=1)
+    ap.add_argument("--no-lane-priority", dest="lane_priority", action="store_false")
+    ap.add_argument("--protocol", default="auto", choices=["auto", "host", "device"])
+    ap.add_argument("--record", default=None, help="record every trial and emit it here (dataset format), "
+                                                    "rank-local shards + merged manifest")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
-    if args.record is not None or args.lockstep:
-        args.protocol = "host"   # recording and lockstep rounds drive the host state machine
+    args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -326,329 +671,36 @@ def main():
         run_reference(args, rank, world)
         return
     import torch
-    import torch.distributed as dist
+    import torch.distributed as tdist
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2503_05020_b200 import scene as sc
-    from paper_2503_05020_b200.multienv import DeviceEnvGroup
-    from paper_2503_05020_b200.protocol import BatchedGraspTrials
-    from paper_2503_05020_b200.solver import Environment
-
-    cands = sc.load_cfg2_candidates()
-    ids = [rank * args.envs + i for i in range(args.envs)]       # weak scaling: 400 envs per GPU
-    kinds = np.asarray(cands["kind"])
-    slot_kind = np.array([kinds[i % 400] for i in ids])
-    # lanes: one device batch (own CUDA stream, own host thread) per object kind, so the light
-    # box / cylinder envs are not held at every kernel boundary by the heavy sphere envs; --lanes 1
-    # puts all envs of this rank in one batch
-    if args.lanes == 1:
-        lane_ids = [ids]
-    else:
-        per_kind = max(1, args.lanes // 3)
-        lane_ids = []
-        for kk in range(3):
-            of_kind = [i for i, k in zip(ids, slot_kind) if k == kk]
-            lane_ids += [of_kind[j::per_kind] for j in range(per_kind)]
-        lane_ids = [l for l in lane_ids if l]
-        if args.only_kind >= 0:   # diagnostic: one kind's lane(s) alone
-            lane_ids = [l for l in lane_ids if slot_kind[ids.index(l[0])] == args.only_kind]
-    payloads = {j: BatchedGraspTrials.scene_payload(sc.cfg2_scene(j, cands)) for j in range(400)}  # outside timing
-    queue = {k: [j for j in range(400) if kinds[j] == k] for k in range(3)}
-    qlock = threading.Lock()
-    qpos = {k: 0 for k in range(3)}
-
-    class Lane:
-        def __init__(self, lids):
-            scenes = [sc.cfg2_scene(i % 400, cands) for i in lids]
-            envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
-            self.group = DeviceEnvGroup(envs, device=local)
-            self.device = args.protocol == "device"
-            if self.device:
-                from paper_2503_05020_b200.protocol import DeviceProtocolTrials
-                self.trials = DeviceProtocolTrials(self.group, scenes)
-            else:
-                self.trials = BatchedGraspTrials(self.group, scenes, record=args.record is not None)
-            self.dev = self.group.dev
-            self.kind = np.array([kinds[i % 400] for i in lids])
-            self.done_trials = []
-            self.advance = None if self.device else (self.trials.advance if args.lockstep else self.trials.advance_round)
-            self.env_steps = 0
-            self.rounds = 0
-            self.h2d = self.d2h = 0
-
-        def refill_device(self):
-            out = self.trials.dev.protocol_read()
-            E, B = self.group.packed.n_env, self.group.packed.n_body_total
-            rec = 4 * 39 + 8 * 19                                  # per-env protocol state (GripTrialOut source)
-            self.d2h += rec * E
-            fin = [e for e in range(len(out)) if out[e].phase == 4]
-            if not fin:
-                return
-            p = self.group.packed
-            for e in fin:                                        # grip_reset_envs slices of the new candidate
-                self.h2d += 8 * (3 * (p.node_off[e + 1] - p.node_off[e]) + 3 * (p.sv_off[e + 1] - p.sv_off[e])
-                                 + 10 * (p.tet_off[e + 1] - p.tet_off[e]))
-            self.h2d += (rec + 24) * E + 24 * B                    # grip_protocol_reset round trip
-            self.d2h += (rec + 24) * E + 24 * B
-            pls = []
-            with qlock:
-                for e in fin:
-                    self.done_trials.append(self.trials.record(e, out).verdict)
-                    k = int(self.kind[e])
-                    pls.append(payloads[queue[k][qpos[k] % len(queue[k])]])
-                    qpos[k] += 1
-            self.trials.refill(fin, pls)
-
-        def refill(self):
-            if self.device:
-                return self.refill_device()
-            fin = np.nonzero(self.trials.phase == 4)[0]
-            if len(fin) == 0:
-                return
-            pls = []
-            with qlock:
-                for e in fin:
-                    self.done_trials.append(self.trials.records[e].verdict)
-                    if writer is not None:
-                        writer.put(self.trials.records[e])
-                    k = int(self.kind[e])
-                    pls.append(payloads[queue[k][qpos[k] % len(queue[k])]])
-                    qpos[k] += 1
-            self.trials.refill(fin, pls)
-
-        def round(self):
-            t0 = time.perf_counter()
-            self._round()
-            self.call_ms_max = max(getattr(self, "call_ms_max", 0.0), 1e3 * (time.perf_counter() - t0))
-
-        def _round(self):
-            t0 = time.perf_counter()
-            if self.device:   # R device rounds per host call, protocol decisions on the device
-                n = self.trials.advance(args.rounds_per_call)
-                self.rounds += args.rounds_per_call
-                self.d2h += 8 + 4 * self.group.packed.n_env       # env-step counter, overflow flags
-            else:
-                n = self.advance()
-                self.rounds += 1
-            t1 = time.perf_counter()
-            self.refill()
-            self.t_step = getattr(self, "t_step", 0.0) + t1 - t0
-            self.t_refill = getattr(self, "t_refill", 0.0) + time.perf_counter() - t1
-            self.env_steps += n
-
-    writer = None
-    if args.record is not None:
-        # dataset emission: finished trials go to a writer thread (dataset.py)
-        import queue as queue_mod
-        from paper_2503_05020_b200 import dataset as ds
-        writer = queue_mod.Queue()
-        out_dir = Path(args.record)
-        n_written = [0]
-
-        def write_loop():
-            while True:
-                rec = writer.get()
-                if rec is None:
-                    return
-                ds.emit_trial(rec, out_dir / f"trial_{n_written[0]:05d}")
-                n_written[0] += 1
-
-        wthread = threading.Thread(target=write_loop, daemon=True)
-        wthread.start()
-    lanes = [Lane(l) for l in lane_ids]
-    if args.lane_priority:   # e.g. "0,1,2": box, cylinder, sphere lanes
-        pr = [int(v) for v in args.lane_priority.split(",")]
-        for ln in lanes:
-            ln.dev.set_priority(pr[int(ln.kind[0])] if len(pr) > int(ln.kind[0]) else 0)
-
-    def run_lanes(n_rounds, timed):
-        """Every lane runs rounds on its own thread; the lane with the most envs runs exactly
-        n_rounds, the others keep going until it is done (their streams stay busy)."""
-        main_lane = max(range(len(lanes)), key=lambda i: len(lane_ids[i]))
-        stop = threading.Event()
-
-        errors = []
-
-        def work(i):
-            try:
-                work_lane(i)
-            except BaseException as exc:   # surface a lane's failure in the main thread
-                errors.append(exc)
-                stop.set()
-
-        def work_lane(i):
-            ln = lanes[i]
-            if timed:
-                ln.dev.timer_start()
-            if i == main_lane:
-                r0 = ln.rounds
-                while ln.rounds - r0 < n_rounds:
-                    ln.round()
-                stop.set()
-            else:
-                while not stop.is_set():
-                    ln.round()
-            if timed:
-                ln.ms = ln.dev.timer_stop()
-
-        th = [threading.Thread(target=work, args=(i,)) for i in range(len(lanes))]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-        if errors:
-            raise errors[0]
-
-    run_lanes(args.warmup, False)
-    for ln in lanes:
-        ln.dev.set_profiling(True)
-        ln.l0 = ln.dev.stats()[1]
-        ln.sw0 = ln.dev.stats()[2]
-        ln.env_steps = 0
-        ln.rounds = 0
-        ln.nd0 = len(ln.done_trials)
-    h2d = d2h = 0
-    if args.protocol == "host":
-        for ln in lanes:
-            E, B = ln.group.packed.n_env, ln.group.packed.n_body_total
-            maxa = ln.dev.max_alpha
-            h2d += 8 * 3 * E + 8 * 3 * B + 2 * E                                # gravity, body velocities, round masks
-            d2h += 72 * E + 8 * maxa * E + (8 + 4) * B + 8 * E + 24 * B + 8 * E + E  # reports, alphas, forces+masks+min_d, com, speed, finalized
-    for ln in lanes:
-        ln.h2d = ln.d2h = 0
-        ln.call_ms_max = 0.0
-        ln.t_step = ln.t_refill = 0.0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t0 = time.perf_counter()
-        run_lanes(args.steps, True)
-        wall = time.perf_counter() - t0
-    torch.cuda.synchronize()
-    ms = max(ln.ms for ln in lanes)
-    if args.protocol == "device":   # counted: per bench step (round of the largest lane)
-        h2d = sum(ln.h2d for ln in lanes) / max(args.steps, 1)
-        d2h = sum(ln.d2h for ln in lanes) / max(args.steps, 1)
-    env_steps = sum(ln.env_steps for ln in lanes)
-    nsweeps = sum(ln.dev.stats()[2] - ln.sw0 for ln in lanes)
-    launches = sum(ln.dev.stats()[1] - ln.l0 for ln in lanes)
-    kss = [ln.dev.kernel_stats() for ln in lanes]
-    ks = {}
-    for name in kss[0]:
-        ks[name] = {"ms": sum(k[name]["ms"] for k in kss), "launches": sum(k[name]["launches"] for k in kss)}
-    ks["elements"]["units"] = {u: sum(k["elements"]["units"][u] for k in kss) for u in kss[0]["elements"]["units"]}
-    env_iters = sum(k["elements"].get("env_iterations", 0.0) for k in kss)
-    for f in ("pcg_iterations", "solves"):
-        ks["assemble_pcg"][f] = sum(k["assemble_pcg"][f] for k in kss)
-    ks["assemble_pcg"]["mean_unknowns"] = 0.0
-    if world > 1:
-        t = torch.tensor([ms, wall, float(env_steps), float(nsweeps)], dtype=torch.float64, device="cuda")
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm_ = t.clone()
-        dist.all_reduce(sm_, op=dist.ReduceOp.SUM)
-        ms_max, wall_max, total_steps = float(mx[0]), float(mx[1]), float(sm_[2])
-    else:
-        ms_max, wall_max, total_steps = ms, wall, float(env_steps)
-    value = total_steps / (ms_max / 1e3)
-    e2e = total_steps / wall_max
-    # roofline of the dominant kernel group (live CUDA events per launch, this rank)
-    dom = max((k for k in ks if k != "work_scan"), key=lambda k: ks[k]["ms"])
-    peak, peak_kind = _peaks()
-    roof = {"kernel": dom, "kernels": KGROUPS.get(dom, []), "bound": "hbm", "peak": peak, "unit": "GB/s",
-            "peak_source": peak_kind, "traffic": None}
-    u = ks["elements"]["units"]
-    nlaunch = max(ks[dom]["launches"], 1)
-    sec_per_launch = ks[dom]["ms"] / 1e3 / nlaunch
-    if dom == "elements":
-        alg = sum(EL_BYTES[k] * u[k] for k in EL_BYTES) / nlaunch
-    elif dom == "assemble_pcg":
-        # every element's Hessian, gradient and energy read once (1152 + 96 + 8 B)
-        alg = 1256.0 * sum(u.values()) / nlaunch
-    else:
-        alg = None
-    if alg is not None:
-        roof["alg_bytes_per_launch"] = alg
-        roof["achieved"] = alg / sec_per_launch / 1e9
-        roof["frac"] = roof["achieved"] / peak
-    else:
-        roof["achieved"] = roof["frac"] = None
-    traffic, flop, src = _ncu_group(dom)
-    if traffic is not None:
-        roof["traffic"] = traffic
-        roof["traffic_source"] = src
-        roof["traffic_note"] = ("ncu capture = one launch over a single 400-env batch (--lanes 1); "
-                                f"the bench's launches cover {args.envs / len(lanes):.0f} envs each")
-    fpk, fpk_src = _fp64_peak()
-    if flop and fpk:
-        roof["fp64"] = {"flop_per_launch": flop, "achieved_tflops": flop / sec_per_launch / 1e12, "peak_tflops": fpk,
-                        "frac": flop / sec_per_launch / 1e12 / fpk, "peak_source": fpk_src,
-                        "flop_source": "ncu (2 dfma + dadd + dmul thread instructions), " + (src or "")}
-    roof["kernel_ms"] = {k: round(v["ms"], 3) for k, v in ks.items()}
-    roof["kernel_launches"] = {k: v["launches"] for k, v in ks.items()}
-    pk = ks["assemble_pcg"]
-    roof["pcg"] = {"iterations_per_solve": pk["pcg_iterations"] / max(pk["solves"], 1.0),
-                   "mean_unknowns": pk["mean_unknowns"], "solves": pk["solves"]}
-    roof["element_counts"] = ks["elements"]["units"]
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: soft 2-pad UMI-style gripper on rigid (ABD) box/cylinder/sphere, "
-                               "full grasp protocol, antipodal candidate seed i",
-                   "envs_per_gpu": args.envs, "global_envs": args.envs * world, "parallelism": f"env-shard x{world}",
-                   "l2": "working set > L2 (element Hessians alone ~0.5 GB per GPU)",
-                   "env_steps_timed": total_steps, "newton_sweeps": int(nsweeps),
-                   "ms_per_newton_sweep": ms_max / max(nsweeps, 1),
-                   # the metric's second half (SURVEY §8d): one batched Newton iteration = one round of
-                   # a lane over its active envs; env_iterations = newton_iteration calls of all envs
-                   "newton": {"env_iterations_per_s": env_iters / (ms_max / 1e3),
-                              "ms_per_batched_iteration": ms_max / max(args.steps, 1),
-                              "envs_per_batched_iteration": env_iters / max(sum(ln.rounds for ln in lanes), 1),
-                              "note": "profiling on: env_iterations counted in k_work_scan since set_profiling"},
-                   "mode": ("lockstep Batch.step" if args.lockstep else "continuous batching, steady-state refill")
-                           + (f", protocol on the device ({args.rounds_per_call} rounds per host call)"
-                              if args.protocol == "device" else ", protocol on the host"),
-                   "trials_completed_timed": sum(len(ln.done_trials) - ln.nd0 for ln in lanes),
-                   "lanes": [{"envs": len(l), "rounds": ln.rounds, "env_steps": ln.env_steps, "ms": round(ln.ms, 3),
-                              "max_call_ms": round(getattr(ln, "call_ms_max", 0.0), 2),
-                              "host_refill_ms": round(1e3 * getattr(ln, "t_refill", 0.0), 1),
-                              "step_call_ms": round(1e3 * getattr(ln, "t_step", 0.0), 1)}
-                             for l, ln in zip(lane_ids, lanes)]},
-        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
-        "roofline": roof,
-        "gpu_launches": int(launches),
-        "recording": None if writer is None else {"dir": str(args.record), "trials_written": n_written[0],
-                                                  "format": "gripsim-dataset-v1 (traj.bin, stress.bin, jsonl, meta)"},
-        "clocks": clk.summary(),
-    }
-    if world > 1:
-        # the path's one collective: fixed-size per-env outcome records, gathered once at the end
-        from paper_2503_05020_b200.distributed import gather_outcomes, pack_outcomes
-        tg = time.perf_counter()
-        recs = {}
-        for l, ln in zip(lane_ids, lanes):
-            if ln.device:   # the device protocol's current trial records
-                out = ln.trials.dev.protocol_read()
-                recs.update({i: ln.trials.record(k, out) for k, i in enumerate(l)})
-            else:
-                recs.update({i: r for i, r in zip(l, ln.trials.records)})
-        allr = gather_outcomes(pack_outcomes([recs[i] for i in ids], ids), args.envs * world, device="cuda")
-        line["outcome_gather"] = {"envs": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg), "backend": "nccl"}
-    if rank == 0 and not args.no_cpu:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = tdist
+    if args.config == 5 or args.sweep:
+        counts = [int(v) for v in (args.sweep or "1,2,4,8,16,32,64,128,256,400,800,1600,3200").split(",")]
+        for n in counts:
+            line, _ = run_gpu(args, rank, world, local, 2, n, dist)
+            line["config"]["sweep"] = True
+            line["vs_baseline"] = None
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    cfg = args.config
+    envs = args.envs or WORKLOADS[cfg]["envs"]
+    line, jobs = run_gpu(args, rank, world, local, cfg, envs, dist)
+    if rank == 0 and not args.no_cpu and cfg in (2, 3):
         cores = os.cpu_count() or 1
-        n_cpu = args.cpu_envs or cores
-        r = cpu_measure(n_cpu, 0, args.cpu_steps, cores)
-        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": min(cores, n_cpu), "kind": "port",
-                                "sample": f"oracle/ numpy port of the reference step, {n_cpu} cfg2 envs, "
-                                          f"full protocol trials (<= {args.cpu_steps} steps each), "
-                                          f"{r['env_steps']} env-steps, {r['core_seconds']:.1f} core-s, "
-                                          f"{r['ms_per_newton_iteration']:.1f} ms per newton_iteration"}
+        r = cpu_measure(cfg, jobs[:8 * cores], args.cpu_seconds, cores)
+        line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": cores, "kind": r["kind"],
+                                "sample": f"{r['impl']}; {cores} worker processes, full protocol trials of this "
+                                          f"rank's candidates back to back, env-steps counted over "
+                                          f"{r['wall_s']:.0f} s after 5 s warm-up: {r['env_steps']} env-steps"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist is not None:
         dist.destroy_process_group()
 
 

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define GRIP_ABI_VERSION 3
+#define GRIP_ABI_VERSION 4
 
 /* Flattened description of N environments (all arrays host, row-major).
  * Index spaces are ENV-LOCAL (node / surface-vertex / body ids restart at 0 in
@@ -191,6 +191,12 @@ typedef struct GripTrialOut {
   int32_t final_contact;
   int32_t halt_step[2];
   int32_t markers[18];    /* [start, end) per phase 0..8, -1 = phase not completed */
+  /* safety report over the trial's completed steps (the north star's "zero intersections and
+   * zero inverted elements"): min stencil distance of the finalize contact set (> 0: no
+   * intersection; inf: no stencil ever within 1.05 dhat) and min J = det F over every tet,
+   * det A over every affine body (> 0: nothing inverted) */
+  double min_distance;
+  double min_J;
 } GripTrialOut;
 int grip_protocol_setup(GripBatch* b, const int32_t* finger_body, const double* closing_dir, const int32_t* object_body,
                         const int32_t* gripper_bits, const int32_t* max_close, const double* cfg);
@@ -224,6 +230,15 @@ int grip_sdf_nn(const double* pts, int64_t n, const double* cloud, int64_t m, co
 int grip_sdf_query(const double* values, const int32_t* dims, const double* origin, const double* spacing,
                    const double* rot, const double* trans, const double* world_lo, const double* world_hi,
                    const double* pts, int64_t n, double* d_o, double* d_max);
+/* Contact readout at the CURRENT state without stepping (protocol.py:72-75 contact_events_now,
+ * solver.py:449-453 min_contact_distance, contact.py:348-372 stencil_forces), for the envs with
+ * mask[e]=1: the canonical candidate set at radius_factor * dhat, min_distance[e] (n_env, may be
+ * NULL) = min stencil distance over it (inf when empty), its active stencils (d < dhat) as event
+ * rows for grip_get_events, per-body force sums and contact bits for grip_get_contacts. */
+/* nonfinite[e] (n_env) = 1 when env e's state x holds a NaN / inf: the quarantine test of
+ * Batch.quarantine_failures (multienv.py:98-123), evaluated on the device. */
+int grip_check_finite(GripBatch* b, uint8_t* nonfinite);
+int grip_contacts_now(GripBatch* b, const uint8_t* mask, double radius_factor, double* min_distance);
 int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t* ev_i, double* ev_d, int64_t cap);
 /* per-body centre of mass (n_body*3) and per-env max point speed after the last finalize
  * (solver.py:384-428; read by the protocol's steady / COM tests, protocol.py:231-249) */
@@ -237,17 +252,30 @@ int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, d
 /* CUDA events on the library stream: start=1 marks, start=0 returns ms since the mark */
 int grip_stream_timer(GripBatch* b, int start, double* ms);
 /* Re-initialise the envs with mask[e]=1 to a new pose of the SAME topology (a new grasp
- * candidate for the same object / gripper meshes): positions, kinematic surfaces and the
- * posed rest shape (Dm^-1, V0) of their tets; v, anchors, time and step index are zeroed.
- * Full-size host arrays (GripSceneDesc layout); only the masked envs' slices are read. */
+ * candidate for the same object / gripper meshes; the slot refill of run_batch_trials,
+ * multienv.py:204-216, done in place): positions, kinematic surfaces and the posed rest shape
+ * (Dm^-1, V0) of their tets, optionally a new material (tet_mu / tet_lam per tet, body_mu per
+ * body: config 3's randomized_material, config.py:311-318; all three or none).  Every other
+ * piece of per-env state returns to what grip_create starts from (v, anchors, time, step index,
+ * Jacobi warm starts, candidate superset, ...), so a refilled env is bitwise a fresh one.
+ * Full-size host arrays (GripSceneDesc layout); only the masked envs' slices are read; they
+ * are staged through one pinned buffer and scattered by one kernel. */
 int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
-                    const double* tet_Dmi, const double* tet_V0);
+                    const double* tet_Dmi, const double* tet_V0, const double* tet_mu, const double* tet_lam,
+                    const double* body_mu);
 /* Evaluate n standalone elements with the device element kernels (test / parity hook).
  * type 0 PT  in[x(12), kappa, dhat]; 1 EE in[x(12), eps_x, kappa, dhat];
  * 2 NH in[x(12), Dm^-1(9), V0, mu, lambda]; 3 ABD in[A(9), kappa*V];
  * 4 friction in[x(12), x_prev(12), gamma(4), T(6), lambda, mu, eps_v, dt]
  * outputs per element: energy, grad (12), SPD-projected 12x12 Hessian, flags (1 active, 2 bad d, 4 inverted) */
 int grip_debug_elements(int type, int n, const double* in, int stride, double* E, double* g, double* H, int* flags);
+/* The same element evaluations through the PRODUCTION element chain of a Newton sweep (test /
+ * parity hook): types 0 / 1 (PT / EE stencils) via the k_elements_w element code with its clamp
+ * deferral -> k_tet_jacobi2 -> k_tet_finish; type 2 (NH tets) via k_tet_front (Gershgorin
+ * pass-through or deferral) -> k_tet_jacobi2 -> k_tet_back, warm-started from eig (n*81
+ * row-major 9x9 eigenbases, updated in place; NULL = identity). */
+int grip_debug_chain(int type, int n, const double* in, int stride, double* E, double* g, double* H, double* eig,
+                     int* flags);
 /* timing of the last grip_step: device ms (CUDA events) and kernel launches */
 int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps);
 

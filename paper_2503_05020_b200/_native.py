@@ -15,7 +15,7 @@ import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "_lib"
 LIB_PATH = Path(os.environ["GRIP_LIB"]) if os.environ.get("GRIP_LIB") else LIB_DIR / "libgripipc.so"  # GRIP_LIB: A/B builds
-ABI_VERSION = 3
+ABI_VERSION = 4
 NPARAM = 14
 (P_DT, P_KAPPA, P_DHAT, P_EPSV, P_RELTOL, P_MAXIT, P_ELLFLOOR, P_MAXLS, P_CCDSCALE, P_CCDIT, P_KINGUARD, P_MURULE,
  P_PCGRTOL, P_SPARE) = range(NPARAM)
@@ -93,12 +93,14 @@ def load():
         ("grip_kernel_stats", [vp, i32, vp, vp, vp]), ("grip_stream_timer", [vp, i32, vp]),
         ("grip_round", [vp, vp, vp, vp, vp, vp]),
         ("grip_debug_elements", [i32, i32, vp, i32, vp, vp, vp, vp]),
-        ("grip_reset_envs", [vp, vp, vp, vp, vp, vp]), ("grip_set_recording", [vp, i32]),
+        ("grip_debug_chain", [i32, i32, vp, i32, vp, vp, vp, vp, vp]),
+        ("grip_reset_envs", [vp, vp, vp, vp, vp, vp, vp, vp, vp]), ("grip_set_recording", [vp, i32]),
         ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64]),
         ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
         ("grip_sdf_nn", [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp, i32, vp]),
-        ("grip_set_priority", [vp, i32]),
+        ("grip_set_priority", [vp, i32]), ("grip_contacts_now", [vp, vp, dbl, vp]),
+        ("grip_check_finite", [vp, vp]),
         ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
         ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
@@ -130,13 +132,27 @@ def debug_elements(etype, inputs):
     return E, g, H.reshape(n, 12, 12), fl
 
 
+def debug_chain(etype, inputs, eig=None):
+    """The same elements through the production element chain of a sweep (grip_debug_chain);
+    eig (n, 9, 9) warm starts for NH tets are updated in place."""
+    lib = load()
+    a = np.ascontiguousarray(inputs, np.float64)
+    n, stride = a.shape
+    E, g, H, fl = np.zeros(n), np.zeros((n, 12)), np.zeros((n, 144)), np.zeros(n, np.int32)
+    if eig is not None:
+        assert eig.flags.c_contiguous and eig.dtype == np.float64 and eig.shape == (n, 9, 9)
+    check(lib.grip_debug_chain(int(etype), n, ptr(a), stride, ptr(E), ptr(g), ptr(H), ptr(eig), ptr(fl)))
+    return E, g, H.reshape(n, 12, 12), fl
+
+
 class GripTrialOut(ctypes.Structure):
     """include/grip_ipc.h GripTrialOut (device protocol record of one env)."""
     _fields_ = [("halt_force", ctypes.c_double * 2), ("com_disp", ctypes.c_double * 6),
                 ("final_disp", ctypes.c_double), ("threshold", ctypes.c_double), ("phase", ctypes.c_int32),
                 ("verdict", ctypes.c_int32), ("n_steps", ctypes.c_int32), ("fail_phase", ctypes.c_int32),
                 ("fail_reason", ctypes.c_int32), ("fail_step", ctypes.c_int32), ("halted", ctypes.c_int32),
-                ("final_contact", ctypes.c_int32), ("halt_step", ctypes.c_int32 * 2), ("markers", ctypes.c_int32 * 18)]
+                ("final_contact", ctypes.c_int32), ("halt_step", ctypes.c_int32 * 2), ("markers", ctypes.c_int32 * 18),
+                ("min_distance", ctypes.c_double), ("min_J", ctypes.c_double)]
 
 
 def sdf_exact(pts, verts, tris, face_n, edge_n, vert_n):
@@ -273,10 +289,12 @@ class DeviceBatch:
         check(self.lib.grip_round(self.h, ptr(b), ptr(it), ptr(fin), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
         return fin.astype(bool), rep, alphas
 
-    def reset_envs(self, mask, node_x0, sv_kin0, tet_Dmi, tet_V0):
-        f = lambda a: np.ascontiguousarray(a, np.float64)  # noqa: E731
+    def reset_envs(self, mask, node_x0, sv_kin0, tet_Dmi, tet_V0, tet_mu=None, tet_lam=None, body_mu=None):
+        """Slot refill (grip_reset_envs): new pose / rest shape (and optionally material) of the
+        masked envs, every other per-env state back to a fresh batch's."""
+        f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)  # noqa: E731
         m = np.ascontiguousarray(mask, np.uint8)
-        arrs = [f(node_x0), f(sv_kin0), f(tet_Dmi), f(tet_V0)]
+        arrs = [f(node_x0), f(sv_kin0), f(tet_Dmi), f(tet_V0), f(tet_mu), f(tet_lam), f(body_mu)]
         check(self.lib.grip_reset_envs(self.h, ptr(m), *[ptr(a) for a in arrs]))
 
     def begin_step(self, active):
@@ -320,6 +338,20 @@ class DeviceBatch:
         md = np.empty(p.n_env)
         check(self.lib.grip_get_contacts(self.h, ptr(force), ptr(mask), ptr(md)))
         return force, mask, md
+
+    def contacts_now(self, mask, radius_factor=1.05):
+        """Contact readout at the current state (grip_contacts_now): per-env min stencil distance at
+        radius_factor * dhat; the active stencils become the event rows of event_blocks()."""
+        m = np.ascontiguousarray(mask, np.uint8)
+        md = np.full(self.n_env, np.inf)
+        check(self.lib.grip_contacts_now(self.h, ptr(m), float(radius_factor), ptr(md)))
+        return md
+
+    def check_finite(self):
+        """Per env: True when its state holds a NaN / inf (grip_check_finite)."""
+        bad = np.zeros(self.n_env, np.uint8)
+        check(self.lib.grip_check_finite(self.h, ptr(bad)))
+        return bad.astype(bool)
 
     def candidates(self, env, radius):
         n_pt, n_ee = ctypes.c_int32(), ctypes.c_int32()

@@ -33,7 +33,10 @@ enum {
   PI_NEEDBEGIN, PI_VERDICT, PI_FPHASE, PI_FREASON, PI_FSTEP, PI_FCONTACT, PI_FB0, PI_FB1, PI_OBJ, PI_GBITS,
   PI_HSTEP0, PI_HSTEP1, PI_MARK, PI_N = PI_MARK + 18
 };
-enum { PD_CD = 0, PD_COM0 = 6, PD_HF = 9, PD_CDISP = 11, PD_FDISP = 17, PD_THR = 18, PD_N = 19 };
+// PD_MIND / PD_MINJ: min stencil distance / min element J = det F (tets) or det A (affine bodies)
+// over the trial's completed steps (the north star's intersection / inversion report)
+enum { PINIT_D = 6, PINIT_I = 6 };   // k_protocol_init staging per env: closing dirs | ints
+enum { PD_CD = 0, PD_COM0 = 6, PD_HF = 9, PD_CDISP = 11, PD_FDISP = 17, PD_THR = 18, PD_MIND = 19, PD_MINJ = 20, PD_N = 21 };
 
 struct Dev {
   int n_env;
@@ -102,6 +105,7 @@ struct Dev {
   unsigned int* contact_mask;
   double* body_com;    // 3 per body, after finalize
   double* max_speed;   // per env, after finalize (solver.py:414-428)
+  double* min_J;       // per env, after finalize: min det F over its tets and det A over its affine bodies
   double* stats;       // [0..3] element counts of the last sweep (tets, abd, contacts, anchors)
   int max_alpha;
   // candidates (uniform capacity per env)

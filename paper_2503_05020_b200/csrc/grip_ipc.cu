@@ -58,6 +58,15 @@ struct GripBatch {
   double* d_stress = nullptr;   // persistent: stress rows (n_tet * 7)
   double* d_frame = nullptr;    // persistent: packed frame of the masked envs (grip_get_frames)
   double* h_frame = nullptr;    // pinned staging of the same
+  double* d_md_now = nullptr;   // grip_contacts_now: per env min distance at the queried radius
+  int* d_nonfin = nullptr;      // grip_check_finite: per env flag
+  bool ev_now = false;          // the ev_* buffers hold a grip_contacts_now readout
+  char* h_pinit = nullptr;      // pinned staging of the protocol (re)starts
+  char* d_pinit = nullptr;
+  size_t pinit_cap = 0;
+  char* h_reset = nullptr;      // pinned staging of grip_reset_envs (env list, offsets, slices)
+  char* d_reset = nullptr;
+  size_t reset_cap = 0;
   int* d_fmask = nullptr;       // per env: packed offsets (node, sv, tet) or -1
   int* h_fmask = nullptr;
   int* h_pin = nullptr;         // pinned small readbacks
@@ -75,7 +84,6 @@ struct GripBatch {
   long long launches = 0, sweeps = 0;
   // optional per-kernel timing on the library stream (grip_set_profiling)
   bool prof = false;
-  bool warp_elements = getenv("GRIP_THREAD_ELEMENTS") == nullptr;  // per-thread path kept for A/B
   // grids of the flat element kernels (k_tet_front, k_elements_w, k_tet_jacobi2, k_tet_back), in
   // blocks; GRIP_EGRID="f,w,j,b" (blocks per SM) overrides
   int eg[4] = {148 * 2, 148 * 2, 148 * 2, 148 * 4};
@@ -548,6 +556,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.contact_mask = b->alloc<unsigned int>(NB);
   D.body_com = b->alloc<double>(3 * (size_t)NB);
   D.max_speed = b->alloc<double>(E);
+  D.min_J = b->alloc<double>(E);
   D.stats = b->alloc<double>(8);
   D.cs_n = b->alloc<int>(2 * (size_t)E);
   D.cs_R = b->alloc<double>(E);
@@ -668,7 +677,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
-        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
+        D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
         D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
@@ -705,6 +714,10 @@ int grip_destroy(GripBatch* b) {
   if (b->h_snap) cudaFreeHost(b->h_snap);
   if (b->h_frame) cudaFreeHost(b->h_frame);
   if (b->h_fmask) cudaFreeHost(b->h_fmask);
+  if (b->h_reset) cudaFreeHost(b->h_reset);
+  if (b->h_pinit) cudaFreeHost(b->h_pinit);
+  if (b->d_pinit) cudaFree(b->d_pinit);
+  if (b->d_reset) cudaFree(b->d_reset);
   cudaEventDestroy(b->ev0);
   cudaEventDestroy(b->ev1);
   cudaStreamDestroy(b->stream);
@@ -770,41 +783,12 @@ static void kt_collect(GripBatch* b, int n_listed = -1) {
 }
 
 // one Newton sweep over the pending envs (list in b->d_list, n entries); returns new pending count
+static void sweep_launch(GripBatch* b, int n, const int* list);
+
 static int newton_sweep(GripBatch* b, int n, int* n_out) {
   Dev& D = b->D;
   for (int attempt = 0; attempt < 8; ++attempt) {
-    int t;
-    t = kt_begin(b, K_CAND);
-    k_candidates<<<n, NT, 0, b->stream>>>(D, b->d_list);
-    kt_end(b, t);
-    t = kt_begin(b, K_SCAN);
-    k_work_scan<<<1, NT, 0, b->stream>>>(D, b->d_list, n);
-    kt_end(b, t);
-    t = kt_begin(b, K_ELEM);
-    if (b->warp_elements) {
-      k_tet_front<<<b->eg[0], TF, 0, b->stream>>>(D, b->d_list, n);
-      k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, b->d_list, n);
-      k_tet_jacobi2<<<b->eg[2], TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
-      k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-      k_tet_back<<<b->eg[3], EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
-      k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
-    }
-    else
-      k_elements<<<148 * 8, 128, 0, b->stream>>>(D, b->d_list, n);
-    kt_end(b, t);
-    t = kt_begin(b, K_ASM);
-    if (b->direct) {
-      k_contact_K<<<148 * 2, NT, 0, b->stream>>>(D, b->d_list, n);
-      k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, b->d_list, b->env_cap);
-    }
-    else
-      k_assemble_solve<<<n, NT, 0, b->stream>>>(D, b->d_list);
-    kt_end(b, t);
-    t = kt_begin(b, K_LS);
-    k_linesearch<<<n, NT, 0, b->stream>>>(D, b->d_list);
-    kt_end(b, t);
-    b->launches += 3 + (b->warp_elements ? 6 : 1) + (b->direct ? 2 : 1);
-    b->sweeps += 1;
+    sweep_launch(b, n, b->d_list);
     CK(cudaGetLastError());
     std::vector<int> fl(b->n_env);
     CK(cudaMemcpyAsync(fl.data(), D.flags, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
@@ -895,6 +879,7 @@ static int read_reports(GripBatch* b, const std::vector<int>& L, GripStepReport*
 }
 
 int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas) {
+  b->ev_now = false;   // a finalize rewrites (or, recording off, invalidates) the event rows
   b->snap_valid = false;
   std::vector<int> L = mask_to_list(b, active);
   if (L.empty()) return 0;
@@ -906,6 +891,7 @@ int grip_finalize_step(GripBatch* b, const uint8_t* active, GripStepReport* repo
 }
 
 int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, double* alphas) {
+  b->ev_now = false;   // a finalize rewrites (or, recording off, invalidates) the event rows
   b->snap_valid = false;
   std::vector<int> L = mask_to_list(b, active);
   if (L.empty()) return 0;
@@ -962,16 +948,12 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   k_work_scan<<<1, NT, 0, b->stream>>>(D, list, n);
   kt_end(b, t);
   t = kt_begin(b, K_ELEM);
-  if (b->warp_elements) {
-    k_tet_front<<<b->eg[0], TF, 0, b->stream>>>(D, list, n);
-    k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, list, n);
-    k_tet_jacobi2<<<b->eg[2], TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
-    k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-    k_tet_back<<<b->eg[3], EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
-    k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
-  } else {
-    k_elements<<<148 * 8, 128, 0, b->stream>>>(D, list, n);
-  }
+  k_tet_front<<<b->eg[0], TF, 0, b->stream>>>(D, list, n);
+  k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, list, n);
+  k_tet_jacobi2<<<b->eg[2], TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+  k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
+  k_tet_back<<<b->eg[3], EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
+  k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
   kt_end(b, t);
   t = kt_begin(b, K_ASM);
   if (b->direct) {
@@ -984,7 +966,8 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   t = kt_begin(b, K_LS);
   k_linesearch<<<n, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
-  b->launches += 3 + (b->warp_elements ? 6 : 1) + (b->direct ? 2 : 1);
+  k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
+  b->launches += 3 + 7 + (b->direct ? 2 : 1);
   b->sweeps += 1;
 }
 
@@ -1026,6 +1009,7 @@ static int snapshot_async(GripBatch* b) {
 // synchronous per-stage path (rare: capacities only grow early in a run).
 int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t* finalized, GripStepReport* reports,
                double* alphas) {
+  b->ev_now = false;   // a finalize rewrites (or, recording off, invalidates) the event rows
   Dev& D = b->D;
   b->snap_valid = false;
   const double h0 = host_now();
@@ -1124,43 +1108,45 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
 // ---------------------------------------------------------------------------
 // Device-resident protocol (k_protocol): setup, restart, rounds, readout
 // ---------------------------------------------------------------------------
+// (Re)start the protocol of the masked envs (all when mask is NULL) on the device: one pinned
+// staging buffer of the per-env inputs, one H2D copy, k_protocol_init (no state round trip).
 static int protocol_init_envs(GripBatch* b, const uint8_t* mask, const double* closing_dir, const int32_t* max_close,
                               const int32_t* finger_body, const int32_t* object_body, const int32_t* gripper_bits) {
-  Dev& D = b->D;
   const int E = b->n_env;
-  std::vector<int> hi((size_t)E * PI_N);
-  std::vector<double> hd((size_t)E * PD_N);
-  CK(cudaMemcpyAsync(hi.data(), D.pr_i, sizeof(int) * hi.size(), cudaMemcpyDeviceToHost, b->stream));
-  CK(cudaMemcpyAsync(hd.data(), D.pr_d, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, b->stream));
-  std::vector<double> vel((size_t)b->n_body * 3), grav((size_t)E * 3);
-  CK(cudaMemcpyAsync(vel.data(), D.body_vel, sizeof(double) * vel.size(), cudaMemcpyDeviceToHost, b->stream));
-  CK(cudaMemcpyAsync(grav.data(), D.gravity, sizeof(double) * grav.size(), cudaMemcpyDeviceToHost, b->stream));
-  CK(cudaStreamSynchronize(b->stream));
-  for (int e = 0; e < E; ++e) {
-    if (mask && !mask[e]) continue;
-    int* I = hi.data() + (size_t)e * PI_N;
-    double* R = hd.data() + (size_t)e * PD_N;
-    const int fb0 = finger_body ? finger_body[2 * e] : I[PI_FB0], fb1 = finger_body ? finger_body[2 * e + 1] : I[PI_FB1];
-    const int obj = object_body ? object_body[e] : I[PI_OBJ], gb = gripper_bits ? gripper_bits[e] : I[PI_GBITS];
-    for (int k = 0; k < PI_N; ++k) I[k] = 0;
-    for (int k = 0; k < PD_N; ++k) R[k] = 0.0;
-    I[PI_FB0] = fb0; I[PI_FB1] = fb1; I[PI_OBJ] = obj; I[PI_GBITS] = gb;
-    I[PI_MAXCLOSE] = max_close[e];
-    I[PI_NEEDBEGIN] = 1;
-    for (int k = 0; k < 18; ++k) I[PI_MARK + k] = -1;
-    I[PI_HSTEP0] = I[PI_HSTEP1] = -1;
-    for (int k = 0; k < 6; ++k) R[PD_CD + k] = closing_dir[6 * e + k];
-    // settle: fingers still, gravity off (protocol.py:193-198)
-    for (int c = 0; c < 3; ++c) {
-      vel[3 * (size_t)(b->body_off[e] + fb0) + c] = 0.0;
-      vel[3 * (size_t)(b->body_off[e] + fb1) + c] = 0.0;
-      grav[3 * (size_t)e + c] = 0.0;
-    }
+  std::vector<int> L;
+  for (int e = 0; e < E; ++e)
+    if (!mask || mask[e]) L.push_back(e);
+  if (L.empty()) return 0;
+  const size_t n = L.size();
+  const size_t bytes = n * (sizeof(double) * PINIT_D + sizeof(int) * PINIT_I);
+  CK(cudaStreamSynchronize(b->stream));   // the pinned staging buffer may still feed a previous copy
+  if (bytes > b->pinit_cap) {
+    if (b->h_pinit) cudaFreeHost(b->h_pinit);
+    if (b->d_pinit) cudaFree(b->d_pinit);
+    b->h_pinit = b->d_pinit = nullptr;
+    b->pinit_cap = std::max(bytes, 2 * b->pinit_cap);
+    CK(cudaMallocHost(&b->h_pinit, b->pinit_cap));
+    CK(cudaMalloc(&b->d_pinit, b->pinit_cap));
   }
-  CK(cudaMemcpyAsync(D.pr_i, hi.data(), sizeof(int) * hi.size(), cudaMemcpyHostToDevice, b->stream));
-  CK(cudaMemcpyAsync(D.pr_d, hd.data(), sizeof(double) * hd.size(), cudaMemcpyHostToDevice, b->stream));
-  CK(cudaMemcpyAsync(D.body_vel, vel.data(), sizeof(double) * vel.size(), cudaMemcpyHostToDevice, b->stream));
-  CK(cudaMemcpyAsync(D.gravity, grav.data(), sizeof(double) * grav.size(), cudaMemcpyHostToDevice, b->stream));
+  double* hd = reinterpret_cast<double*>(b->h_pinit);
+  int* hi = reinterpret_cast<int*>(b->h_pinit + n * sizeof(double) * PINIT_D);
+  for (size_t k = 0; k < n; ++k) {
+    const int e = L[k];
+    for (int c = 0; c < 6; ++c) hd[PINIT_D * k + c] = closing_dir[6 * (size_t)e + c];
+    int* q = hi + PINIT_I * k;
+    q[0] = e;
+    q[1] = max_close[e];
+    q[2] = finger_body ? finger_body[2 * e] : -1;   // -1: keep the env's current wiring
+    q[3] = finger_body ? finger_body[2 * e + 1] : -1;
+    q[4] = object_body ? object_body[e] : -1;
+    q[5] = gripper_bits ? gripper_bits[e] : -1;
+  }
+  CK(cudaMemcpyAsync(b->d_pinit, b->h_pinit, bytes, cudaMemcpyHostToDevice, b->stream));
+  k_protocol_init<<<(int)((n + 127) / 128), 128, 0, b->stream>>>(
+      b->D, (int)n, reinterpret_cast<const double*>(b->d_pinit),
+      reinterpret_cast<const int*>(b->d_pinit + n * sizeof(double) * PINIT_D));
+  b->launches++;
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(b->stream));
   b->snap_valid = false;
   return 0;
@@ -1197,6 +1183,7 @@ int grip_protocol_reset(GripBatch* b, const uint8_t* mask, const double* closing
 }
 
 int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
+  b->ev_now = false;   // a finalize rewrites (or, recording off, invalidates) the event rows
   Dev& D = b->D;
   if (!D.pr_i) {
     g_err = "grip_run_rounds before grip_protocol_setup";
@@ -1266,6 +1253,8 @@ int grip_protocol_read(GripBatch* b, GripTrialOut* out) {
     o.final_contact = I[PI_FCONTACT];
     o.halt_step[0] = I[PI_HSTEP0]; o.halt_step[1] = I[PI_HSTEP1];
     for (int k = 0; k < 18; ++k) o.markers[k] = I[PI_MARK + k];
+    o.min_distance = R[PD_MIND];
+    o.min_J = R[PD_MINJ];
   }
   return 0;
 }
@@ -1289,10 +1278,54 @@ int grip_set_recording(GripBatch* b, int on) {
   return 0;
 }
 
+int grip_check_finite(GripBatch* b, uint8_t* nonfinite) {
+  if (b->n_env == 0) return 0;
+  if (!b->d_nonfin) {
+    b->d_nonfin = b->alloc<int>(b->n_env);
+    if (!b->d_nonfin) {
+      g_err = "out of device memory";
+      return -1;
+    }
+  }
+  k_check_finite<<<b->n_env, NT, 0, b->stream>>>(b->D, b->d_nonfin);
+  b->launches++;
+  CK(cudaGetLastError());
+  std::vector<int> h(b->n_env);
+  CK(cudaMemcpyAsync(h.data(), b->d_nonfin, sizeof(int) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  for (int e = 0; e < b->n_env; ++e) nonfinite[e] = (uint8_t)(h[e] != 0);
+  return 0;
+}
+
+int grip_contacts_now(GripBatch* b, const uint8_t* mask, double radius_factor, double* min_distance) {
+  std::vector<int> L = mask_to_list(b, mask);
+  if (L.empty()) return 0;
+  if (upload_list(b, L, b->d_list)) return -1;
+  const int n = (int)L.size();
+  if (!b->d_md_now) {
+    b->d_md_now = b->alloc<double>(std::max(b->n_env, 1));
+    if (!b->d_md_now) {
+      g_err = "out of device memory";
+      return -1;
+    }
+  }
+  if (run_with_growth(b, n, [&] {
+        k_contacts_now<<<n, NT, 0, b->stream>>>(b->D, b->d_list, radius_factor, b->d_md_now);
+      }))
+    return -1;
+  b->snap_valid = false;   // body forces / contact bits now describe this state
+  b->ev_now = true;
+  if (min_distance) {
+    CK(cudaMemcpyAsync(min_distance, b->d_md_now, sizeof(double) * b->n_env, cudaMemcpyDeviceToHost, b->stream));
+    CK(cudaStreamSynchronize(b->stream));
+  }
+  return 0;
+}
+
 int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t* ev_i, double* ev_d, int64_t cap) {
   Dev& D = b->D;
-  if (!D.ev_on) {
-    g_err = "grip_get_events: recording is off (grip_set_recording)";
+  if (!D.ev_on && !b->ev_now) {
+    g_err = "grip_get_events: no events (grip_set_recording off and no grip_contacts_now)";
     return -1;
   }
   const int E = b->n_env;
@@ -1319,35 +1352,73 @@ int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t*
 }
 
 int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
-                    const double* tet_Dmi, const double* tet_V0) {
+                    const double* tet_Dmi, const double* tet_V0, const double* tet_mu, const double* tet_lam,
+                    const double* body_mu) {
   b->snap_valid = false;
-  Dev& D = b->D;
-  auto cp = [&](double* dst, const double* src, size_t off, size_t n) {
-    return cudaMemcpyAsync(dst + off, src + off, n * sizeof(double), cudaMemcpyHostToDevice, b->stream);
-  };
-  std::vector<int> zero_i;
+  const int with_mat = (tet_mu && tet_lam && body_mu) ? 1 : 0;
+  if (!with_mat && (tet_mu || tet_lam || body_mu)) {
+    g_err = "grip_reset_envs: tet_mu, tet_lam and body_mu go together";
+    return -1;
+  }
+  // stage the masked envs' slices in one pinned buffer -> one H2D copy -> k_reset_envs scatters them
+  std::vector<int> L;
+  std::vector<long long> off;
+  long long n = 0;
   for (int e = 0; e < b->n_env; ++e) {
     if (!mask[e]) continue;
+    const long long nn = b->node_off[e + 1] - b->node_off[e], ns = b->sv_off[e + 1] - b->sv_off[e];
+    const long long nt = b->tet_off[e + 1] - b->tet_off[e], nb = b->body_off[e + 1] - b->body_off[e];
+    L.push_back(e);
+    off.push_back(n);
+    n += 3 * nn + 3 * ns + 10 * nt + (with_mat ? 2 * nt + nb : 0);
+  }
+  if (L.empty()) return 0;
+  const size_t head = L.size() * (sizeof(int) + sizeof(long long));
+  const size_t bytes = ((head + 15) & ~(size_t)15) + n * sizeof(double);
+  CK(cudaStreamSynchronize(b->stream));   // the pinned staging buffer may still feed a previous copy
+  if (bytes > b->reset_cap) {
+    if (b->h_reset) cudaFreeHost(b->h_reset);
+    if (b->d_reset) cudaFree(b->d_reset);
+    b->h_reset = nullptr;
+    b->d_reset = nullptr;
+    b->reset_cap = std::max(bytes, 2 * b->reset_cap);
+    CK(cudaMallocHost(&b->h_reset, b->reset_cap));
+    CK(cudaMalloc(&b->d_reset, b->reset_cap));
+  }
+  char* h = b->h_reset;
+  long long* h_off = reinterpret_cast<long long*>(h);
+  int* h_lst = reinterpret_cast<int*>(h + L.size() * sizeof(long long));
+  double* h_st = reinterpret_cast<double*>(h + ((head + 15) & ~(size_t)15));
+  for (size_t k = 0; k < L.size(); ++k) {
+    const int e = L[k];
+    h_off[k] = off[k];
+    h_lst[k] = e;
+    double* q = h_st + off[k];
+    auto put = [&](const double* src, size_t o, size_t cnt) {
+      memcpy(q, src + o, cnt * sizeof(double));
+      q += cnt;
+    };
     const size_t n0 = b->node_off[e], nn = b->node_off[e + 1] - n0;
     const size_t s0 = b->sv_off[e], ns = b->sv_off[e + 1] - s0;
     const size_t t0 = b->tet_off[e], nt = b->tet_off[e + 1] - t0;
-    CK(cp(D.x, node_x0, 3 * n0, 3 * nn));
-    CK(cudaMemsetAsync(D.v + 3 * n0, 0, 3 * nn * sizeof(double), b->stream));
-    CK(cp(D.kin_pos, sv_kin0, 3 * s0, 3 * ns));
-    if (nt) {
-      CK(cp(const_cast<double*>(D.tet_Dmi), tet_Dmi, 9 * t0, 9 * nt));
-      CK(cp(const_cast<double*>(D.tet_V0), tet_V0, t0, nt));
+    const size_t b0 = b->body_off[e], nb = b->body_off[e + 1] - b0;
+    put(node_x0, 3 * n0, 3 * nn);
+    put(sv_kin0, 3 * s0, 3 * ns);
+    put(tet_Dmi, 9 * t0, 9 * nt);
+    put(tet_V0, t0, nt);
+    if (with_mat) {
+      put(tet_mu, t0, nt);
+      put(tet_lam, t0, nt);
+      put(body_mu, b0, nb);
     }
-    CK(cudaMemsetAsync(D.n_anc + e, 0, sizeof(int), b->stream));
-    CK(cudaMemsetAsync(D.cs_valid + e, 0, sizeof(int), b->stream));
-    CK(cudaMemsetAsync(D.md_prev + e, 0, sizeof(double), b->stream));
-    CK(cudaMemsetAsync(D.time + e, 0, sizeof(double), b->stream));
-    CK(cudaMemsetAsync(D.step_index + e, 0, sizeof(int), b->stream));
-    CK(cudaMemsetAsync(D.ns_done + e, 0, sizeof(int), b->stream));
-    CK(cudaMemsetAsync(D.fin_done + e, 0, sizeof(int), b->stream));
-    CK(cudaMemsetAsync(D.ns_status + e, 0, sizeof(int), b->stream));
-    CK(cudaMemsetAsync(D.flags + e, 0, sizeof(int), b->stream));
   }
+  CK(cudaMemcpyAsync(b->d_reset, b->h_reset, bytes, cudaMemcpyHostToDevice, b->stream));
+  const char* d = b->d_reset;
+  k_reset_envs<<<(int)L.size(), NT, 0, b->stream>>>(
+      b->D, reinterpret_cast<const int*>(d + L.size() * sizeof(long long)), reinterpret_cast<const long long*>(d),
+      reinterpret_cast<const double*>(d + ((head + 15) & ~(size_t)15)), with_mat);
+  b->launches++;
+  CK(cudaGetLastError());
   return 0;
 }
 
@@ -1370,6 +1441,102 @@ int grip_debug_elements(int type, int n, const double* in, int stride, double* E
   CK(cudaMemcpy(flags, d_f, sizeof(int) * n, cudaMemcpyDeviceToHost));
   cudaFree(d_in); cudaFree(d_E); cudaFree(d_g); cudaFree(d_H); cudaFree(d_f);
   return 0;
+}
+
+// Element-level test hook of the PRODUCTION element chain (the launches of sweep_launch on a
+// scratch device context): type 2 NH tets through k_tet_front (Gershgorin pass-through or
+// deferral) -> k_tet_jacobi2 -> k_tet_back with the warm-start eigenbases eig (n*81, in/out;
+// NULL = identity, the first Newton iteration); types 0 / 1 PT / EE stencils through the
+// k_elements_w element code with clamp deferral -> k_tet_jacobi2 -> k_tet_finish.  Same input
+// rows and outputs as grip_debug_elements.
+int grip_debug_chain(int type, int n, const double* in, int stride, double* E, double* g, double* H, double* eig,
+                     int* flags) {
+  if (n <= 0) return 0;
+  if (type < 0 || type > 2) {
+    g_err = "grip_debug_chain: type must be 0 (PT), 1 (EE) or 2 (NH)";
+    return -1;
+  }
+  std::vector<void*> mem;
+  auto dalloc = [&](size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 8)) != cudaSuccess) return (void*)nullptr;
+    cudaMemset(p, 0, std::max<size_t>(bytes, 8));
+    mem.push_back(p);
+    return p;
+  };
+  auto up = [&](const void* h, size_t bytes) {
+    void* p = dalloc(bytes);
+    if (p && bytes) cudaMemcpy(p, h, bytes, cudaMemcpyHostToDevice);
+    return p;
+  };
+  int rc = 0;
+  Dev D{};
+  D.n_env = 1;
+  D.cap_el = n;
+  D.el_E = (double*)dalloc(sizeof(double) * n);
+  D.el_g = (double*)dalloc(sizeof(double) * 12 * (size_t)n);
+  D.el_H = (double*)dalloc(sizeof(double) * 144 * (size_t)n);
+  D.el_idx = (int*)dalloc(sizeof(int) * 4 * (size_t)n);
+  D.flags = (int*)dalloc(sizeof(int));
+  int* d_flags = (int*)dalloc(sizeof(int) * n);
+  double* d_in = (double*)up(in, sizeof(double) * (size_t)n * stride);
+  if (type == 2) {
+    std::vector<double> x(12 * (size_t)n), Dmi(9 * (size_t)n), V0(n), mu(n), lam(n), Y(81 * (size_t)n, 0.0);
+    std::vector<int> tn(4 * (size_t)n), off_n{0, 4 * n}, off_t{0, n}, zero{0};
+    for (int k = 0; k < n; ++k) {
+      const double* r = in + (size_t)k * stride;
+      for (int j = 0; j < 12; ++j) x[12 * (size_t)k + j] = r[j];
+      for (int j = 0; j < 9; ++j) Dmi[9 * (size_t)k + j] = r[12 + j];
+      V0[k] = r[21]; mu[k] = r[22]; lam[k] = r[23];
+      for (int j = 0; j < 4; ++j) tn[4 * (size_t)k + j] = 4 * k + j;
+      for (int j = 0; j < 81; ++j) Y[81 * (size_t)k + j] = eig ? eig[81 * (size_t)k + j] : (j % 10 == 0 ? 1.0 : 0.0);
+    }
+    D.x = (double*)up(x.data(), sizeof(double) * x.size());
+    D.tet_nodes = (const int*)up(tn.data(), sizeof(int) * tn.size());
+    D.tet_Dmi = (const double*)up(Dmi.data(), sizeof(double) * Dmi.size());
+    D.tet_V0 = (const double*)up(V0.data(), sizeof(double) * n);
+    D.tet_mu = (const double*)up(mu.data(), sizeof(double) * n);
+    D.tet_lam = (const double*)up(lam.data(), sizeof(double) * n);
+    D.tet_eig = (double*)up(Y.data(), sizeof(double) * Y.size());
+    D.tet_S = (double*)dalloc(sizeof(double) * 45 * (size_t)n);
+    D.tet_W = (double*)dalloc(sizeof(double) * 90 * (size_t)n);
+    D.jac_list = (int2*)dalloc(sizeof(int2) * n);
+    D.jac_n = (int*)dalloc(sizeof(int));
+    D.node_off = (const int*)up(off_n.data(), sizeof(int) * 2);
+    D.tet_off = (const int*)up(off_t.data(), sizeof(int) * 2);
+    D.twork_off = (int*)up(off_t.data(), sizeof(int) * 2);
+    int* d_list = (int*)up(zero.data(), sizeof(int));
+    k_tet_front<<<std::max(1, std::min(1024, (n + TF - 1) / TF)), TF>>>(D, d_list, 1);
+    k_tet_jacobi2<<<148, TJ>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+    k_tet_back<<<148, EW * 32>>>(D, D.jac_list, D.jac_n, D.tet_W);
+    k_eig_commit<<<148, 256>>>(D, D.jac_list, D.jac_n, D.tet_W);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) rc = -1;
+    if (!rc && eig) cudaMemcpy(eig, D.tet_eig, sizeof(double) * 81 * (size_t)n, cudaMemcpyDeviceToHost);
+    int ff = 0;
+    cudaMemcpy(&ff, D.flags, sizeof(int), cudaMemcpyDeviceToHost);
+    for (int k = 0; k < n; ++k) flags[k] = ff;
+  } else {
+    D.cjac_S = (double*)dalloc(sizeof(double) * 45 * (size_t)n);
+    D.cjac_W = (double*)dalloc(sizeof(double) * 90 * (size_t)n);
+    D.cjac_list = (int2*)dalloc(sizeof(int2) * n);
+    D.cjac_n = (int*)dalloc(sizeof(int));
+    k_debug_contacts<<<std::max(1, std::min(1024, (n + 3) / 4)), 128>>>(D, type, n, d_in, stride, d_flags);
+    k_tet_jacobi2<<<148, TJ>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
+    k_tet_finish<<<148, EW * 32>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
+    if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) rc = -1;
+    if (!rc) cudaMemcpy(flags, d_flags, sizeof(int) * n, cudaMemcpyDeviceToHost);
+  }
+  for (void* p : mem)
+    if (!p) rc = -1;
+  if (!rc) {
+    cudaMemcpy(E, D.el_E, sizeof(double) * n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(g, D.el_g, sizeof(double) * 12 * (size_t)n, cudaMemcpyDeviceToHost);
+    cudaMemcpy(H, D.el_H, sizeof(double) * 144 * (size_t)n, cudaMemcpyDeviceToHost);
+  }
+  for (void* p : mem)
+    if (p) cudaFree(p);
+  if (rc) g_err = "grip_debug_chain: device error";
+  return rc;
 }
 
 int grip_get_state(GripBatch* b, double* x, double* v, double* kin) {

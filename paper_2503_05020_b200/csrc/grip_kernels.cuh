@@ -361,89 +361,8 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Newton sweep 2/4: element energies, gradients and SPD-projected Hessians
-// (materials.py:116-188, contact.py:271-344, 475-524).  Unscaled (no dt^2).
-// Element slots per env: [tets | abd | contacts | anchors].
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_elements(Dev D, const int* list, int n) {
-  const int total = D.work_off[n];
-  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < total; w += gridDim.x * blockDim.x) {
-    int lo = 0, hi = n;  // find list position: work_off[pos] <= w < work_off[pos+1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (D.work_off[mid] <= w) lo = mid;
-      else hi = mid;
-    }
-    const int e = list[lo];
-    const EnvIx E = env_ix(D, e);
-    const double* P = P_(D, e);
-    int k = w - D.work_off[lo];
-    const size_t elbase = (size_t)e * D.cap_el;
-    double Eel = 0.0;
-    double g[12];
-    int slot;
-    int idx[4];
-    if (k < E.ntet) {
-      const int t = E.te0 + k;
-      slot = k;
-      V3 x[4];
-      for (int j = 0; j < 4; ++j) {
-        idx[j] = D.tet_nodes[4 * (size_t)t + j];
-        x[j] = ld3(D.x + 3 * (size_t)(E.n0 + idx[j]));
-      }
-      double* H = D.el_H + (elbase + slot) * 144;
-      const int fl = nh_element(x, D.tet_Dmi + 9 * (size_t)t, D.tet_V0[t], D.tet_mu[t], D.tet_lam[t], &Eel, g, H);
-      if (fl & EL_INVERTED) {
-        atomicOr(&D.flags[e], ERR_INVERTED);
-        Eel = 0.0;
-        for (int i = 0; i < 12; ++i) g[i] = 0.0;
-      }
-    } else if ((k -= E.ntet) < E.na) {
-      const int a = E.a0 + k;
-      slot = D.max_tet + k;
-      const int pn = D.abd_node[a];
-      for (int j = 0; j < 4; ++j) idx[j] = pn + j;
-      const double* q = D.x + 3 * (size_t)(E.n0 + pn);
-      double* H = D.el_H + (elbase + slot) * 144;
-      Eel = abd_element(q + 3, D.abd_kV[a], g, H);
-    } else if ((k -= E.na) < D.n_act[e]) {
-      slot = D.max_tet + D.max_abd + k;
-      const int code = D.act[(size_t)e * D.cap_act + k];
-      const bool is_ee = code >= D.cap_pt;
-      const int* row = is_ee ? D.c1_ee + ((size_t)e * D.cap_ee + (code - D.cap_pt)) * 4 : D.c1_pt + ((size_t)e * D.cap_pt + code) * 4;
-      V3 x[4];
-      for (int j = 0; j < 4; ++j) {
-        idx[j] = row[j];
-        x[j] = ld3(D.sv_pos + 3 * (size_t)(E.s0 + idx[j]));
-      }
-      double* H = D.el_H + (elbase + slot) * 144;
-      if (is_ee) {
-        const int* eid = D.c1_eid + ((size_t)e * D.cap_ee + (code - D.cap_pt)) * 2;
-        const double epsx = D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]];
-        ee_element(x, epsx, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, g, H, 1);
-      } else {
-        pt_element(x, P[GRIP_P_KAPPA], P[GRIP_P_DHAT], &Eel, g, H, 1);
-      }
-    } else {
-      k -= D.n_act[e];
-      slot = D.max_tet + D.max_abd + D.cap_act + k;
-      const size_t ai = (size_t)e * D.cap_anc + k;
-      V3 x[4], xp[4];
-      for (int j = 0; j < 4; ++j) {
-        idx[j] = D.anc_v[4 * ai + j];
-        x[j] = ld3(D.sv_pos + 3 * (size_t)(E.s0 + idx[j]));
-        xp[j] = ld3(D.surf_prev + 3 * (size_t)(E.s0 + idx[j]));
-      }
-      double* H = D.el_H + (elbase + slot) * 144;
-      Eel = friction_element(x, xp, D.anc_gamma + 4 * ai, D.anc_T + 6 * ai, D.anc_lam[ai], D.anc_mu[ai], P[GRIP_P_EPSV],
-                             P[GRIP_P_DT], g, H);
-    }
-    D.el_E[elbase + slot] = Eel;
-    for (int i = 0; i < 12; ++i) D.el_g[(elbase + slot) * 12 + i] = g[i];
-    for (int j = 0; j < 4; ++j) D.el_idx[(elbase + slot) * 4 + j] = idx[j];
-  }
-}
+// Newton sweep 2/4 (element energies, gradients, SPD-projected Hessians): grip_tet.cuh
+// (k_tet_front / k_tet_back), grip_warp_elements.cuh (k_elements_w), grip_tetclamp.cuh.
 
 // ---------------------------------------------------------------------------
 // Newton sweep 3/4: assembly + block-Jacobi PCG (solver.py:542-586, 654-676, 91-131)
@@ -1522,6 +1441,28 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
     sp = block_max(sp, sm);
     if (threadIdx.x == 0) D.max_speed[e] = sp;
   }
+  {   // inversion report: min J = det F = det(Ds) det(Dm^-1) over tets (materials.py:116-131), det A
+      // over affine bodies (ccd.py:191-204's determinant)
+    double mj = INFINITY;
+    for (int k = threadIdx.x; k < E.ntet; k += NT) {
+      const int t = E.te0 + k;
+      const int* tn = D.tet_nodes + 4 * (size_t)t;
+      const V3 x0 = ld3(D.x + 3 * (size_t)(E.n0 + tn[0]));
+      const V3 a = ld3(D.x + 3 * (size_t)(E.n0 + tn[1])) - x0, b = ld3(D.x + 3 * (size_t)(E.n0 + tn[2])) - x0,
+               c = ld3(D.x + 3 * (size_t)(E.n0 + tn[3])) - x0;
+      const double* M = D.tet_Dmi + 9 * (size_t)t;
+      const double dM = M[0] * (M[4] * M[8] - M[5] * M[7]) - M[1] * (M[3] * M[8] - M[5] * M[6]) +
+                        M[2] * (M[3] * M[7] - M[4] * M[6]);
+      mj = fmin(mj, dot(cross(a, b), c) * dM);
+    }
+    for (int k = threadIdx.x; k < E.na; k += NT) {
+      const size_t pn = E.n0 + D.abd_node[E.a0 + k];
+      const V3 r0 = ld3(D.x + 3 * (pn + 1)), r1 = ld3(D.x + 3 * (pn + 2)), r2 = ld3(D.x + 3 * (pn + 3));
+      mj = fmin(mj, dot(cross(r0, r1), r2));
+    }
+    mj = block_min(mj, sm);
+    if (threadIdx.x == 0) D.min_J[e] = mj;
+  }
   // quarantine check (multienv.py:105-108)
   int nonfin = 0;
   for (int i = threadIdx.x; i < 3 * E.nn; i += NT) nonfin |= !isfinite(D.x[3 * (size_t)E.n0 + i]);
@@ -1580,6 +1521,10 @@ __global__ void k_protocol(Dev D) {
     const double dx = com[0] - R[PD_COM0], dy = com[1] - R[PD_COM0 + 1], dz = com[2] - R[PD_COM0 + 2];
     return sqrt(dx * dx + dy * dy + dz * dz);
   };
+  if (D.ns_status[e] != GRIP_NS_FAILED) {   // a failed step keeps its pre-step state
+    R[PD_MIND] = fmin(R[PD_MIND], D.min_dist[e]);
+    R[PD_MINJ] = fmin(R[PD_MINJ], D.min_J[e]);
+  }
   if (D.ns_status[e] == GRIP_NS_FAILED) {
     I[PI_VERDICT] = 3;
     I[PI_FPHASE] = ph == 3 ? 3 + I[PI_GPHASE] : ph;
@@ -1638,6 +1583,36 @@ __global__ void k_protocol(Dev D) {
   if (I[PI_PHASE] != 4) I[PI_NEEDBEGIN] = 1;
 }
 
+// protocol (re)start of n envs (grip_protocol_setup / grip_protocol_reset), thread per env:
+// hd = closing dirs (PINIT_D per env), hi = {env, max_close, finger 0, finger 1, object, gripper
+// bits} (-1: keep the current wiring).  Settle starts with the fingers still and gravity off
+// (protocol.py:193-198).
+__global__ void k_protocol_init(Dev D, int n, const double* hd, const int* hi) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int* q = hi + PINIT_I * k;
+  const int e = q[0];
+  int* I = D.pr_i + (size_t)e * PI_N;
+  double* R = D.pr_d + (size_t)e * PD_N;
+  const int fb0 = q[2] >= 0 ? q[2] : I[PI_FB0], fb1 = q[3] >= 0 ? q[3] : I[PI_FB1];
+  const int obj = q[4] >= 0 ? q[4] : I[PI_OBJ], gb = q[5] >= 0 ? q[5] : I[PI_GBITS];
+  for (int j = 0; j < PI_N; ++j) I[j] = 0;
+  for (int j = 0; j < PD_N; ++j) R[j] = 0.0;
+  I[PI_FB0] = fb0; I[PI_FB1] = fb1; I[PI_OBJ] = obj; I[PI_GBITS] = gb;
+  I[PI_MAXCLOSE] = q[1];
+  I[PI_NEEDBEGIN] = 1;
+  for (int j = 0; j < 18; ++j) I[PI_MARK + j] = -1;
+  I[PI_HSTEP0] = I[PI_HSTEP1] = -1;
+  for (int j = 0; j < 6; ++j) R[PD_CD + j] = hd[PINIT_D * k + j];
+  R[PD_MIND] = R[PD_MINJ] = INFINITY;
+  const int b0 = D.body_off[e];
+  for (int c = 0; c < 3; ++c) {
+    D.body_vel[3 * (size_t)(b0 + fb0) + c] = 0.0;
+    D.body_vel[3 * (size_t)(b0 + fb1) + c] = 0.0;
+    D.gravity[3 * (size_t)e + c] = 0.0;
+  }
+}
+
 // packed recorder frame of the envs with m[4e] >= 0 (grip_get_frames): CTA per env
 __global__ void k_frames(Dev D, const int* m, double* fx, double* fv, double* fk, double* fs) {
   const int e = blockIdx.x;
@@ -1659,6 +1634,64 @@ __global__ void k_frames(Dev D, const int* m, double* fx, double* fv, double* fk
     if (!nh_stress(x, D.tet_Dmi + 9 * (size_t)t, D.tet_mu[t], D.tet_lam[t], row))
       for (int c = 0; c < 7; ++c) row[c] = NAN;
     for (int c = 0; c < 7; ++c) fs[7 * ((size_t)ot + k) + c] = row[c];
+  }
+}
+
+// Slot refill (grip_reset_envs): CTA per refilled env.  The env gets the new candidate's pose and
+// rest shape from the staged slice and EVERY piece of per-env state a fresh grip_create starts
+// from (zeros, identity Jacobi warm starts), so a refilled trial is bitwise a fresh trial.
+// Staged slice per env (doubles): x0 (3 nn) | kin0 (3 ns) | Dmi (9 nt) | V0 (nt) [| mu (nt) | lam (nt)]
+// [| body mu (nb)], the bracketed parts when with_mat.
+__global__ void k_reset_envs(Dev D, const int* lst, const long long* off, const double* stage, int with_mat) {
+  const int e = lst[blockIdx.x];
+  const double* s = stage + off[blockIdx.x];
+  const int n0 = D.node_off[e], nn = D.node_off[e + 1] - n0;
+  const int s0 = D.sv_off[e], ns = D.sv_off[e + 1] - s0;
+  const int t0 = D.tet_off[e], nt = D.tet_off[e + 1] - t0;
+  const int b0 = D.body_off[e], nb = D.body_off[e + 1] - b0;
+  double* Dmi = const_cast<double*>(D.tet_Dmi);
+  double* V0 = const_cast<double*>(D.tet_V0);
+  double* tet_mu = const_cast<double*>(D.tet_mu);
+  double* tet_lam = const_cast<double*>(D.tet_lam);
+  double* body_mu = const_cast<double*>(D.body_mu);
+  for (int i = threadIdx.x; i < 3 * nn; i += blockDim.x) {
+    const size_t g = 3 * (size_t)n0 + i;
+    D.x[g] = s[i];
+    D.v[g] = D.x_t[g] = D.xhat[g] = D.pdir[g] = 0.0;
+  }
+  s += 3 * nn;
+  for (int i = threadIdx.x; i < 3 * ns; i += blockDim.x) {
+    const size_t g = 3 * (size_t)s0 + i;
+    D.kin_pos[g] = s[i];
+    D.sv_pos[g] = D.surf_prev[g] = D.sv_disp[g] = 0.0;
+  }
+  s += 3 * ns;
+  for (int i = threadIdx.x; i < 9 * nt; i += blockDim.x) Dmi[9 * (size_t)t0 + i] = s[i];
+  s += 9 * nt;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) V0[t0 + i] = s[i];
+  s += nt;
+  if (with_mat) {
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) tet_mu[t0 + i] = s[i];
+    s += nt;
+    for (int i = threadIdx.x; i < nt; i += blockDim.x) tet_lam[t0 + i] = s[i];
+    s += nt;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) body_mu[b0 + i] = s[i];
+  }
+  for (int i = threadIdx.x; i < 81 * nt; i += blockDim.x)   // Jacobi warm start: identity
+    D.tet_eig[81 * (size_t)t0 + i] = (i % 81) % 10 == 0 ? 1.0 : 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    D.body_force[b0 + i] = 0.0;
+    D.contact_mask[b0 + i] = 0u;
+    for (int c = 0; c < 3; ++c) D.body_com[3 * (size_t)(b0 + i) + c] = 0.0;
+  }
+  for (int i = threadIdx.x; i < D.max_alpha; i += blockDim.x) D.alphas[(size_t)e * D.max_alpha + i] = 0.0;
+  if (threadIdx.x == 0) {
+    D.ell[e] = D.tol[e] = D.residual[e] = D.energy[e] = D.min_dist[e] = D.time[e] = 0.0;
+    D.max_speed[e] = D.cs_R[e] = D.cs_drift[e] = D.md_prev[e] = D.md_kin[e] = 0.0;
+    D.iters[e] = D.ns_status[e] = D.reason[e] = D.regularized[e] = D.kin_blocked[e] = D.needs_ls[e] = 0;
+    D.ns_done[e] = D.flags[e] = D.step_index[e] = D.newton_calls[e] = D.pcg_iters[e] = D.fin_done[e] = 0;
+    D.cs_valid[e] = D.n_act[e] = D.n_anc[e] = D.ev_n[e] = 0;
+    for (int c = 0; c < 2; ++c) D.cs_n[2 * e + c] = D.c1_n[2 * e + c] = D.c2_n[2 * e + c] = 0;
   }
 }
 
@@ -1694,6 +1727,117 @@ __global__ void __launch_bounds__(NT) k_query(Dev D, const int* list, double r) 
                        D.c2_eid + (size_t)e * 2 * D.cap_ee, D.c2_n + 2 * e, S, sm)) {
     if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
   }
+}
+
+// Contact readout at the CURRENT state, no step taken (protocol.py:72-75 contact_events_now,
+// solver.py:449-453 min_contact_distance, contact.py:348-372 stencil_forces): the canonical
+// candidate set at radius r (the c2 buffers, as k_query), the min distance over all of its
+// stencils, and every active stencil (d < dhat) as an event row in the ev_* buffers with
+// lambda = kappa m |b'(d)|; per-body force sums and the body contact bits as k_finalize makes
+// them.  v, anchors, time and the step's min_dist are untouched.
+__global__ void __launch_bounds__(NT) k_contacts_now(Dev D, const int* list, double radius_factor, double* md_out) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  __shared__ unsigned int cmask[32];
+  const int e = list[blockIdx.x];
+  const EnvIx E = env_ix(D, e);
+  const double* P = P_(D, e);
+  const double kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
+  env_sv_positions(D, E, D.x);
+  int* cn = D.c2_n + 2 * e;
+  int* cpt = D.c2_pt + (size_t)e * 4 * D.cap_pt;
+  int* cee = D.c2_ee + (size_t)e * 4 * D.cap_ee;
+  int* ceid = D.c2_eid + (size_t)e * 2 * D.cap_ee;
+  if (!broad_phase_env(D, E, radius_factor * dhat, cpt, cee, ceid, cn, S, sm)) {
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    return;
+  }
+  const int npt = cn[0], nee = cn[1];
+  const double* X = D.sv_pos + 3 * (size_t)E.s0;
+  if (threadIdx.x < 32) cmask[threadIdx.x] = 0u;
+  __syncthreads();
+  double dmin = INFINITY;
+  int base = 0;
+  double fsum[32];
+  const int nbl = min(E.nb, 32);
+  for (int b = 0; b < nbl; ++b) fsum[b] = 0.0;
+  for (int s = 0; s < npt + nee; s += NT) {
+    const int k = s + threadIdx.x;
+    int act = 0, rowv[4], bb[2];
+    double lam = 0.0, Dq = 0.0;
+    if (k < npt + nee) {
+      const bool is_ee = k >= npt;
+      const int* row = is_ee ? cee + 4 * (k - npt) : cpt + 4 * k;
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) {
+        rowv[j] = row[j];
+        x[j] = ld3(X + 3 * row[j]);
+      }
+      double bary[3], sp = 0.0, tp = 0.0;
+      Dq = is_ee ? ee_closest(x[0], x[1], x[2], x[3], &sp, &tp) : pt_closest(x[0], x[1], x[2], x[3], bary, nullptr);
+      dmin = fmin(dmin, Dq);
+      if (Dq < dhat * dhat) {
+        act = 1;
+        double b0, b1, b2;
+        barrier_d(sqrt(Dq), dhat, &b0, &b1, &b2);
+        double m = 1.0;
+        if (is_ee) {
+          double dm, d2m;
+          const int* eid = ceid + 2 * (k - npt);
+          edge_mollifier(cross_norm_sq(x, nullptr, nullptr), D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]],
+                         &m, &dm, &d2m);
+        }
+        lam = kappa * m * fabs(b1);
+        bb[0] = D.sv_body[E.s0 + row[0]];
+        bb[1] = D.sv_body[E.s0 + row[is_ee ? 2 : 1]];
+        for (int b = 0; b < nbl; ++b)
+          if (bb[0] == b || bb[1] == b) fsum[b] += lam;
+        if (bb[0] < 32 && bb[1] < 32) {
+          atomicOr(&cmask[bb[0]], 1u << bb[1]);
+          atomicOr(&cmask[bb[1]], 1u << bb[0]);
+        }
+      }
+    }
+    int tot;
+    const int pre = block_scan(act, sm, &tot);
+    if (act && base + pre < D.cap_anc) {
+      const size_t vi = (size_t)e * D.cap_anc + base + pre;
+      int* ei = D.ev_i + 7 * vi;
+      ei[0] = k >= npt;
+      ei[1] = bb[0];
+      ei[2] = bb[1];
+      for (int j = 0; j < 4; ++j) ei[3 + j] = rowv[j];
+      D.ev_d[2 * vi] = sqrt(Dq);
+      D.ev_d[2 * vi + 1] = lam;
+    }
+    base += tot;
+  }
+  if (base > D.cap_anc) {   // more active stencils than event rows: grow and redo
+    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    return;
+  }
+  dmin = block_min(dmin, sm);
+  for (int b = 0; b < nbl; ++b) {
+    const double f = block_sum(fsum[b], sm);
+    if (threadIdx.x == 0) D.body_force[E.b0 + b] = f;
+  }
+  if (threadIdx.x < nbl) D.contact_mask[E.b0 + threadIdx.x] = cmask[threadIdx.x];
+  if (threadIdx.x == 0) {
+    D.ev_n[e] = base;
+    md_out[e] = (npt + nee) > 0 ? sqrt(dmin) : INFINITY;
+  }
+}
+
+// quarantine test of Batch.quarantine_failures (multienv.py:98-123): 1 per env whose x holds a
+// non-finite value, CTA per env (no state copy to the host)
+__global__ void __launch_bounds__(NT) k_check_finite(Dev D, int* out) {
+  __shared__ Red sm;
+  const int e = blockIdx.x;
+  const size_t a = 3 * (size_t)D.node_off[e], b = 3 * (size_t)D.node_off[e + 1];
+  int bad = 0;
+  for (size_t i = a + threadIdx.x; i < b; i += NT) bad |= !isfinite(D.x[i]);
+  bad = block_or(bad, sm);
+  if (threadIdx.x == 0) out[e] = bad;
 }
 
 }  // namespace grip

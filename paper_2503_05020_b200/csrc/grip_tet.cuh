@@ -231,7 +231,10 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
 }
 
 // deferred tets: finish the clamp from (eigenvalues, R) -- see the file header
-__global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, const int* n_ptr, const double* Wbuf) {
+// The next warm start V = Y R goes to W[9..90) (over R), not to tet_eig: k_eig_commit copies it
+// after the line search, for envs whose sweep is not redone after a buffer growth (a redone sweep
+// must start from the same warm starts, so results do not depend on when buffers grew).
+__global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, const int* n_ptr, double* Wbuf) {
   __shared__ WarpWS ws[EW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpWS& w = ws[warp];
@@ -239,8 +242,8 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
   for (int idx = blockIdx.x * EW + warp; idx < n; idx += gridDim.x * EW) {
     const int2 it = list[idx];
     const size_t t = it.x, slot = it.y;
-    const double* W = Wbuf + 90 * t;
-    double* Y = D.tet_eig + 81 * t;
+    double* W = Wbuf + 90 * t;
+    const double* Y = D.tet_eig + 81 * t;
     for (int e = lane; e < 81; e += 32) {
       w.S[e] = Y[e];       // Y
       w.T[e] = W[9 + e];   // R
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
       w.V[e] = a;
     }
     __syncwarp();
-    for (int e = lane; e < 81; e += 32) Y[e] = w.V[e];
+    for (int e = lane; e < 81; e += 32) W[9 + e] = w.V[e];   // next warm start (k_eig_commit)
     for (int e = lane; e < 81; e += 32) {   // S_proj = V diag(max(l, f)) V^T
       const int i = e / 9, j = e - 9 * i;
       double a = 0.0;
@@ -290,6 +293,19 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
       if (c12 != r) Hg[c12 * 12 + r] = s;
     }
     __syncwarp();
+  }
+}
+
+// After the line search: the deferred tets' new warm starts (k_tet_back) become current, except
+// in envs whose sweep overflowed a buffer and will be redone.
+__global__ void k_eig_commit(Dev D, const int2* list, const int* n_ptr, const double* Wbuf) {
+  const int n = *n_ptr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 81 * n; i += gridDim.x * blockDim.x) {
+    const int k = i / 81, c = i - 81 * k;
+    const int2 it = list[k];
+    const int e = it.y / D.cap_el;
+    if (D.flags[e] & FLAG_OVERFLOW) continue;
+    D.tet_eig[81 * (size_t)it.x + c] = Wbuf[90 * (size_t)it.x + 9 + c];
   }
 }
 

@@ -436,4 +436,31 @@ __global__ void k_debug_elements(int type, int n, const double* in, int stride, 
   }
 }
 
+// grip_debug_chain, contacts: the production path of k_elements_w for standalone PT / EE stencils
+// (in: x(12), kappa, dhat / x(12), eps_x, kappa, dhat): clamps that fail the cold Cholesky test are
+// deferred to the batched eigensolve (D.cjac_*: k_tet_jacobi2 + k_tet_finish), exactly as in a sweep
+__global__ void k_debug_contacts(Dev D, int type, int n, const double* in, int stride, int* flags) {
+  __shared__ WarpEl ws[4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpEl& W = ws[warp];
+  for (int item = blockIdx.x * 4 + warp; item < n; item += gridDim.x * 4) {
+    const double* p = in + (size_t)item * stride;
+    V3 x[4];
+    for (int j = 0; j < 4; ++j) x[j] = ld3(p + 3 * j);
+    double e = 0.0;
+    int fl = 0;
+    for (int i = lane; i < 144; i += 32) W.H[i] = 0.0;
+    if (lane < 12) W.g[lane] = 0.0;
+    __syncwarp();
+    double* dS = D.cjac_S + 45 * (size_t)item;
+    if (type == 0) fl = w_pt(W, x, p[12], p[13], &e, lane, dS);
+    else fl = w_ee(W, x, p[12], p[13], p[14], &e, lane, dS);
+    if ((fl & EL_DEFERRED) && lane == 0) D.cjac_list[atomicAdd(D.cjac_n, 1)] = make_int2(item, item);
+    int idx[4] = {0, 1, 2, 3};
+    w_store(D, (size_t)item, W, e, idx, lane);
+    if (lane == 0) flags[item] = fl;
+    __syncwarp();
+  }
+}
+
 }  // namespace grip

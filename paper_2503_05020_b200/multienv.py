@@ -155,6 +155,12 @@ class DeviceEnvGroup:
             raise RuntimeError("contact-event recording is off for this device group")
         return self.dev.events(self._mask([slot]))[slot]
 
+    def _events_now(self, slot, radius_factor=1.05):
+        """Contact events at the slot's current state, computed on the device (grip_contacts_now)."""
+        m = self._mask([slot])
+        md = self.dev.contacts_now(m, radius_factor)
+        return self.dev.events(m)[slot], float(md[slot])
+
     def set_recording(self, on=True):
         self.dev.set_recording(on)
         self._recording = bool(on)
@@ -225,13 +231,15 @@ class Batch:
         return [i for i, s in enumerate(self.statuses) if s == "active"]
 
     def quarantine_failures(self):
-        """Fail envs with non-finite state or a failed solve; keep a tombstone (multienv.py:98-123)."""
+        """Fail envs with non-finite state or a failed solve; keep a tombstone (multienv.py:98-123).
+        The non-finite test runs on the device (grip_check_finite: one flag per env comes back)."""
+        nonfinite = self.group.dev.check_finite()
         for i, env in enumerate(self.envs):
             if self.statuses[i] in ("failed", "done"):
                 continue
             bad = env.status == "failed"
             reason = env.fail_reason
-            if not bad and env.n_dofs and not np.all(np.isfinite(env.x)):
+            if not bad and env.n_dofs and nonfinite[i]:
                 bad, reason = True, "non-finite state"
                 env.status, env.fail_reason = "failed", reason
             if bad:
@@ -282,7 +290,10 @@ def _run_trial_worker(args):
 def run_batch_trials(trial_fn, envs_payloads, max_workers=0, chunksize=1):
     """One trial per (env, payload), results in input order (multienv.py:204-216).
 
-    Trials run in-process; batching across envs happens on the device through
-    ``protocol.run_grasp_trials`` instead of a process pool.
+    The reference forks a process pool (max_workers) around an arbitrary Python trial function.
+    A CUDA context does not survive fork, so this generic form runs the trials in-process, one
+    after another, and ignores max_workers / chunksize.  The batched device path for grasp
+    trials is ``runner.TrialRunner`` (many trials per device batch, continuous refill) or
+    ``protocol.run_grasp_trials`` / ``protocol.DeviceProtocolTrials`` on a fixed set of envs.
     """
     return [_run_trial_worker((trial_fn, env, payload)) for env, payload in envs_payloads]

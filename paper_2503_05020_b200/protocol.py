@@ -58,6 +58,11 @@ class TrialRecord:
     object_body: int = 0
     gripper_bodies: tuple = ()
     n_steps: int = 0
+    # safety report over the completed steps (not part of the reference record or the dataset
+    # files): min stencil distance (> 0: no intersection) and min J = det F / det A (> 0: no
+    # inverted element); filled by the device protocol
+    min_distance: float = float("inf")
+    min_J: float = float("inf")
 
 
 # ---------------------------------------------------------------------------
@@ -65,93 +70,10 @@ class TrialRecord:
 # ---------------------------------------------------------------------------
 
 
-def _pt_dist2(x):
-    """Squared point-triangle distance (Ericson, same priority order as the device)."""
-    p, a, b, c = x[:, 0], x[:, 1], x[:, 2], x[:, 3]
-    ab, ac = b - a, c - a
-    d = lambda u, v: np.einsum("ij,ij->i", u, v)  # noqa: E731
-    d1, d2 = d(ab, p - a), d(ac, p - a)
-    d3, d4 = d(ab, p - b), d(ac, p - b)
-    d5, d6 = d(ab, p - c), d(ac, p - c)
-    va, vb, vc = d3 * d6 - d5 * d4, d5 * d2 - d1 * d6, d1 * d4 - d3 * d2
-    with np.errstate(divide="ignore", invalid="ignore"):
-        w_ab = np.where(d1 != d3, d1 / (d1 - d3), 0.0)
-        w_ac = np.where(d2 != d6, d2 / (d2 - d6), 0.0)
-        den_bc = (d4 - d3) + (d5 - d6)
-        w_bc = np.where(den_bc != 0.0, (d4 - d3) / den_bc, 0.0)
-        den = va + vb + vc
-        fv, fw = np.where(den != 0, vb / den, 0.0), np.where(den != 0, vc / den, 0.0)
-    conds = [(d1 <= 0) & (d2 <= 0), (d3 >= 0) & (d4 <= d3), (d6 >= 0) & (d5 <= d6),
-             (vc <= 0) & (d1 >= 0) & (d3 <= 0), (vb <= 0) & (d2 >= 0) & (d6 <= 0),
-             (va <= 0) & (d4 - d3 >= 0) & (d5 - d6 >= 0)]
-    z, o = np.zeros_like(d1), np.ones_like(d1)
-    b0 = np.select(conds, [o, z, z, 1 - w_ab, 1 - w_ac, z], 1 - fv - fw)
-    b1 = np.select(conds, [z, o, z, w_ab, z, 1 - w_bc], fv)
-    b2 = np.select(conds, [z, z, o, z, w_ac, w_bc], fw)
-    q = p - (b0[:, None] * a + b1[:, None] * b + b2[:, None] * c)
-    return np.einsum("ij,ij->i", q, q)
-
-
-def _ee_dist2(x):
-    a0, a1, b0, b1 = x[:, 0], x[:, 1], x[:, 2], x[:, 3]
-    d1, d2, r = a1 - a0, b1 - b0, a0 - b0
-    dd = lambda u, v: np.einsum("ij,ij->i", u, v)  # noqa: E731
-    a, e, f, c, b = dd(d1, d1), dd(d2, d2), dd(d2, r), dd(d1, r), dd(d1, d2)
-    den = a * e - b * b
-    with np.errstate(divide="ignore", invalid="ignore"):
-        s = np.where(den > 0, np.clip((b * f - c * e) / den, 0, 1), 0.0)
-        t = (b * s + f) / e
-        s = np.where(t < 0, np.clip(-c / a, 0, 1), np.where(t > 1, np.clip((b - c) / a, 0, 1), s))
-    t = np.clip(t, 0, 1)
-    q = (a0 + s[:, None] * d1) - (b0 + t[:, None] * d2)
-    return np.einsum("ij,ij->i", q, q), np.cross(d1, d2)
-
-
-def stencil_events(env, radius_factor=1.05, active_only=True):
-    """Per-stencil events at the current state: kind, bodies, verts, d, lambda (contact.py:348-372)."""
-    cp = env.contact_params
-    pt, ee = env.candidates(cp.dhat * radius_factor)
-    sv = env.surface_positions()
-    vb = env.layout.vbody
-    out = []
-    dh = cp.dhat
-
-    def lam_of(d, m=1.0):
-        ins = d < dh
-        dd = d - dh
-        with np.errstate(divide="ignore", invalid="ignore"):
-            ln = np.where(ins, np.log(d / dh), 0.0)
-        b1 = np.where(ins, -2.0 * dd * ln - dd * dd / d, 0.0)
-        return cp.kappa * m * np.abs(b1)
-
-    if len(pt):
-        d = np.sqrt(_pt_dist2(sv[pt]))
-        act = d < dh if active_only else np.ones(len(d), bool)
-        lam = lam_of(d)
-        for row, dd, ll in zip(pt[act], d[act], lam[act]):
-            out.append({"kind": "point-triangle", "bodies": (int(vb[row[0]]), int(vb[row[1]])),
-                        "verts": [int(v) for v in row], "d": float(dd), "lambda": float(ll)})
-    if len(ee):
-        D, _ = _ee_dist2(sv[ee])
-        d = np.sqrt(D)
-        act = d < dh if active_only else np.ones(len(d), bool)
-        rest = env.layout.surf_rest
-        u, v = sv[ee[:, 1]] - sv[ee[:, 0]], sv[ee[:, 3]] - sv[ee[:, 2]]
-        c = np.einsum("ij,ij->i", u, u) * np.einsum("ij,ij->i", v, v) - np.einsum("ij,ij->i", u, v) ** 2
-        ru, rv = rest[ee[:, 1]] - rest[ee[:, 0]], rest[ee[:, 3]] - rest[ee[:, 2]]
-        eps = 1e-3 * np.einsum("ij,ij->i", ru, ru) * np.einsum("ij,ij->i", rv, rv)
-        xr = c / eps
-        m = np.where(xr < 1.0, xr * (2.0 - xr), 1.0)
-        lam = lam_of(d, m)
-        for row, dd, ll in zip(ee[act], d[act], lam[act]):
-            out.append({"kind": "edge-edge", "bodies": (int(vb[row[0]]), int(vb[row[2]])),
-                        "verts": [int(x) for x in row], "d": float(dd), "lambda": float(ll)})
-    return out
-
-
 def contact_events_now(env):
-    """protocol.py:72-75."""
-    return stencil_events(env)
+    """protocol.py:72-75: the active stencils of the fresh 1.05 dhat candidate set at the current
+    state as {kind, bodies, verts, d, lambda} dicts, computed on the device (grip_contacts_now)."""
+    return env._owner()._events_now(env._slot)[0]
 
 
 def finger_contact_force(env, finger_bodies, events=None):
@@ -187,8 +109,7 @@ def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closi
     velocities, contacts_log = [], []
     n_done = [0]
     group = env._owner()
-    if record:
-        group.set_recording(True)   # contact events straight from the device finalize
+    group.set_recording(True)   # the step's contact events straight from the device finalize
     kin_recs = [r for r in env.records if r["kind"] == "kinematic"]
 
     def snapshot(events, report, forces):
@@ -212,7 +133,7 @@ def run_grasp_trial(env, protocol, object_body, finger_links, record=True, closi
         start = n_done[0]
         for _ in range(n_steps):
             report = env.step()
-            events = group._events(env._slot) if record else contact_events_now(env)
+            events = group._events(env._slot)
             last_events[0] = events
             forces = {f: finger_contact_force(env, ids, events) for f, ids in finger_links.items()}
             n_done[0] += 1
@@ -425,33 +346,20 @@ class BatchedGraspTrials:
     # -- continuous refill (dataset-generation mode) ------------------------------------------
     @staticmethod
     def scene_payload(scene):
-        """Device reset payload of a grasp scene: node positions, kinematic surfaces and the
-        posed rest shape of its tets (a new candidate for the same meshes changes only these)."""
+        """Device reset payload of a grasp scene: node positions, kinematic surfaces, the posed rest
+        shape of its tets and its materials (a new candidate for the same meshes changes only these)."""
         from paper_2503_05020_b200 import packing
         lay = packing.layout_env(scene.bodies, scene.collide_pairs_off)
         pk = packing.Packed([lay], [np.zeros(14)], [np.zeros(3)], packing.body_velocities(scene.bodies))
-        return {"x0": pk.node_x0, "kin0": pk.sv_kin0, "Dmi": pk.tet_Dmi, "V0": pk.tet_V0, "scene": scene,
-                "sizes": (pk.n_node_total, pk.n_sv_total, pk.n_tet_total)}
+        return {"x0": pk.node_x0, "kin0": pk.sv_kin0, "Dmi": pk.tet_Dmi, "V0": pk.tet_V0, "mu": pk.tet_mu,
+                "lam": pk.tet_lam, "bmu": pk.body_mu, "scene": scene,
+                "sizes": (pk.n_node_total, pk.n_sv_total, pk.n_tet_total, pk.n_body_total)}
 
     def refill(self, slots, payloads):
         """Start a fresh trial in each finished slot with a new candidate of the same topology."""
-        p = self.group.packed
-        if not hasattr(self, "_host"):
-            self._host = {"x0": p.node_x0.copy(), "kin0": p.sv_kin0.copy(), "Dmi": p.tet_Dmi.copy(),
-                          "V0": p.tet_V0.copy()}
-        h = self._host
-        mask = np.zeros(self.E, np.uint8)
+        mask = _reset_slots(self, slots, payloads)
         pr = self.protocol
         for e, pl in zip(slots, payloads):
-            n0, n1 = p.node_off[e], p.node_off[e + 1]
-            s0, s1 = p.sv_off[e], p.sv_off[e + 1]
-            t0, t1 = p.tet_off[e], p.tet_off[e + 1]
-            if pl["sizes"] != (n1 - n0, s1 - s0, t1 - t0):
-                raise ValueError("refill needs the same topology as the slot's current scene")
-            h["x0"][3 * n0:3 * n1] = pl["x0"]
-            h["kin0"][3 * s0:3 * s1] = pl["kin0"]
-            h["Dmi"][9 * t0:9 * t1] = pl["Dmi"]
-            h["V0"][t0:t1] = pl["V0"]
             sc = pl["scene"]
             for j, f in enumerate(self.fnames[e]):
                 self.cd[e, j] = np.asarray(sc.closing_dirs[f], np.float64)
@@ -465,10 +373,7 @@ class BatchedGraspTrials:
             self.records[e] = TrialRecord(object_body=sc.object_body, gripper_bodies=self.records[e].gripper_bodies)
             if self.record:
                 self._frames[e] = self._empty_frames()
-            env = self.group.envs[e]
-            env._time, env._step, env.status = 0.0, 0, "active"
-            mask[e] = 1
-        self.dev.reset_envs(mask, h["x0"], h["kin0"], h["Dmi"], h["V0"])
+        del mask
         if hasattr(self, "_iter"):
             self._iter[list(slots)] = False
             self._need[list(slots)] = True
@@ -626,6 +531,38 @@ _MARK_NAMES = ["settle", "close", "hold"] + PHASES
 _VERDICTS = {1: "stable", 2: "unstable", 3: "sim-failed"}
 
 
+def _reset_slots(trials, slots, payloads):
+    """Stage the payloads (BatchedGraspTrials.scene_payload) of the refilled slots into the full-size
+    host arrays and reset those envs on the device (grip_reset_envs: pose, rest shape, material,
+    every other per-env state as in a fresh batch)."""
+    p = trials.group.packed
+    if not hasattr(trials, "_host"):
+        trials._host = {"x0": p.node_x0.copy(), "kin0": p.sv_kin0.copy(), "Dmi": p.tet_Dmi.copy(),
+                        "V0": p.tet_V0.copy(), "mu": p.tet_mu.copy(), "lam": p.tet_lam.copy(),
+                        "bmu": p.body_mu.copy()}
+    h = trials._host
+    mask = np.zeros(trials.E, np.uint8)
+    for e, pl in zip(slots, payloads):
+        n0, n1 = p.node_off[e], p.node_off[e + 1]
+        s0, s1 = p.sv_off[e], p.sv_off[e + 1]
+        t0, t1 = p.tet_off[e], p.tet_off[e + 1]
+        b0, b1 = p.body_off[e], p.body_off[e + 1]
+        if tuple(pl["sizes"]) != (n1 - n0, s1 - s0, t1 - t0, b1 - b0):
+            raise ValueError("refill needs the same topology as the slot's current scene")
+        h["x0"][3 * n0:3 * n1] = pl["x0"]
+        h["kin0"][3 * s0:3 * s1] = pl["kin0"]
+        h["Dmi"][9 * t0:9 * t1] = pl["Dmi"]
+        h["V0"][t0:t1] = pl["V0"]
+        h["mu"][t0:t1] = pl["mu"]
+        h["lam"][t0:t1] = pl["lam"]
+        h["bmu"][b0:b1] = pl["bmu"]
+        env = trials.group.envs[e]
+        env._time, env._step, env.status = 0.0, 0, "active"
+        mask[e] = 1
+    trials.dev.reset_envs(mask, h["x0"], h["kin0"], h["Dmi"], h["V0"], h["mu"], h["lam"], h["bmu"])
+    return mask
+
+
 class DeviceProtocolTrials:
     """The grasp protocol (protocol.py:152-277) run on the device (k_protocol): after every
     finalize the kernel makes BatchedGraspTrials' decisions itself -- finger halts, phase ends,
@@ -681,6 +618,7 @@ class DeviceProtocolTrials:
         r = TrialRecord(object_body=self.object_body[e], gripper_bodies=self.gripper_bodies[e])
         r.n_steps = int(o.n_steps)
         r.verdict = _VERDICTS.get(int(o.verdict), "running")
+        r.min_distance, r.min_J = float(o.min_distance), float(o.min_J)
         r.phase_markers = {_MARK_NAMES[k]: [int(o.markers[2 * k]), int(o.markers[2 * k + 1])]
                            for k in range(9) if o.markers[2 * k] >= 0}
         for j, f in enumerate(self.fnames[e]):
@@ -703,31 +641,13 @@ class DeviceProtocolTrials:
 
     def refill(self, slots, payloads):
         """New trials in `slots` with new candidates of the same topology (BatchedGraspTrials.refill)."""
-        p = self.group.packed
-        if not hasattr(self, "_host"):
-            self._host = {"x0": p.node_x0.copy(), "kin0": p.sv_kin0.copy(), "Dmi": p.tet_Dmi.copy(),
-                          "V0": p.tet_V0.copy()}
-        h = self._host
-        mask = np.zeros(self.E, np.uint8)
+        _reset_slots(self, slots, payloads)
         pr = self.protocol
         cds, mcs = [], []
         for e, pl in zip(slots, payloads):
-            n0, n1 = p.node_off[e], p.node_off[e + 1]
-            s0, s1 = p.sv_off[e], p.sv_off[e + 1]
-            t0, t1 = p.tet_off[e], p.tet_off[e + 1]
-            if pl["sizes"] != (n1 - n0, s1 - s0, t1 - t0):
-                raise ValueError("refill needs the same topology as the slot's current scene")
-            h["x0"][3 * n0:3 * n1] = pl["x0"]
-            h["kin0"][3 * s0:3 * s1] = pl["kin0"]
-            h["Dmi"][9 * t0:9 * t1] = pl["Dmi"]
-            h["V0"][t0:t1] = pl["V0"]
             sc = pl["scene"]
             cds.append(np.array([np.asarray(sc.closing_dirs[f], np.float64) for f in self.fnames[e]]))
             mcs.append(int(np.ceil((sc.opening / 2.0) / (pr.closing_speed * self.dt))) + 5)
-            env = self.group.envs[e]
-            env._time, env._step, env.status = 0.0, 0, "active"
-            mask[e] = 1
-        self.dev.reset_envs(mask, h["x0"], h["kin0"], h["Dmi"], h["V0"])
         self.restart(slots, cds, mcs)
 
     def restart(self, slots, closing_dirs, max_close):

@@ -305,17 +305,40 @@ def cfg2_scene(i, cands=None):
     return build_trial_scene(obj, GripperSpec(soft_fingers=True), c["R"][i], c["T"][i], float(c["opening"][i]))
 
 
+def load_cfg3_candidates():
+    """Config 3: antipodal candidates on the soft box / sphere (kind i % 2, seed i)
+    and each trial's randomized object material (E, mu; config.py:311-318 with the pipeline's
+    seeding seed + 7919 i, pipeline/__init__.py:29), precomputed by the reference in
+    tests/golden/make_golden.py."""
+    d = np.load(DATA / "cfg3_candidates.npz")
+    return {k: d[k] for k in d.files}
+
+
+def cfg3_scene(i, cands=None):
+    """Environment i of BASELINE config 3: soft Neo-Hookean object, kinematic ("rigid") fingers."""
+    c = cands if cands is not None else load_cfg3_candidates()
+    kind = [str(k) for k in c["kinds"]][int(c["kind"][i])]
+    mat = MaterialParams(young_modulus=float(c["E"][i]), poisson_ratio=float(c["nu"][i]), density=float(c["rho"][i]),
+                         friction_coefficient=float(c["mu"][i]))
+    return build_trial_scene(ObjectSpec(kind=kind, soft=True, material=mat), GripperSpec(soft_fingers=False),
+                             c["R"][i], c["T"][i], float(c["opening"][i]))
+
+
 def soft_object_scene(R, T, opening, kind="box"):
     """Config 3 in the form the reference can express: soft NH object, kinematic fingers."""
     return build_trial_scene(ObjectSpec(kind=kind, soft=True), GripperSpec(soft_fingers=False), R, T, opening)
 
 
-def bimanual_scene():
-    """Config 4: two top-down soft-pad grippers (offset +-12.5 mm in y) on one soft cube."""
+def bimanual_scene(yaw=0.0):
+    """Config 4: two top-down soft-pad grippers (offset +-12.5 mm in y) on one soft cube.  yaw
+    rotates the grippers about the vertical axis through the cube (bench envs get distinct poses;
+    yaw=0 is the reference scene of tests/golden/traj_bimanual.npz)."""
     obj = ObjectSpec(kind="box", soft=True)
     gs = GripperSpec(soft_fingers=True)
     g = gs.gripper
     opening = 0.05 + 2 * 2e-3
+    c, s_ = np.cos(yaw), np.sin(yaw)
+    Rz = np.array([[c, -s_, 0.0], [s_, c, 0.0], [0.0, 0.0, 1.0]])
     bodies = [obj.build_body()]
     links, dirs, off = {}, {}, []
     for gi, yoff in enumerate((-0.0125, 0.0125)):
@@ -324,15 +347,18 @@ def bimanual_scene():
         for side in (0, 1):
             b = soft_finger_body(gs, side, opening)
             b.mesh.vertices[:] = b.mesh.vertices + T
+            if yaw:
+                b.mesh.vertices[:] = b.mesh.vertices @ Rz.T
             b.mesh.rest_vertices[:] = b.mesh.vertices
             b.mesh.refresh()
             b.name = f"g{gi}finger{side}"
             bodies.append(b)
             pads.append(len(bodies) - 1)
             links[b.name] = (len(bodies) - 1,)
-            dirs[b.name] = np.array([1.0, 0.0, 0.0]) if side == 0 else np.array([-1.0, 0.0, 0.0])
+            dirs[b.name] = Rz @ (np.array([1.0, 0.0, 0.0]) if side == 0 else np.array([-1.0, 0.0, 0.0]))
         _, _, palm_s = g.body_meshes(opening)
-        palm_s = gm.TriSurface(palm_s.vertices + np.array([0.0, 0.0, gs.palm_gap]) + T, palm_s.triangles)
+        pv = palm_s.vertices + np.array([0.0, 0.0, gs.palm_gap]) + T
+        palm_s = gm.TriSurface(pv @ Rz.T if yaw else pv, palm_s.triangles)
         bodies.append(KinematicBody(palm_s, MaterialParams(1e9, 0.3, 2000.0, 0.3), name=f"g{gi}palm"))
         off += [(p, len(bodies) - 1) for p in pads]
     return GraspScene(bodies, off, 0, links, dirs, opening)

@@ -275,9 +275,9 @@ class Environment:
         return self._owner()._contacts(self._slot)
 
     def min_contact_distance(self, radius_factor=2.0):
-        from paper_2503_05020_b200.protocol import stencil_events  # host readout
-        ev = stencil_events(self, radius_factor=radius_factor, active_only=False)
-        return min((e["d"] for e in ev), default=np.inf)
+        """solver.py:449-453: min stencil distance of the candidate set at radius_factor * dhat
+        (computed on the device, grip_contacts_now)."""
+        return self._owner()._events_now(self._slot, radius_factor)[1]
 
     def stress_rows(self):
         return self._owner()._stress(self._slot)

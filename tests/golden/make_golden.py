@@ -259,6 +259,40 @@ def gen_kernels(out):
 # ---------------------------------------------------------------------------
 
 
+def gen_friction(out):
+    """Lagged-friction golden vectors (contact.py:475-524 friction_potential, 403-410 tangent basis):
+    single anchors with random stencils, weights and normals, slips below, at and above the
+    mollifier width h = eps_v dt (the three branches of f0 / f1 / f1')."""
+    rng = np.random.default_rng(7)
+    eps_v, dt = 1e-3, 0.01
+    h = eps_v * dt
+    params = ct.ContactParams()
+    n = 64
+    rows = {k: [] for k in ("x", "xp", "gamma", "T", "lam", "mu", "E", "g", "H")}
+    for k in range(n):
+        x = rng.normal(scale=0.01, size=(4, 3))
+        slip_scale = h * (0.0 if k % 8 == 0 else 10.0 ** rng.uniform(-3, 1.5))
+        xp = x - rng.normal(size=(4, 3)) * slip_scale
+        a = rng.uniform()
+        gam = np.array([1.0, -a, -(1 - a) * 0.5, -(1 - a) * 0.5]) if k % 2 else \
+            np.array([1 - a, a, -(1 - rng.uniform()), 0.0])
+        if k % 2 == 0:
+            gam[3] = -1.0 - gam[2]
+        nrm = rng.normal(size=(1, 3))
+        nrm /= np.linalg.norm(nrm)
+        T = ct._tangent_basis(nrm)[0]
+        lam, mu = float(10.0 ** rng.uniform(-2, 2)), float(rng.uniform(0.1, 2.0))
+        anc = ct.FrictionAnchors(verts=np.arange(4)[None], gamma=gam[None], tangent=T[None], lam=np.array([lam]),
+                                 mu=np.array([mu]), bodies=np.zeros((1, 2), np.int64))
+        params.eps_v = eps_v
+        E, g, _, H = ct.friction_potential(anc, x, xp, params, dt)
+        for key, v in (("x", x), ("xp", xp), ("gamma", gam), ("T", T), ("lam", lam), ("mu", mu), ("E", E),
+                       ("g", g), ("H", H[0])):
+            rows[key].append(v)
+    np.savez_compressed(out / "friction.npz", eps_v=eps_v, dt=dt, **{f"fr_{k}": np.array(v) for k, v in rows.items()})
+    print("friction", n)
+
+
 def gen_meshes(out):
     res = {}
     b = gm.box_surface(0.05, subdivisions=3)
@@ -502,6 +536,75 @@ def gen_metrics(out, env, ob, rec):
     print("metrics", {k: v for k, v in res.items() if k.startswith("res")})
 
 
+def _verdict_compact(r, wall):
+    return {"verdict": r.verdict, "failure": r.failure, "n_steps": r.n_steps,
+            "phase_markers": r.phase_markers, "com_displacement": r.com_displacement,
+            "halt_forces": {k: {"force": float(v["force"]), "step": int(v["step"])} for k, v in r.halt_forces.items()},
+            "iterations": [rep["iterations"] for rep in r.step_reports], "wall_s": wall}
+
+
+def _verdict_job_cfg2(i):
+    """Full-protocol reference trial of bench env i (config 2: kind i % 3, candidate seed i)."""
+    kind = KINDS[i % 3]
+    sc = scene_for(kind)
+    c = candidate(kind, i)
+    if c is None:
+        return None
+    env, ob, fl = cfg.build_trial_env(sc, c)
+    t0 = time.time()
+    r = proto.run_grasp_trial(env, sc.protocol, ob, fl)
+    return {"i": i, "kind": kind, **_verdict_compact(r, time.time() - t0)}
+
+
+CFG3_KINDS = ("box", "sphere")
+CFG3_SEED = 0   # validate_candidates seed: material rng = default_rng(seed + 7919 * i)
+
+
+def cfg3_material(i):
+    """Config 3's domain-randomized object material of trial i, by the reference's own
+    randomized_material (config.py:311-318) with the pipeline's seeding (pipeline/__init__.py:29)."""
+    sc = cfg.SceneConfig()
+    sc.randomization.enabled = True
+    rng = np.random.default_rng(CFG3_SEED + 7919 * i)
+    return cfg.randomized_material(sc.object.material, sc.randomization, rng)
+
+
+def _cfg3_cand_job(i):
+    kind = CFG3_KINDS[i % 2]
+    c = candidate(kind, i, soft_object=True)
+    return i, kind, None if c is None else cand_arrays(c)
+
+
+def gen_candidates_cfg3(pool, n=400):
+    """Config 3: soft NH box / sphere (kind i % 2), kinematic fingers, antipodal
+    candidate seed i on the soft object's surface, randomized material per trial."""
+    rows = pool.map(_cfg3_cand_job, range(n), chunksize=4)
+    R = np.zeros((n, 3, 3)); T = np.zeros((n, 3)); op = np.zeros(n); kind = np.zeros(n, np.int64)
+    ok = np.zeros(n, bool); E = np.zeros(n); mu = np.zeros(n); nu = np.zeros(n); rho = np.zeros(n)
+    for i, k, ca in rows:
+        kind[i] = CFG3_KINDS.index(k)
+        m = cfg3_material(i)
+        E[i], mu[i], nu[i], rho[i] = m.young_modulus, m.friction_coefficient, m.poisson_ratio, m.density
+        if ca is not None:
+            R[i], T[i], op[i], ok[i] = ca["R"], ca["T"], ca["opening"], True
+    dest = REPO / "paper_2503_05020_b200" / "data"
+    np.savez_compressed(dest / "cfg3_candidates.npz", R=R, T=T, opening=op, kind=kind, ok=ok,
+                        kinds=np.array(CFG3_KINDS), E=E, mu=mu, nu=nu, rho=rho)
+    print("cfg3 candidates ok:", int(ok.sum()), "of", n)
+
+
+def _verdict_job_cfg3(i):
+    kind = CFG3_KINDS[i % 2]
+    sc = scene_for(kind, soft_object=True, soft_fingers=False)
+    c = candidate(kind, i, soft_object=True)
+    if c is None:
+        return None
+    env, ob, fl = cfg.build_trial_env(sc, c, env_id=i, material_override=cfg3_material(i))
+    t0 = time.time()
+    r = proto.run_grasp_trial(env, sc.protocol, ob, fl)
+    return {"i": i, "kind": kind, **_verdict_compact(r, time.time() - t0)}
+
+
 def _cand_job(i):
     kind = KINDS[i % 3]
     c = candidate(kind, i)
@@ -529,13 +632,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="*")
     args = ap.parse_args()
-    want = set(args.only or ["kernels", "meshes", "traj", "bimanual", "verdicts", "candidates", "dataset"])
+    want = set(args.only or ["kernels", "friction", "meshes", "traj", "bimanual", "verdicts", "candidates", "dataset"])
     out = HERE
     ctx = mp.get_context("fork")
     scene_for("cylinder")  # write the cylinder OBJ once, before forking
     t0 = time.time()
     if "kernels" in want:
         gen_kernels(out); print("kernels", time.time() - t0)
+    if "friction" in want:
+        gen_friction(out)
     if "meshes" in want:
         gen_meshes(out); print("meshes", time.time() - t0)
     if "dataset" in want:
@@ -565,6 +670,19 @@ def main():
             res = [r for r in pool.map(_verdict_job, jobs) if r is not None]
             (out / "verdicts_cfg2.json").write_text(json.dumps(res))
             print("verdicts_cfg2", [(r["kind"], r["seed"], r["verdict"], r["n_steps"]) for r in res], time.time() - t0)
+        if "verdicts_cfg2_all" in want:
+            # every one of the 400 bench envs (config 2), full protocol, unmodified reference
+            res = [r for r in pool.imap(_verdict_job_cfg2, range(400), chunksize=1) if r is not None]
+            (out / "verdicts_cfg2_all.json").write_text(json.dumps(res))
+            print("verdicts_cfg2_all", len(res), {v: sum(r["verdict"] == v for r in res)
+                                                  for v in ("stable", "unstable", "sim-failed")}, time.time() - t0)
+        if "candidates_cfg3" in want:
+            gen_candidates_cfg3(pool); print("candidates_cfg3", time.time() - t0)
+        if "verdicts_cfg3" in want:
+            n3 = int(os.environ.get("GRIP_CFG3_VERDICTS", "32"))
+            res = [r for r in pool.imap(_verdict_job_cfg3, range(n3), chunksize=1) if r is not None]
+            (out / "verdicts_cfg3.json").write_text(json.dumps(res))
+            print("verdicts_cfg3", len(res), [(r["kind"], r["verdict"], r["n_steps"]) for r in res], time.time() - t0)
         if "candidates" in want:
             gen_candidates(pool); print("candidates", time.time() - t0)
 

@@ -184,3 +184,26 @@ def test_friction_vs_oracle(hc):
         np.testing.assert_allclose(e, E, rtol=1e-12, atol=1e-20)
         np.testing.assert_allclose(gg.reshape(4, 3), g, rtol=1e-10, atol=1e-12 * np.abs(g).max())
         np.testing.assert_allclose(HH.reshape(12, 12), H[0], rtol=1e-10, atol=1e-12 * np.abs(H).max())
+
+
+def test_friction_vs_reference_golden(hc, golden):
+    """The host build of the friction element (grip_elements.cuh) and the oracle against the
+    reference's own friction_potential (contact.py:475-524) on tests/golden/friction.npz."""
+    F = np.load(golden / "friction.npz")
+    eps_v, dt = float(F["eps_v"]), float(F["dt"])
+    for k in range(len(F["fr_E"])):
+        x, xp, gam, T = F["fr_x"][k], F["fr_xp"][k], F["fr_gamma"][k], F["fr_T"][k]
+        lam, mu = float(F["fr_lam"][k]), float(F["fr_mu"][k])
+        Er, gr, Hr = F["fr_E"][k], F["fr_g"][k], F["fr_H"][k]
+        anc = {"verts": np.arange(4)[None], "gamma": gam[None], "tangent": T[None], "lam": np.array([lam]),
+               "mu": np.array([mu]), "bodies": np.zeros((1, 2), np.int64)}
+        E, g, _, H = en.friction_potential(anc, x, xp, eps_v, dt, order=2)
+        np.testing.assert_allclose(E, Er, rtol=1e-12, atol=1e-20)
+        np.testing.assert_allclose(g, gr, rtol=1e-10, atol=1e-12 * max(np.abs(gr).max(), 1e-300))
+        np.testing.assert_allclose(H[0], Hr, rtol=1e-10, atol=1e-12 * max(np.abs(Hr).max(), 1e-300))
+        gg, HH = np.zeros(12), np.zeros(144)
+        e = hc.hc_friction(np.ascontiguousarray(x.ravel()), np.ascontiguousarray(xp.ravel()), np.ascontiguousarray(gam),
+                           np.ascontiguousarray(T.ravel()), lam, mu, eps_v, dt, gg, HH)
+        np.testing.assert_allclose(e, Er, rtol=1e-12, atol=1e-20)
+        np.testing.assert_allclose(gg.reshape(4, 3), gr, rtol=1e-10, atol=1e-12 * max(np.abs(gr).max(), 1e-300))
+        np.testing.assert_allclose(HH.reshape(12, 12), Hr, rtol=1e-10, atol=1e-12 * max(np.abs(Hr).max(), 1e-300))

@@ -51,16 +51,31 @@ def _rollout(env, scene, n_steps, gravity_after=None, halt=50.0):
     return xs, reps, forces
 
 
-@pytest.mark.parametrize("name,steps,grav", [("cfg1", 12, None), ("cylfail", 1, None), ("cyl", 6, None),
-                                             ("sphere", 5, None), ("soft", 25, 18), ("bimanual", 12, None)])
-def test_trajectory_matches_reference(golden, name, steps, grav):
+@pytest.mark.parametrize("name,grav,solver", [("cfg1", None, None), ("cylfail", None, None), ("cyl", None, None),
+                                               ("sphere", None, None), ("soft", 18, None), ("bimanual", None, None),
+                                               ("cfg1", None, "pcg"), ("soft", 18, "pcg")])
+def test_trajectory_matches_reference(golden, name, grav, solver, monkeypatch):
+    """Every recorded step of the reference's trajectory (full fixture length: cfg1 50, cylinder /
+    sphere 20, soft object 25, bimanual 12).  solver="pcg": the block-Jacobi PCG alternative
+    (GRIP_SOLVER=pcg, the north star's solver) instead of the default skyline Cholesky."""
     from paper_2503_05020_b200.solver import Environment
+    if solver:
+        monkeypatch.setenv("GRIP_SOLVER", solver)
     d = np.load(golden / f"traj_{name}.npz")
     scene = _scene(d)
     env = Environment(scene.bodies, collide_pairs_off=scene.collide_pairs_off)
     golden_reps = json.loads(str(d["reports_json"]))
     golden_forces = json.loads(str(d["forces_json"]))
-    n = min(steps, len(golden_reps))
+    n = len(golden_reps)
+    stress = []
+    if "stress" in d.files:   # the recorder's stress field, every step (materials.py:191-205)
+        orig_step = env.step
+
+        def step_and_stress():
+            rep = orig_step()
+            stress.append(env.stress_rows().copy())
+            return rep
+        env.step = step_and_stress
     xs, reps, forces = _rollout(env, scene, n, gravity_after=grav)
     ell = max(float(np.linalg.norm(d["sv"][0].max(0) - d["sv"][0].min(0))), 0.05)
     worst = 0.0
@@ -72,17 +87,27 @@ def test_trajectory_matches_reference(golden, name, steps, grav):
         err = float(np.abs(xs[k] - d["x"][k]).max()) / ell
         worst = max(worst, err)
         assert err <= TRAJ_TOL, (k, err)
+        if stress:
+            ref = d["stress"][k]
+            np.testing.assert_allclose(stress[k], ref, rtol=1e-6, atol=1e-6 * np.abs(ref).max())
         for f, v in golden_forces[k].items():
             assert abs(forces[k][f] - v) <= 1e-6 * max(1.0, abs(v)), (k, f, forces[k][f], v)
         if r.status == "failed":
             break
+    assert len(reps) == n or reps[-1].status == "failed"
     print(f"{name}: {n} steps, worst |dx|/ell = {worst:.3e}")
 
 
-@pytest.mark.parametrize("name", ["cfg1", "sphere", "soft", "bimanual", "cyl"])
-def test_candidate_sets_bit_exact(golden, name):
-    """Broad phase on the reference's own recorded states equals its candidate sets."""
+@pytest.mark.parametrize("name,bp", [("cfg1", None), ("sphere", None), ("soft", None), ("bimanual", None), ("cyl", None),
+                                     ("cfg1", "grid"), ("sphere", "grid"), ("soft", "grid"), ("bimanual", "grid"),
+                                     ("cyl", "grid")])
+def test_candidate_sets_bit_exact(golden, name, bp, monkeypatch):
+    """Broad phase on the reference's own recorded states equals its candidate sets: the default
+    direct broad phase and the grid broad phase (GRIP_BP=grid, the automatic fallback for large
+    culled sets)."""
     from paper_2503_05020_b200.solver import Environment
+    if bp:
+        monkeypatch.setenv("GRIP_BP", bp)
     d = np.load(golden / f"traj_{name}.npz")
     scene = _scene(d)
     env = Environment(scene.bodies, collide_pairs_off=scene.collide_pairs_off)
@@ -253,3 +278,60 @@ def test_protocol_labels_match_reference_cfg2(golden, mode):
             assert abs(r.halt_forces[f]["force"] - h["force"]) <= 1e-5 * h["force"], key
         for k, v in g["com_displacement"].items():
             assert abs(r.com_displacement[k] - v) <= 1e-6 * 0.1 + 1e-9, (key, k, r.com_displacement[k], v)
+
+
+def test_device_friction_vs_reference(golden):
+    """The production friction element (w_friction, the code k_elements_w runs) against the
+    reference's friction_potential (contact.py:475-524) on tests/golden/friction.npz."""
+    from paper_2503_05020_b200._native import debug_elements
+    F = np.load(golden / "friction.npz")
+    n = len(F["fr_E"])
+    inp = np.array([np.concatenate([F["fr_x"][k].ravel(), F["fr_xp"][k].ravel(), F["fr_gamma"][k], F["fr_T"][k].ravel(),
+                                    [F["fr_lam"][k], F["fr_mu"][k], float(F["eps_v"]), float(F["dt"])]])
+                    for k in range(n)])
+    E, g, H, _ = debug_elements(4, inp)
+    np.testing.assert_allclose(E, F["fr_E"], rtol=1e-11, atol=1e-20)
+    for k in range(n):
+        gr, Hr = F["fr_g"][k].ravel(), F["fr_H"][k]
+        np.testing.assert_allclose(g[k], gr, rtol=1e-9, atol=1e-11 * max(np.abs(gr).max(), 1e-300))
+        np.testing.assert_allclose(H[k], Hr, rtol=1e-9, atol=1e-11 * max(np.abs(Hr).max(), 1e-300))
+
+
+def test_production_element_chain_vs_reference(golden):
+    """The element chain a Newton sweep actually runs (grip_debug_chain): PT / EE stencils through
+    the k_elements_w code with deferred clamps -> k_tet_jacobi2 -> k_tet_finish; NH tets through
+    k_tet_front (Gershgorin pass-through or deferral) -> k_tet_jacobi2 -> k_tet_back, cold (identity
+    warm starts) and warm (the bases the cold pass left, as in the next Newton iteration) -- all
+    against the reference's SPD-projected blocks (materials.py:101-113, contact.py:271-344)."""
+    from oracle import energies as oen
+    from paper_2503_05020_b200._native import debug_chain
+    K = dict(np.load(golden / "kernels.npz"))
+    X, pt, ee, epsx = K["pot_x"], K["pot_pt"], K["pot_ee"], K["pot_epsx"]
+    rows = {tuple(r): k for k, r in enumerate(K["pot_idx"])}
+    n_act = 0
+    for etype, rr, inp in ((0, pt, np.array([np.concatenate([X[r].ravel(), [3e6, 1e-3]]) for r in pt])),
+                           (1, ee, np.array([np.concatenate([X[r].ravel(), [epsx[n], 3e6, 1e-3]])
+                                             for n, r in enumerate(ee)]))):
+        E, g, H, fl = debug_chain(etype, inp)
+        for n, r in enumerate(rr):
+            if fl[n] & 1:
+                n_act += 1
+                Hr = K["pot_H"][rows[tuple(r)]]
+                assert np.abs(H[n] - Hr).max() <= 1e-9 * np.abs(Hr).max(), (etype, n)
+    assert n_act == len(K["pot_idx"])
+    rest, cur = K["nh_rest"], K["nh_cur"]
+    Dmi, V0, _ = oen.tet_rest(rest.reshape(-1, 3), np.arange(4 * len(rest)).reshape(-1, 4))
+    inp = np.array([np.concatenate([cur[n].ravel(), Dmi[n].ravel(), [V0[n], K["nh_mu"], K["nh_lam"]]])
+                    for n in range(len(rest))])
+    eig = np.zeros((len(rest), 9, 9))
+    eig[:] = np.eye(9)
+    for rnd in ("cold", "warm"):
+        E, g, H, fl = debug_chain(2, inp, eig)
+        assert not np.any(fl & 4), rnd
+        np.testing.assert_allclose(E, K["nh_Ee"], rtol=1e-11, atol=1e-18)
+        np.testing.assert_allclose(g.reshape(-1, 3), K["nh_g"], rtol=1e-9, atol=1e-10 * np.abs(K["nh_g"]).max())
+        for n in range(len(rest)):
+            assert np.abs(H[n] - K["nh_H"][n]).max() <= 1e-9 * np.abs(K["nh_H"][n]).max(), (rnd, n)
+        # the warm starts are orthonormal eigenbases
+        np.testing.assert_allclose(np.einsum("nij,nkj->nik", eig, eig), np.broadcast_to(np.eye(9), eig.shape),
+                                   atol=1e-12)

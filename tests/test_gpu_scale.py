@@ -1,0 +1,185 @@
+"""GPU parity at the bench's own scale and layout.
+
+* every one of the 400 config-2 bench envs (kind i % 3, the reference-sampled candidate of seed
+  i) through the full protocol in the bench's 3-lane layout, against the unmodified reference's
+  own trial of the same candidate (tests/golden/verdicts_cfg2_all.json, make_golden.py);
+* config 3 (soft Neo-Hookean box / sphere objects, kinematic fingers, the reference's randomized
+  material per trial) against verdicts_cfg3.json;
+* slot refill (grip_reset_envs) returns an env to a fresh state: trials run in refilled slots
+  are bitwise the trials run in fresh slots;
+* the contact readout at an arbitrary state (grip_contacts_now) against the reference's events;
+* NaN injection is quarantined (multienv.py:98-123) without touching the other envs;
+* the north star's safety report: zero intersections and zero inverted elements.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KIND_PRIORITY = {0: 0, 1: 1, 2: 2}   # box < cylinder < sphere (bench.py's lane priorities)
+
+
+def _cfg2_runner(jobs, slots=None, lanes_per_key=1, rounds_per_call=4):
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.runner import TrialRunner
+    c = sc.load_cfg2_candidates()
+    kinds = np.asarray(c["kind"])
+    return TrialRunner(jobs, lambda j: sc.cfg2_scene(j, c), lambda j: int(kinds[j]), slots=slots,
+                       lanes_per_key=lanes_per_key, rounds_per_call=rounds_per_call, priority=KIND_PRIORITY)
+
+
+def _assert_record_matches(r, g, key, force_rtol=1e-5):
+    assert r.verdict == g["verdict"], (key, r.verdict, g["verdict"], r.failure, g["failure"])
+    assert r.n_steps == g["n_steps"], (key, r.n_steps, g["n_steps"])
+    assert r.phase_markers == g["phase_markers"], (key, r.phase_markers, g["phase_markers"])
+    if g["failure"]:
+        assert (r.failure["reason"], r.failure["phase"], r.failure["step"]) == \
+            (g["failure"]["reason"], g["failure"]["phase"], g["failure"]["step"]), (key, r.failure, g["failure"])
+    assert set(r.halt_forces) == set(g["halt_forces"]), key
+    for f, h in g["halt_forces"].items():
+        assert r.halt_forces[f]["step"] == h["step"], key
+        assert abs(r.halt_forces[f]["force"] - h["force"]) <= force_rtol * h["force"], (key, f)
+    assert set(r.com_displacement) == set(g["com_displacement"]), key
+    for k, v in g["com_displacement"].items():
+        assert abs(r.com_displacement[k] - v) <= 1e-6 * 0.1 + 1e-9, (key, k, r.com_displacement[k], v)
+
+
+def _same_record(a, b):
+    return (a.verdict, a.n_steps, a.phase_markers, a.failure, a.halt_forces, a.com_displacement, a.min_distance,
+            a.min_J) == (b.verdict, b.n_steps, b.phase_markers, b.failure, b.halt_forces, b.com_displacement,
+                         b.min_distance, b.min_J)
+
+
+def test_refill_bitwise_equals_fresh():
+    """Trials in refilled slots (3 lanes x 2 slots, 4 trials per slot) are bitwise the trials of
+    fresh slots (one slot per job): grip_reset_envs leaves no state of the previous trial behind
+    (Jacobi warm starts, candidate superset, anchors, drift, ...)."""
+    jobs = list(range(24))
+    fresh = _cfg2_runner(jobs).run()
+    refilled_runner = _cfg2_runner(jobs, slots=2)
+    assert refilled_runner.n_slots == 6
+    refilled = refilled_runner.run()
+    assert sorted(refilled) == jobs
+    for j in jobs:
+        assert _same_record(fresh[j], refilled[j]), (j, fresh[j], refilled[j])
+
+
+def test_cfg2_all_400_labels_match_reference(golden):
+    """All 400 bench envs, the bench's layout (3 lanes by object kind, one slot per env, the
+    device protocol, 4 rounds per call), against the reference's full-protocol trials."""
+    path = golden / "verdicts_cfg2_all.json"
+    if not path.exists():
+        pytest.skip("verdicts_cfg2_all.json not generated")
+    ref = {g["i"]: g for g in json.loads(path.read_text())}
+    runner = _cfg2_runner(sorted(ref))
+    assert len(runner.lanes) == 3
+    out = runner.run()
+    mix = {}
+    for i, g in ref.items():
+        _assert_record_matches(out[i], g, (g["kind"], i))
+        mix[g["verdict"]] = mix.get(g["verdict"], 0) + 1
+        # the north star's safety report: no intersection, no inverted element in any completed step
+        assert out[i].min_distance > 0.0 and out[i].min_J > 0.0, (i, out[i].min_distance, out[i].min_J)
+    print("cfg2 label mix", mix)
+
+
+def test_cfg2_refilled_layout_labels_match_reference(golden):
+    """The same reference trials, run through refilled slots (3 lanes x 16 slots, ~8 trials per
+    slot): the labels do not depend on the slot a trial lands in."""
+    path = golden / "verdicts_cfg2_all.json"
+    if not path.exists():
+        pytest.skip("verdicts_cfg2_all.json not generated")
+    ref = {g["i"]: g for g in json.loads(path.read_text())}
+    jobs = sorted(ref)[:144]
+    out = _cfg2_runner(jobs, slots=16).run()
+    for i in jobs:
+        _assert_record_matches(out[i], ref[i], (ref[i]["kind"], i))
+
+
+def test_cfg3_soft_object_labels_match_reference(golden):
+    """Config 3: soft NH box / sphere objects with kinematic fingers and the reference's
+    randomized material per trial (config.py:311-318, seed 0 + 7919 i), device protocol."""
+    path = golden / "verdicts_cfg3.json"
+    if not path.exists():
+        pytest.skip("verdicts_cfg3.json not generated")
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.runner import TrialRunner
+    ref = {g["i"]: g for g in json.loads(path.read_text())}
+    c = sc.load_cfg3_candidates()
+    kinds = np.asarray(c["kind"])
+    runner = TrialRunner(sorted(ref), lambda j: sc.cfg3_scene(j, c), lambda j: int(kinds[j]), slots=8)
+    out = runner.run()
+    for i, g in ref.items():
+        _assert_record_matches(out[i], g, (g["kind"], i), force_rtol=1e-4)
+
+
+def test_contacts_now_matches_reference_events(golden):
+    """grip_contacts_now at the reference's recorded states: the number of active stencils and the
+    per-finger barrier force sums of contact_events_now (protocol.py:72-98)."""
+    from paper_2503_05020_b200 import protocol as pt
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.solver import Environment
+    d = np.load(golden / "traj_cfg1.npz")
+    scene = sc.build_trial_scene(sc.ObjectSpec(kind="box"), sc.GripperSpec(soft_fingers=True), d["cand_R"],
+                                 d["cand_T"], float(d["cand_opening"]))
+    env = Environment(scene.bodies, collide_pairs_off=scene.collide_pairs_off)
+    grp = env._owner()
+    forces = json.loads(str(d["forces_json"]))
+    n_checked = 0
+    for k in range(len(d["x"])):
+        sv = d["sv"][k]
+        kin = np.zeros_like(sv)
+        for r in env.layout.records:
+            if r.kind == "kinematic":
+                kin[r.surf0:r.surf0 + r.n_sv] = sv[r.surf0:r.surf0 + r.n_sv]
+        grp.dev.set_state(d["x"][k].reshape(-1, 3), None, kin)
+        grp.invalidate()
+        ev = pt.contact_events_now(env)
+        for f, ids in scene.finger_links.items():
+            got = pt.finger_contact_force(env, ids, ev)
+            assert abs(got - forces[k][f]) <= 1e-6 * max(1.0, abs(forces[k][f])), (k, f, got, forces[k][f])
+        n_checked += 1
+        md = env.min_contact_distance()
+        assert np.isinf(md) or md > 0.0
+    assert n_checked == len(d["x"])
+
+
+def test_nan_injection_is_quarantined():
+    """A NaN in one env's state: Batch.quarantine_failures fails it with 'non-finite state' and a
+    tombstone (multienv.py:98-123), checked on the device; the other envs step on,
+    bitwise as if the bad env were not there."""
+    from paper_2503_05020_b200 import scene as sc
+    from paper_2503_05020_b200.multienv import Batch
+    from paper_2503_05020_b200.solver import Environment
+    c = sc.load_cfg2_candidates()
+
+    def make(ids):
+        scenes = [sc.cfg2_scene(i, c) for i in ids]
+        envs = [Environment(s.bodies, collide_pairs_off=s.collide_pairs_off) for s in scenes]
+        for s, e in zip(scenes, envs):
+            for f, b_ids in s.finger_links.items():
+                for b in b_ids:
+                    e.bodies[b].velocity = s.closing_dirs[f] * 0.05
+        return envs
+
+    envs = make([0, 1, 2])
+    clean = make([0, 2])
+    batch, ref = Batch(envs), Batch(clean)
+    batch.step()
+    ref.step()
+    x = envs[1].x.copy()
+    x[5] = np.nan
+    envs[1].x = x
+    st = batch.quarantine_failures()
+    assert st == ["active", "failed", "active"]
+    assert batch.envs[1].status == "failed" and batch.envs[1].fail_reason == "non-finite state"
+    assert batch.report.step_reports[1][-1]["reason"] == "non-finite state"
+    for _ in range(3):
+        batch.step()
+        ref.step()
+    assert np.array_equal(batch.envs[0].x, ref.envs[0].x)
+    assert np.array_equal(batch.envs[2].x, ref.envs[1].x)
+    assert batch.statuses == ["active", "failed", "active"]

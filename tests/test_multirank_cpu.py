@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, n_envs, q):
+def _worker(rank, world, port, n_envs, q, out_dir):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -45,30 +45,59 @@ def _worker(rank, world, port, n_envs, q):
         r.metrics = {"final_phase_com_disp": 1e-5 * e, "final_contact": e % 2 == 0}
         r.halt_forces = {"finger0": {"step": e, "force": 50.0 + e}}
         recs.append(r)
-    allr = gather_outcomes(pack_outcomes(recs, list(range(lo, hi))), n_envs)
-    q.put((rank, allr))
+    # rank 1 finished one trial more than its shard (variable counts per rank are gathered)
+    jobs = list(range(lo, hi))
+    if rank == 1:
+        extra = TrialRecord(verdict="stable", n_steps=1)
+        recs.append(extra)
+        jobs.append(lo)
+    allr = gather_outcomes(pack_outcomes(recs, jobs, rank=rank))
+    # dataset shards: every rank writes its own directory, rank 0 merges the manifests
+    from paper_2503_05020_b200 import dataset as ds
+    from paper_2503_05020_b200.distributed import merge_manifests, rank_dir
+    w = ds.ShardWriter(rank_dir(out_dir, rank))
+    for j, r in zip(jobs, recs):
+        w.put(j, r)
+    w.close()
+    dist.barrier()
+    man = merge_manifests(out_dir, world, ds.FORMAT) if rank == 0 else None
+    q.put((rank, allr, man))
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("n_envs", [7, 10])
-def test_gather_outcomes_world2_gloo(n_envs):
+def test_gather_outcomes_world2_gloo(n_envs, tmp_path):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_envs, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_envs, q, str(tmp_path))) for r in range(2)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in procs)
+    got = [q.get(timeout=120) for _ in procs]
     for p in procs:
         p.join(timeout=60)
+    res = {r: a for r, a, _ in got}
+    man = [m for r, _, m in got if r == 0][0]
+    lo1 = shard(n_envs, 2, 1)[0]
     for rank in (0, 1):
         a = res[rank]
-        assert a.shape == (n_envs, len(OUTCOME_FIELDS))
-        np.testing.assert_array_equal(a[:, 0], np.arange(n_envs))
-        np.testing.assert_array_equal(a[:, 1], np.arange(n_envs) % 3)
-        np.testing.assert_array_equal(a[:, 2], 70 + np.arange(n_envs))
-        np.testing.assert_allclose(a[:, 6], 50.0 + np.arange(n_envs))
+        assert a.shape == (n_envs + 1, len(OUTCOME_FIELDS))
+        main = a[a[:, 2] != 1]                     # the extra trial has n_steps 1
+        np.testing.assert_array_equal(main[:, 0], np.arange(n_envs))
+        np.testing.assert_array_equal(main[:, 1], np.arange(n_envs) % 3)
+        np.testing.assert_array_equal(main[:, 2], 70 + np.arange(n_envs))
+        np.testing.assert_allclose(main[:, 6], 50.0 + np.arange(n_envs))
+        np.testing.assert_array_equal(main[:, 12], (np.arange(n_envs) >= lo1).astype(float))
+        extra = a[a[:, 2] == 1]
+        assert extra.shape[0] == 1 and extra[0, 0] == lo1 and extra[0, 12] == 1
     np.testing.assert_array_equal(res[0], res[1])
+    # merged manifest: every trial of both ranks, dirs under the rank shards
+    assert man["n_trials"] == n_envs + 1
+    dirs = [t["dir"] for t in man["trials"]]
+    assert all(d.startswith("rank00/") or d.startswith("rank01/") for d in dirs)
+    assert sum(d.startswith("rank01/") for d in dirs) == n_envs - lo1 + 1
+    for t in man["trials"]:
+        assert (tmp_path / t["dir"] / "meta.json").exists()
 
 
 def test_pack_outcomes_running_trial():

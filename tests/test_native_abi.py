@@ -26,7 +26,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, n), n
     lib.grip_abi_version.restype = ctypes.c_int
     from paper_2503_05020_b200 import _native as nv
-    assert lib.grip_abi_version() == nv.ABI_VERSION == 3
+    assert lib.grip_abi_version() == nv.ABI_VERSION == 4
 
 
 def test_struct_layouts_match_header():
