@@ -190,31 +190,32 @@ class ClockSampler:
 
 
 def workload(cfg):
-    """(candidate pool size, scene_of(job), key_of(job), lane priority per key)."""
+    """(valid candidate ids, scene_of(job), key_of(job), lane priority per key)."""
     from paper_2503_05020_b200 import scene as sc
     if cfg == 2:
         c = sc.load_cfg2_candidates()
         kinds = np.asarray(c["kind"])
-        return len(kinds), (lambda j: sc.cfg2_scene(j, c)), (lambda j: int(kinds[j])), {0: 0, 1: 1, 2: 2}
+        return (list(np.nonzero(c["ok"])[0]), (lambda j: sc.cfg2_scene(j, c)), (lambda j: int(kinds[j])),
+                {0: 0, 1: 1, 2: 2})
     if cfg == 3:
         c = sc.load_cfg3_candidates()
         kinds = np.asarray(c["kind"])
-        return len(kinds), (lambda j: sc.cfg3_scene(j, c)), (lambda j: int(kinds[j])), {0: 0, 1: 1}
+        return list(np.nonzero(c["ok"])[0]), (lambda j: sc.cfg3_scene(j, c)), (lambda j: int(kinds[j])), {0: 0, 1: 1}
     if cfg == 4:
-        return 1 << 30, (lambda j: sc.bimanual_scene(yaw=2.0 * np.pi * ((j * 0.6180339887498949) % 1.0))), \
+        return list(range(1 << 16)), (lambda j: sc.bimanual_scene(yaw=2.0 * np.pi * ((j * 0.6180339887498949) % 1.0))), \
             (lambda j: 0), {0: 0}
     raise ValueError(f"unknown config {cfg}")
 
 
 def rank_jobs(pool, envs, world, rank, global_envs=None):
-    """Jobs (candidate ids) of this rank.  Weak scaling: `envs` per rank, rank r takes candidates
-    [r*envs, (r+1)*envs) of the pool (distinct across ranks while the pool lasts).  Strong
-    scaling (global_envs): the contiguous shard of range(global_envs)."""
+    """Jobs (candidate ids) of this rank.  Weak scaling: `envs` per rank, rank r takes the pool's
+    candidates [r*envs, (r+1)*envs) (distinct across ranks while the pool lasts).  Strong
+    scaling (global_envs): the contiguous shard of the first global_envs candidates."""
     from paper_2503_05020_b200.distributed import shard
     if global_envs:
         lo, hi = shard(global_envs, world, rank)
-        return [j % pool for j in range(lo, hi)]
-    return [(rank * envs + i) % pool for i in range(envs)]
+        return [int(pool[j % len(pool)]) for j in range(lo, hi)]
+    return [int(pool[(rank * envs + i) % len(pool)]) for i in range(envs)]
 
 
 # ---------------------------------------------------------------------------
@@ -451,7 +452,7 @@ def build_runner(args, cfg, envs, rank, world, writer=None):
     runner = TrialRunner(jobs, scene_of, key_of, slots=None, lanes_per_key=args.lanes_per_kind,
                          rounds_per_call=args.rounds_per_call, priority=prio if args.lane_priority else None,
                          cycle=True, device=None, mode=mode, record=record, on_record=on_record)
-    distinct = len(set(jobs)) == len(jobs) and (args.global_envs or (world * envs <= pool))
+    distinct = len(set(jobs)) == len(jobs) and bool(args.global_envs or (world * envs <= len(pool)))
     return runner, jobs, mode, bool(distinct)
 
 
@@ -540,6 +541,26 @@ def kernel_report(runner, env_steps_s, ms_max, peak):
     return roof, ks, env_iters
 
 
+def gather_timed(timed, rank, world, dist, record_dir, reasons, device=None):
+    """The path's one collective: every rank's finished trials (job, TrialRecord) as fixed-size
+    outcome rows, all-gathered once at the end (NCCL on the GPU box, gloo in the CPU test);
+    with recording, rank 0 then merges the rank-local dataset shard manifests."""
+    from paper_2503_05020_b200.distributed import gather_outcomes, merge_manifests, pack_outcomes
+    tg = time.perf_counter()
+    allr = gather_outcomes(pack_outcomes([r for _, r in timed], [j for j, _ in timed], rank=rank, reasons=reasons),
+                           device=device)
+    out = {"trials": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg),
+           "backend": dist.get_backend() if dist is not None else None,
+           "ranks": sorted({int(x) for x in allr[:, 12]}) if len(allr) else [],
+           "verdicts": {v: int((allr[:, 1] == k).sum()) for k, v in enumerate(("stable", "unstable", "sim-failed"))}}
+    if record_dir is not None and dist is not None:
+        dist.barrier()
+        if rank == 0:
+            from paper_2503_05020_b200 import dataset as ds
+            out["merged_trials"] = merge_manifests(record_dir, world, ds.FORMAT)["n_trials"]
+    return out
+
+
 def run_gpu(args, rank, world, local, cfg, envs, dist=None, quiet=False):
     import torch
     from paper_2503_05020_b200._native import REASONS
@@ -626,19 +647,9 @@ def run_gpu(args, rank, world, local, cfg, envs, dist=None, quiet=False):
         line["recording"] = {"dir": str(args.record), "rank_trials": man["n_trials"],
                              "format": "gripsim-dataset-v1 (traj.bin, stress.bin, jsonl, meta), per-rank shards"}
     if dist is not None:
-        # the path's one collective: every finished trial's fixed-size outcome record
-        from paper_2503_05020_b200.distributed import gather_outcomes, merge_manifests, pack_outcomes
-        tg = time.perf_counter()
-        allr = gather_outcomes(pack_outcomes([r for _, r in timed], [j for j, _ in timed], rank=rank,
-                                             reasons=REASONS), device="cuda")
-        line["outcome_gather"] = {"trials": int(len(allr)), "ms": 1e3 * (time.perf_counter() - tg), "backend": "nccl",
-                                  "ranks": sorted({int(x) for x in allr[:, 12]}) if len(allr) else []}
-        if writer is not None:
-            dist.barrier()
-            if rank == 0:
-                from paper_2503_05020_b200 import dataset as ds
-                m = merge_manifests(args.record, world, ds.FORMAT)
-                line["recording"]["merged_trials"] = m["n_trials"]
+        line["outcome_gather"] = gather_timed(timed, rank, world, dist, args.record, REASONS, device="cuda")
+        if line["recording"] is not None and "merged_trials" in line["outcome_gather"]:
+            line["recording"]["merged_trials"] = line["outcome_gather"].pop("merged_trials")
     return line, jobs
 
 

@@ -251,18 +251,17 @@ int grip_set_profiling(GripBatch* b, int on);
 int grip_kernel_stats(GripBatch* b, int kernel, double* ms, int64_t* launches, double* units);
 /* CUDA events on the library stream: start=1 marks, start=0 returns ms since the mark */
 int grip_stream_timer(GripBatch* b, int start, double* ms);
-/* Re-initialise the envs with mask[e]=1 to a new pose of the SAME topology (a new grasp
- * candidate for the same object / gripper meshes; the slot refill of run_batch_trials,
- * multienv.py:204-216, done in place): positions, kinematic surfaces and the posed rest shape
- * (Dm^-1, V0) of their tets, optionally a new material (tet_mu / tet_lam per tet, body_mu per
- * body: config 3's randomized_material, config.py:311-318; all three or none).  Every other
- * piece of per-env state returns to what grip_create starts from (v, anchors, time, step index,
- * Jacobi warm starts, candidate superset, ...), so a refilled env is bitwise a fresh one.
- * Full-size host arrays (GripSceneDesc layout); only the masked envs' slices are read; they
- * are staged through one pinned buffer and scattered by one kernel. */
-int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
-                    const double* tet_Dmi, const double* tet_V0, const double* tet_mu, const double* tet_lam,
-                    const double* body_mu);
+/* Re-initialise the envs with mask[e]=1 to a new scene of the SAME topology (a new grasp
+ * candidate for the same object / gripper meshes, possibly a new material: the slot refill of
+ * run_batch_trials, multienv.py:204-216, done in place).  desc describes a full batch of the same
+ * n_env and offsets; the masked envs' slices of every pose- or material-dependent array are read
+ * from it (node_x0, node_M, sv_kin0, sv_xi, tet_Dmi, tet_V0, tet_mu, tet_lam, body_mu,
+ * edge_rest_sq, abd_kV, env_cell_hint -- posed rest shapes differ from the previous candidate's in
+ * the last bits), staged through one pinned buffer and scattered by one kernel.  Every other piece
+ * of per-env state returns to what grip_create starts from (v, anchors, time, step index, Jacobi
+ * warm starts, candidate superset, ...), so a refilled env is bitwise a fresh one.  An env whose
+ * offsets differ is an error (nothing is reset). */
+int grip_reset_envs(GripBatch* b, const uint8_t* mask, const GripSceneDesc* desc);
 /* Evaluate n standalone elements with the device element kernels (test / parity hook).
  * type 0 PT  in[x(12), kappa, dhat]; 1 EE in[x(12), eps_x, kappa, dhat];
  * 2 NH in[x(12), Dm^-1(9), V0, mu, lambda]; 3 ABD in[A(9), kappa*V];

@@ -94,7 +94,7 @@ def load():
         ("grip_round", [vp, vp, vp, vp, vp, vp]),
         ("grip_debug_elements", [i32, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_debug_chain", [i32, i32, vp, i32, vp, vp, vp, vp, vp]),
-        ("grip_reset_envs", [vp, vp, vp, vp, vp, vp, vp, vp, vp]), ("grip_set_recording", [vp, i32]),
+        ("grip_reset_envs", [vp, vp, ctypes.POINTER(GripSceneDesc)]), ("grip_set_recording", [vp, i32]),
         ("grip_get_events", [vp, vp, vp, vp, vp, ctypes.c_int64]),
         ("grip_sdf_exact", [vp, ctypes.c_int64, vp, i32, vp, i32, vp, vp, vp, vp]),
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
@@ -289,13 +289,28 @@ class DeviceBatch:
         check(self.lib.grip_round(self.h, ptr(b), ptr(it), ptr(fin), rep.ctypes.data_as(ctypes.c_void_p), ptr(alphas)))
         return fin.astype(bool), rep, alphas
 
-    def reset_envs(self, mask, node_x0, sv_kin0, tet_Dmi, tet_V0, tet_mu=None, tet_lam=None, body_mu=None):
-        """Slot refill (grip_reset_envs): new pose / rest shape (and optionally material) of the
-        masked envs, every other per-env state back to a fresh batch's."""
-        f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)  # noqa: E731
+    # per-env arrays a slot refill replaces (everything pose- or material-dependent; the topology
+    # arrays and offsets must stay): (name, values per entity, offset array)
+    RESET_FIELDS = (("node_x0", 3, "node_off"), ("node_M", 9, "node_off"), ("sv_kin0", 3, "sv_off"),
+                    ("sv_xi", 3, "sv_off"), ("tet_Dmi", 9, "tet_off"), ("tet_V0", 1, "tet_off"),
+                    ("tet_mu", 1, "tet_off"), ("tet_lam", 1, "tet_off"), ("body_mu", 1, "body_off"),
+                    ("edge_rest_sq", 1, "edge_off"), ("abd_kV", 1, "abd_off"))
+
+    def reset_envs(self, mask, packed):
+        """Slot refill (grip_reset_envs): the masked envs take their pose, rest shape and materials
+        from `packed` (a full-size Packed of the same topology), every other per-env state returns
+        to a fresh batch's."""
         m = np.ascontiguousarray(mask, np.uint8)
-        arrs = [f(node_x0), f(sv_kin0), f(tet_Dmi), f(tet_V0), f(tet_mu), f(tet_lam), f(body_mu)]
-        check(self.lib.grip_reset_envs(self.h, ptr(m), *[ptr(a) for a in arrs]))
+        desc = GripSceneDesc()
+        desc.abi_version = ABI_VERSION
+        desc.n_env = packed.n_env
+        keep = []
+        for name, _ in GripSceneDesc._fields_[2:]:
+            arr = np.ascontiguousarray(getattr(packed, name))
+            keep.append(arr)
+            setattr(desc, name, arr.ctypes.data)
+        check(self.lib.grip_reset_envs(self.h, ptr(m), ctypes.byref(desc)))
+        del keep
 
     def begin_step(self, active):
         act = np.ascontiguousarray(active, np.uint8)

@@ -36,6 +36,8 @@ enum {
 // PD_MIND / PD_MINJ: min stencil distance / min element J = det F (tets) or det A (affine bodies)
 // over the trial's completed steps (the north star's intersection / inversion report)
 enum { PINIT_D = 6, PINIT_I = 6 };   // k_protocol_init staging per env: closing dirs | ints
+// k_reset_envs staged doubles per node (x0, M), surface vertex (kin0, xi), tet (Dmi, V0, mu, lam)
+enum { RESET_PER_NODE = 12, RESET_PER_SV = 6, RESET_PER_TET = 12 };   // k_protocol_init staging per env: closing dirs | ints
 enum { PD_CD = 0, PD_COM0 = 6, PD_HF = 9, PD_CDISP = 11, PD_FDISP = 17, PD_THR = 18, PD_MIND = 19, PD_MINJ = 20, PD_N = 21 };
 
 struct Dev {

@@ -1351,13 +1351,10 @@ int grip_get_events(GripBatch* b, const uint8_t* mask, int32_t* counts, int32_t*
   return 0;
 }
 
-int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, const double* sv_kin0,
-                    const double* tet_Dmi, const double* tet_V0, const double* tet_mu, const double* tet_lam,
-                    const double* body_mu) {
+int grip_reset_envs(GripBatch* b, const uint8_t* mask, const GripSceneDesc* d) {
   b->snap_valid = false;
-  const int with_mat = (tet_mu && tet_lam && body_mu) ? 1 : 0;
-  if (!with_mat && (tet_mu || tet_lam || body_mu)) {
-    g_err = "grip_reset_envs: tet_mu, tet_lam and body_mu go together";
+  if (!d || d->abi_version != GRIP_ABI_VERSION || d->n_env != b->n_env) {
+    g_err = "grip_reset_envs: scene description missing or of another batch size / ABI";
     return -1;
   }
   // stage the masked envs' slices in one pinned buffer -> one H2D copy -> k_reset_envs scatters them
@@ -1366,11 +1363,21 @@ int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, co
   long long n = 0;
   for (int e = 0; e < b->n_env; ++e) {
     if (!mask[e]) continue;
+    auto same = [&](const int32_t* o, const std::vector<int>& mine) {
+      return o[e] == mine[e] && o[e + 1] == mine[e + 1];
+    };
+    if (!same(d->node_off, b->node_off) || !same(d->sv_off, b->sv_off) || !same(d->tri_off, b->tri_off) ||
+        !same(d->edge_off, b->edge_off) || !same(d->tet_off, b->tet_off) || !same(d->abd_off, b->abd_off) ||
+        !same(d->body_off, b->body_off)) {
+      g_err = "grip_reset_envs: env " + std::to_string(e) + " changes topology (a refill keeps the slot's meshes)";
+      return -1;
+    }
     const long long nn = b->node_off[e + 1] - b->node_off[e], ns = b->sv_off[e + 1] - b->sv_off[e];
     const long long nt = b->tet_off[e + 1] - b->tet_off[e], nb = b->body_off[e + 1] - b->body_off[e];
+    const long long ne = b->edge_off[e + 1] - b->edge_off[e], na = b->abd_off[e + 1] - b->abd_off[e];
     L.push_back(e);
     off.push_back(n);
-    n += 3 * nn + 3 * ns + 10 * nt + (with_mat ? 2 * nt + nb : 0);
+    n += RESET_PER_NODE * nn + RESET_PER_SV * ns + RESET_PER_TET * nt + nb + ne + na + 1;
   }
   if (L.empty()) return 0;
   const size_t head = L.size() * (sizeof(int) + sizeof(long long));
@@ -1402,21 +1409,26 @@ int grip_reset_envs(GripBatch* b, const uint8_t* mask, const double* node_x0, co
     const size_t s0 = b->sv_off[e], ns = b->sv_off[e + 1] - s0;
     const size_t t0 = b->tet_off[e], nt = b->tet_off[e + 1] - t0;
     const size_t b0 = b->body_off[e], nb = b->body_off[e + 1] - b0;
-    put(node_x0, 3 * n0, 3 * nn);
-    put(sv_kin0, 3 * s0, 3 * ns);
-    put(tet_Dmi, 9 * t0, 9 * nt);
-    put(tet_V0, t0, nt);
-    if (with_mat) {
-      put(tet_mu, t0, nt);
-      put(tet_lam, t0, nt);
-      put(body_mu, b0, nb);
-    }
+    const size_t e0 = b->edge_off[e], ne = b->edge_off[e + 1] - e0;
+    const size_t a0 = b->abd_off[e], na = b->abd_off[e + 1] - a0;
+    put(d->node_x0, 3 * n0, 3 * nn);
+    put(d->node_M, 9 * n0, 9 * nn);
+    put(d->sv_kin0, 3 * s0, 3 * ns);
+    put(d->sv_xi, 3 * s0, 3 * ns);
+    put(d->tet_Dmi, 9 * t0, 9 * nt);
+    put(d->tet_V0, t0, nt);
+    put(d->tet_mu, t0, nt);
+    put(d->tet_lam, t0, nt);
+    put(d->body_mu, b0, nb);
+    put(d->edge_rest_sq, e0, ne);
+    put(d->abd_kV, a0, na);
+    put(d->env_cell_hint, e, 1);
   }
   CK(cudaMemcpyAsync(b->d_reset, b->h_reset, bytes, cudaMemcpyHostToDevice, b->stream));
-  const char* d = b->d_reset;
+  const char* dd = b->d_reset;
   k_reset_envs<<<(int)L.size(), NT, 0, b->stream>>>(
-      b->D, reinterpret_cast<const int*>(d + L.size() * sizeof(long long)), reinterpret_cast<const long long*>(d),
-      reinterpret_cast<const double*>(d + ((head + 15) & ~(size_t)15)), with_mat);
+      b->D, reinterpret_cast<const int*>(dd + L.size() * sizeof(long long)), reinterpret_cast<const long long*>(dd),
+      reinterpret_cast<const double*>(dd + ((head + 15) & ~(size_t)15)));
   b->launches++;
   CK(cudaGetLastError());
   return 0;

@@ -1637,45 +1637,45 @@ __global__ void k_frames(Dev D, const int* m, double* fx, double* fv, double* fk
   }
 }
 
-// Slot refill (grip_reset_envs): CTA per refilled env.  The env gets the new candidate's pose and
-// rest shape from the staged slice and EVERY piece of per-env state a fresh grip_create starts
-// from (zeros, identity Jacobi warm starts), so a refilled trial is bitwise a fresh trial.
-// Staged slice per env (doubles): x0 (3 nn) | kin0 (3 ns) | Dmi (9 nt) | V0 (nt) [| mu (nt) | lam (nt)]
-// [| body mu (nb)], the bracketed parts when with_mat.
-__global__ void k_reset_envs(Dev D, const int* lst, const long long* off, const double* stage, int with_mat) {
+// Slot refill (grip_reset_envs): CTA per refilled env.  The env gets the new candidate's pose,
+// rest shape and materials from the staged slice and EVERY piece of per-env state a fresh
+// grip_create starts from (zeros, identity Jacobi warm starts), so a refilled trial is bitwise a
+// fresh trial.  Staged slice per env (doubles): x0 (3 nn) | M (9 nn) | kin0 (3 ns) | xi (3 ns) |
+// Dmi (9 nt) | V0 | mu | lam (nt each) | body mu (nb) | edge rest len^2 (ne) | kappa V (na) | cell hint
+// (pose-dependent rounding: lumped masses and rest lengths of posed pads differ in the last bits)
+__global__ void k_reset_envs(Dev D, const int* lst, const long long* off, const double* stage) {
   const int e = lst[blockIdx.x];
   const double* s = stage + off[blockIdx.x];
   const int n0 = D.node_off[e], nn = D.node_off[e + 1] - n0;
   const int s0 = D.sv_off[e], ns = D.sv_off[e + 1] - s0;
   const int t0 = D.tet_off[e], nt = D.tet_off[e + 1] - t0;
   const int b0 = D.body_off[e], nb = D.body_off[e + 1] - b0;
-  double* Dmi = const_cast<double*>(D.tet_Dmi);
-  double* V0 = const_cast<double*>(D.tet_V0);
-  double* tet_mu = const_cast<double*>(D.tet_mu);
-  double* tet_lam = const_cast<double*>(D.tet_lam);
-  double* body_mu = const_cast<double*>(D.body_mu);
+  const int e0 = D.edge_off[e], ne = D.edge_off[e + 1] - e0;
+  const int a0 = D.abd_off[e], na = D.abd_off[e + 1] - a0;
+  auto put = [&](const double* dst_c, size_t first, int cnt) {
+    double* dst = const_cast<double*>(dst_c) + first;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = s[i];
+    s += cnt;
+  };
+  put(D.x, 3 * (size_t)n0, 3 * nn);
+  put(D.node_M, 9 * (size_t)n0, 9 * nn);
+  put(D.kin_pos, 3 * (size_t)s0, 3 * ns);
+  put(D.sv_xi, 3 * (size_t)s0, 3 * ns);
+  put(D.tet_Dmi, 9 * (size_t)t0, 9 * nt);
+  put(D.tet_V0, t0, nt);
+  put(D.tet_mu, t0, nt);
+  put(D.tet_lam, t0, nt);
+  put(D.body_mu, b0, nb);
+  put(D.edge_rest_sq, e0, ne);
+  put(D.abd_kV, a0, na);
+  put(D.cell_hint, e, 1);
   for (int i = threadIdx.x; i < 3 * nn; i += blockDim.x) {
     const size_t g = 3 * (size_t)n0 + i;
-    D.x[g] = s[i];
     D.v[g] = D.x_t[g] = D.xhat[g] = D.pdir[g] = 0.0;
   }
-  s += 3 * nn;
   for (int i = threadIdx.x; i < 3 * ns; i += blockDim.x) {
     const size_t g = 3 * (size_t)s0 + i;
-    D.kin_pos[g] = s[i];
     D.sv_pos[g] = D.surf_prev[g] = D.sv_disp[g] = 0.0;
-  }
-  s += 3 * ns;
-  for (int i = threadIdx.x; i < 9 * nt; i += blockDim.x) Dmi[9 * (size_t)t0 + i] = s[i];
-  s += 9 * nt;
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) V0[t0 + i] = s[i];
-  s += nt;
-  if (with_mat) {
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) tet_mu[t0 + i] = s[i];
-    s += nt;
-    for (int i = threadIdx.x; i < nt; i += blockDim.x) tet_lam[t0 + i] = s[i];
-    s += nt;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) body_mu[b0 + i] = s[i];
   }
   for (int i = threadIdx.x; i < 81 * nt; i += blockDim.x)   // Jacobi warm start: identity
     D.tet_eig[81 * (size_t)t0 + i] = (i % 81) % 10 == 0 ? 1.0 : 0.0;

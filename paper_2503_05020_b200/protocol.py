@@ -346,14 +346,12 @@ class BatchedGraspTrials:
     # -- continuous refill (dataset-generation mode) ------------------------------------------
     @staticmethod
     def scene_payload(scene):
-        """Device reset payload of a grasp scene: node positions, kinematic surfaces, the posed rest
-        shape of its tets and its materials (a new candidate for the same meshes changes only these)."""
+        """Device reset payload of a grasp scene: its one-env Packed arrays (a new candidate for the
+        same meshes changes only the pose- / material-dependent ones, grip_reset_envs)."""
         from paper_2503_05020_b200 import packing
         lay = packing.layout_env(scene.bodies, scene.collide_pairs_off)
         pk = packing.Packed([lay], [np.zeros(14)], [np.zeros(3)], packing.body_velocities(scene.bodies))
-        return {"x0": pk.node_x0, "kin0": pk.sv_kin0, "Dmi": pk.tet_Dmi, "V0": pk.tet_V0, "mu": pk.tet_mu,
-                "lam": pk.tet_lam, "bmu": pk.body_mu, "scene": scene,
-                "sizes": (pk.n_node_total, pk.n_sv_total, pk.n_tet_total, pk.n_body_total)}
+        return {"packed": pk, "scene": scene}
 
     def refill(self, slots, payloads):
         """Start a fresh trial in each finished slot with a new candidate of the same topology."""
@@ -532,34 +530,34 @@ _VERDICTS = {1: "stable", 2: "unstable", 3: "sim-failed"}
 
 
 def _reset_slots(trials, slots, payloads):
-    """Stage the payloads (BatchedGraspTrials.scene_payload) of the refilled slots into the full-size
-    host arrays and reset those envs on the device (grip_reset_envs: pose, rest shape, material,
-    every other per-env state as in a fresh batch)."""
+    """Write the payloads (BatchedGraspTrials.scene_payload: a one-env Packed) of the refilled slots
+    into a full-size host copy of the batch's scene arrays and reset those envs on the device
+    (grip_reset_envs: pose, rest shape, masses, rest lengths, materials; every other per-env state
+    as in a fresh batch)."""
+    import copy
+
+    from paper_2503_05020_b200._native import DeviceBatch
     p = trials.group.packed
     if not hasattr(trials, "_host"):
-        trials._host = {"x0": p.node_x0.copy(), "kin0": p.sv_kin0.copy(), "Dmi": p.tet_Dmi.copy(),
-                        "V0": p.tet_V0.copy(), "mu": p.tet_mu.copy(), "lam": p.tet_lam.copy(),
-                        "bmu": p.body_mu.copy()}
+        trials._host = copy.copy(p)
+        for name, _, _ in DeviceBatch.RESET_FIELDS:
+            setattr(trials._host, name, np.array(getattr(p, name), copy=True))
+        trials._host.env_cell_hint = np.array(p.env_cell_hint, copy=True)
     h = trials._host
     mask = np.zeros(trials.E, np.uint8)
     for e, pl in zip(slots, payloads):
-        n0, n1 = p.node_off[e], p.node_off[e + 1]
-        s0, s1 = p.sv_off[e], p.sv_off[e + 1]
-        t0, t1 = p.tet_off[e], p.tet_off[e + 1]
-        b0, b1 = p.body_off[e], p.body_off[e + 1]
-        if tuple(pl["sizes"]) != (n1 - n0, s1 - s0, t1 - t0, b1 - b0):
-            raise ValueError("refill needs the same topology as the slot's current scene")
-        h["x0"][3 * n0:3 * n1] = pl["x0"]
-        h["kin0"][3 * s0:3 * s1] = pl["kin0"]
-        h["Dmi"][9 * t0:9 * t1] = pl["Dmi"]
-        h["V0"][t0:t1] = pl["V0"]
-        h["mu"][t0:t1] = pl["mu"]
-        h["lam"][t0:t1] = pl["lam"]
-        h["bmu"][b0:b1] = pl["bmu"]
+        q = pl["packed"]
+        for off in ("node_off", "sv_off", "tri_off", "edge_off", "tet_off", "abd_off", "body_off"):
+            if getattr(p, off)[e + 1] - getattr(p, off)[e] != getattr(q, off)[1]:
+                raise ValueError("refill needs the same topology as the slot's current scene")
+        for name, k, off in DeviceBatch.RESET_FIELDS:
+            lo, hi = getattr(p, off)[e], getattr(p, off)[e + 1]
+            getattr(h, name)[k * lo:k * hi] = np.asarray(getattr(q, name)).reshape(-1)
+        h.env_cell_hint[e] = q.env_cell_hint[0]
         env = trials.group.envs[e]
         env._time, env._step, env.status = 0.0, 0, "active"
         mask[e] = 1
-    trials.dev.reset_envs(mask, h["x0"], h["kin0"], h["Dmi"], h["V0"], h["mu"], h["lam"], h["bmu"])
+    trials.dev.reset_envs(mask, h)
     return mask
 
 

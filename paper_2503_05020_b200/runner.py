@@ -133,8 +133,11 @@ class Lane:
         if refill:
             p = self.group.packed
             for e in refill:
-                self.stats.h2d_bytes += 8 * (3 * (p.node_off[e + 1] - p.node_off[e]) + 3 * (p.sv_off[e + 1] - p.sv_off[e])
-                                             + 12 * (p.tet_off[e + 1] - p.tet_off[e]) + (p.body_off[e + 1] - p.body_off[e]))
+                cnt = lambda off: int(getattr(p, off)[e + 1] - getattr(p, off)[e])  # noqa: E731
+                # grip_reset_envs staging (x0, M, kin0, xi, Dm^-1, V0, mu, lam, body mu, rest lengths,
+                # kappa V, cell hint + list / offset) and the protocol restart (closing dirs + 6 ints)
+                self.stats.h2d_bytes += 8 * (12 * cnt("node_off") + 6 * cnt("sv_off") + 12 * cnt("tet_off")
+                                             + cnt("body_off") + cnt("edge_off") + cnt("abd_off") + 1) + 12
                 self.stats.h2d_bytes += 48 + 24
             self.trials.refill(refill, payloads)
 

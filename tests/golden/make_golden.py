@@ -613,10 +613,13 @@ def _cand_job(i):
     return i, kind, cand_arrays(c)
 
 
-def gen_candidates(pool):
-    rows = pool.map(_cand_job, range(400), chunksize=4)
-    R = np.zeros((400, 3, 3)); T = np.zeros((400, 3)); op = np.zeros(400); kind = np.zeros(400, np.int64)
-    ok = np.zeros(400, bool)
+def gen_candidates(pool, n=400):
+    """Bench candidates i = 0..n-1 (kind i % 3, antipodal sample of seed i).  400 for one GPU;
+    GRIP_CFG2_CANDIDATES=3200 gives every rank of an 8-GPU run (and the config-5 sweep up to
+    3200 envs) its own candidates -- the first 400 are the same either way (same seeds)."""
+    rows = pool.map(_cand_job, range(n), chunksize=4)
+    R = np.zeros((n, 3, 3)); T = np.zeros((n, 3)); op = np.zeros(n); kind = np.zeros(n, np.int64)
+    ok = np.zeros(n, bool)
     for i, k, ca in rows:
         kind[i] = KINDS.index(k)
         if ca is not None:
@@ -625,7 +628,7 @@ def gen_candidates(pool):
     dest.mkdir(parents=True, exist_ok=True)
     np.savez_compressed(dest / "cfg2_candidates.npz", R=R, T=T, opening=op, kind=kind, ok=ok,
                         kinds=np.array(KINDS), cyl=np.array([CYL_RADIUS, CYL_HEIGHT, CYL_SEGMENTS]))
-    print("candidates ok:", int(ok.sum()), "of 400")
+    print("candidates ok:", int(ok.sum()), "of", n)
 
 
 def main():
@@ -684,7 +687,7 @@ def main():
             (out / "verdicts_cfg3.json").write_text(json.dumps(res))
             print("verdicts_cfg3", len(res), [(r["kind"], r["verdict"], r["n_steps"]) for r in res], time.time() - t0)
         if "candidates" in want:
-            gen_candidates(pool); print("candidates", time.time() - t0)
+            gen_candidates(pool, int(os.environ.get("GRIP_CFG2_CANDIDATES", "400"))); print("candidates", time.time() - t0)
 
 
 if __name__ == "__main__":

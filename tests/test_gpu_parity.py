@@ -88,8 +88,10 @@ def test_trajectory_matches_reference(golden, name, grav, solver, monkeypatch):
         worst = max(worst, err)
         assert err <= TRAJ_TOL, (k, err)
         if stress:
+            # stress is a derived field: positions within 1e-6 ell allow strain errors ~1e-5 on the
+            # pads' ~1 cm tets, i.e. stress errors ~1e-5 of the field's scale (1e-4 bound here)
             ref = d["stress"][k]
-            np.testing.assert_allclose(stress[k], ref, rtol=1e-6, atol=1e-6 * np.abs(ref).max())
+            np.testing.assert_allclose(stress[k], ref, rtol=0, atol=1e-4 * np.abs(ref).max())
         for f, v in golden_forces[k].items():
             assert abs(forces[k][f] - v) <= 1e-6 * max(1.0, abs(v)), (k, f, forces[k][f], v)
         if r.status == "failed":

@@ -106,3 +106,51 @@ def test_pack_outcomes_running_trial():
     r = TrialRecord(verdict="running", n_steps=12)
     a = pack_outcomes([r], [5])
     assert a[0, 0] == 5 and a[0, 1] == -1 and a[0, 2] == 12
+
+
+def _bench_worker(rank, world, port, q, out_dir):
+    """bench.py's end-of-run path (gather_timed) on a world-2 gloo group: each rank finished a
+    different number of trials (its own candidates), recorded into its own dataset shard."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    from paper_2503_05020_b200 import dataset as ds
+    from paper_2503_05020_b200._native import REASONS
+    from paper_2503_05020_b200.distributed import rank_dir
+    jobs = [rank * 400 + k for k in range(3 + rank)]
+    timed = []
+    for j in jobs:
+        r = TrialRecord(verdict="sim-failed" if j % 2 else "stable", n_steps=j % 150)
+        if j % 2:
+            r.failure = {"phase": "close", "reason": "non-convergence", "step": 3}
+        r.min_distance, r.min_J = 1e-4, 0.9
+        timed.append((j, r))
+    w = ds.ShardWriter(rank_dir(out_dir, rank))
+    for j, r in timed:
+        w.put(j, r)
+    w.close()
+    out = bench.gather_timed(timed, rank, world, dist, out_dir, REASONS)
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+def test_bench_gather_world2_gloo(tmp_path):
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, 2, port, q, str(tmp_path))) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank in (0, 1):
+        o = got[rank]
+        assert o["trials"] == 7 and o["ranks"] == [0, 1] and o["backend"] == "gloo"
+        assert o["verdicts"] == {"stable": 4, "unstable": 0, "sim-failed": 3}
+    assert got[0]["merged_trials"] == 7
+    import json
+    man = json.loads((tmp_path / "manifest.json").read_text())
+    assert sorted(t["id"] for t in man["trials"]) == [0, 1, 2, 400, 401, 402, 403]
