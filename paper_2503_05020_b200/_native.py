@@ -100,7 +100,7 @@ def load():
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
         ("grip_sdf_nn", [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp, i32, vp]),
         ("grip_set_priority", [vp, i32]), ("grip_contacts_now", [vp, vp, dbl, vp]),
-        ("grip_check_finite", [vp, vp]),
+        ("grip_check_finite", [vp, vp]), ("grip_cta_records", [vp, vp, ctypes.c_int64, vp, i32]),
         ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
         ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
@@ -361,6 +361,21 @@ class DeviceBatch:
         md = np.full(self.n_env, np.inf)
         check(self.lib.grip_contacts_now(self.h, ptr(m), float(radius_factor), ptr(md)))
         return md
+
+    CTA_KERNELS = ("begin", "candidates", "assemble_direct", "line_search", "finalize")
+
+    def cta_records(self, reset=True, cap=1 << 21):
+        """Per-CTA timing records (GRIP_CTA_TIMING builds): structured array seq, kernel, env, sm,
+        t0 (ns, low 32 bits of the global timer), dur (ns)."""
+        raw = np.zeros((cap, 4), np.uint64)
+        n = ctypes.c_int64()
+        check(self.lib.grip_cta_records(self.h, ptr(raw), cap, ctypes.byref(n), int(reset)))
+        r = raw[:n.value]
+        out = np.zeros(len(r), [("seq", "<u8"), ("kernel", "<i4"), ("env", "<i4"), ("sm", "<i4"), ("t0", "<u8"),
+                                ("dur", "<u8")])
+        out["seq"], out["kernel"], out["env"] = r[:, 0], (r[:, 1] >> np.uint64(32)), r[:, 1] & np.uint64(0xffffffff)
+        out["sm"], out["t0"], out["dur"] = r[:, 2], r[:, 3] >> np.uint64(32), r[:, 3] & np.uint64(0xffffffff)
+        return out
 
     def check_finite(self):
         """Per env: True when its state holds a NaN / inf (grip_check_finite)."""

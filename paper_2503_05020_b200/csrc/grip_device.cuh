@@ -178,7 +178,43 @@ struct Dev {
   int* sc_off;        // ... per env 2*(max_free+1): per dense node item offsets, fill cursors
   int dense_k;        // 1: the element kernel writes el_K / el_kn (direct solver)
   double* sv_g;      // per env 3*max_sv
+  unsigned long long launch_seq;   // host launch counter, captured by value at every launch
+  unsigned long long* cta_rec;     // GRIP_CTA_TIMING builds: 4 per CTA (seq, kernel << 32 | env, smid, t0 << 32 | t1)
+  unsigned int* cta_n;
+  unsigned int cta_cap;
 };
+
+// per-CTA wall time (GRIP_CTA_TIMING builds only; the per-env CTA histograms of profiles/):
+// thread 0 stamps %globaltimer at entry and, through the destructor, at every exit
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct CtaTimer {
+  const Dev& D;
+  int kid, env;
+  unsigned long long t0;
+  __device__ CtaTimer(const Dev& d, int k, int e) : D(d), kid(k), env(e), t0(threadIdx.x == 0 ? gtimer() : 0ull) {}
+  __device__ ~CtaTimer() {
+    if (threadIdx.x != 0 || !D.cta_rec) return;
+    const unsigned long long t1 = gtimer();
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    const unsigned i = atomicAdd(D.cta_n, 1u);
+    if (i >= D.cta_cap) return;
+    unsigned long long* r = D.cta_rec + 4 * (size_t)i;
+    r[0] = D.launch_seq;
+    r[1] = ((unsigned long long)kid << 32) | (unsigned)env;
+    r[2] = sm;
+    r[3] = ((t0 & 0xffffffffull) << 32) | (t1 - t0 > 0xffffffffull ? 0xffffffffull : t1 - t0);
+  }
+};
+#ifdef GRIP_CTA_TIMING
+#define CTA_TIMER(kid, e) CtaTimer cta_timer_(D, kid, e)
+#else
+#define CTA_TIMER(kid, e) do {} while (0)
+#endif
 
 __device__ __forceinline__ const double* P_(const Dev& D, int e) { return D.params + (size_t)e * GRIP_NPARAM; }
 

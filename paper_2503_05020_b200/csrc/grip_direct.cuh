@@ -667,6 +667,7 @@ __global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* lis
   AsmShared& A = S.A;
   Red& sm = A.sm;
   const int e = list[blockIdx.x];
+  CTA_TIMER(2, e);
   if (D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);

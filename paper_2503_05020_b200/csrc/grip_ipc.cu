@@ -82,6 +82,7 @@ struct GripBatch {
   int max_it = 100;
   double last_ms = 0.0;
   long long launches = 0, sweeps = 0;
+  unsigned long long seq_ctr = 0;   // D.launch_seq source (per-CTA timing records)
   // optional per-kernel timing on the library stream (grip_set_profiling)
   bool prof = false;
   // grids of the flat element kernels (k_tet_front, k_elements_w, k_tet_jacobi2, k_tet_back), in
@@ -658,6 +659,11 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
     take(b->s_flags, E); take(b->s_done, E); take(b->s_st, E); take(b->s_rs, E); take(b->s_it, E); take(b->s_kb, E);
     take(b->s_rg, E); take(b->s_si, E); take(b->s_nc, E); take(b->s_pi, E); take(b->s_cmask, NBd);
   }
+#ifdef GRIP_CTA_TIMING
+  D.cta_cap = 1u << 21;
+  D.cta_rec = b->alloc<unsigned long long>(4 * (size_t)D.cta_cap);
+  D.cta_n = b->alloc<unsigned int>(1);
+#endif
   for (void* p : b->owned)
     if (!p) {
       g_err = "out of device memory";
@@ -942,6 +948,7 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
 static void sweep_launch(GripBatch* b, int n, const int* list) {
   Dev& D = b->D;
   int t = kt_begin(b, K_CAND);
+  D.launch_seq = ++b->seq_ctr;
   k_candidates<<<n, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   t = kt_begin(b, K_SCAN);
@@ -958,12 +965,14 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   t = kt_begin(b, K_ASM);
   if (b->direct) {
     k_contact_K<<<148 * 2, NT, 0, b->stream>>>(D, list, n);
-    k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
+    D.launch_seq = ++b->seq_ctr;
+  k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
   } else {
     k_assemble_solve<<<n, NT, 0, b->stream>>>(D, list);
   }
   kt_end(b, t);
   t = kt_begin(b, K_LS);
+  D.launch_seq = ++b->seq_ctr;
   k_linesearch<<<n, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
@@ -1195,10 +1204,12 @@ int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
   CK(cudaMemsetAsync(D.pr_steps, 0, sizeof(unsigned long long), b->stream));
   for (int r = 0; r < rounds; ++r) {
     int t = kt_begin(b, K_BEGIN);
+    D.launch_seq = ++b->seq_ctr;
     k_begin<<<E, NT, 0, b->stream>>>(D, b->d_ident);
     kt_end(b, t);
     sweep_launch(b, E, b->d_ident);
     t = kt_begin(b, K_FIN);
+    D.launch_seq = ++b->seq_ctr;
     k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
     kt_end(b, t);
     k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
@@ -1549,6 +1560,19 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
     if (p) cudaFree(p);
   if (rc) g_err = "grip_debug_chain: device error";
   return rc;
+}
+
+int grip_cta_records(GripBatch* b, uint64_t* out, int64_t cap, int64_t* n, int reset) {
+  *n = 0;
+  if (!b->D.cta_rec) return 0;   // not a GRIP_CTA_TIMING build
+  unsigned cnt = 0;
+  CK(cudaMemcpyAsync(&cnt, b->D.cta_n, sizeof(unsigned), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  const int64_t m = std::min<int64_t>({(int64_t)cnt, (int64_t)b->D.cta_cap, cap});
+  if (out && m > 0) CK(cudaMemcpy(out, b->D.cta_rec, sizeof(uint64_t) * 4 * (size_t)m, cudaMemcpyDeviceToHost));
+  *n = m;
+  if (reset) CK(cudaMemsetAsync(b->D.cta_n, 0, sizeof(unsigned), b->stream));
+  return 0;
 }
 
 int grip_get_state(GripBatch* b, double* x, double* v, double* kin) {

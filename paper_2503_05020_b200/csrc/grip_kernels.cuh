@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
   const int e = list[blockIdx.x];
+  CTA_TIMER(0, e);
   // device protocol: only envs whose protocol asked for a new step
   if (D.round_mode && !D.pr_i[(size_t)e * PI_N + PI_NEEDBEGIN]) return;
   begin_env(D, e, sm, S);
@@ -263,6 +264,7 @@ __global__ void __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
   const int e = list[blockIdx.x];
+  CTA_TIMER(1, e);
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dhat = P[GRIP_P_DHAT];
@@ -1082,6 +1084,7 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
   const int e = list[blockIdx.x];
+  CTA_TIMER(3, e);
   if (D.ns_done[e] || !D.needs_ls[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
@@ -1264,6 +1267,7 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
   __shared__ BPShared S;
   __shared__ unsigned int cmask[32];
   const int e = list[blockIdx.x];
+  CTA_TIMER(4, e);
   if (only_done && (!D.ns_done[e] || D.fin_done[e] || (D.flags[e] & FLAG_OVERFLOW))) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);

@@ -26,7 +26,7 @@ def _num(v):
     return float(v.split()[0].replace(",", ""))
 
 
-def main(rep, out):
+def main(rep, out, note=None):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, units = rows[0], rows[1]
@@ -46,7 +46,7 @@ def main(rep, out):
             pass
         res.append(d)
     with open(out, "w") as f:
-        json.dump(res, f, indent=1)
+        json.dump({"meta": {"note": note or "", "units_per_round": None}, "rows": res} if note else res, f, indent=1)
     for d in res:
         print(d["kernel"], d.get("gpu__time_duration.sum"), "issue", d.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
               "dram", d.get("dram__bytes_read.sum"), d.get("dram__bytes_write.sum"), "fp64 GFLOP",
@@ -54,4 +54,4 @@ def main(rep, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
