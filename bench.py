@@ -505,7 +505,7 @@ def kernel_report(runner, env_steps_s, ms_max, peak):
     traffic, flop, meta, src = _ncu_group(dom)
     if traffic is not None:
         # the capture's per-round figures rescaled to the timed launches by element units per launch
-        cap_units = sum((meta or {}).get("units_per_round", {}).values()) or None
+        cap_units = sum(((meta or {}).get("units_per_round") or {}).values()) or None
         timed_units = sum(units.values()) / nl if dom == "elements" or dom == "assemble_pcg" else None
         s = (timed_units / cap_units) if (cap_units and timed_units) else 1.0
         roof["traffic"] = traffic * s

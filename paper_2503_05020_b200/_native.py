@@ -371,10 +371,11 @@ class DeviceBatch:
         n = ctypes.c_int64()
         check(self.lib.grip_cta_records(self.h, ptr(raw), cap, ctypes.byref(n), int(reset)))
         r = raw[:n.value]
-        out = np.zeros(len(r), [("seq", "<u8"), ("kernel", "<i4"), ("env", "<i4"), ("sm", "<i4"), ("t0", "<u8"),
-                                ("dur", "<u8")])
+        out = np.zeros(len(r), [("seq", "<u8"), ("kernel", "<i4"), ("env", "<i4"), ("sm", "<i4"), ("info", "<u4"),
+                                ("t0", "<u8"), ("dur", "<u8")])
         out["seq"], out["kernel"], out["env"] = r[:, 0], (r[:, 1] >> np.uint64(32)), r[:, 1] & np.uint64(0xffffffff)
-        out["sm"], out["t0"], out["dur"] = r[:, 2], r[:, 3] >> np.uint64(32), r[:, 3] & np.uint64(0xffffffff)
+        out["sm"], out["info"] = r[:, 2] & np.uint64(0xffff), r[:, 2] >> np.uint64(16)
+        out["t0"], out["dur"] = r[:, 3] >> np.uint64(32), r[:, 3] & np.uint64(0xffffffff)
         return out
 
     def check_finite(self):

@@ -4,6 +4,7 @@
 // bitwise reproducible and independent of how many envs share the launch
 // (SPEC "batch-of-N bitwise equals batch-of-1").
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -157,7 +158,8 @@ struct Dev {
   int bp_qm_min;     // direct broad phase: groups with > bp_qm_min lane-mode iterations use query mode
   float bp_qm_fac;   //   when that costs <= bp_qm_fac x the lane-mode iterations (GRIP_BP_QM=min,fac)
   int bp_mode;       // broad phase: 0 direct over culled primitives with grid fallback, 1 grid only (GRIP_BP)
-  int* bp_cells;     // per env cap_cells
+  int* bp_cells;     // per env cap_cells (grid path)
+  int* bp_scr;       // per env 4 max(max_tri, max_edge) + max_sv (direct path: compacted ids, vertices, queries)
   double* bp_aabb;   // per env 6*max(max_tri, max_edge)
   int* bp_cnt;       // per env max(max_sv, max_edge) + 1
   int* bp_tmp;       // per env max(cap_pt, cap_ee)
@@ -169,6 +171,7 @@ struct Dev {
   double* dense_L;   // per env dense_stride doubles (direct solve when the matrix exceeds shared memory)
   size_t dense_stride;
   double *c_u, *c_w; // per env 3*max_sv
+  double* ls_y;       // per env LS_NA*3*max_sv: trial surface positions of the line search's energy passes
   double* c_r;       // per env 12*(cap_act+cap_anc)
   int *inc_ptr, *inc; // per env max_sv+1 ; 4*(cap_act+cap_anc)
   double* el_K;       // direct solve, per contact slot (env (cap_act+cap_anc)): dt^2 J^T H J, lower triangle over
@@ -194,10 +197,13 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct CtaTimer {
   const Dev& D;
   int kid, env;
+  bool on;
+  unsigned info = 0;   // kernel-specific detail bits (CTA_INFO), stored above the SM id
   unsigned long long t0;
-  __device__ CtaTimer(const Dev& d, int k, int e) : D(d), kid(k), env(e), t0(threadIdx.x == 0 ? gtimer() : 0ull) {}
+  __device__ CtaTimer(const Dev& d, int k, int e, bool o = true)
+      : D(d), kid(k), env(e), on(o), t0(threadIdx.x == 0 ? gtimer() : 0ull) {}
   __device__ ~CtaTimer() {
-    if (threadIdx.x != 0 || !D.cta_rec) return;
+    if (!on || threadIdx.x != 0 || !D.cta_rec) return;
     const unsigned long long t1 = gtimer();
     unsigned sm;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -206,14 +212,20 @@ struct CtaTimer {
     unsigned long long* r = D.cta_rec + 4 * (size_t)i;
     r[0] = D.launch_seq;
     r[1] = ((unsigned long long)kid << 32) | (unsigned)env;
-    r[2] = sm;
+    r[2] = sm | ((unsigned long long)info << 16);
     r[3] = ((t0 & 0xffffffffull) << 32) | (t1 - t0 > 0xffffffffull ? 0xffffffffull : t1 - t0);
   }
 };
 #ifdef GRIP_CTA_TIMING
 #define CTA_TIMER(kid, e) CtaTimer cta_timer_(D, kid, e)
+#define CTA_TIMER_IF(on, kid, e) CtaTimer cta_timer_(D, kid, e, on)
+#define CTA_INFO(v) (cta_timer_.info |= (v))
+#define CTA_INFO_ADD(v) (cta_timer_.info += (v))
 #else
+#define CTA_INFO(v) do {} while (0)
+#define CTA_INFO_ADD(v) do {} while (0)
 #define CTA_TIMER(kid, e) do {} while (0)
+#define CTA_TIMER_IF(on, kid, e) do {} while (0)
 #endif
 
 __device__ __forceinline__ const double* P_(const Dev& D, int e) { return D.params + (size_t)e * GRIP_NPARAM; }
@@ -253,6 +265,29 @@ __device__ double block_red(double v, Red& sm) {
   }
   __syncthreads();
   return sm.d[32];
+}
+// N <= 4 block sums at once, each through exactly block_red<0>'s tree (bitwise the same values)
+template <int N>
+__device__ void block_sum_n(double* v, Red& sm) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = wsum(v[k]);
+  __syncthreads();
+  if (l == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) sm.d[4 * w + k] = v[k];
+  __syncthreads();
+  if (w == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double r = l < NWARP ? sm.d[4 * l + k] : 0.0;
+      r = wsum(r);
+      if (l == 0) sm.d[32 + k] = r;
+    }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) v[k] = sm.d[32 + k];
+  __syncthreads();
 }
 __device__ __forceinline__ double block_sum(double v, Red& sm) { return block_red<0>(v, sm); }
 __device__ __forceinline__ double block_max(double v, Red& sm) { return block_red<1>(v, sm); }
@@ -390,7 +425,35 @@ struct BPShared {
   double bb[32][6];   // per-body surface AABB (culling: primitives far from every partner body)
   int rs[32], re[32]; // per-body range of the compacted primitive list (direct path)
   unsigned char gmode[BP_MAXG];   // direct path: per 32-query group, 1 = queries one by one
+  int cl_val[4];                  // cluster broad phase: rank 0's counts, read by the other ranks (DSMEM)
 };
+
+// A thread-block cluster working on ONE env's broad phase (the rebuild of a candidate superset
+// is the heavy-env tail of its kernel: an O(queries x partners) pass that would otherwise run on
+// one SM while the launch waits for it).  Rank 0 compacts the culled primitives / queries; the
+// 32-query groups are dealt out round-robin over the ranks for both passes; rank 0 turns the
+// per-query counts into write offsets between the passes; counts travel through distributed
+// shared memory.  n == 1 is the plain CTA-per-env path.
+struct BPCl {
+  int rank, n;
+};
+__device__ __forceinline__ BPCl bp_solo() { return BPCl{0, 1}; }
+__device__ __forceinline__ void cl_sync(const BPCl& c) {
+  if (c.n > 1) {
+    __threadfence();   // rank 0's global writes (compacted lists, offsets) before the other ranks read them
+    cooperative_groups::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+}
+// value rank 0 left in its shared slot before a cl_sync; ends with a cl_sync so rank 0's shared
+// memory outlives every remote read
+__device__ __forceinline__ int cl_from0(const BPCl& c, int* slot) {
+  if (c.n == 1) return *slot;
+  const int v = *cooperative_groups::this_cluster().map_shared_rank(slot, 0);
+  cl_sync(c);
+  return v;
+}
 
 struct Grid {
   double lox, loy, loz, ih;
@@ -765,10 +828,12 @@ __device__ __forceinline__ int lower_bound_int(const int* a, int n, int key) {
 // -> S.rs / S.re.  Returns the survivor count.
 template <int K>
 __device__ int bp_compact(const Dev& D, const EnvIx& E, const double* X, const int* prim, int n, const int* blo,
-                          const int* bhi, double rc, int* cid, int* cv, double* cb, BPShared& S, Red& sm) {
+                          const int* bhi, double rc, int* cid, int* cv, double* cb, BPShared& S, Red& sm,
+                          const BPCl& cl) {
   const uint32_t* pm = D.body_pairmask + E.b0;
   const int* vb = D.sv_body + E.s0;
   int ns = 0;
+  if (cl.rank == 0)
   for (int s0 = 0; s0 < n; s0 += NT) {
     const int i = s0 + threadIdx.x;
     int keep = 0;
@@ -797,6 +862,11 @@ __device__ int bp_compact(const Dev& D, const EnvIx& E, const double* X, const i
       o[0] = l.x; o[1] = l.y; o[2] = l.z; o[3] = u.x; o[4] = u.y; o[5] = u.z;
     }
     ns += tot;
+  }
+  if (cl.n > 1) {
+    if (cl.rank == 0 && threadIdx.x == 0) S.cl_val[0] = ns;
+    cl_sync(cl);
+    ns = cl_from0(cl, &S.cl_val[0]);
   }
   __syncthreads();
   if (threadIdx.x < E.nb) {
@@ -884,7 +954,7 @@ __device__ __forceinline__ void bp_emit(const BPShared& S, int kt, int q0, int q
 template <int K>
 __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, const int* qid, int np, const int* cid,
                         const int* cv, const double* cb, double r, int* cnt, int* out, int* out_eid, int cap,
-                        BPShared& S, Red& sm) {
+                        BPShared& S, Red& sm, const BPCl& cl) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int ngroups = (nq + 31) >> 5;
@@ -892,7 +962,8 @@ __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, c
   int total = 0;
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 0)
-      for (int q = threadIdx.x; q < nq; q += NT) cnt[q] = 0;
+      for (int q = threadIdx.x; q < nq; q += NT)
+        if ((q >> 5) % cl.n == cl.rank) cnt[q] = 0;
     for (int p0 = 0; p0 < np; p0 += BP_TILE) {
       const int p1 = min(np, p0 + BP_TILE);
       __syncthreads();
@@ -906,7 +977,7 @@ __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, c
         __syncthreads();
       }
       // phase 1: each warp takes whole groups, decides their mode, runs the lane-mode ones
-      for (int g = warp; g < ngroups; g += NWARP) {
+      for (int g = cl.rank + cl.n * warp; g < ngroups; g += cl.n * NWARP) {   // this rank's groups
         const int q = 32 * g + lane;
         const bool valid = q < nq;
         BPQuery<K> Q;
@@ -949,7 +1020,7 @@ __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, c
       if (modes)
         for (int base = 0; base < nq; base += 32 * NWARP) {
           const int q = base + warp + NWARP * lane;
-          const bool mine = q < nq && S.gmode[q >> 5];
+          const bool mine = q < nq && (q >> 5) % cl.n == cl.rank && S.gmode[q >> 5];
           const unsigned todo = __ballot_sync(0xffffffffu, mine);
           if (!todo) continue;
           BPQuery<K> Q;
@@ -988,23 +1059,34 @@ __device__ int bp_pairs(const Dev& D, const EnvIx& E, const double* X, int nq, c
     }
     __syncthreads();
     if (pass == 0) {
-      total = block_scan_array(cnt, nq, sm);
+      if (cl.n == 1) {
+        total = block_scan_array(cnt, nq, sm);
+      } else {   // every rank's counts -> rank 0 turns them into write offsets -> every rank
+        cl_sync(cl);
+        if (cl.rank == 0) {
+          total = block_scan_array(cnt, nq, sm);
+          if (threadIdx.x == 0) S.cl_val[2] = total;
+        }
+        cl_sync(cl);
+        total = cl_from0(cl, &S.cl_val[2]);
+      }
       if (total > cap) return total;
     }
   }
+  if (cl.n > 1) cl_sync(cl);   // every rank done with the compacted lists before they are reused
   return total;
 }
 
 // returns false on output overflow (*too_big: the culled sets are too large for the direct
 // path; nothing was written and the caller runs the grid)
 __device__ bool broad_phase_direct(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
-                                   int* out_n, BPShared& S, Red& sm, bool* too_big) {
+                                   int* out_n, BPShared& S, Red& sm, bool* too_big, const BPCl& cl) {
   const double* X = D.sv_pos + 3 * (size_t)E.s0;
   const int* tris = D.tris + 3 * (size_t)E.t0;
   const int* edges = D.edges + 2 * (size_t)E.ed0;
   const int Mx = max(D.max_tri, D.max_edge);
   double* cb = D.bp_aabb + (size_t)E.e * 6 * Mx;
-  int* cid = D.bp_cells + (size_t)E.e * D.cap_cells;   // [0, Mx) ids, [Mx, 4 Mx) vertices, [4 Mx, ..) queries
+  int* cid = D.bp_scr + (size_t)E.e * (4 * Mx + D.max_sv);   // [0, Mx) ids, [Mx, 4 Mx) vertices, [4 Mx, ..) queries
   int* cv = cid + Mx;
   int* qid = cid + 4 * Mx;
   int* cnt = D.bp_cnt + (size_t)E.e * (max(D.max_sv, D.max_edge) + 1);
@@ -1031,8 +1113,9 @@ __device__ bool broad_phase_direct(const Dev& D, const EnvIx& E, double r, int* 
   __syncthreads();
   const double rc = r + 1e-9 * fmax(r, D.cell_hint[E.e]);
   // ---------------- point-triangle ----------------
-  const int nts = bp_compact<3>(D, E, X, tris, E.nt, D.body_tri_lo, D.body_tri_hi, rc, cid, cv, cb, S, sm);
+  const int nts = bp_compact<3>(D, E, X, tris, E.nt, D.body_tri_lo, D.body_tri_hi, rc, cid, cv, cb, S, sm, cl);
   int nq = 0;
+  if (cl.rank == 0)
   for (int s0 = 0; s0 < E.ns; s0 += NT) {
     const int v = s0 + threadIdx.x;
     int keep = 0;
@@ -1045,21 +1128,26 @@ __device__ bool broad_phase_direct(const Dev& D, const EnvIx& E, double r, int* 
     if (keep) qid[nq + pre] = v;
     nq += tot;
   }
+  if (cl.n > 1) {
+    if (cl.rank == 0 && threadIdx.x == 0) S.cl_val[1] = nq;
+    cl_sync(cl);
+    nq = cl_from0(cl, &S.cl_val[1]);
+  }
   __syncthreads();
   if ((double)nq * nts + 0.5 * (1.5 * nts) * (1.5 * nts) > (double)BP_DIRECT_MAX) {
     *too_big = true;
     return false;
   }
-  const int npt = bp_pairs<3>(D, E, X, nq, qid, nts, cid, cv, cb, r, cnt, out_pt, nullptr, D.cap_pt, S, sm);
+  const int npt = bp_pairs<3>(D, E, X, nq, qid, nts, cid, cv, cb, r, cnt, out_pt, nullptr, D.cap_pt, S, sm, cl);
   int nee = 0;
   bool ok = npt <= D.cap_pt;
   // ---------------- edge-edge ----------------
   if (ok) {
-    const int nes = bp_compact<2>(D, E, X, edges, E.ne, D.body_edge_lo, D.body_edge_hi, rc, cid, cv, cb, S, sm);
-    nee = bp_pairs<2>(D, E, X, nes, nullptr, nes, cid, cv, cb, r, cnt, out_ee, out_eid, D.cap_ee, S, sm);
+    const int nes = bp_compact<2>(D, E, X, edges, E.ne, D.body_edge_lo, D.body_edge_hi, rc, cid, cv, cb, S, sm, cl);
+    nee = bp_pairs<2>(D, E, X, nes, nullptr, nes, cid, cv, cb, r, cnt, out_ee, out_eid, D.cap_ee, S, sm, cl);
     ok = nee <= D.cap_ee;
   }
-  if (threadIdx.x == 0) {
+  if (cl.rank == 0 && threadIdx.x == 0) {
     out_n[0] = npt;
     out_n[1] = nee;
   }
@@ -1069,13 +1157,20 @@ __device__ bool broad_phase_direct(const Dev& D, const EnvIx& E, double r, int* 
 
 // Candidate stencils of one env at radius r (see broad_phase_grid for the contract).
 __device__ bool broad_phase_env(const Dev& D, const EnvIx& E, double r, int* out_pt, int* out_ee, int* out_eid,
-                                int* out_n, BPShared& S, Red& sm) {
+                                int* out_n, BPShared& S, Red& sm, const BPCl& cl = BPCl{0, 1}) {
   if (D.bp_mode == 0 && E.ns > 0) {
     bool too_big = false;
-    const bool ok = broad_phase_direct(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm, &too_big);
+    const bool ok = broad_phase_direct(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm, &too_big, cl);
     if (!too_big) return ok;
   }
-  return broad_phase_grid(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm);
+  if (cl.n == 1) return broad_phase_grid(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm);
+  // the grid fallback (rare: very large culled sets) runs on rank 0, the others wait for its verdict
+  if (cl.rank == 0) {
+    const bool ok = broad_phase_grid(D, E, r, out_pt, out_ee, out_eid, out_n, S, sm);
+    if (threadIdx.x == 0) S.cl_val[3] = ok ? 1 : 0;
+  }
+  cl_sync(cl);
+  return cl_from0(cl, &S.cl_val[3]) != 0;
 }
 
 // Exact candidate set at radius r as an order-preserving filter of a superset computed at

@@ -600,6 +600,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
     D.cap_cells = 64;
   }
   D.bp_aabb = b->alloc<double>((size_t)E * 6 * std::max(max_tri, max_edge));
+  D.bp_scr = b->alloc<int>((size_t)E * (4 * std::max(max_tri, max_edge) + max_sv));
   D.bp_cnt = b->alloc<int>((size_t)E * (std::max(max_sv, max_edge) + 1));
   D.pcg_x = b->alloc<double>((size_t)E * 3 * max_free);
   D.pcg_r = b->alloc<double>((size_t)E * 3 * max_free);
@@ -631,6 +632,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   }
   D.c_u = b->alloc<double>((size_t)E * 3 * max_sv);
   D.c_w = b->alloc<double>((size_t)E * 3 * max_sv);
+  D.ls_y = b->alloc<double>((size_t)E * LS_NA * 3 * max_sv);
   D.sv_g = b->alloc<double>((size_t)E * 3 * max_sv);
   D.inc_ptr = b->alloc<int>((size_t)E * (max_sv + 1));
   D.dense_k = b->direct ? 1 : 0;
@@ -681,8 +683,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
-        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
-        D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.c_r,
+        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_scr, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
+        D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
         D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
@@ -949,7 +951,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   Dev& D = b->D;
   int t = kt_begin(b, K_CAND);
   D.launch_seq = ++b->seq_ctr;
-  k_candidates<<<n, NT, 0, b->stream>>>(D, list);
+  k_candidates<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   t = kt_begin(b, K_SCAN);
   k_work_scan<<<1, NT, 0, b->stream>>>(D, list, n);

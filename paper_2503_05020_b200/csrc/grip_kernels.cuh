@@ -55,15 +55,16 @@ __device__ __forceinline__ void cs_moved(const Dev& D, int e, double dmax) {
 
 // make D.cs_* a superset at radius >= need for the current positions (D.sv_pos); built with
 // the skin GRIP_SKIN * dhat on top, so that it survives the next small moves
-__device__ bool ensure_superset(const Dev& D, const EnvIx& E, double need, double dhat, BPShared& S, Red& sm) {
+__device__ bool ensure_superset(const Dev& D, const EnvIx& E, double need, double dhat, BPShared& S, Red& sm,
+                                const BPCl& cl = BPCl{0, 1}) {
   const int e = E.e;
   const bool valid = cs_covers(D, e, need);
   __syncthreads();
   if (valid) return true;
   const double R = fmax(need, superset_radius(D, e, dhat)) + D.ss_skin * dhat;
   const bool ok = broad_phase_env(D, E, R, D.cs_pt + (size_t)e * 4 * D.cap_pt, D.cs_ee + (size_t)e * 4 * D.cap_ee,
-                                  D.cs_eid + (size_t)e * 2 * D.cap_ee, D.cs_n + 2 * e, S, sm);
-  if (threadIdx.x == 0) {
+                                  D.cs_eid + (size_t)e * 2 * D.cap_ee, D.cs_n + 2 * e, S, sm, cl);
+  if (cl.rank == 0 && threadIdx.x == 0) {
     D.cs_R[e] = R;
     D.cs_drift[e] = 0.0;
     D.cs_valid[e] = ok ? 1 : 0;
@@ -260,31 +261,40 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
 // Newton sweep 1/4: surface positions, candidate set at 1.05 dhat, active stencils
 // (solver.py:652-653, contact.py:283-309)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
+// A cluster of BP_CL CTAs per env: a superset rebuild is split over the cluster (BPCl), the rest
+// runs on rank 0; the other ranks of an env whose superset still covers exit at once.
+constexpr int BP_CL = 4;
+__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
-  const int e = list[blockIdx.x];
-  CTA_TIMER(1, e);
+  const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
+  const int e = list[blockIdx.x / BP_CL];
+  CTA_TIMER_IF(cl.rank == 0, 1, e);
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dhat = P[GRIP_P_DHAT];
   // finished (or failed in begin_step) envs of a round list; an env whose begin_step overflowed
-  // this round keeps its flag and is re-run by the host after growth
+  // this round keeps its flag and is re-run by the host after growth (rank 0 clears the flags
+  // of a live env only: every rank reads the same skip decision)
   const bool skip = D.ns_done[e] || (D.flags[e] & FLAG_OVERFLOW);
+  const bool covered = cs_covers(D, e, 1.05 * dhat);
   __syncthreads();
-  if (skip) return;
-  if (threadIdx.x == 0) {
+  if (skip || (cl.rank != 0 && covered)) return;
+  if (cl.rank == 0 && threadIdx.x == 0) {
     D.flags[e] = 0;
     D.newton_calls[e] += 1;
   }
-  env_sv_positions(D, E, D.x);
+  if (cl.rank == 0) env_sv_positions(D, E, D.x);
+  if (!covered) CTA_INFO(1u);
+  if (!covered) cl_sync(cl);   // the positions rank 0 wrote, before the cluster's broad phase
   int* cn = D.c1_n + 2 * e;
   int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
   int* cee = D.c1_ee + (size_t)e * 4 * D.cap_ee;
-  if (!ensure_superset(D, E, 1.05 * dhat, dhat, S, sm)) {
-    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+  if (!ensure_superset(D, E, 1.05 * dhat, dhat, S, sm, covered ? BPCl{0, 1} : cl)) {
+    if (cl.rank == 0 && threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
+  if (cl.rank != 0) return;
   filter_from_superset(D, E, dhat * 1.05, cpt, cee, D.c1_eid + (size_t)e * 2 * D.cap_ee, cn, sm);
   const int npt = cn[0], nee = cn[1];
   const double* X = D.sv_pos + 3 * (size_t)E.s0;
@@ -984,100 +994,155 @@ __global__ void __launch_bounds__(NT) k_assemble_solve(Dev D, const int* list) {
 // ---------------------------------------------------------------------------
 
 // incremental potential at x + a p with candidate set c2; +inf if invalid
-__device__ double env_energy(const Dev& D, const EnvIx& E, double a, const int* cpt, int npt, const int* cee,
-                             const int* ceid, int nee, Red& sm) {
+// Total incremental potential at the NA trial points x + a[k] p (solver.py:518-533 _energy_only):
+// inertia + dt^2 (elastic + orthogonality + barrier over the frozen candidate set + friction),
+// +inf on an inverted element, a non-positive distance or a non-finite total.  One pass over the
+// elements serves all NA points (their loads shared); every value goes through the same per-thread
+// order and reduction tree as a single evaluation, so each out[k] is bitwise the 1-point result.
+constexpr int LS_NA = 4;
+template <int NA>
+__device__ void env_energy_n(const Dev& D, const EnvIx& E, const double* a, const int* cpt, int npt, const int* cee,
+                             const int* ceid, int nee, double* out, Red& sm) {
   const int e = E.e;
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], kappa = P[GRIP_P_KAPPA], dhat = P[GRIP_P_DHAT];
-  double* Y = D.c_u + (size_t)e * 3 * D.max_sv;  // trial sv positions (scratch)
+  const size_t ys = 3 * (size_t)D.max_sv;
+  double* Y = D.ls_y + (size_t)e * LS_NA * ys;   // trial sv positions (scratch), NA slices
   // trial surface positions: surface_positions(x + a p) (solver.py:525)
   for (int i = threadIdx.x; i < E.ns; i += NT) {
     const int g = E.s0 + i;
     const int kind = D.sv_kind[g];
-    V3 y;
     if (kind == 2) {
-      y = ld3(D.kin_pos + 3 * (size_t)g);
+      const V3 y = ld3(D.kin_pos + 3 * (size_t)g);
+#pragma unroll
+      for (int k = 0; k < NA; ++k) st3(Y + k * ys + 3 * i, y);
+      continue;
+    }
+    const size_t nb = E.n0 + D.sv_node[g];
+    if (kind == 0) {
+      const V3 xv = ld3(D.x + 3 * nb), pv = ld3(D.pdir + 3 * nb);
+#pragma unroll
+      for (int k = 0; k < NA; ++k) st3(Y + k * ys + 3 * i, xv + a[k] * pv);
     } else {
-      const size_t nb = E.n0 + D.sv_node[g];
-      if (kind == 0) {
-        y = ld3(D.x + 3 * nb) + a * ld3(D.pdir + 3 * nb);
-      } else {
+      double xq[12], pq[12];
+      for (int c = 0; c < 12; ++c) {
+        xq[c] = D.x[3 * nb + c];
+        pq[c] = D.pdir[3 * nb + c];
+      }
+      const V3 xi = ld3(D.sv_xi + 3 * g);
+#pragma unroll
+      for (int k = 0; k < NA; ++k) {
         double q[12];
-        for (int c = 0; c < 12; ++c) q[c] = D.x[3 * nb + c] + a * D.pdir[3 * nb + c];
-        V3 xi = ld3(D.sv_xi + 3 * g);
-        y = V3{q[0] + xi.x * q[3] + xi.y * q[4] + xi.z * q[5], q[1] + xi.x * q[6] + xi.y * q[7] + xi.z * q[8],
-               q[2] + xi.x * q[9] + xi.y * q[10] + xi.z * q[11]};
+        for (int c = 0; c < 12; ++c) q[c] = xq[c] + a[k] * pq[c];
+        st3(Y + k * ys + 3 * i, V3{q[0] + xi.x * q[3] + xi.y * q[4] + xi.z * q[5],
+                                   q[1] + xi.x * q[6] + xi.y * q[7] + xi.z * q[8],
+                                   q[2] + xi.x * q[9] + xi.y * q[10] + xi.z * q[11]});
       }
     }
-    st3(Y + 3 * i, y);
   }
   __syncthreads();
-  int bad = 0;
-  double ein = 0.0, eel = 0.0, ec = 0.0, ef = 0.0;
+  int bad = 0;   // bit k: trial point k is invalid
+  double ein[NA], eel[NA], ec[NA], ef[NA];
+#pragma unroll
+  for (int k = 0; k < NA; ++k) ein[k] = eel[k] = ec[k] = ef[k] = 0.0;
   for (int n = threadIdx.x; n < E.nn; n += NT) {
     const size_t g = E.n0 + n;
     const double* M = D.node_M + 9 * g;
-    double d[3];
-    for (int c = 0; c < 3; ++c) d[c] = (D.x[3 * g + c] + a * D.pdir[3 * g + c]) - D.xhat[3 * g + c];
-    for (int r = 0; r < 3; ++r) ein += d[r] * (M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2]);
+    double xg[3], pg[3], xh[3];
+    for (int c = 0; c < 3; ++c) {
+      xg[c] = D.x[3 * g + c];
+      pg[c] = D.pdir[3 * g + c];
+      xh[c] = D.xhat[3 * g + c];
+    }
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      double d[3];
+      for (int c = 0; c < 3; ++c) d[c] = (xg[c] + a[k] * pg[c]) - xh[c];
+      for (int r = 0; r < 3; ++r) ein[k] += d[r] * (M[3 * r] * d[0] + M[3 * r + 1] * d[1] + M[3 * r + 2] * d[2]);
+    }
   }
   for (int t = threadIdx.x; t < E.ntet; t += NT) {
     const int tg = E.te0 + t;
-    V3 x[4];
+    V3 xv[4], pv[4];
     for (int j = 0; j < 4; ++j) {
       const size_t g = E.n0 + D.tet_nodes[4 * (size_t)tg + j];
-      x[j] = ld3(D.x + 3 * g) + a * ld3(D.pdir + 3 * g);
+      xv[j] = ld3(D.x + 3 * g);
+      pv[j] = ld3(D.pdir + 3 * g);
     }
-    double el = 0.0;
-    if (nh_element(x, D.tet_Dmi + 9 * (size_t)tg, D.tet_V0[tg], D.tet_mu[tg], D.tet_lam[tg], &el, nullptr, nullptr) &
-        EL_INVERTED)
-      bad = 1;
-    else
-      eel += el;
-  }
-  for (int k = threadIdx.x; k < E.na; k += NT) {
-    const size_t g = E.n0 + D.abd_node[E.a0 + k];
-    double Am[9];
-    for (int c = 0; c < 9; ++c) Am[c] = D.x[3 * g + 3 + c] + a * D.pdir[3 * g + 3 + c];
-    eel += abd_element(Am, D.abd_kV[E.a0 + k], nullptr, nullptr);
-  }
-  for (int k = threadIdx.x; k < npt + nee; k += NT) {
-    const bool is_ee = k >= npt;
-    const int* row = is_ee ? cee + 4 * (k - npt) : cpt + 4 * k;
-    V3 x[4];
-    for (int j = 0; j < 4; ++j) x[j] = ld3(Y + 3 * row[j]);
-    double el = 0.0;
-    int fl;
-    if (is_ee) {
-      const int* eid = ceid + 2 * (k - npt);
-      fl = ee_element(x, D.edge_rest_sq[E.ed0 + eid[0]] * D.edge_rest_sq[E.ed0 + eid[1]], kappa, dhat, &el, nullptr,
-                      nullptr, 0);
-    } else {
-      fl = pt_element(x, kappa, dhat, &el, nullptr, nullptr, 0);
+    const double* Dmi = D.tet_Dmi + 9 * (size_t)tg;
+    const double V0 = D.tet_V0[tg], mu = D.tet_mu[tg], lam = D.tet_lam[tg];
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) x[j] = xv[j] + a[k] * pv[j];
+      double el = 0.0;
+      if (nh_element(x, Dmi, V0, mu, lam, &el, nullptr, nullptr) & EL_INVERTED) bad |= 1 << k;
+      else eel[k] += el;
     }
-    if (fl & EL_BAD_D) bad = 1;
-    else if (fl & EL_ACTIVE) ec += el;
+  }
+  for (int m = threadIdx.x; m < E.na; m += NT) {
+    const size_t g = E.n0 + D.abd_node[E.a0 + m];
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      double Am[9];
+      for (int c = 0; c < 9; ++c) Am[c] = D.x[3 * g + 3 + c] + a[k] * D.pdir[3 * g + 3 + c];
+      eel[k] += abd_element(Am, D.abd_kV[E.a0 + m], nullptr, nullptr);
+    }
+  }
+  for (int m = threadIdx.x; m < npt + nee; m += NT) {
+    const bool is_ee = m >= npt;
+    const int* row = is_ee ? cee + 4 * (m - npt) : cpt + 4 * m;
+    int rv[4];
+    for (int j = 0; j < 4; ++j) rv[j] = row[j];
+    const double epsx = is_ee ? D.edge_rest_sq[E.ed0 + ceid[2 * (m - npt)]] * D.edge_rest_sq[E.ed0 + ceid[2 * (m - npt) + 1]]
+                              : 0.0;
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) x[j] = ld3(Y + k * ys + 3 * rv[j]);
+      double el = 0.0;
+      const int fl = is_ee ? ee_element(x, epsx, kappa, dhat, &el, nullptr, nullptr, 0)
+                           : pt_element(x, kappa, dhat, &el, nullptr, nullptr, 0);
+      if (fl & EL_BAD_D) bad |= 1 << k;
+      else if (fl & EL_ACTIVE) ec[k] += el;
+    }
   }
   const int nanc = D.n_anc[e];
-  for (int k = threadIdx.x; k < nanc; k += NT) {
-    const size_t ai = (size_t)e * D.cap_anc + k;
-    V3 x[4], xp[4];
+  for (int m = threadIdx.x; m < nanc; m += NT) {
+    const size_t ai = (size_t)e * D.cap_anc + m;
+    int sv[4];
+    V3 xp[4];
     for (int j = 0; j < 4; ++j) {
-      const int s = D.anc_v[4 * ai + j];
-      x[j] = ld3(Y + 3 * s);
-      xp[j] = ld3(D.surf_prev + 3 * (size_t)(E.s0 + s));
+      sv[j] = D.anc_v[4 * ai + j];
+      xp[j] = ld3(D.surf_prev + 3 * (size_t)(E.s0 + sv[j]));
     }
-    ef += friction_element(x, xp, D.anc_gamma + 4 * ai, D.anc_T + 6 * ai, D.anc_lam[ai], D.anc_mu[ai], P[GRIP_P_EPSV],
-                           dt, nullptr, nullptr);
+#pragma unroll
+    for (int k = 0; k < NA; ++k) {
+      V3 x[4];
+      for (int j = 0; j < 4; ++j) x[j] = ld3(Y + k * ys + 3 * sv[j]);
+      ef[k] += friction_element(x, xp, D.anc_gamma + 4 * ai, D.anc_T + 6 * ai, D.anc_lam[ai], D.anc_mu[ai],
+                                P[GRIP_P_EPSV], dt, nullptr, nullptr);
+    }
   }
   bad = block_or(bad, sm);
-  ein = 0.5 * block_sum(ein, sm);
-  eel = block_sum(eel, sm);
-  ec = block_sum(ec, sm);
-  ef = block_sum(ef, sm);
-  if (bad) return INFINITY;
-  const double tot = ein + dt * dt * (eel + ec + ef);
-  return isfinite(tot) ? tot : INFINITY;
+  double v[4];
+#pragma unroll
+  for (int k = 0; k < NA; ++k) v[k] = ein[k];
+  block_sum_n<NA>(v, sm);
+#pragma unroll
+  for (int k = 0; k < NA; ++k) ein[k] = 0.5 * v[k], v[k] = eel[k];
+  block_sum_n<NA>(v, sm);
+#pragma unroll
+  for (int k = 0; k < NA; ++k) eel[k] = v[k], v[k] = ec[k];
+  block_sum_n<NA>(v, sm);
+#pragma unroll
+  for (int k = 0; k < NA; ++k) ec[k] = v[k], v[k] = ef[k];
+  block_sum_n<NA>(v, sm);
+#pragma unroll
+  for (int k = 0; k < NA; ++k) {
+    const double tot = ein[k] + dt * dt * (eel[k] + ec[k] + v[k]);
+    out[k] = ((bad >> k) & 1) || !isfinite(tot) ? INFINITY : tot;
+  }
 }
 
 __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
@@ -1112,6 +1177,7 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
     if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
+  if (!reuse) CTA_INFO(1u);
   const int npt = cn[0], nee = cn[1];
   double alpha0 = 1.0;
   if (npt + nee > 0) {
@@ -1148,6 +1214,7 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
       if (tmin <= 1.0) {
         double a = scaling * tmin;
         bool okall = false;
+        CTA_INFO(2u);
         for (int it = 0; it < 60; ++it) {
           int neg = 0;
           for (int t = threadIdx.x; t < E.ntet; t += NT) {
@@ -1197,15 +1264,34 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
     }
     alpha0 = fmin(alpha0, okv ? a : 0.0);
   }
-  // backtracking on strict decrease (solver.py:702-720)
-  const double E0 = env_energy(D, E, 0.0, cpt, npt, cee, ceid, nee, sm);
-  double alpha = alpha0, Et = INFINITY;
-  bool accepted = false;
+  // backtracking on strict decrease (solver.py:702-720): E0 and the first trial share one energy
+  // pass; after a rejection the next LS_NA halvings are evaluated together (the first that
+  // decreases is taken, exactly the sequential loop's choice: alpha halves exactly)
   const int maxls = (int)P[GRIP_P_MAXLS];
-  for (int it = 0; it < maxls; ++it) {
-    Et = env_energy(D, E, alpha, cpt, npt, cee, ceid, nee, sm);
-    if (Et < E0) { accepted = true; break; }
-    alpha *= 0.5;
+  double alpha = alpha0, Et = INFINITY, E0;
+  bool accepted = false;
+  {
+    const double a2[2] = {0.0, alpha};
+    double e2[2];
+    env_energy_n<2>(D, E, a2, cpt, npt, cee, ceid, nee, e2, sm);
+    E0 = e2[0];
+    if (maxls > 0) {
+      Et = e2[1];
+      if (Et < E0) accepted = true;
+      else alpha *= 0.5;
+    }
+  }
+  for (int it = 1; it < maxls && !accepted; it += LS_NA) {
+    double av[LS_NA], ev[LS_NA];
+    for (int k = 0; k < LS_NA; ++k) av[k] = k == 0 ? alpha : av[k - 1] * 0.5;
+    env_energy_n<LS_NA>(D, E, av, cpt, npt, cee, ceid, nee, ev, sm);
+    CTA_INFO_ADD(1u << 8);
+    for (int k = 0; k < LS_NA && it + k < maxls; ++k) {
+      Et = ev[k];
+      alpha = av[k];
+      if (Et < E0) { accepted = true; break; }
+    }
+    if (!accepted) alpha *= 0.5;
   }
   if (!accepted) {
     if (threadIdx.x == 0) {

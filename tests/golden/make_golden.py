@@ -405,6 +405,11 @@ def traj_cfg(kind, seed, n_steps, soft_object=False, soft_fingers=True, gravity_
                               "soft_fingers": soft_fingers})
 
 
+# config-3 object: the soft sphere lattice (sphere_tet_lattice, mesh.py:400) under kinematic fingers
+SOFT_SPHERE_JOBS = [("softsphere", dict(kind="sphere", seed=1, n_steps=25, soft_object=True, soft_fingers=False,
+                                        gravity_after=18))]
+
+
 def _traj_job(args):
     name, kw = args
     t0 = time.time()
@@ -658,6 +663,10 @@ def main():
                 ("soft", dict(kind="box", seed=0, n_steps=25, soft_object=True, soft_fingers=False,
                               gravity_after=18)),
             ]
+            if os.environ.get("GRIP_TRAJ_ONLY"):
+                jobs = [j for j in jobs + SOFT_SPHERE_JOBS if j[0] in os.environ["GRIP_TRAJ_ONLY"].split(",")]
+            else:
+                jobs += SOFT_SPHERE_JOBS
             for name, dt_ in pool.map(_traj_job, jobs):
                 print("traj", name, round(dt_, 1))
         if "bimanual" in want:

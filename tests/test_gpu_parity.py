@@ -52,11 +52,12 @@ def _rollout(env, scene, n_steps, gravity_after=None, halt=50.0):
 
 
 @pytest.mark.parametrize("name,grav,solver", [("cfg1", None, None), ("cylfail", None, None), ("cyl", None, None),
-                                               ("sphere", None, None), ("soft", 18, None), ("bimanual", None, None),
+                                               ("sphere", None, None), ("soft", 18, None), ("softsphere", 18, None),
+                                               ("bimanual", None, None),
                                                ("cfg1", None, "pcg"), ("soft", 18, "pcg")])
 def test_trajectory_matches_reference(golden, name, grav, solver, monkeypatch):
     """Every recorded step of the reference's trajectory (full fixture length: cfg1 50, cylinder /
-    sphere 20, soft object 25, bimanual 12).  solver="pcg": the block-Jacobi PCG alternative
+    sphere 20, soft box / soft sphere object 25, bimanual 12).  solver="pcg": the block-Jacobi PCG alternative
     (GRIP_SOLVER=pcg, the north star's solver) instead of the default skyline Cholesky."""
     from paper_2503_05020_b200.solver import Environment
     if solver:
@@ -100,7 +101,8 @@ def test_trajectory_matches_reference(golden, name, grav, solver, monkeypatch):
     print(f"{name}: {n} steps, worst |dx|/ell = {worst:.3e}")
 
 
-@pytest.mark.parametrize("name,bp", [("cfg1", None), ("sphere", None), ("soft", None), ("bimanual", None), ("cyl", None),
+@pytest.mark.parametrize("name,bp", [("cfg1", None), ("sphere", None), ("soft", None), ("softsphere", None),
+                                     ("bimanual", None), ("cyl", None),
                                      ("cfg1", "grid"), ("sphere", "grid"), ("soft", "grid"), ("bimanual", "grid"),
                                      ("cyl", "grid")])
 def test_candidate_sets_bit_exact(golden, name, bp, monkeypatch):

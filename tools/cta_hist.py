@@ -57,6 +57,7 @@ def main():
         recs.append((li, int(ln.key), r))
     for k, name in enumerate(DeviceBatch.CTA_KERNELS):
         spans, ratios, durs, per_lane = [], [], [], {}
+        infos, longest_info = [], []
         for li, key, r in recs:
             rk = r[r["kernel"] == k]
             for seq in np.unique(rk["seq"]):
@@ -72,6 +73,8 @@ def main():
                 spans.append(span)
                 ratios.append(span / m)
                 durs.extend(c["dur"][work].tolist())
+                infos.extend(c["info"][work].tolist())
+                longest_info.append(int(c["info"][work][np.argmax(c["dur"][work])]))
                 per_lane.setdefault(key, []).append(span)
         if not durs:
             continue
@@ -87,6 +90,16 @@ def main():
             "span_us_by_lane_key": {str(kk): float(np.mean(v)) / 1e3 for kk, v in per_lane.items()},
             "hist_ns_log2_edges": bins, "hist_counts": hist.tolist(),
         }
+        # kernel-specific CTA detail (CTA_INFO): line search bit 0 = fresh broad phase, bit 1 =
+        # tet filter halvings, bits 8.. = extra energy passes; candidates bit 0 = superset rebuild
+        iv = np.array(infos)
+        by = {}
+        for v in np.unique(iv):
+            sel = iv == v
+            by[str(int(v))] = {"ctas": int(sel.sum()), "mean_us": float(d[sel].mean()) / 1e3,
+                               "max_us": float(d[sel].max()) / 1e3,
+                               "launches_where_longest": int(sum(1 for x in longest_info if x == v))}
+        out["kernels"][name]["by_info"] = by
         print(name, json.dumps({kk: out["kernels"][name][kk] for kk in ("launch_span_us", "cta_us", "span_over_mean_cta")}))
     Path(args.out).write_text(json.dumps(out, indent=1))
 
