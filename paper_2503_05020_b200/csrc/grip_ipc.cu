@@ -753,7 +753,7 @@ int grip_begin_step(GripBatch* b, const uint8_t* active) {
   if (L.empty()) return 0;
   if (upload_list(b, L, b->d_list)) return -1;
   const int n = (int)L.size();
-  return run_with_growth(b, n, [&] { k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list); });
+  return run_with_growth(b, n, [&] { k_begin<<<n * BP_CL, NT, 0, b->stream>>>(b->D, b->d_list); });
 }
 
 // kernel ids for grip_kernel_stats
@@ -909,7 +909,7 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
   int n = (int)L.size();
   if (run_with_growth(b, n, [&] {
         int t = kt_begin(b, K_BEGIN);
-        k_begin<<<n, NT, 0, b->stream>>>(b->D, b->d_list);
+        k_begin<<<n * BP_CL, NT, 0, b->stream>>>(b->D, b->d_list);
         kt_end(b, t);
       }))
     return -1;
@@ -975,7 +975,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   kt_end(b, t);
   t = kt_begin(b, K_LS);
   D.launch_seq = ++b->seq_ctr;
-  k_linesearch<<<n, NT, 0, b->stream>>>(D, list);
+  k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
   b->launches += 3 + 7 + (b->direct ? 2 : 1);
@@ -1036,7 +1036,7 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
   CK(cudaMemcpyAsync(b->d_list2, b->h_lists + E, sizeof(int) * n, cudaMemcpyHostToDevice, b->stream));
   if (nb) {
     const int t = kt_begin(b, K_BEGIN);
-    k_begin<<<nb, NT, 0, b->stream>>>(D, b->d_list);
+    k_begin<<<nb * BP_CL, NT, 0, b->stream>>>(D, b->d_list);
     kt_end(b, t);
     b->launches++;
   }
@@ -1071,7 +1071,7 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
     if (!ovB.empty()) {
       if (upload_list(b, ovB, b->d_list)) return -1;
       const int m = (int)ovB.size();
-      if (run_with_growth(b, m, [&] { k_begin<<<m, NT, 0, b->stream>>>(D, b->d_list); })) return -1;
+      if (run_with_growth(b, m, [&] { k_begin<<<m * BP_CL, NT, 0, b->stream>>>(D, b->d_list); })) return -1;
     }
     std::vector<int> S2 = ovB;
     S2.insert(S2.end(), ovS.begin(), ovS.end());
@@ -1207,7 +1207,7 @@ int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
   for (int r = 0; r < rounds; ++r) {
     int t = kt_begin(b, K_BEGIN);
     D.launch_seq = ++b->seq_ctr;
-    k_begin<<<E, NT, 0, b->stream>>>(D, b->d_ident);
+    k_begin<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
     kt_end(b, t);
     sweep_launch(b, E, b->d_ident);
     t = kt_begin(b, K_FIN);

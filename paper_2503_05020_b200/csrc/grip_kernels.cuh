@@ -114,16 +114,20 @@ __device__ double env_ccd(const Dev& D, const EnvIx& E, const int* pt, int npt, 
 // ---------------------------------------------------------------------------
 // begin_step (solver.py:590-645)
 // ---------------------------------------------------------------------------
-__device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S);
+__device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S, const BPCl& cl);
 
-__global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
+// A cluster of BP_CL CTAs per env, for the kinematic CCD's broad phase (see k_linesearch); rank 0
+// does everything else.
+__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT) k_begin(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
-  const int e = list[blockIdx.x];
-  CTA_TIMER(0, e);
+  const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
+  const int e = list[blockIdx.x / BP_CL];
+  CTA_TIMER_IF(cl.rank == 0, 0, e);
   // device protocol: only envs whose protocol asked for a new step
   if (D.round_mode && !D.pr_i[(size_t)e * PI_N + PI_NEEDBEGIN]) return;
-  begin_env(D, e, sm, S);
+  begin_env(D, e, sm, S, cl);
+  if (cl.rank != 0) return;
   if (D.round_mode) {
     __syncthreads();
     if (threadIdx.x == 0 && !(D.flags[e] & FLAG_OVERFLOW)) {   // an overflowed begin is redone later
@@ -133,14 +137,17 @@ __global__ void __launch_bounds__(NT) k_begin(Dev D, const int* list) {
   }
 }
 
-__device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
+__device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S, const BPCl& cl) {
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dt = P[GRIP_P_DT], dhat = P[GRIP_P_DHAT];
-  if (threadIdx.x == 0) D.fin_done[e] = 0;
-  for (int i = threadIdx.x; i < 3 * E.nn; i += NT) D.x_t[3 * (size_t)E.n0 + i] = D.x[3 * (size_t)E.n0 + i];
-  env_sv_positions(D, E, D.x);
-  for (int i = threadIdx.x; i < 3 * E.ns; i += NT) D.surf_prev[3 * (size_t)E.s0 + i] = D.sv_pos[3 * (size_t)E.s0 + i];
+  const bool r0 = cl.rank == 0;
+  if (r0 && threadIdx.x == 0) D.fin_done[e] = 0;
+  if (r0) {
+    for (int i = threadIdx.x; i < 3 * E.nn; i += NT) D.x_t[3 * (size_t)E.n0 + i] = D.x[3 * (size_t)E.n0 + i];
+    env_sv_positions(D, E, D.x);
+    for (int i = threadIdx.x; i < 3 * E.ns; i += NT) D.surf_prev[3 * (size_t)E.s0 + i] = D.sv_pos[3 * (size_t)E.s0 + i];
+  }
   // which bodies move: kinematic with v != 0, soft with a prescribed mask and v != 0
   int moving = 0;
   for (int b = threadIdx.x; b < E.nb; b += NT) {
@@ -154,6 +161,7 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
     }
   }
   moving = block_or(moving, sm);
+  if (!moving && !r0) return;   // no broad phase: nothing for the other ranks (inputs are static)
   double alpha = 1.0;
   if (moving) {
     double md = 0.0;
@@ -164,23 +172,25 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
       const double* vb = D.body_vel + 3 * (size_t)(E.b0 + D.sv_body[g]);
       if (kind == 2) d = V3{vb[0] * dt, vb[1] * dt, vb[2] * dt};
       if (kind == 0 && !D.node_free[E.n0 + D.sv_node[g]]) d = V3{vb[0] * dt, vb[1] * dt, vb[2] * dt};
-      st3(D.sv_disp + 3 * (size_t)g, d);
+      if (r0) st3(D.sv_disp + 3 * (size_t)g, d);
       md = fmax(md, norm(d));
     }
     md = block_max(md, sm);
-    if (threadIdx.x == 0) D.md_kin[e] = md;
     int* cn = D.c2_n + 2 * e;
     const double rk = dhat + 2.0 * md;
     const bool reuse = cs_covers(D, e, rk);
-    __syncthreads();
+    cl_sync(cl);   // every rank has its decision before rank 0 changes its inputs
+    if (!r0 && reuse) return;
+    if (r0 && threadIdx.x == 0) D.md_kin[e] = md;
     if (reuse) {
       filter_from_superset(D, E, rk, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
                            D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, sm);
     } else if (!broad_phase_env(D, E, rk, D.c2_pt + (size_t)e * 4 * D.cap_pt, D.c2_ee + (size_t)e * 4 * D.cap_ee,
-                                D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm)) {
-      if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_BEGIN;
+                                D.c2_eid + (size_t)e * 2 * D.cap_ee, cn, S, sm, cl)) {
+      if (r0 && threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_BEGIN;
       return;
     }
+    if (!r0) return;
     if (cn[0] + cn[1] > 0) {
       int bad = 0;
       alpha = env_ccd(D, E, D.c2_pt + (size_t)e * 4 * D.cap_pt, cn[0], D.c2_ee + (size_t)e * 4 * D.cap_ee, cn[1],
@@ -263,7 +273,6 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S) {
 // ---------------------------------------------------------------------------
 // A cluster of BP_CL CTAs per env: a superset rebuild is split over the cluster (BPCl), the rest
 // runs on rank 0; the other ranks of an env whose superset still covers exit at once.
-constexpr int BP_CL = 4;
 __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
@@ -1145,21 +1154,26 @@ __device__ void env_energy_n(const Dev& D, const EnvIx& E, const double* a, cons
   }
 }
 
-__global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
+// A cluster of BP_CL CTAs per env: every rank computes the step's max surface displacement and
+// whether the candidate superset covers dhat + 2 md; after one cluster barrier (the decision's
+// inputs are only written by rank 0 after it) the other ranks exit, or join a fresh broad phase
+// (BPCl) and then exit; rank 0 runs the line search.
+__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
-  const int e = list[blockIdx.x];
-  CTA_TIMER(3, e);
+  const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
+  const int e = list[blockIdx.x / BP_CL];
+  CTA_TIMER_IF(cl.rank == 0, 3, e);
   if (D.ns_done[e] || !D.needs_ls[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dhat = P[GRIP_P_DHAT], scaling = P[GRIP_P_CCDSCALE];
   // disp = G p and its max norm
-  env_sv_positions(D, E, D.x);
+  if (cl.rank == 0) env_sv_positions(D, E, D.x);
   double md = 0.0;
   for (int i = threadIdx.x; i < E.ns; i += NT) {
     V3 d = sv_dir(D, E, i, D.pdir);
-    st3(D.sv_disp + 3 * (size_t)(E.s0 + i), d);
+    if (cl.rank == 0) st3(D.sv_disp + 3 * (size_t)(E.s0 + i), d);
     md = fmax(md, norm(d));
   }
   md = block_max(md, sm);
@@ -1169,14 +1183,16 @@ __global__ void __launch_bounds__(NT) k_linesearch(Dev D, const int* list) {
   int* ceid = D.c2_eid + (size_t)e * 2 * D.cap_ee;
   const double r2 = dhat + 2.0 * md;
   const bool reuse = cs_covers(D, e, r2);
-  __syncthreads();
-  if (threadIdx.x == 0) D.md_prev[e] = md;
+  cl_sync(cl);
+  if (cl.rank != 0 && reuse) return;
+  if (cl.rank == 0 && threadIdx.x == 0) D.md_prev[e] = md;
   if (reuse) {
     filter_from_superset(D, E, r2, cpt, cee, ceid, cn, sm);
-  } else if (!broad_phase_env(D, E, r2, cpt, cee, ceid, cn, S, sm)) {
-    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+  } else if (!broad_phase_env(D, E, r2, cpt, cee, ceid, cn, S, sm, cl)) {
+    if (cl.rank == 0 && threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
     return;
   }
+  if (cl.rank != 0) return;
   if (!reuse) CTA_INFO(1u);
   const int npt = cn[0], nee = cn[1];
   double alpha0 = 1.0;
