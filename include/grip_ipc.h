@@ -22,8 +22,9 @@
  *   grip_query_candidates          <- broad_phase (geometry/broadphase.py:101-155)
  *   grip_stress                    <- materials.compute_stress (materials.py:191-205)
  *
- * All pointers are HOST pointers; the library owns its device memory and its
- * CUDA stream.  Per-environment failures are data (GripStepReport.status),
+ * Pointers are HOST pointers except in the *_device entry points (device pointers, e.g. torch
+ * tensors' data_ptr()); the library owns its device memory and by default its CUDA stream
+ * (grip_set_stream hands it a caller's stream).  Per-environment failures are data (GripStepReport.status),
  * never return codes.  Return codes: 0 ok, <0 error (see grip_last_error()).
  */
 #ifndef GRIP_IPC_H
@@ -149,6 +150,13 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
 int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t* finalized,
                GripStepReport* reports, double* alphas);
 int grip_get_state(GripBatch* b, double* x, double* v, double* kin /* n_sv*3, or NULL */);
+/* Run the batch on a caller's cudaStream_t (NULL: the library's own stream again); queued work on
+ * the previous stream is finished first; the caller keeps ownership of its stream. */
+int grip_set_stream(GripBatch* b, void* stream);
+/* Device-pointer forms (torch tensors): stream-ordered copies on the batch's stream, no sync.
+ * x, v: n_node*3, kin: n_sv*3; gravity: n_env*3, body_vel: n_body*3 (any may be NULL). */
+int grip_get_state_device(GripBatch* b, double* x, double* v, double* kin);
+int grip_set_controls_device(GripBatch* b, const double* gravity, const double* body_vel);
 int grip_set_state(GripBatch* b, const double* x, const double* v, const double* kin);
 int grip_get_surface(GripBatch* b, double* sv /* n_sv*3 */);
 /* per env-local body pair: summed barrier force (lambda) of active stencils at the

@@ -100,7 +100,8 @@ def load():
         ("grip_get_frames", [vp, vp, vp, vp, vp, vp]),
         ("grip_sdf_nn", [vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp, i32, vp]),
         ("grip_set_priority", [vp, i32]), ("grip_contacts_now", [vp, vp, dbl, vp]),
-        ("grip_check_finite", [vp, vp]), ("grip_cta_records", [vp, vp, ctypes.c_int64, vp, i32]),
+        ("grip_check_finite", [vp, vp]), ("grip_set_stream", [vp, vp]),
+        ("grip_get_state_device", [vp, vp, vp, vp]), ("grip_set_controls_device", [vp, vp, vp]), ("grip_cta_records", [vp, vp, ctypes.c_int64, vp, i32]),
         ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
         ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
@@ -336,6 +337,38 @@ class DeviceBatch:
         check(self.lib.grip_get_state(self.h, ptr(x), ptr(v), ptr(kin)))
         return x, v, kin
 
+    # -- torch interop: a caller's stream and device tensors (no host round trip) ---------------
+    def set_stream(self, stream=None):
+        """Run on a torch.cuda.Stream (or a raw cudaStream_t int); None: the library's own stream."""
+        handle = None if stream is None else (stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+        check(self.lib.grip_set_stream(self.h, ctypes.c_void_p(handle) if handle else None))
+
+    def state_tensors(self, out=None):
+        """x, v (n_node, 3) and kinematic positions (n_sv, 3) as float64 CUDA tensors, copied
+        device-to-device on the batch's stream (grip_get_state_device)."""
+        import torch
+        p = self.packed
+        dev = torch.device("cuda", torch.cuda.current_device())
+        x, v, kin = out or (torch.empty((p.n_node_total, 3), dtype=torch.float64, device=dev),
+                            torch.empty((p.n_node_total, 3), dtype=torch.float64, device=dev),
+                            torch.empty((p.n_sv_total, 3), dtype=torch.float64, device=dev))
+        for t in (x, v, kin):
+            if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError("state tensors must be contiguous float64 CUDA tensors")
+        check(self.lib.grip_get_state_device(self.h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(v.data_ptr()),
+                                             ctypes.c_void_p(kin.data_ptr())))
+        return x, v, kin
+
+    def set_controls_tensors(self, gravity=None, body_vel=None):
+        """Per-env gravity (n_env, 3) and per-body velocities (n_body, 3) from float64 CUDA tensors."""
+        def dp(t):
+            if t is None:
+                return None
+            if t.dtype.is_floating_point is False or not t.is_cuda or not t.is_contiguous() or t.element_size() != 8:
+                raise ValueError("control tensors must be contiguous float64 CUDA tensors")
+            return ctypes.c_void_p(t.data_ptr())
+        check(self.lib.grip_set_controls_device(self.h, dp(gravity), dp(body_vel)))
+
     def set_state(self, x=None, v=None, kin=None):
         f = lambda a: None if a is None else np.ascontiguousarray(a, np.float64)  # noqa: E731
         x, v, kin = f(x), f(v), f(kin)
@@ -480,7 +513,7 @@ class DeviceBatch:
     def set_profiling(self, on=True):
         check(self.lib.grip_set_profiling(self.h, int(on)))
 
-    KERNELS = ("begin", "candidates", "work_scan", "elements", "assemble_pcg", "line_search", "finalize")
+    KERNELS = ("begin", "candidates", "work_scan", "elements", "assemble_pcg", "line_search", "finalize", "tets")
 
     def kernel_stats(self):
         out = {}
