@@ -72,9 +72,13 @@ EL_BYTES = {"tets": 16 + 96 + 72 + 24 + EL_OUT,        # node ids, 4 positions, 
 ASM_BYTES = 1256.0   # per element: its Hessian, gradient and energy read once by the assembly
 
 # kernel groups as timed live (grip_kernel_stats) -> the kernels of the ncu capture; launches per round
-KGROUPS = {"elements": {"k_tet_front": 1, "k_elements_w": 1, "k_tet_jacobi2": 2, "k_tet_back": 1, "k_tet_finish": 1},
+# (k_tet_jacobi2 runs twice per round: the tets' launch on the second stream with the tet grid, the
+# contacts' on the main stream with 148 blocks -- told apart by grid size in the capture)
+KGROUPS = {"tets": {"k_tet_scan": 1, "k_tet_front": 1, "k_tet_jacobi2@tet": 1, "k_tet_back": 1},
+           "elements": {"k_elements_w": 1, "k_tet_jacobi2@contact": 1, "k_tet_finish": 1},
            "assemble_pcg": {"k_contact_K": 1, "k_assemble_direct": 1}, "candidates": {"k_candidates": 1},
-           "line_search": {"k_linesearch": 1}, "begin": {"k_begin": 1}, "finalize": {"k_finalize": 1}}
+           "line_search": {"k_linesearch": 1, "k_eig_commit": 1}, "begin": {"k_begin": 1}, "finalize": {"k_finalize": 1}}
+EL_GROUP = {"tets": ("tets",), "elements": ("affine", "contacts", "anchors")}
 NCU_FULL = [ROOT / "profiles" / "r2_ncu_full.json", ROOT / "profiles" / "r1_ncu_full_v5.json"]
 
 
@@ -99,6 +103,9 @@ def _ncu_group(group):
         acc = {}
         for d in rows:
             k = d["kernel"].split("::")[-1].split("(")[0]
+            if k == "k_tet_jacobi2":
+                grid = int(float(str(d.get("launch__grid_size", "0")).split()[0].replace(",", "")))
+                k += "@contact" if grid == 148 else "@tet"
             if k not in KGROUPS.get(group, {}):
                 continue
             b = 0.0
@@ -495,7 +502,9 @@ def kernel_report(runner, env_steps_s, ms_max, peak):
     nl = max(ks[dom]["launches"], 1)
     sec_per_launch = ks[dom]["ms"] / 1e3 / nl
     el_alg = sum(EL_BYTES[k] * units[k] for k in EL_BYTES)
-    alg = {"elements": el_alg, "assemble_pcg": ASM_BYTES * sum(units.values())}.get(dom)
+    alg = {g: sum(EL_BYTES[k] * units[k] for k in ks_) for g, ks_ in EL_GROUP.items()}
+    alg["assemble_pcg"] = ASM_BYTES * sum(units.values())
+    alg = alg.get(dom)
     if alg is not None:
         roof["alg_bytes_per_launch"] = alg / nl
         roof["achieved"] = alg / nl / sec_per_launch / 1e9
@@ -506,7 +515,7 @@ def kernel_report(runner, env_steps_s, ms_max, peak):
     if traffic is not None:
         # the capture's per-round figures rescaled to the timed launches by element units per launch
         cap_units = sum(((meta or {}).get("units_per_round") or {}).values()) or None
-        timed_units = sum(units.values()) / nl if dom == "elements" or dom == "assemble_pcg" else None
+        timed_units = sum(units.values()) / nl if dom in ("elements", "tets", "assemble_pcg") else None
         s = (timed_units / cap_units) if (cap_units and timed_units) else 1.0
         roof["traffic"] = traffic * s
         roof["traffic_source"] = src

@@ -113,6 +113,7 @@ struct Dev {
   int max_alpha;
   // candidates (uniform capacity per env)
   int cap_pt, cap_ee;
+  unsigned* need;    // 4: the largest pt / ee / active / anchor count that overflowed its capacity (growth sizes)
   int *c1_pt, *c1_ee, *c1_eid, *c1_n;   // c1_n[2e]=n_pt, [2e+1]=n_ee
   int *c2_pt, *c2_ee, *c2_eid, *c2_n;
   // candidate superset at radius cs_R >= every radius needed before x changes; exact sets are
@@ -132,6 +133,8 @@ struct Dev {
   int* n_anc;
   double *el_E, *el_g, *el_H;
   int* el_idx;
+  int* tflag;        // per env: ERR_INVERTED from k_tet_front this sweep (its own word: the tet chain runs
+                     // on the second stream, concurrently with k_candidates writing flags)
   int* work_off;     // per list position (n+1)
   int* cwork_off;    // per list position (n+1): contact / friction elements only
   int* twork_off;    // per list position (n+1): tets only (k_tet_front)
@@ -698,7 +701,11 @@ __device__ bool broad_phase_grid(const Dev& D, const EnvIx& E, double r, int* ou
             npt = block_scan_array(cnt, E.ns, sm);
             if (threadIdx.x == 0) cnt[E.ns] = npt;
             __syncthreads();
-            if (npt > D.cap_pt) { ok = false; break; }
+            if (npt > D.cap_pt) {
+            if (threadIdx.x == 0) atomicMax(&D.need[0], (unsigned)npt);
+            ok = false;
+            break;
+          }
           }
         }
       }
@@ -774,7 +781,11 @@ __device__ bool broad_phase_grid(const Dev& D, const EnvIx& E, double r, int* ou
           nee = block_scan_array(cnt, E.ne, sm);
           if (threadIdx.x == 0) cnt[E.ne] = nee;
           __syncthreads();
-          if (nee > D.cap_ee) { ok = false; break; }
+          if (nee > D.cap_ee) {
+            if (threadIdx.x == 0) atomicMax(&D.need[1], (unsigned)nee);
+            ok = false;
+            break;
+          }
         }
       }
     }
@@ -1142,11 +1153,13 @@ __device__ bool broad_phase_direct(const Dev& D, const EnvIx& E, double r, int* 
   const int npt = bp_pairs<3>(D, E, X, nq, qid, nts, cid, cv, cb, r, cnt, out_pt, nullptr, D.cap_pt, S, sm, cl);
   int nee = 0;
   bool ok = npt <= D.cap_pt;
+  if (!ok && cl.rank == 0 && threadIdx.x == 0) atomicMax(&D.need[0], (unsigned)npt);
   // ---------------- edge-edge ----------------
   if (ok) {
     const int nes = bp_compact<2>(D, E, X, edges, E.ne, D.body_edge_lo, D.body_edge_hi, rc, cid, cv, cb, S, sm, cl);
     nee = bp_pairs<2>(D, E, X, nes, nullptr, nes, cid, cv, cb, r, cnt, out_ee, out_eid, D.cap_ee, S, sm, cl);
     ok = nee <= D.cap_ee;
+    if (!ok && cl.rank == 0 && threadIdx.x == 0) atomicMax(&D.need[1], (unsigned)nee);
   }
   if (cl.rank == 0 && threadIdx.x == 0) {
     out_n[0] = npt;

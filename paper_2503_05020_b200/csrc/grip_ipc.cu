@@ -33,6 +33,13 @@ thread_local std::string g_err;
     }                                                                                       \
   } while (0)
 
+// in void launch helpers: remember the first error; the caller's next CK'd call reports it
+#define CK_VOID(call)                                                                       \
+  do {                                                                                      \
+    cudaError_t _e = (call);                                                                \
+    if (_e != cudaSuccess && g_err.empty()) g_err = std::string(#call) + ": " + cudaGetErrorString(_e); \
+  } while (0)
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -44,6 +51,9 @@ struct DBuf {
 struct GripBatch {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;   // the library's stream (stream may be a caller's, grip_set_stream)
+  cudaStream_t aux = nullptr;          // second stream: the tet chain of a sweep, forked / joined by events
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Dev D{};
   int n_env = 0, n_node = 0, n_sv = 0, n_tet = 0, n_abd = 0, n_body = 0, n_free = 0, n_blk = 0;
@@ -197,14 +207,25 @@ int alloc_dynamic(GripBatch* b, bool keep_anchors, int old_cap_anc) {
   return 0;
 }
 
+// Grow only the capacities that overflowed, to 1.25x the largest count the kernels reported
+// (D.need); buffers are per-env uniform, so one heavy env must not double every array of a
+// 3200-env batch.  A flagged overflow with no recorded need (should not happen) doubles all.
 int grow(GripBatch* b) {
   Dev& D = b->D;
   const int old_anc = D.cap_anc;
-  D.cap_pt *= 2;
-  D.cap_ee *= 2;
-  D.cap_act *= 2;
-  D.cap_anc *= 2;
-  D.cap_cells *= 2;
+  unsigned need[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(need, D.need, sizeof(need), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  int* caps[4] = {&D.cap_pt, &D.cap_ee, &D.cap_act, &D.cap_anc};
+  bool any = false;
+  for (int k = 0; k < 4; ++k)
+    if ((long long)need[k] > *caps[k]) {
+      *caps[k] = std::max(*caps[k] + 1, (int)std::min<long long>((long long)need[k] * 5 / 4 + 8, 1ll << 30));
+      any = true;
+    }
+  if (!any)
+    for (int k = 0; k < 4; ++k) *caps[k] *= 2;
+  CK(cudaMemsetAsync(D.need, 0, sizeof(need), b->stream));
   return alloc_dynamic(b, true, old_anc);
 }
 
@@ -254,6 +275,10 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   GripBatch* b = new GripBatch();
   b->device = device;
   CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
+  b->own_stream = b->stream;
+  CK(cudaStreamCreateWithFlags(&b->aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreate(&b->ev0));
   CK(cudaEventCreate(&b->ev1));
   const int E = d->n_env;
@@ -577,10 +602,12 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.md_prev = b->alloc<double>(E);
   D.md_kin = b->alloc<double>(E);
   D.bp_lc = b->alloc<int>((size_t)E * 3 * std::max(max_tri, max_edge));
+  D.need = b->alloc<unsigned>(4);
   D.c1_n = b->alloc<int>(2 * (size_t)E);
   D.c2_n = b->alloc<int>(2 * (size_t)E);
   D.n_act = b->alloc<int>(E);
   D.n_anc = b->alloc<int>(E);
+  D.tflag = b->alloc<int>(E);
   D.work_off = b->alloc<int>(E + 1);
   D.cwork_off = b->alloc<int>(E + 1);
   D.twork_off = b->alloc<int>(E + 1);
@@ -682,8 +709,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.surf_prev, D.kin_pos, D.sv_disp, D.ell, D.tol, D.residual, D.energy, D.alphas, D.min_dist, D.time, D.iters,
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
-        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
-        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_scr, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
+        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.tflag, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
+        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_scr, D.need, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
@@ -728,7 +755,10 @@ int grip_destroy(GripBatch* b) {
   if (b->d_reset) cudaFree(b->d_reset);
   cudaEventDestroy(b->ev0);
   cudaEventDestroy(b->ev1);
-  cudaStreamDestroy(b->stream);
+  cudaStreamDestroy(b->own_stream);   // a caller's stream (grip_set_stream) is the caller's
+  cudaStreamDestroy(b->aux);
+  cudaEventDestroy(b->ev_fork);
+  cudaEventDestroy(b->ev_join);
   delete b;
   return 0;
 }
@@ -757,9 +787,9 @@ int grip_begin_step(GripBatch* b, const uint8_t* active) {
 }
 
 // kernel ids for grip_kernel_stats
-enum { K_BEGIN = 0, K_CAND, K_SCAN, K_ELEM, K_ASM, K_LS, K_FIN, K_OTHER };
+enum { K_BEGIN = 0, K_CAND, K_SCAN, K_ELEM, K_ASM, K_LS, K_FIN, K_TET };
 
-static int kt_begin(GripBatch* b, int kid) {
+static int kt_begin(GripBatch* b, int kid, cudaStream_t st = nullptr) {
   if (!b->prof) return -1;
   const int pair = (int)b->pending_k.size();
   while ((int)b->kev.size() < 2 * (pair + 1)) {
@@ -767,12 +797,12 @@ static int kt_begin(GripBatch* b, int kid) {
     cudaEventCreate(&ev);
     b->kev.push_back(ev);
   }
-  cudaEventRecord(b->kev[2 * pair], b->stream);
+  cudaEventRecord(b->kev[2 * pair], st ? st : b->stream);
   b->pending_k.push_back({kid, pair});
   return pair;
 }
-static void kt_end(GripBatch* b, int pair) {
-  if (pair >= 0) cudaEventRecord(b->kev[2 * pair + 1], b->stream);
+static void kt_end(GripBatch* b, int pair, cudaStream_t st = nullptr) {
+  if (pair >= 0) cudaEventRecord(b->kev[2 * pair + 1], st ? st : b->stream);
 }
 // fold the recorded launch times into the per-kernel totals (after a stream sync)
 static void kt_collect(GripBatch* b, int n_listed = -1) {
@@ -949,7 +979,19 @@ int grip_step(GripBatch* b, const uint8_t* active, GripStepReport* reports, doub
 // the sweep kernels over a device list of n envs, no host synchronisation
 static void sweep_launch(GripBatch* b, int n, const int* list) {
   Dev& D = b->D;
-  int t = kt_begin(b, K_CAND);
+  // fork: the tet chain (energy, gradient, deflated Hessian, batched eigen-clamp) depends on x
+  // only, so it runs on the second stream while the candidates and the contact / ABD / friction
+  // elements run on the main one; they join before the assembly
+  CK_VOID(cudaEventRecord(b->ev_fork, b->stream));
+  CK_VOID(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
+  int t = kt_begin(b, K_TET, b->aux);
+  k_tet_scan<<<1, NT, 0, b->aux>>>(D, list, n);
+  k_tet_front<<<b->eg[0], TF, 0, b->aux>>>(D, list, n);
+  k_tet_jacobi2<<<b->eg[2], TJ, 0, b->aux>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
+  k_tet_back<<<b->eg[3], EW * 32, 0, b->aux>>>(D, D.jac_list, D.jac_n, D.tet_W);
+  kt_end(b, t, b->aux);
+  CK_VOID(cudaEventRecord(b->ev_join, b->aux));
+  t = kt_begin(b, K_CAND);
   D.launch_seq = ++b->seq_ctr;
   k_candidates<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
@@ -957,18 +999,16 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   k_work_scan<<<1, NT, 0, b->stream>>>(D, list, n);
   kt_end(b, t);
   t = kt_begin(b, K_ELEM);
-  k_tet_front<<<b->eg[0], TF, 0, b->stream>>>(D, list, n);
   k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, list, n);
-  k_tet_jacobi2<<<b->eg[2], TJ, 0, b->stream>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
   k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
-  k_tet_back<<<b->eg[3], EW * 32, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
   k_tet_finish<<<148 * 2, EW * 32, 0, b->stream>>>(D, D.cjac_list, D.cjac_n, D.cjac_W, nullptr);
   kt_end(b, t);
+  CK_VOID(cudaStreamWaitEvent(b->stream, b->ev_join, 0));   // join
   t = kt_begin(b, K_ASM);
   if (b->direct) {
     k_contact_K<<<148 * 2, NT, 0, b->stream>>>(D, list, n);
     D.launch_seq = ++b->seq_ctr;
-  k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
+    k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
   } else {
     k_assemble_solve<<<n, NT, 0, b->stream>>>(D, list);
   }
@@ -978,7 +1018,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
-  b->launches += 3 + 7 + (b->direct ? 2 : 1);
+  b->launches += 4 + 3 + 3 + (b->direct ? 2 : 1) + 2;
   b->sweeps += 1;
 }
 
@@ -1278,11 +1318,45 @@ int grip_set_priority(GripBatch* b, int priority) {
   int lo = 0, hi = 0;   // CUDA: numerically lower = higher priority (hi <= lo)
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   const int p = std::max(hi, std::min(lo, lo - priority));
+  const bool using_own = b->stream == b->own_stream;
   CK(cudaStreamSynchronize(b->stream));
   cudaStream_t s = nullptr;
   CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, p));
-  CK(cudaStreamDestroy(b->stream));
-  b->stream = s;
+  CK(cudaStreamDestroy(b->own_stream));
+  b->own_stream = s;
+  if (using_own) b->stream = s;
+  CK(cudaStreamSynchronize(b->aux));
+  cudaStream_t a = nullptr;
+  CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, p));
+  CK(cudaStreamDestroy(b->aux));
+  b->aux = a;
+  return 0;
+}
+
+// Run the batch on a caller's CUDA stream (e.g. a torch.cuda.Stream's handle) from now on, or on
+// the library's own stream again with stream == NULL.  Work already queued on the previous stream
+// is finished first; the caller keeps ownership of its stream.
+int grip_set_stream(GripBatch* b, void* stream) {
+  CK(cudaStreamSynchronize(b->stream));
+  b->stream = stream ? static_cast<cudaStream_t>(stream) : b->own_stream;
+  return 0;
+}
+
+// Device-pointer forms of the state / control transfers (torch tensors' data pointers): copies
+// queued on the batch's stream, no synchronisation (stream order is the caller's contract).
+int grip_get_state_device(GripBatch* b, double* x, double* v, double* kin) {
+  if (x) CK(cudaMemcpyAsync(x, b->D.x, 3 * sizeof(double) * b->n_node, cudaMemcpyDeviceToDevice, b->stream));
+  if (v) CK(cudaMemcpyAsync(v, b->D.v, 3 * sizeof(double) * b->n_node, cudaMemcpyDeviceToDevice, b->stream));
+  if (kin) CK(cudaMemcpyAsync(kin, b->D.kin_pos, 3 * sizeof(double) * b->n_sv, cudaMemcpyDeviceToDevice, b->stream));
+  return 0;
+}
+
+int grip_set_controls_device(GripBatch* b, const double* gravity, const double* body_vel) {
+  if (gravity)
+    CK(cudaMemcpyAsync(b->D.gravity, gravity, 3 * sizeof(double) * b->n_env, cudaMemcpyDeviceToDevice, b->stream));
+  if (body_vel)
+    CK(cudaMemcpyAsync(b->D.body_vel, body_vel, 3 * sizeof(double) * b->n_body, cudaMemcpyDeviceToDevice, b->stream));
+  b->snap_valid = false;
   return 0;
 }
 
@@ -1503,6 +1577,7 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
   D.el_H = (double*)dalloc(sizeof(double) * 144 * (size_t)n);
   D.el_idx = (int*)dalloc(sizeof(int) * 4 * (size_t)n);
   D.flags = (int*)dalloc(sizeof(int));
+  D.tflag = (int*)dalloc(sizeof(int));
   int* d_flags = (int*)dalloc(sizeof(int) * n);
   double* d_in = (double*)up(in, sizeof(double) * (size_t)n * stride);
   if (type == 2) {
@@ -1538,7 +1613,7 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
     if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) rc = -1;
     if (!rc && eig) cudaMemcpy(eig, D.tet_eig, sizeof(double) * 81 * (size_t)n, cudaMemcpyDeviceToHost);
     int ff = 0;
-    cudaMemcpy(&ff, D.flags, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&ff, D.tflag, sizeof(int), cudaMemcpyDeviceToHost);
     for (int k = 0; k < n; ++k) flags[k] = ff;
   } else {
     D.cjac_S = (double*)dalloc(sizeof(double) * 45 * (size_t)n);

@@ -330,28 +330,31 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candida
   if (threadIdx.x == 0) {
     D.n_act[e] = base;
     if (bad) D.flags[e] |= ERR_CONTACT_D;
-    if (base > D.cap_act) D.flags[e] |= FLAG_OVERFLOW;
+    if (base > D.cap_act) {
+      D.flags[e] |= FLAG_OVERFLOW;
+      atomicMax(&D.need[2], (unsigned)base);
+    }
   }
 }
 
 // exclusive scan of per-env element work over the pending list (single CTA)
+// exclusive scan of per-env contact / ABD element work over the pending list (single CTA)
 __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n) {
   __shared__ Red sm;
   int base = 0;
-  double ct = 0.0, ca = 0.0, cc = 0.0, cf = 0.0, cn = 0.0;   // cn: envs iterating (newton_iteration calls)
-  int cbase = 0, tbase = 0, ebase = 0;
+  double ca = 0.0, cc = 0.0, cf = 0.0, cn = 0.0;   // cn: envs iterating (newton_iteration calls)
+  int cbase = 0, ebase = 0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
-    int w = 0, wc = 0, wt = 0, we = 0;
+    int w = 0, wc = 0, we = 0;
     if (i < n) {
       const int e = list[i];
       if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e]) {
         const int nt = D.tet_off[e + 1] - D.tet_off[e], na = D.abd_off[e + 1] - D.abd_off[e];
         wc = D.n_act[e] + D.n_anc[e];
         w = nt + na + wc;
-        wt = nt;
         we = na + wc;
-        ct += nt; ca += na; cc += D.n_act[e]; cf += D.n_anc[e]; cn += 1.0;
+        ca += na; cc += D.n_act[e]; cf += D.n_anc[e]; cn += 1.0;
       }
     }
     int tot;
@@ -361,24 +364,50 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
     const int cpre = block_scan(wc, sm, &tot);
     if (i < n) D.cwork_off[i] = cbase + cpre;
     cbase += tot;
-    const int tpre = block_scan(wt, sm, &tot);
-    if (i < n) D.twork_off[i] = tbase + tpre;
-    tbase += tot;
     const int epre = block_scan(we, sm, &tot);
     if (i < n) D.ework_off[i] = ebase + epre;
     ebase += tot;
   }
-  ct = block_sum(ct, sm); ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
+  ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
   cn = block_sum(cn, sm);
   if (threadIdx.x == 0) {
     D.work_off[n] = base;
     D.cwork_off[n] = cbase;
-    D.twork_off[n] = tbase;
     D.ework_off[n] = ebase;
-    *D.jac_n = 0;   // the element kernel appends deferred tet / contact clamps
-    *D.cjac_n = 0;
-    D.stats[0] += ct; D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;
+    *D.cjac_n = 0;   // k_elements_w appends deferred contact clamps
+    D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;
     D.stats[7] += cn;
+  }
+}
+
+// The tet chain's scan (second stream): tets of every pending env that is not done.  It cannot
+// read the overflow flags k_candidates is writing concurrently; an env whose candidates
+// overflow computes its tets anyway (its assembly is skipped, its warm starts not committed).
+__global__ void __launch_bounds__(NT) k_tet_scan(Dev D, const int* list, int n) {
+  __shared__ Red sm;
+  double ct = 0.0;
+  int tbase = 0;
+  for (int s = 0; s < n; s += NT) {
+    const int i = s + threadIdx.x;
+    int wt = 0;
+    if (i < n) {
+      const int e = list[i];
+      D.tflag[e] = 0;
+      if (!D.ns_done[e]) {
+        wt = D.tet_off[e + 1] - D.tet_off[e];
+        ct += wt;
+      }
+    }
+    int tot;
+    const int tpre = block_scan(wt, sm, &tot);
+    if (i < n) D.twork_off[i] = tbase + tpre;
+    tbase += tot;
+  }
+  ct = block_sum(ct, sm);
+  if (threadIdx.x == 0) {
+    D.twork_off[n] = tbase;
+    *D.jac_n = 0;   // k_tet_front appends deferred tet clamps
+    D.stats[0] += ct;
   }
 }
 
@@ -623,7 +652,7 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
   Red& sm = A.sm;
   const int e = E.e;
   // element-level failures, in the reference's raise order (_elastic before contact)
-  if (D.flags[e] & ERR_INVERTED) { fail_env(D, e, GRIP_R_INVERTED); return false; }
+  if (D.tflag[e] & ERR_INVERTED) { fail_env(D, e, GRIP_R_INVERTED); return false; }
   if (D.flags[e] & ERR_CONTACT_D) { fail_env(D, e, GRIP_R_CONTACT_D); return false; }
   const size_t elbase = (size_t)e * D.cap_el;
   const int nce = D.n_act[e] + D.n_anc[e];
@@ -1494,7 +1523,10 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
     base += tot;
   }
   if (base > D.cap_anc && !failed) {
-    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_FIN;
+    if (threadIdx.x == 0) {
+      D.flags[e] |= FLAG_OVERFLOW | FLAG_OVF_FIN;
+      atomicMax(&D.need[3], (unsigned)base);
+    }
     return;
   }
   dmin = block_min(dmin, sm);
@@ -1919,7 +1951,10 @@ __global__ void __launch_bounds__(NT) k_contacts_now(Dev D, const int* list, dou
     base += tot;
   }
   if (base > D.cap_anc) {   // more active stencils than event rows: grow and redo
-    if (threadIdx.x == 0) D.flags[e] |= FLAG_OVERFLOW;
+    if (threadIdx.x == 0) {
+      D.flags[e] |= FLAG_OVERFLOW;
+      atomicMax(&D.need[3], (unsigned)base);
+    }
     return;
   }
   dmin = block_min(dmin, sm);

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
       const double J = det3(F);
       double* Hg = D.el_H + slot * 144;
       if (!(J > 0.0)) {
-        atomicOr(&D.flags[e], ERR_INVERTED);
+        atomicOr(&D.tflag[e], ERR_INVERTED);
         D.el_E[slot] = 0.0;
 #pragma unroll
         for (int j = 0; j < 12; ++j) D.el_g[slot * 12 + j] = 0.0;
