@@ -16,6 +16,7 @@
 namespace grip {
 
 constexpr int PW = 8;       // panel width = envelope alignment
+constexpr int RE_MAXP = 128;  // panels per segment with a row bound (longer segments: no pruning)
 constexpr int MAXSEG = 8;   // independent segments factored concurrently (2 warp groups)
 
 struct DirShared {
@@ -24,6 +25,7 @@ struct DirShared {
   int nseg;                // independent row segments ahead of the tail (hub) rows
   int sc_next;             // sky_scatter_rows: next node (dynamic schedule)
   int seg[MAXSEG + 1];     // segment starts, seg[nseg] = tail start (DOFs)
+  int rend[2][RE_MAXP];    // sky_panels: per panel, end of the rows whose envelope reaches it (per group)
 };
 
 // dynamic shared memory in front of the skyline: rdiag[nd] | xv[nd] | fcd[nd] | ro[nd+1] | fcn[max_free]
@@ -314,22 +316,53 @@ __device__ __forceinline__ void trail_row(const Sky& S, int i, int kb, int wb, i
   }
 }
 
-__device__ bool sky_panels(const Sky& S, double* rdiag, int c0, int c1, int x0, int n, const Grp& G, int* okf) {
+// L[i][j] -= L[i][panel] . L[j][panel] for one entry (the same c order as a row-wise update, so
+// the same doubles); rows whose envelope starts after the panel are structurally zero in it
+__device__ __forceinline__ void trail_pair(const Sky& S, int i, int j, int kb, int wb) {
+  if (S.fc[i] > kb || S.fc[j] > kb) return;
+  const double* pi = &S.at(i, kb);
+  const double* pj = &S.at(j, kb);
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < PW; ++c)
+    if (c < wb) acc += pi[c] * pj[c];
+  S.at(i, j) -= acc;
+}
+
+// Trailing update of a panel as a flat list of (row, column) entries (not a warp per row: a
+// banded row has only ~ the bandwidth of columns, so most lanes of a row-wise warp idled).
+// Rows [j0, re) (re: the last row whose envelope reaches the panel, from the group's rend
+// table) x columns [j0, row], then the extra rows [x0, n) x columns [j0, c1).  The group's first
+// warp takes the next diagonal block's rows [j0, j0 + nb) (look-ahead), the other warps the rest.
+__device__ bool sky_panels(const Sky& S, double* rdiag, int c0, int c1, int x0, int n, const Grp& G, int* okf,
+                           int* rend) {
   static_assert(NT / 64 >= 2, "look-ahead needs two warps per group");
   const int lane = G.t & 31;
   if (c0 >= c1) return true;
+  const int np = (c1 - c0 + PW - 1) / PW;
+  const bool pruned = np <= RE_MAXP;
+  if (pruned) {   // rend[p] = 1 + last row whose envelope starts in panel p (prefix max below)
+    for (int p = G.t; p < np; p += G.nt) rend[p] = 0;
+    G.sync();
+    for (int i = c0 + G.t; i < c1; i += G.nt)   // (tail rows' envelopes start before the tail)
+      atomicMax(&rend[S.fc[i] <= c0 ? 0 : (S.fc[i] - c0) / PW], i + 1);
+  }
   if (G.w == 0) {
     const bool ok = diag_factor(S, rdiag, c0, min(PW, c1 - c0), lane);
     if (lane == 0) *okf = ok;
   }
   G.sync();
+  int reach = c0;   // running prefix max of rend
   for (int kb = c0; kb < c1; kb += PW) {
     if (!*okf) return false;
     const int wb = min(PW, c1 - kb);
     const int j0 = kb + wb;
-    const int nrow = (c1 - j0) + (n - x0);
+    if (pruned) reach = max(reach, rend[(kb - c0) / PW]);
+    const int re = pruned ? min(max(reach, j0), c1) : c1;
+    const int nband = re - j0, ntail = n - x0;
+    const int nrow = nband + ntail;
     for (int t = G.t; t < nrow; t += G.nt) {   // panel rows: r * L_kk^T = row
-      const int i = t < c1 - j0 ? j0 + t : x0 + t - (c1 - j0);
+      const int i = t < nband ? j0 + t : x0 + t - nband;
       if (S.fc[i] > kb) continue;
       double* pi = &S.at(i, kb);
       double r[PW];
@@ -357,16 +390,31 @@ __device__ bool sky_panels(const Sky& S, double* rdiag, int c0, int c1, int x0, 
     G.sync();
     const int nb = min(PW, c1 - j0);   // rows of the next diagonal block
     if (G.w == 0) {
-      for (int t = 0; t < nb; ++t) trail_row(S, j0 + t, kb, wb, j0, c1, lane);
+      for (int u = lane; u < nb * (nb + 1) / 2; u += 32) {
+        int ii = 0;
+        while ((ii + 1) * (ii + 2) / 2 <= u) ++ii;
+        trail_pair(S, j0 + ii, j0 + u - ii * (ii + 1) / 2, kb, wb);
+      }
       if (nb > 0) {
         __syncwarp();
         const bool ok = diag_factor(S, rdiag, j0, nb, lane);
         if (lane == 0) *okf = ok;
       }
     } else {
-      for (int t = nb + G.w - 1; t < nrow; t += G.nw - 1) {
-        const int i = t < c1 - j0 ? j0 + t : x0 + t - (c1 - j0);
-        trail_row(S, i, kb, wb, j0, c1, lane);
+      const int m = nband, t0 = nb * (nb + 1) / 2;
+      const int nbandp = m > nb ? m * (m + 1) / 2 - t0 : 0;
+      const int ntot = nbandp + ntail * (c1 - j0);
+      for (int u = G.t - 32; u < ntot; u += G.nt - 32) {
+        if (u < nbandp) {
+          const int t = u + t0;
+          int ii = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+          while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+          while (ii * (ii + 1) / 2 > t) --ii;
+          trail_pair(S, j0 + ii, j0 + t - ii * (ii + 1) / 2, kb, wb);
+        } else {
+          const int v = u - nbandp, w = c1 - j0;
+          trail_pair(S, x0 + v / w, j0 + v % w, kb, wb);
+        }
       }
     }
     G.sync();
@@ -401,9 +449,21 @@ __device__ bool sky_cholesky(const Sky& S, double* rdiag, int n, DirShared& sh) 
   const int gi = G.id == 0 ? 0 : G.id - 1, ng = G.id == 0 ? 1 : 2;
   if (threadIdx.x == 0) { sh.ok[0] = 1; sh.ok[1] = 1; }
   __syncthreads();
+#ifdef GRIP_PHASE_TIMING
+  long long c_t0 = clock64();
+#endif
   for (int q = gi; q < ns; q += ng)
-    if (!sky_panels(S, rdiag, sh.seg[q], sh.seg[q + 1], h, n, G, &sh.ok[gi])) break;
+    if (!sky_panels(S, rdiag, sh.seg[q], sh.seg[q + 1], h, n, G, &sh.ok[gi], sh.rend[gi])) break;
   __syncthreads();
+#ifdef GRIP_PHASE_TIMING
+  long long c_t1 = clock64();
+  if (threadIdx.x == 0) {
+    GSTAT(56, c_t1 - c_t0);
+    GSTAT(59, ns);
+    GSTAT(60, n);
+    GSTAT(61, n - h);
+  }
+#endif
   if (!sh.ok[0] || !sh.ok[1]) return false;
   if (h > 0) {   // tail x tail -= sum over segment columns (fixed-order warp reduction)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -425,7 +485,14 @@ __device__ bool sky_cholesky(const Sky& S, double* rdiag, int n, DirShared& sh) 
     __syncthreads();
   }
   const Grp A{(int)threadIdx.x, NT, (int)threadIdx.x >> 5, NWARP, 0};
-  const bool ok = sky_panels(S, rdiag, h, n, n, n, A, &sh.ok[0]);
+#ifdef GRIP_PHASE_TIMING
+  long long c_t2 = clock64();
+  if (threadIdx.x == 0) GSTAT(57, c_t2 - c_t1);
+#endif
+  const bool ok = sky_panels(S, rdiag, h, n, n, n, A, &sh.ok[0], sh.rend[0]);
+#ifdef GRIP_PHASE_TIMING
+  if (threadIdx.x == 0) GSTAT(58, clock64() - c_t2);
+#endif
   return ok;
 }
 

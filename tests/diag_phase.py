@@ -19,3 +19,5 @@ print("nseg>=2", v[43], "shifted", v[44], "chol cyc when nseg<2", v[45] / max(v[
 pn = ["incidence", "energy", "grad_sv", "grad_nodes+abd", "nonfinite", "static_blocks"]
 for k, nm in enumerate(pn):
     print(f"  prologue.{nm:15s} {v[48 + k] / v[8]:10.0f}")
+print(f"cholesky: segment panels {v[56] / v[8]:.0f}  tail x tail {v[57] / v[8]:.0f}  hub panels {v[58] / v[8]:.0f}"
+      f"  mean segments {v[59] / v[8]:.2f}  mean n {v[60] / v[8]:.1f}  mean tail {v[61] / v[8]:.1f}")
