@@ -138,7 +138,7 @@ struct Dev {
   int* work_off;     // per list position (n+1)
   int* cwork_off;    // per list position (n+1): contact / friction elements only
   int* twork_off;    // per list position (n+1): tets only (k_tet_front)
-  int* ework_off;    // per list position (n+1): abd + contacts + anchors (k_elements_w)
+  int* swork_off;    // per list position (n+1): static 3x3 blocks of H_ff (k_static)
   // anchors (persist across steps)
   int* anc_v;        // 4
   double *anc_gamma, *anc_T, *anc_lam, *anc_mu;   // 4, 6, 1, 1

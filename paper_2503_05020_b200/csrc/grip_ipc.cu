@@ -613,7 +613,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.twork_off = b->alloc<int>(E + 1);
   D.ev_n = b->alloc<int>(E);
   D.ev_on = 0;
-  D.ework_off = b->alloc<int>(E + 1);
+  D.swork_off = b->alloc<int>(E + 1);
   D.max_sv = max_sv; D.max_tri = max_tri; D.max_edge = max_edge; D.max_free = max_free;
   D.max_node = max_node; D.max_tet = max_tet; D.max_abd = max_abd;
   D.cap_pt = std::max(2048, 16 * max_sv);
@@ -709,7 +709,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.surf_prev, D.kin_pos, D.sv_disp, D.ell, D.tol, D.residual, D.energy, D.alphas, D.min_dist, D.time, D.iters,
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
-        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.tflag, D.work_off, D.cwork_off, D.twork_off, D.ework_off, D.anc_v,
+        D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.tflag, D.work_off, D.cwork_off, D.twork_off, D.swork_off, D.anc_v,
         D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_scr, D.need, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
@@ -989,6 +989,8 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   k_tet_front<<<b->eg[0], TF, 0, b->aux>>>(D, list, n);
   k_tet_jacobi2<<<b->eg[2], TJ, 0, b->aux>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
   k_tet_back<<<b->eg[3], EW * 32, 0, b->aux>>>(D, D.jac_list, D.jac_n, D.tet_W);
+  k_abd_w<<<(n + EW - 1) / EW, EW * 32, 0, b->aux>>>(D, list, n);
+  k_static<<<148 * 4, NT, 0, b->aux>>>(D, list, n);
   kt_end(b, t, b->aux);
   CK_VOID(cudaEventRecord(b->ev_join, b->aux));
   t = kt_begin(b, K_CAND);
@@ -1018,7 +1020,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
-  b->launches += 4 + 3 + 3 + (b->direct ? 2 : 1) + 2;
+  b->launches += 6 + 3 + 3 + (b->direct ? 2 : 1) + 2;
   b->sweeps += 1;
 }
 

@@ -339,22 +339,22 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candida
 
 // exclusive scan of per-env element work over the pending list (single CTA)
 // exclusive scan of per-env contact / ABD element work over the pending list (single CTA)
+// exclusive scan of per-env contact / friction element work over the pending list (single CTA)
 __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n) {
   __shared__ Red sm;
   int base = 0;
-  double ca = 0.0, cc = 0.0, cf = 0.0, cn = 0.0;   // cn: envs iterating (newton_iteration calls)
-  int cbase = 0, ebase = 0;
+  double cc = 0.0, cf = 0.0, cn = 0.0;   // cn: envs iterating (newton_iteration calls)
+  int cbase = 0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
-    int w = 0, wc = 0, we = 0;
+    int w = 0, wc = 0;
     if (i < n) {
       const int e = list[i];
       if (!(D.flags[e] & FLAG_OVERFLOW) && !D.ns_done[e]) {
         const int nt = D.tet_off[e + 1] - D.tet_off[e], na = D.abd_off[e + 1] - D.abd_off[e];
         wc = D.n_act[e] + D.n_anc[e];
         w = nt + na + wc;
-        we = na + wc;
-        ca += na; cc += D.n_act[e]; cf += D.n_anc[e]; cn += 1.0;
+        cc += D.n_act[e]; cf += D.n_anc[e]; cn += 1.0;
       }
     }
     int tot;
@@ -364,18 +364,14 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
     const int cpre = block_scan(wc, sm, &tot);
     if (i < n) D.cwork_off[i] = cbase + cpre;
     cbase += tot;
-    const int epre = block_scan(we, sm, &tot);
-    if (i < n) D.ework_off[i] = ebase + epre;
-    ebase += tot;
   }
-  ca = block_sum(ca, sm); cc = block_sum(cc, sm); cf = block_sum(cf, sm);
+  cc = block_sum(cc, sm); cf = block_sum(cf, sm);
   cn = block_sum(cn, sm);
   if (threadIdx.x == 0) {
     D.work_off[n] = base;
     D.cwork_off[n] = cbase;
-    D.ework_off[n] = ebase;
     *D.cjac_n = 0;   // k_elements_w appends deferred contact clamps
-    D.stats[1] += ca; D.stats[2] += cc; D.stats[3] += cf;
+    D.stats[2] += cc; D.stats[3] += cf;
     D.stats[7] += cn;
   }
 }
@@ -385,29 +381,72 @@ __global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n)
 // overflow computes its tets anyway (its assembly is skipped, its warm starts not committed).
 __global__ void __launch_bounds__(NT) k_tet_scan(Dev D, const int* list, int n) {
   __shared__ Red sm;
-  double ct = 0.0;
-  int tbase = 0;
+  double ct = 0.0, ca = 0.0;
+  int tbase = 0, sbase = 0;
   for (int s = 0; s < n; s += NT) {
     const int i = s + threadIdx.x;
-    int wt = 0;
+    int wt = 0, ws = 0;
     if (i < n) {
       const int e = list[i];
       D.tflag[e] = 0;
       if (!D.ns_done[e]) {
         wt = D.tet_off[e + 1] - D.tet_off[e];
+        const int f0 = D.free_off[e], f1 = D.free_off[e + 1];
+        ws = D.sb_rowptr[f1] - D.sb_rowptr[f0];
         ct += wt;
+        ca += D.abd_off[e + 1] - D.abd_off[e];
       }
     }
     int tot;
     const int tpre = block_scan(wt, sm, &tot);
     if (i < n) D.twork_off[i] = tbase + tpre;
     tbase += tot;
+    const int spre = block_scan(ws, sm, &tot);
+    if (i < n) D.swork_off[i] = sbase + spre;
+    sbase += tot;
   }
   ct = block_sum(ct, sm);
+  ca = block_sum(ca, sm);
   if (threadIdx.x == 0) {
     D.twork_off[n] = tbase;
+    D.swork_off[n] = sbase;
     *D.jac_n = 0;   // k_tet_front appends deferred tet clamps
     D.stats[0] += ct;
+    D.stats[1] += ca;
+  }
+}
+
+// Static block values of H_ff (mass + dt^2 x tet / ABD element blocks, solver.py:542-586's
+// M + dt^2 H_el part) for every listed env, thread per 3x3 block, chip-wide on the second stream
+// after the tet back-end (each block's contributions in their stored order: the same sums the
+// assembly kernel formed itself before)
+__global__ void __launch_bounds__(NT) k_static(Dev D, const int* list, int n) {
+  const int total = D.swork_off[n];
+  for (int item = blockIdx.x * blockDim.x + threadIdx.x; item < total; item += gridDim.x * blockDim.x) {
+    int lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (D.swork_off[mid] <= item) lo = mid;
+      else hi = mid;
+    }
+    const int e = list[lo];
+    const int f0 = D.free_off[e];
+    const int b = D.sb_rowptr[f0] + item - D.swork_off[lo];
+    const int f = D.sb_row[b] - f0;
+    const size_t elbase = (size_t)e * D.cap_el;
+    const double dt = D.params[(size_t)e * GRIP_NPARAM + GRIP_P_DT], dt2 = dt * dt;
+    double v[9];
+    for (int i = 0; i < 9; ++i) v[i] = 0.0;
+    for (int q = D.sbc_ptr[b]; q < D.sbc_ptr[b + 1]; ++q) {
+      const int code = D.sbc[q];
+      const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
+      const double* H = D.el_H + (elbase + sl) * 144;
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
+    }
+    const bool diag = D.sb_col[b] == f;
+    const double* M = D.node_M + 9 * (size_t)(D.node_off[e] + D.free_node[f0 + f]);
+    for (int i = 0; i < 9; ++i) D.sb_val[9 * (size_t)b + i] = (diag ? M[i] : 0.0) + dt2 * v[i];
   }
 }
 
@@ -825,25 +864,7 @@ __device__ bool asm_prologue(const Dev& D, const EnvIx& E, AsmShared& A, double 
   nonfinite = block_or(nonfinite, sm);
   if (nonfinite) { fail_env(D, e, GRIP_R_NONFINITE); return false; }
   PPH(4);
-  // ---- static block values (mass + dt^2 * element blocks) ----
-  const int blk0 = D.sb_rowptr[E.f0], nblk = D.sb_rowptr[E.f0 + E.nf] - blk0;
-  for (int t = threadIdx.x; t < nblk; t += NT) {   // one block per thread
-    const int b = blk0 + t;
-    const int f = D.sb_row[b] - E.f0;
-    double v[9];
-    for (int i = 0; i < 9; ++i) v[i] = 0.0;
-    for (int q = D.sbc_ptr[b]; q < D.sbc_ptr[b + 1]; ++q) {
-      const int code = D.sbc[q];
-      const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
-      const double* H = D.el_H + (elbase + sl) * 144;
-      for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
-    }
-    const bool diag = D.sb_col[b] == f;
-    const double* M = D.node_M + 9 * (size_t)(E.n0 + D.free_node[E.f0 + f]);
-    for (int i = 0; i < 9; ++i) D.sb_val[9 * (size_t)b + i] = (diag ? M[i] : 0.0) + dt2 * v[i];
-  }
-  __syncthreads();
+  // static block values (mass + dt^2 * element blocks): k_static, on the second stream
   PPH(5);
 #undef PPH
   *Etot_out = Etot;

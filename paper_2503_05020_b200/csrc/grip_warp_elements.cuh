@@ -340,29 +340,23 @@ __global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* lis
   __shared__ WarpEl ws[EW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpEl& W = ws[warp];
-  const int total = D.ework_off[n];   // tets run thread-per-tet in k_tet_front
+  const int total = D.cwork_off[n];   // contacts + anchors (tets and ABD bodies: second stream)
   for (int item = blockIdx.x * EW + warp; item < total; item += gridDim.x * EW) {
     int lo = 0, hi = n;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (D.ework_off[mid] <= item) lo = mid;
+      if (D.cwork_off[mid] <= item) lo = mid;
       else hi = mid;
     }
     const int e = list[lo];
     const EnvIx E = env_ix(D, e);
     const double* P = P_(D, e);
-    int k = item - D.ework_off[lo];
+    int k = item - D.cwork_off[lo];
     const size_t elbase = (size_t)e * D.cap_el;
     double Eel = 0.0;
     int idx[4];
     size_t slot;
-    if (k < E.na) {
-      const int a = E.a0 + k;
-      slot = elbase + D.max_tet + k;
-      const int pn = D.abd_node[a];
-      for (int j = 0; j < 4; ++j) idx[j] = pn + j;
-      Eel = w_abd(W, D.x + 3 * (size_t)(E.n0 + pn) + 3, D.abd_kV[a], lane);
-    } else if ((k -= E.na) < D.n_act[e]) {
+    if (k < D.n_act[e]) {
       slot = elbase + D.max_tet + D.max_abd + k;
       const int code = D.act[(size_t)e * D.cap_act + k];
       const bool is_ee = code >= D.cap_pt;
@@ -399,6 +393,30 @@ __global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* lis
     }
     w_store(D, slot, W, Eel, idx, lane);
     __syncwarp();
+  }
+}
+
+// ABD orthogonality elements (materials.py:161-188) of the listed envs, warp per env: they depend on
+// x only, so they run on the second stream with the tets, ahead of the static blocks
+__global__ void __launch_bounds__(EW * 32) k_abd_w(Dev D, const int* list, int n) {
+  __shared__ WarpEl ws[EW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpEl& W = ws[warp];
+  for (int pos = blockIdx.x * EW + warp; pos < n; pos += gridDim.x * EW) {
+    const int e = list[pos];
+    if (D.ns_done[e]) continue;
+    const EnvIx E = env_ix(D, e);
+    const size_t elbase = (size_t)e * D.cap_el;
+    for (int k = 0; k < E.na; ++k) {
+      const int a = E.a0 + k;
+      const size_t slot = elbase + D.max_tet + k;
+      const int pn = D.abd_node[a];
+      int idx[4];
+      for (int j = 0; j < 4; ++j) idx[j] = pn + j;
+      const double Eel = w_abd(W, D.x + 3 * (size_t)(E.n0 + pn) + 3, D.abd_kV[a], lane);
+      w_store(D, slot, W, Eel, idx, lane);
+      __syncwarp();
+    }
   }
 }
 
