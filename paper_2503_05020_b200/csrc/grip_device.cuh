@@ -113,6 +113,7 @@ struct Dev {
   int max_alpha;
   // candidates (uniform capacity per env)
   int cap_pt, cap_ee;
+  unsigned* cand_done;   // k_candidates: env CTAs finished (the last one scans the contact work)
   unsigned* need;    // 4: the largest pt / ee / active / anchor count that overflowed its capacity (growth sizes)
   int *c1_pt, *c1_ee, *c1_eid, *c1_n;   // c1_n[2e]=n_pt, [2e+1]=n_ee
   int *c2_pt, *c2_ee, *c2_eid, *c2_n;

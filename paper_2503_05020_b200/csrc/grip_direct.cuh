@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(NT) k_contact_K(Dev D, const int* list, int n)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   KWS& w = ws[warp];
   const int total = D.cwork_off[n];
-  // flat over the contact elements of all listed envs (cwork_off from k_work_scan), warp each
+  // flat over the contact elements of all listed envs (cwork_off from k_candidates' last CTA), warp each
   for (int item = blockIdx.x * NWARP + warp; item < total; item += gridDim.x * NWARP) {
     int lo = 0, hi = n;
     while (hi - lo > 1) {

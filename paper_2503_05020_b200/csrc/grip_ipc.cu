@@ -603,6 +603,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.md_kin = b->alloc<double>(E);
   D.bp_lc = b->alloc<int>((size_t)E * 3 * std::max(max_tri, max_edge));
   D.need = b->alloc<unsigned>(4);
+  D.cand_done = b->alloc<unsigned>(1);
   D.c1_n = b->alloc<int>(2 * (size_t)E);
   D.c2_n = b->alloc<int>(2 * (size_t)E);
   D.n_act = b->alloc<int>(E);
@@ -710,7 +711,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.ns_status, D.reason, D.regularized, D.kin_blocked, D.needs_ls, D.ns_done, D.flags, D.step_index,
         D.newton_calls, D.pcg_iters, D.body_force, D.contact_mask, D.c1_pt, D.c1_ee, D.c1_eid, D.c1_n, D.c2_pt,
         D.c2_ee, D.c2_eid, D.c2_n, D.act, D.n_act, D.n_anc, D.el_E, D.el_g, D.el_H, D.el_idx, D.tflag, D.work_off, D.cwork_off, D.twork_off, D.swork_off, D.anc_v,
-        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_scr, D.need, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
+        D.anc_gamma, D.anc_T, D.anc_lam, D.anc_mu, D.anc_b, D.ev_i, D.ev_d, D.ev_n, D.bp_cells, D.bp_scr, D.need, D.cand_done, D.bp_aabb, D.bp_cnt, D.bp_tmp, D.pcg_x,
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
@@ -997,9 +998,6 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   D.launch_seq = ++b->seq_ctr;
   k_candidates<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
-  t = kt_begin(b, K_SCAN);
-  k_work_scan<<<1, NT, 0, b->stream>>>(D, list, n);
-  kt_end(b, t);
   t = kt_begin(b, K_ELEM);
   k_elements_w<<<b->eg[1], EW * 32, 0, b->stream>>>(D, list, n);
   k_tet_jacobi2<<<148, TJ, 0, b->stream>>>(D.cjac_list, D.cjac_n, D.cjac_S, D.cjac_W);
@@ -1020,7 +1018,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
   k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
-  b->launches += 6 + 3 + 3 + (b->direct ? 2 : 1) + 2;
+  b->launches += 6 + 2 + 3 + (b->direct ? 2 : 1) + 2;
   b->sweeps += 1;
 }
 

@@ -273,12 +273,9 @@ __device__ void begin_env(const Dev& D, int e, Red& sm, BPShared& S, const BPCl&
 // ---------------------------------------------------------------------------
 // A cluster of BP_CL CTAs per env: a superset rebuild is split over the cluster (BPCl), the rest
 // runs on rank 0; the other ranks of an env whose superset still covers exit at once.
-__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
-  __shared__ Red sm;
-  __shared__ BPShared S;
-  const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
-  const int e = list[blockIdx.x / BP_CL];
-  CTA_TIMER_IF(cl.rank == 0, 1, e);
+__device__ void work_scan_body(const Dev& D, const int* list, int n, Red& sm);
+
+__device__ __forceinline__ void cand_env(const Dev& D, int e, const BPCl& cl, BPShared& S, Red& sm) {
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
   const double dhat = P[GRIP_P_DHAT];
@@ -294,7 +291,6 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candida
     D.newton_calls[e] += 1;
   }
   if (cl.rank == 0) env_sv_positions(D, E, D.x);
-  if (!covered) CTA_INFO(1u);
   if (!covered) cl_sync(cl);   // the positions rank 0 wrote, before the cluster's broad phase
   int* cn = D.c1_n + 2 * e;
   int* cpt = D.c1_pt + (size_t)e * 4 * D.cap_pt;
@@ -337,11 +333,34 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candida
   }
 }
 
-// exclusive scan of per-env element work over the pending list (single CTA)
-// exclusive scan of per-env contact / ABD element work over the pending list (single CTA)
-// exclusive scan of per-env contact / friction element work over the pending list (single CTA)
-__global__ void __launch_bounds__(NT) k_work_scan(Dev D, const int* list, int n) {
+// Newton sweep 1/4 (see cand_env).  The last env CTA to finish also scans the per-env contact
+// work for the element kernels (the scan used to be its own single-CTA launch on the critical
+// path): every rank-0 CTA publishes its env's results, fences and counts itself in.
+__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
   __shared__ Red sm;
+  __shared__ BPShared S;
+  __shared__ int last;
+  const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
+  const int e = list[blockIdx.x / BP_CL];
+  CTA_TIMER_IF(cl.rank == 0, 1, e);
+  cand_env(D, e, cl, S, sm);
+  if (cl.rank != 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const int n = gridDim.x / BP_CL;
+    last = atomicAdd(D.cand_done, 1u) == (unsigned)(n - 1);
+    if (last) {
+      __threadfence();
+      *D.cand_done = 0u;
+    }
+  }
+  __syncthreads();
+  if (last) work_scan_body(D, list, gridDim.x / BP_CL, sm);
+}
+
+// exclusive scan of per-env contact / friction element work over the pending list (one CTA)
+__device__ void work_scan_body(const Dev& D, const int* list, int n, Red& sm) {
   int base = 0;
   double cc = 0.0, cf = 0.0, cn = 0.0;   // cn: envs iterating (newton_iteration calls)
   int cbase = 0;
