@@ -1244,19 +1244,32 @@ int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
   b->snap_valid = false;
   D.round_mode = 1;
   CK(cudaMemsetAsync(D.pr_steps, 0, sizeof(unsigned long long), b->stream));
+  // round r: [begin] sweep [finalize + protocol]; the finalize / protocol of round r and the begin
+  // of round r + 1 are one launch (k_bound)
+  static const bool fuse = getenv("GRIP_NO_BOUND") == nullptr;   // A/B switch
   for (int r = 0; r < rounds; ++r) {
     int t = kt_begin(b, K_BEGIN);
     D.launch_seq = ++b->seq_ctr;
-    k_begin<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
+    if (r == 0 || !fuse) {
+      if (r > 0) {
+        k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
+        k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
+        b->launches += 2;
+      }
+      k_begin<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
+    } else {
+      k_bound<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
+    }
     kt_end(b, t);
     sweep_launch(b, E, b->d_ident);
-    t = kt_begin(b, K_FIN);
-    D.launch_seq = ++b->seq_ctr;
-    k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
-    kt_end(b, t);
-    k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
-    b->launches += 3;
+    b->launches += 1;
   }
+  int t = kt_begin(b, K_FIN);
+  D.launch_seq = ++b->seq_ctr;
+  k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
+  kt_end(b, t);
+  k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
+  b->launches += 2;
   CK(cudaGetLastError());
   unsigned long long steps = 0;
   std::vector<int> fl(E);

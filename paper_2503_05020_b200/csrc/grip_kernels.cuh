@@ -1433,12 +1433,18 @@ __global__ void __launch_bounds__(NT) k_compact(Dev D, const int* list, int n, i
 // ---------------------------------------------------------------------------
 // finalize_step (solver.py:733-762) + contact readout (protocol.py:72-98)
 // ---------------------------------------------------------------------------
+__device__ void finalize_env(const Dev& D, int e, int only_done, Red& sm, BPShared& S, unsigned int* cmask);
+
 __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int only_done = 0) {
   __shared__ Red sm;
   __shared__ BPShared S;
   __shared__ unsigned int cmask[32];
   const int e = list[blockIdx.x];
   CTA_TIMER(4, e);
+  finalize_env(D, e, only_done, sm, S, cmask);
+}
+
+__device__ void finalize_env(const Dev& D, int e, int only_done, Red& sm, BPShared& S, unsigned int* cmask) {
   if (only_done && (!D.ns_done[e] || D.fin_done[e] || (D.flags[e] & FLAG_OVERFLOW))) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
@@ -1667,9 +1673,41 @@ __global__ void __launch_bounds__(NT) k_finalize(Dev D, const int* list, int onl
 // ---------------------------------------------------------------------------
 __constant__ double kGravDir[6][3] = {{1, 0, 0}, {-1, 0, 0}, {0, 1, 0}, {0, -1, 0}, {0, 0, 1}, {0, 0, -1}};
 
+__device__ void protocol_env(const Dev& D, int e);
+
 __global__ void k_protocol(Dev D) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= D.n_env) return;
+  protocol_env(D, e);
+}
+
+// One round boundary of the device protocol in one launch: finalize_step of the envs that finished
+// the previous round's sweep, their protocol decision (thread 0), then begin_step of the envs the
+// protocol asks to step (a cluster per env, as k_begin).  The decision inputs of begin (the
+// protocol state, body velocities, supersets) are written by rank 0 before one cluster barrier.
+__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT) k_bound(Dev D, const int* list) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  __shared__ unsigned int cmask[32];
+  const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
+  const int e = list[blockIdx.x / BP_CL];
+  if (cl.rank == 0) {
+    finalize_env(D, e, 1, sm, S, cmask);
+    __syncthreads();
+    if (threadIdx.x == 0) protocol_env(D, e);
+  }
+  cl_sync(cl);
+  if (!D.pr_i[(size_t)e * PI_N + PI_NEEDBEGIN]) return;
+  begin_env(D, e, sm, S, cl);
+  if (cl.rank != 0) return;
+  __syncthreads();
+  if (threadIdx.x == 0 && !(D.flags[e] & FLAG_OVERFLOW)) {   // an overflowed begin is redone later
+    D.pr_i[(size_t)e * PI_N + PI_NEEDBEGIN] = 0;
+    D.pr_i[(size_t)e * PI_N + PI_INSTEP] = 1;
+  }
+}
+
+__device__ void protocol_env(const Dev& D, int e) {
   int* I = D.pr_i + (size_t)e * PI_N;
   double* R = D.pr_d + (size_t)e * PD_N;
   if (!I[PI_INSTEP] || !D.fin_done[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
