@@ -21,8 +21,12 @@ __device__ unsigned long long g_phase[64];   // diagnostic counters (grip_debug_
 #endif
 
 
-constexpr int NT = 256;           // threads per env CTA
+#ifndef GRIP_NT
+#define GRIP_NT 256
+#endif
+constexpr int NT = GRIP_NT;       // threads per env CTA (256; GRIP_NT=512 builds are an A/B experiment)
 constexpr int NWARP = NT / 32;
+constexpr int NT_MINB3 = NT == 256 ? 3 : 1;   // CTAs per SM the heavy CTA-per-env kernels are built for
 constexpr int MAXC = 4096;        // broad-phase grid cells per env
 
 // error / flag bits per env and Newton sweep
@@ -238,7 +242,7 @@ __device__ __forceinline__ const double* P_(const Dev& D, int e) { return D.para
 // block reductions (fixed shuffle tree -> deterministic)
 // ---------------------------------------------------------------------------
 struct Red {
-  double d[40];
+  double d[4 * NWARP + 8];   // block_sum_n: 4 values per warp, then its results; block_red: [0, NWARP), [32]
   int i[40];
 };
 
@@ -286,11 +290,11 @@ __device__ void block_sum_n(double* v, Red& sm) {
     for (int k = 0; k < N; ++k) {
       double r = l < NWARP ? sm.d[4 * l + k] : 0.0;
       r = wsum(r);
-      if (l == 0) sm.d[32 + k] = r;
+      if (l == 0) sm.d[4 * NWARP + k] = r;
     }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < N; ++k) v[k] = sm.d[32 + k];
+  for (int k = 0; k < N; ++k) v[k] = sm.d[4 * NWARP + k];
   __syncthreads();
 }
 __device__ __forceinline__ double block_sum(double v, Red& sm) { return block_red<0>(v, sm); }

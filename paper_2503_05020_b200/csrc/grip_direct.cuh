@@ -611,7 +611,9 @@ struct KWS {
   int knn;
 };
 
-__global__ void __launch_bounds__(NT) k_contact_K(Dev D, const int* list, int n) {
+constexpr int KT = 256;   // k_contact_K: flat kernel, warp per element
+__global__ void __launch_bounds__(KT) k_contact_K(Dev D, const int* list, int n) {
+  constexpr int NWARP = KT / 32;
   __shared__ KWS ws[NWARP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   KWS& w = ws[warp];
@@ -729,7 +731,7 @@ extern __shared__ double dyn_smem[];
 #endif
 
 // Newton sweep 3/4 (direct): assembly + skyline Cholesky solve of H_ff p = -g_f
-__global__ void __launch_bounds__(NT, 3) k_assemble_direct(Dev D, const int* list, int env_cap) {
+__global__ void __launch_bounds__(NT, NT_MINB3) k_assemble_direct(Dev D, const int* list, int env_cap) {
   __shared__ DirShared S;
   AsmShared& A = S.A;
   Red& sm = A.sm;

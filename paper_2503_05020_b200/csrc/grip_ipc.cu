@@ -1006,7 +1006,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   CK_VOID(cudaStreamWaitEvent(b->stream, b->ev_join, 0));   // join
   t = kt_begin(b, K_ASM);
   if (b->direct) {
-    k_contact_K<<<148 * 2, NT, 0, b->stream>>>(D, list, n);
+    k_contact_K<<<148 * 2, KT, 0, b->stream>>>(D, list, n);
     D.launch_seq = ++b->seq_ctr;
     k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
   } else {

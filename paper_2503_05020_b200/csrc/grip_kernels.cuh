@@ -336,7 +336,7 @@ __device__ __forceinline__ void cand_env(const Dev& D, int e, const BPCl& cl, BP
 // Newton sweep 1/4 (see cand_env).  The last env CTA to finish also scans the per-env contact
 // work for the element kernels (the scan used to be its own single-CTA launch on the critical
 // path): every rank-0 CTA publishes its env's results, fences and counts itself in.
-__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, 3) k_candidates(Dev D, const int* list) {
+__global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT, NT_MINB3) k_candidates(Dev D, const int* list) {
   __shared__ Red sm;
   __shared__ BPShared S;
   __shared__ int last;

@@ -13,6 +13,9 @@
 namespace grip {
 
 constexpr int TJ = 128;   // threads per k_tet_jacobi2 block (64 matrices)
+#ifndef GRIP_JAC_TOL
+#define GRIP_JAC_TOL 1e-32   // stop when the squared off-diagonal Frobenius norm is below this fraction
+#endif
 
 __host__ __device__ constexpr int up9(int i, int j) { return i * 9 - i * (i - 1) / 2 + (j - i); }   // i <= j
 
@@ -88,7 +91,7 @@ __global__ void __launch_bounds__(TJ) k_tet_jacobi2(const int2* list, const int*
           else off += v * v;
         }
       off *= 2.0;
-      if (off <= 1e-32 * (dg + off) || off == 0.0) break;
+      if (off <= GRIP_JAC_TOL * (dg + off) || off == 0.0) break;
       jround2<0>(s, Rr); jround2<1>(s, Rr); jround2<2>(s, Rr);
       jround2<3>(s, Rr); jround2<4>(s, Rr); jround2<5>(s, Rr);
       jround2<6>(s, Rr); jround2<7>(s, Rr); jround2<8>(s, Rr);
