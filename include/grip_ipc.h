@@ -286,7 +286,7 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
 /* Per-CTA wall-time records of the CTA-per-env kernels (builds with -DGRIP_CTA_TIMING only; 0
  * records otherwise): 4 uint64 per CTA = launch sequence number, kernel << 32 | env (kernel 0 begin,
  * 1 candidates, 2 assemble_direct, 3 line search, 4 finalize), SM id, start (low 32 bits of the ns
- * globaltimer) << 32 | duration (ns).  reset=1 clears the buffer after the copy. */
+ * globaltimer) << 32 | duration (ns); kernel 5 = k_bound (finalize + protocol + begin).  reset=1 clears the buffer after the copy. */
 int grip_cta_records(GripBatch* b, uint64_t* out, int64_t cap, int64_t* n, int reset);
 /* timing of the last grip_step: device ms (CUDA events) and kernel launches */
 int grip_last_step_stats(GripBatch* b, double* device_ms, int64_t* launches, int64_t* newton_sweeps);

@@ -395,7 +395,7 @@ class DeviceBatch:
         check(self.lib.grip_contacts_now(self.h, ptr(m), float(radius_factor), ptr(md)))
         return md
 
-    CTA_KERNELS = ("begin", "candidates", "assemble_direct", "line_search", "finalize")
+    CTA_KERNELS = ("begin", "candidates", "assemble_direct", "line_search", "finalize", "bound")
 
     def cta_records(self, reset=True, cap=1 << 21):
         """Per-CTA timing records (GRIP_CTA_TIMING builds): structured array seq, kernel, env, sm,

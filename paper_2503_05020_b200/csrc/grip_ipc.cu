@@ -53,7 +53,8 @@ struct GripBatch {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;   // the library's stream (stream may be a caller's, grip_set_stream)
   cudaStream_t aux = nullptr;          // second stream: the tet chain of a sweep, forked / joined by events
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t aux2 = nullptr;         // third stream: the ABD elements (one warp-level element per env)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_abd = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   Dev D{};
   int n_env = 0, n_node = 0, n_sv = 0, n_tet = 0, n_abd = 0, n_body = 0, n_free = 0, n_blk = 0;
@@ -277,6 +278,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   CK(cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking));
   b->own_stream = b->stream;
   CK(cudaStreamCreateWithFlags(&b->aux, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&b->aux2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&b->ev_abd, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
   CK(cudaEventCreate(&b->ev0));
@@ -758,6 +761,8 @@ int grip_destroy(GripBatch* b) {
   cudaEventDestroy(b->ev1);
   cudaStreamDestroy(b->own_stream);   // a caller's stream (grip_set_stream) is the caller's
   cudaStreamDestroy(b->aux);
+  cudaStreamDestroy(b->aux2);
+  cudaEventDestroy(b->ev_abd);
   cudaEventDestroy(b->ev_fork);
   cudaEventDestroy(b->ev_join);
   delete b;
@@ -985,12 +990,15 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   // elements run on the main one; they join before the assembly
   CK_VOID(cudaEventRecord(b->ev_fork, b->stream));
   CK_VOID(cudaStreamWaitEvent(b->aux, b->ev_fork, 0));
+  CK_VOID(cudaStreamWaitEvent(b->aux2, b->ev_fork, 0));
+  k_abd_w<<<(n + EW - 1) / EW, EW * 32, 0, b->aux2>>>(D, list, n);   // third stream: x only
+  CK_VOID(cudaEventRecord(b->ev_abd, b->aux2));
   int t = kt_begin(b, K_TET, b->aux);
   k_tet_scan<<<1, NT, 0, b->aux>>>(D, list, n);
   k_tet_front<<<b->eg[0], TF, 0, b->aux>>>(D, list, n);
   k_tet_jacobi2<<<b->eg[2], TJ, 0, b->aux>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
   k_tet_back<<<b->eg[3], EW * 32, 0, b->aux>>>(D, D.jac_list, D.jac_n, D.tet_W);
-  k_abd_w<<<(n + EW - 1) / EW, EW * 32, 0, b->aux>>>(D, list, n);
+  CK_VOID(cudaStreamWaitEvent(b->aux, b->ev_abd, 0));   // the ABD blocks, before the static sums
   k_static<<<148 * 4, NT, 0, b->aux>>>(D, list, n);
   kt_end(b, t, b->aux);
   CK_VOID(cudaEventRecord(b->ev_join, b->aux));
@@ -1343,6 +1351,10 @@ int grip_set_priority(GripBatch* b, int priority) {
   CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, p));
   CK(cudaStreamDestroy(b->aux));
   b->aux = a;
+  CK(cudaStreamSynchronize(b->aux2));
+  CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, p));
+  CK(cudaStreamDestroy(b->aux2));
+  b->aux2 = a;
   return 0;
 }
 

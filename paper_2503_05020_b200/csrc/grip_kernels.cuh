@@ -1691,6 +1691,7 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT) k_bound(Dev 
   __shared__ unsigned int cmask[32];
   const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
   const int e = list[blockIdx.x / BP_CL];
+  CTA_TIMER_IF(cl.rank == 0, 5, e);
   if (cl.rank == 0) {
     finalize_env(D, e, 1, sm, S, cmask);
     __syncthreads();

@@ -336,7 +336,10 @@ __device__ __forceinline__ void w_store(const Dev& D, size_t slot, WarpEl& W, do
 constexpr int EW = 8;  // warps per block of k_elements_w
 
 // Newton sweep 2/4 (warp per element): element slots per env [tets | abd | contacts | anchors]
-__global__ void __launch_bounds__(EW * 32, 2) k_elements_w(Dev D, const int* list, int n) {
+#ifndef GRIP_EW_MINB
+#define GRIP_EW_MINB 2   // blocks per SM k_elements_w is compiled for (register cap 128)
+#endif
+__global__ void __launch_bounds__(EW * 32, GRIP_EW_MINB) k_elements_w(Dev D, const int* list, int n) {
   __shared__ WarpEl ws[EW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpEl& W = ws[warp];
