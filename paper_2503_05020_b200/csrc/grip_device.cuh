@@ -61,6 +61,7 @@ struct Dev {
   const int* dense_fc;       // per env-dense position (global free offset): lowest statically coupled position
   const int* dense_tail;     // per env: first dense position of the hub (last) body
   const int* sb_row;         // per block: global free row
+  const int* sb_dst;         // per block: dense (row, col) node positions << 16 | ..., -1 above the diagonal
   double* tet_S;             // per tet 45: warm-rotated S~ (upper) awaiting the batched eigensolve
   double* tet_W;             // per tet 90: its eigenvalues (9) and rotation R (81, row-major)
   int2* jac_list;            // (tet, element slot) of the tets whose clamp was deferred this sweep

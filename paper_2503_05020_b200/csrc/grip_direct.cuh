@@ -102,13 +102,21 @@ __device__ void sky_static(const Dev& D, const EnvIx& E, const Sky& S, int n) {
   const int tot = S.ro[n];
   for (int i = threadIdx.x; i < tot; i += NT) S.L[i] = 0.0;
   __syncthreads();
-  const int b0 = D.sb_rowptr[E.f0], nb9 = 9 * (D.sb_rowptr[E.f0 + E.nf] - b0);
-  for (int t = threadIdx.x; t < nb9; t += NT) {
-    const int b = b0 + t / 9, q = t - 9 * (t / 9);
-    const int pf = perm[D.sb_row[b] - E.f0], pf2 = perm[D.sb_col[b]];
-    if (pf2 > pf) continue;   // the mirrored block lands in the lower triangle
-    const int i = 3 * pf + q / 3, j = 3 * pf2 + q % 3;
-    if (i >= j) S.at(i, j) = D.sb_val[9 * (size_t)b + q];
+  const int b0 = D.sb_rowptr[E.f0], nb = D.sb_rowptr[E.f0 + E.nf] - b0;
+  (void)perm;
+  for (int t = threadIdx.x; t < nb; t += NT) {   // a block per thread, its 9 values loaded at once
+    const int b = b0 + t;
+    const int dst = D.sb_dst[b];
+    if (dst < 0) continue;   // the mirrored block lands in the lower triangle
+    const int pf = dst >> 16, pf2 = dst & 0xffff;
+    double v[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) v[q] = D.sb_val[9 * (size_t)b + q];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int i = 3 * pf + q / 3, j = 3 * pf2 + q % 3;
+      if (i >= j) S.at(i, j) = v[q];
+    }
   }
   __syncthreads();
 }

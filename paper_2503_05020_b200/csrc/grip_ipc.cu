@@ -506,6 +506,18 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   }
   D.dense_tail = b->upload(dense_tail.data(), E);
   D.sb_row = b->upload(sb_row.data(), sb_row.size());
+  {   // per static block: its dense (row node, column node) positions packed, -1 for upper-triangle
+      // blocks (their mirror carries the values): one load per block in the skyline fill
+    std::vector<int> sb_dst(sb_row.size(), -1);
+    for (int e = 0; e < E; ++e) {
+      const int f0 = free_off[e];
+      for (int q = sb_rowptr[f0]; q < sb_rowptr[free_off[e + 1]]; ++q) {
+        const int pf = dense_perm[sb_row[q]], pf2 = dense_perm[f0 + sb_col[q]];
+        if (pf2 <= pf) sb_dst[q] = (pf << 16) | pf2;
+      }
+    }
+    D.sb_dst = b->upload(sb_dst.data(), sb_dst.size());
+  }
   D.sv_kind = b->upload(d->sv_kind, NS);
   D.sv_node = b->upload(d->sv_node, NS);
   D.sv_xi = b->upload(d->sv_xi, 3 * (size_t)NS);
@@ -718,7 +730,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.sb_dst, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
