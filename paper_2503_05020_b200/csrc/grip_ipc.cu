@@ -1265,20 +1265,21 @@ int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
   D.round_mode = 1;
   CK(cudaMemsetAsync(D.pr_steps, 0, sizeof(unsigned long long), b->stream));
   // round r: [begin] sweep [finalize + protocol]; the finalize / protocol of round r and the begin
-  // of round r + 1 are one launch (k_bound)
-  static const bool fuse = getenv("GRIP_NO_BOUND") == nullptr;   // A/B switch
+  // of round r + 1 are one 4-CTA cluster launch (k_bound). GRIP_SPLIT_BOUND=1 splits it into
+  // finalize + protocol (CTA per env) then begin (cluster), so no cluster rank idles through the
+  // finalize: measured 1-2 % slower on the bench (one more launch on the lane's critical path).
+  static const bool fuse = getenv("GRIP_SPLIT_BOUND") == nullptr;
   for (int r = 0; r < rounds; ++r) {
     int t = kt_begin(b, K_BEGIN);
     D.launch_seq = ++b->seq_ctr;
-    if (r == 0 || !fuse) {
+    if (r > 0 && fuse) {
+      k_bound<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
+    } else {
       if (r > 0) {
-        k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
-        k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
-        b->launches += 2;
+        k_finalize_protocol<<<E, NT, 0, b->stream>>>(D, b->d_ident);
+        b->launches += 1;
       }
       k_begin<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
-    } else {
-      k_bound<<<E * BP_CL, NT, 0, b->stream>>>(D, b->d_ident);
     }
     kt_end(b, t);
     sweep_launch(b, E, b->d_ident);
@@ -1286,10 +1287,9 @@ int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
   }
   int t = kt_begin(b, K_FIN);
   D.launch_seq = ++b->seq_ctr;
-  k_finalize<<<E, NT, 0, b->stream>>>(D, b->d_ident, 1);
+  k_finalize_protocol<<<E, NT, 0, b->stream>>>(D, b->d_ident);
   kt_end(b, t);
-  k_protocol<<<(E + 127) / 128, 128, 0, b->stream>>>(D);
-  b->launches += 2;
+  b->launches += 1;
   CK(cudaGetLastError());
   unsigned long long steps = 0;
   std::vector<int> fl(E);

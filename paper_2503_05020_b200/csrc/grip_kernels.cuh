@@ -1708,6 +1708,19 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT) k_bound(Dev 
   }
 }
 
+// finalize_step + the protocol decision of the envs that finished the round's sweep, one CTA per env
+// (the device protocol's round end; the next round's begin_step is a cluster launch of its own)
+__global__ void __launch_bounds__(NT) k_finalize_protocol(Dev D, const int* list) {
+  __shared__ Red sm;
+  __shared__ BPShared S;
+  __shared__ unsigned int cmask[32];
+  const int e = list[blockIdx.x];
+  CTA_TIMER(4, e);
+  finalize_env(D, e, 1, sm, S, cmask);
+  __syncthreads();
+  if (threadIdx.x == 0) protocol_env(D, e);
+}
+
 __device__ void protocol_env(const Dev& D, int e) {
   int* I = D.pr_i + (size_t)e * PI_N;
   double* R = D.pr_d + (size_t)e * PD_N;
