@@ -13,6 +13,10 @@
 
 namespace grip {
 
+// Tet Hessians are stored as their packed lower triangle (78 of the slot's 144 doubles): the
+// symmetric 12x12 written and read once instead of twice (k_static is the only reader).
+__host__ __device__ constexpr int tri12(int r, int c) { return r * (r + 1) / 2 + c; }   // c <= r
+
 #ifdef GRIP_PHASE_TIMING
 __device__ unsigned long long g_phase[64];   // diagnostic counters (grip_debug_phase)
 #define GSTAT(k, v) atomicAdd(&g_phase[k], (unsigned long long)(v))

@@ -47,7 +47,6 @@ struct Sky {
 __device__ int sky_build(const Dev& D, const EnvIx& E, int* fcn, int* fcd, int* ro, DirShared& sh) {
   Red& sm = sh.A.sm;
   const int e = E.e, nf = E.nf, n = 3 * nf;
-  const int* perm = D.dense_perm + E.f0;
   for (int p = threadIdx.x; p < nf; p += NT) fcn[p] = D.dense_fc[E.f0 + p];
   __syncthreads();
   const int na = D.n_act[e], nce = na + D.n_anc[e];
@@ -97,13 +96,10 @@ __device__ int sky_build(const Dev& D, const EnvIx& E, int* fcn, int* fcd, int* 
 // H_ff into the skyline: the static blocks from sb_val (mass, dt^2 element blocks and any
 // shift), then dt^2 J^T H J of the contact / friction elements (sky_scatter_contacts)
 __device__ void sky_static(const Dev& D, const EnvIx& E, const Sky& S, int n) {
-  const int e = E.e;
-  const int* perm = D.dense_perm + E.f0;
   const int tot = S.ro[n];
   for (int i = threadIdx.x; i < tot; i += NT) S.L[i] = 0.0;
   __syncthreads();
   const int b0 = D.sb_rowptr[E.f0], nb = D.sb_rowptr[E.f0 + E.nf] - b0;
-  (void)perm;
   for (int t = threadIdx.x; t < nb; t += NT) {   // a block per thread, its 9 values loaded at once
     const int b = b0 + t;
     const int dst = D.sb_dst[b];
@@ -140,7 +136,7 @@ __device__ void sky_scatter_rows(const Dev& D, const EnvIx& E, const Sky& S, Dir
   int* off = D.sc_off + (size_t)e * 2 * (D.max_free + 1);
   int* cur = off + (D.max_free + 1);
   int* lst = D.sc_lst + (size_t)e * 8 * (D.cap_act + D.cap_anc);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   auto slot_of = [&](int k) { return cs0 + (k < na ? k : D.cap_act + (k - na)); };
   for (int p = threadIdx.x; p < nf; p += NT) off[p] = 0;
   __syncthreads();

@@ -1090,7 +1090,7 @@ int grip_round(GripBatch* b, const uint8_t* begin, const uint8_t* iter, uint8_t*
     if (begin && begin[e]) b->h_lists[nb++] = e;
     if ((begin && begin[e]) || (iter && iter[e])) b->h_lists[E + n++] = e;
   }
-  if (finalized) memset(finalized, 0, E);
+  if (finalized) memset(finalized, 0, (size_t)(E > 0 ? E : 0));
   if (n == 0) return 0;
   if (nb) CK(cudaMemcpyAsync(b->d_list, b->h_lists, sizeof(int) * nb, cudaMemcpyHostToDevice, b->stream));
   CK(cudaMemcpyAsync(b->d_list2, b->h_lists + E, sizeof(int) * n, cudaMemcpyHostToDevice, b->stream));
@@ -1669,6 +1669,14 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
     cudaMemcpy(E, D.el_E, sizeof(double) * n, cudaMemcpyDeviceToHost);
     cudaMemcpy(g, D.el_g, sizeof(double) * 12 * (size_t)n, cudaMemcpyDeviceToHost);
     cudaMemcpy(H, D.el_H, sizeof(double) * 144 * (size_t)n, cudaMemcpyDeviceToHost);
+    if (type == 2)   // tets: unpack the stored lower triangle (tri12) in place, last slot entry first
+      for (int k = 0; k < n; ++k) {
+        double* h = H + 144 * (size_t)k;
+        double lo[78];
+        memcpy(lo, h, sizeof lo);
+        for (int r = 0; r < 12; ++r)
+          for (int c = 0; c <= r; ++c) h[r * 12 + c] = h[c * 12 + r] = lo[tri12(r, c)];
+      }
   }
   for (void* p : mem)
     if (p) cudaFree(p);

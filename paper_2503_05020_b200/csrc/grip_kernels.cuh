@@ -460,8 +460,16 @@ __global__ void __launch_bounds__(NT) k_static(Dev D, const int* list, int n) {
       const int code = D.sbc[q];
       const int sl = code >> 4, sa = (code >> 2) & 3, sbb = code & 3;
       const double* H = D.el_H + (elbase + sl) * 144;
-      for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
+      if (sl < D.max_tet) {   // tets: packed lower triangle (grip_tet.cuh)
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) {
+            const int r = 3 * sa + i, c = 3 * sbb + j;
+            v[3 * i + j] += H[r >= c ? tri12(r, c) : tri12(c, r)];
+          }
+      } else {
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) v[3 * i + j] += H[(3 * sa + i) * 12 + 3 * sbb + j];
+      }
     }
     const bool diag = D.sb_col[b] == f;
     const double* M = D.node_M + 9 * (size_t)(D.node_off[e] + D.free_node[f0 + f]);

@@ -16,6 +16,7 @@
 // k_tet_back (one warp per deferred tet): V = Y R (the next warm start), S_proj =
 //   V diag(max(l, f)) V^T, H = Q S_proj Q^T + f/4 on equal components (translations lifted to
 //   f = 1e-12 max|l|, exactly the reference's clamp of the 12x12 matrix).
+// Both write H packed (tri12): 624 B per tet instead of the 1152 B of the full matrix.
 #pragma once
 #include "grip_tetclamp.cuh"
 
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
         D.el_E[slot] = 0.0;
 #pragma unroll
         for (int j = 0; j < 12; ++j) D.el_g[slot * 12 + j] = 0.0;
-        for (int j = 0; j < 144; ++j) Hg[j] = 0.0;
+        for (int j = 0; j < 78; ++j) Hg[j] = 0.0;
       } else {
         double A[9];
         {
@@ -205,14 +206,13 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
 #pragma unroll
             for (int M = 0; M < 4; ++M) WW[4 * m + M] = w[3 * m] * w[3 * M] + w[3 * m + 1] * w[3 * M + 1] + w[3 * m + 2] * w[3 * M + 2];
 #pragma unroll
-          for (int r = 0; r < 12; ++r)
+          for (int q = 0; q < 12; ++q)
 #pragma unroll
-            for (int q = r; q < 12; ++q) {
+            for (int r = 0; r <= q; ++r) {
               const int m = r / 3, c = r % 3, M = q / 3, C = q % 3;
               const double v = V0 * ((c == C ? mu * WW[4 * m + M] : 0.0) + c2 * WA[3 * M + c] * WA[3 * m + C] +
                                      c3 * WA[3 * m + c] * WA[3 * M + C]) + (c == C ? f4 : 0.0);
-              Hg[r * 12 + q] = v;
-              if (q != r) Hg[q * 12 + r] = v;
+              Hg[tri12(q, r)] = v;
             }
         } else {
           defer = true;
@@ -283,14 +283,13 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
     }
     __syncwarp();
     double* Hg = D.el_H + slot * 144;
-    for (int q = lane; q < 78; q += 32) {
+    for (int q = lane; q < 78; q += 32) {   // kTri78 is the packed lower-triangle order: q = tri12(r, c12)
       const int rc = kTri78[q], r = rc >> 4, c12 = rc & 15;   // column <= row
       const int m = r / 3, c = r - 3 * m;
       double s = (c == c12 % 3) ? 0.25 * f : 0.0;
 #pragma unroll
       for (int i = 0; i < 3; ++i) s += kHelm[i][m] * w.T[(3 * i + c) * 12 + c12];
-      Hg[r * 12 + c12] = s;
-      if (c12 != r) Hg[c12 * 12 + r] = s;
+      Hg[q] = s;
     }
     __syncwarp();
   }
