@@ -1684,6 +1684,19 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
   return rc;
 }
 
+#ifdef GRIP_JAC_HIST
+// diagnostic build only (tools/jac_hist.py): the Jacobi sweep histogram, [2][GRIP_JAC_MAXSWEEP + 1]
+int grip_jac_hist(unsigned long long* out, int reset) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, g_jac_hist, sizeof(g_jac_hist)));
+  if (reset) {
+    static unsigned long long z[2][GRIP_JAC_MAXSWEEP + 1] = {};
+    CK(cudaMemcpyToSymbol(g_jac_hist, z, sizeof(z)));
+  }
+  return 0;
+}
+#endif
+
 int grip_cta_records(GripBatch* b, uint64_t* out, int64_t cap, int64_t* n, int reset) {
   *n = 0;
   if (!b->D.cta_rec) return 0;   // not a GRIP_CTA_TIMING build

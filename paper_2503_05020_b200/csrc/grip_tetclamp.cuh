@@ -16,6 +16,12 @@ constexpr int TJ = 128;   // threads per k_tet_jacobi2 block (64 matrices)
 #ifndef GRIP_JAC_TOL
 #define GRIP_JAC_TOL 1e-32   // stop when the squared off-diagonal Frobenius norm is below this fraction
 #endif
+#ifndef GRIP_JAC_MAXSWEEP
+#define GRIP_JAC_MAXSWEEP 30
+#endif
+#ifdef GRIP_JAC_HIST   // diagnostic build: histogram of Jacobi sweeps, [0] tets (warm) / [1] contacts (cold)
+__device__ unsigned long long g_jac_hist[2][GRIP_JAC_MAXSWEEP + 1];
+#endif
 
 __host__ __device__ constexpr int up9(int i, int j) { return i * 9 - i * (i - 1) / 2 + (j - i); }   // i <= j
 
@@ -80,7 +86,8 @@ __global__ void __launch_bounds__(TJ) k_tet_jacobi2(const int2* list, const int*
     for (int r = 0; r < 5; ++r)
 #pragma unroll
       for (int c = 0; c < 9; ++c) Rr[r][c] = (5 * h + r == c) ? 1.0 : 0.0;
-    for (int sweep = 0; sweep < 30; ++sweep) {
+    int sweep = 0;
+    for (; sweep < GRIP_JAC_MAXSWEEP; ++sweep) {
       double off = 0.0, dg = 0.0;
 #pragma unroll
       for (int i = 0; i < 9; ++i)
@@ -96,6 +103,11 @@ __global__ void __launch_bounds__(TJ) k_tet_jacobi2(const int2* list, const int*
       jround2<3>(s, Rr); jround2<4>(s, Rr); jround2<5>(s, Rr);
       jround2<6>(s, Rr); jround2<7>(s, Rr); jround2<8>(s, Rr);
     }
+#ifdef GRIP_JAC_HIST
+    if (h == 0) atomicAdd(&g_jac_hist[gridDim.x == 148 ? 1 : 0][sweep], 1ull);   // contacts: the 148-block launch
+#else
+    (void)sweep;
+#endif
     double* W = Wbuf + 90 * (size_t)t;
     if (h == 0) {
 #pragma unroll
