@@ -87,7 +87,12 @@ struct Dev {
   const double* tet_V0;
   const double* tet_mu;
   const double* tet_lam;
-  double* tet_eig;           // per tet 9x9: eigenvectors of its deflated Hessian (Jacobi warm start)
+  double* tet_eig;           // per tet 9x9: eigenvectors of its deflated Hessian (Jacobi warm start),
+                             // two halves of eig_half doubles: env e reads half eig_par[e], its
+                             // deferred tets' next bases go to the other half (tet_eig_cur / _next)
+  size_t eig_half;
+  int* eig_par;              // per env: the half holding its current warm starts
+  int* eig_swept;            // per env: its tets went through this sweep (k_tet_scan; k_linesearch commits)
   const int* abd_node;
   const double* abd_kV;
   const uint8_t* body_kind;
@@ -242,6 +247,29 @@ struct CtaTimer {
 #endif
 
 __device__ __forceinline__ const double* P_(const Dev& D, int e) { return D.params + (size_t)e * GRIP_NPARAM; }
+
+// the warm-start halves of env e (see Dev::tet_eig)
+__device__ __forceinline__ double* tet_eig_cur(const Dev& D, int e, size_t t) {
+  return D.tet_eig + (D.eig_par[e] ? D.eig_half : 0) + 81 * t;
+}
+__device__ __forceinline__ double* tet_eig_next(const Dev& D, int e, size_t t) {
+  return D.tet_eig + (D.eig_par[e] ? 0 : D.eig_half) + 81 * t;
+}
+
+// At the end of an env's line search (the sweep's last kernel that can flag an overflow): a swept
+// env without overflow makes its new warm starts current; an overflowed env's sweep is redone from
+// the same bases (results independent of when buffers grew).
+struct EigCommit {
+  const Dev& D;
+  int e;
+  bool on;
+  __device__ EigCommit(const Dev& d, int env, bool o) : D(d), e(env), on(o) {}
+  __device__ ~EigCommit() {
+    if (!on || threadIdx.x != 0 || !D.eig_swept[e]) return;
+    if (!(D.flags[e] & FLAG_OVERFLOW)) D.eig_par[e] ^= 1;
+    D.eig_swept[e] = 0;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // block reductions (fixed shuffle tree -> deterministic)

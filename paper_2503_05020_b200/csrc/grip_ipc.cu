@@ -534,9 +534,17 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
     std::vector<double> eye(81 * (size_t)std::max(NTET, 1), 0.0);
     for (int t = 0; t < std::max(NTET, 1); ++t)
       for (int k = 0; k < 9; ++k) eye[81 * (size_t)t + 10 * k] = 1.0;
+    eye.resize(2 * eye.size(), 0.0);   // both warm-start halves (Dev::tet_eig)
+    for (size_t q = eye.size() / 2; q < eye.size(); ++q) eye[q] = eye[q - eye.size() / 2];
     D.tet_eig = b->upload(eye.data(), eye.size());
+    D.eig_half = eye.size() / 2;
   D.tet_S = b->alloc<double>(45 * (size_t)std::max(NTET, 1));
   D.tet_W = b->alloc<double>(90 * (size_t)std::max(NTET, 1));
+  {
+    std::vector<int> z(std::max(E, 1), 0);
+    D.eig_par = b->upload(z.data(), z.size());
+    D.eig_swept = b->upload(z.data(), z.size());
+  }
   D.jac_list = b->alloc<int2>((size_t)std::max(NTET, 1));
   D.jac_n = b->alloc<int>(1);
   }
@@ -730,7 +738,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.sb_dst, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.sb_dst, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n, D.eig_par, D.eig_swept};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -1037,8 +1045,7 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   D.launch_seq = ++b->seq_ctr;
   k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
   kt_end(b, t);
-  k_eig_commit<<<148 * 4, 256, 0, b->stream>>>(D, D.jac_list, D.jac_n, D.tet_W);
-  b->launches += 6 + 2 + 3 + (b->direct ? 2 : 1) + 2;
+  b->launches += 6 + 2 + 3 + (b->direct ? 2 : 1) + 1;
   b->sweeps += 1;
 }
 
@@ -1634,7 +1641,11 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
     D.tet_V0 = (const double*)up(V0.data(), sizeof(double) * n);
     D.tet_mu = (const double*)up(mu.data(), sizeof(double) * n);
     D.tet_lam = (const double*)up(lam.data(), sizeof(double) * n);
+    Y.resize(2 * Y.size(), 0.0);   // warm-start halves: the bases in half 0, the new ones land in half 1
     D.tet_eig = (double*)up(Y.data(), sizeof(double) * Y.size());
+    D.eig_half = 81 * (size_t)n;
+    D.eig_par = (int*)up(zero.data(), sizeof(int));
+    D.eig_swept = (int*)up(zero.data(), sizeof(int));
     D.tet_S = (double*)dalloc(sizeof(double) * 45 * (size_t)n);
     D.tet_W = (double*)dalloc(sizeof(double) * 90 * (size_t)n);
     D.jac_list = (int2*)dalloc(sizeof(int2) * n);
@@ -1646,9 +1657,8 @@ int grip_debug_chain(int type, int n, const double* in, int stride, double* E, d
     k_tet_front<<<std::max(1, std::min(1024, (n + TF - 1) / TF)), TF>>>(D, d_list, 1);
     k_tet_jacobi2<<<148, TJ>>>(D.jac_list, D.jac_n, D.tet_S, D.tet_W);
     k_tet_back<<<148, EW * 32>>>(D, D.jac_list, D.jac_n, D.tet_W);
-    k_eig_commit<<<148, 256>>>(D, D.jac_list, D.jac_n, D.tet_W);
     if (cudaGetLastError() != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) rc = -1;
-    if (!rc && eig) cudaMemcpy(eig, D.tet_eig, sizeof(double) * 81 * (size_t)n, cudaMemcpyDeviceToHost);
+    if (!rc && eig) cudaMemcpy(eig, D.tet_eig + D.eig_half, sizeof(double) * 81 * (size_t)n, cudaMemcpyDeviceToHost);
     int ff = 0;
     cudaMemcpy(&ff, D.tflag, sizeof(int), cudaMemcpyDeviceToHost);
     for (int k = 0; k < n; ++k) flags[k] = ff;

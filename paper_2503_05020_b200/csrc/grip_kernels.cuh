@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(NT) k_tet_scan(Dev D, const int* list, int n) 
     if (i < n) {
       const int e = list[i];
       D.tflag[e] = 0;
+      D.eig_swept[e] = !D.ns_done[e];
       if (!D.ns_done[e]) {
         wt = D.tet_off[e + 1] - D.tet_off[e];
         const int f0 = D.free_off[e], f1 = D.free_off[e + 1];
@@ -1241,6 +1242,7 @@ __global__ void __cluster_dims__(BP_CL, 1, 1) __launch_bounds__(NT) k_linesearch
   const BPCl cl{(int)cooperative_groups::this_cluster().block_rank(), BP_CL};
   const int e = list[blockIdx.x / BP_CL];
   CTA_TIMER_IF(cl.rank == 0, 3, e);
+  EigCommit commit_(D, e, cl.rank == 0);   // on every return path of rank 0
   if (D.ns_done[e] || !D.needs_ls[e] || (D.flags[e] & FLAG_OVERFLOW)) return;
   const EnvIx E = env_ix(D, e);
   const double* P = P_(D, e);
@@ -1915,8 +1917,12 @@ __global__ void k_reset_envs(Dev D, const int* lst, const long long* off, const 
     const size_t g = 3 * (size_t)s0 + i;
     D.sv_pos[g] = D.surf_prev[g] = D.sv_disp[g] = 0.0;
   }
-  for (int i = threadIdx.x; i < 81 * nt; i += blockDim.x)   // Jacobi warm start: identity
+  for (int i = threadIdx.x; i < 81 * nt; i += blockDim.x)   // Jacobi warm start: identity, in half 0
     D.tet_eig[81 * (size_t)t0 + i] = (i % 81) % 10 == 0 ? 1.0 : 0.0;
+  if (threadIdx.x == 0) {
+    D.eig_par[e] = 0;
+    D.eig_swept[e] = 0;
+  }
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     D.body_force[b0 + i] = 0.0;
     D.contact_mask[b0 + i] = 0u;

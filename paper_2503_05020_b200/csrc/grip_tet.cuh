@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
           }
         // S~ = Y^T S Y (Y = previous eigenbasis, row-major), streamed column by column of Y;
         // upper entries to tet_S, Gershgorin bounds on the fly
-        const double* Y = D.tet_eig + 81 * (size_t)t;
+        const double* Y = tet_eig_cur(D, e, t);
         double* St = D.tet_S + 45 * (size_t)t;
         double rad[9], dg[9];
 #pragma unroll
@@ -194,7 +194,12 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
           dm = fmax(dm, fabs(dg[i]));
         }
         if (glo > 1e-12 * ghi) {
-          // nothing clamped: H itself plus the reference's lifted translation modes
+          // nothing clamped: the warm start carries over to the next half; H itself plus the
+          // reference's lifted translation modes
+          {
+            double* Yn = tet_eig_next(D, e, t);
+            for (int q = 0; q < 81; ++q) Yn[q] = Y[q];
+          }
           const double f4 = 0.25 * (1e-12 * dm);
           double WA[12], WW[16];
 #pragma unroll
@@ -231,10 +236,10 @@ __global__ void __launch_bounds__(TF) k_tet_front(Dev D, const int* list, int n)
 }
 
 // deferred tets: finish the clamp from (eigenvalues, R) -- see the file header
-// The next warm start V = Y R goes to W[9..90) (over R), not to tet_eig: k_eig_commit copies it
-// after the line search, for envs whose sweep is not redone after a buffer growth (a redone sweep
+// The next warm start V = Y R goes to the env's other warm-start half (tet_eig_next); the line
+// search makes it current unless the env's sweep is redone after a buffer growth (a redone sweep
 // must start from the same warm starts, so results do not depend on when buffers grew).
-__global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, const int* n_ptr, double* Wbuf) {
+__global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, const int* n_ptr, const double* Wbuf) {
   __shared__ WarpWS ws[EW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpWS& w = ws[warp];
@@ -242,8 +247,9 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
   for (int idx = blockIdx.x * EW + warp; idx < n; idx += gridDim.x * EW) {
     const int2 it = list[idx];
     const size_t t = it.x, slot = it.y;
-    double* W = Wbuf + 90 * t;
-    const double* Y = D.tet_eig + 81 * t;
+    const int env = (int)(slot / D.cap_el);
+    const double* W = Wbuf + 90 * t;
+    const double* Y = tet_eig_cur(D, env, t);
     for (int e = lane; e < 81; e += 32) {
       w.S[e] = Y[e];       // Y
       w.T[e] = W[9 + e];   // R
@@ -260,7 +266,10 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
       w.V[e] = a;
     }
     __syncwarp();
-    for (int e = lane; e < 81; e += 32) W[9 + e] = w.V[e];   // next warm start (k_eig_commit)
+    {
+      double* Yn = tet_eig_next(D, env, t);
+      for (int q = lane; q < 81; q += 32) Yn[q] = w.V[q];   // next warm start
+    }
     for (int e = lane; e < 81; e += 32) {   // S_proj = V diag(max(l, f)) V^T
       const int i = e / 9, j = e - 9 * i;
       double a = 0.0;
@@ -292,19 +301,6 @@ __global__ void __launch_bounds__(EW * 32) k_tet_back(Dev D, const int2* list, c
       Hg[q] = s;
     }
     __syncwarp();
-  }
-}
-
-// After the line search: the deferred tets' new warm starts (k_tet_back) become current, except
-// in envs whose sweep overflowed a buffer and will be redone.
-__global__ void k_eig_commit(Dev D, const int2* list, const int* n_ptr, const double* Wbuf) {
-  const int n = *n_ptr;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 81 * n; i += gridDim.x * blockDim.x) {
-    const int k = i / 81, c = i - 81 * k;
-    const int2 it = list[k];
-    const int e = it.y / D.cap_el;
-    if (D.flags[e] & FLAG_OVERFLOW) continue;
-    D.tet_eig[81 * (size_t)it.x + c] = Wbuf[90 * (size_t)it.x + 9 + c];
   }
 }
 
