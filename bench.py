@@ -458,7 +458,8 @@ def build_runner(args, cfg, envs, rank, world, writer=None):
     on_record = None if writer is None else (lambda j, r: writer.put(j, r))
     runner = TrialRunner(jobs, scene_of, key_of, slots=None, lanes_per_key=args.lanes_per_kind,
                          rounds_per_call=args.rounds_per_call, priority=prio if args.lane_priority else None,
-                         cycle=True, device=None, mode=mode, record=record, on_record=on_record)
+                         cycle=True, device=None, mode=mode, record=record, on_record=on_record,
+                         pipeline=not getattr(args, "no_pipeline", False))
     distinct = len(set(jobs)) == len(jobs) and bool(args.global_envs or (world * envs <= len(pool)))
     return runner, jobs, mode, bool(distinct)
 
@@ -676,6 +677,8 @@ def main():
     ap.add_argument("--rounds-per-step", type=int, default=16)
     ap.add_argument("--rounds-per-call", type=int, default=4, help="device protocol: rounds per host call")
     ap.add_argument("--lanes-per-kind", type=int, default=1)
+    ap.add_argument("--no-pipeline", action="store_true", help="device protocol: wait for each call before "
+                    "enqueuing the next (no host / device overlap)")
     ap.add_argument("--no-lane-priority", dest="lane_priority", action="store_false")
     ap.add_argument("--protocol", default="auto", choices=["auto", "host", "device"])
     ap.add_argument("--record", default=None, help="record every trial and emit it here (dataset format), "

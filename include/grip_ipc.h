@@ -215,6 +215,15 @@ int grip_protocol_reset(GripBatch* b, const uint8_t* mask, const double* closing
  * envs simply resume.  *env_steps = time steps completed. */
 int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps);
 int grip_protocol_read(GripBatch* b, GripTrialOut* out /* n_env */);
+/* Pipelined form of grip_run_rounds + grip_protocol_read (replaces the same reference loop,
+ * pipeline/__init__.py:51-70 around protocol.py:152-277): enqueue the rounds and an async
+ * readout of the env-step counter and every env's GripTrialOut, return at once with a ticket;
+ * at most two calls in flight.  grip_rounds_wait blocks until that call's readout landed and
+ * returns it (out may be NULL); a capacity overflow seen there drains the stream and grows.
+ * Refills (grip_reset_envs / grip_protocol_reset) issued between the two queue behind the
+ * call in flight, so the host's collect-and-refill overlaps the device's next call. */
+int grip_run_rounds_async(GripBatch* b, int rounds, int32_t* ticket);
+int grip_rounds_wait(GripBatch* b, int32_t ticket, int64_t* env_steps, GripTrialOut* out /* n_env or NULL */);
 /* One recorder frame (protocol.py:113-146) of the envs with mask[e]=1, packed in env order:
  * x, v (their nodes * 3), kin (their surface vertices * 3: kinematic positions, zeros for
  * the others) and stress (their tets * 7, materials.py:191-205).  Any output may be NULL. */

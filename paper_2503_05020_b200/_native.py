@@ -104,6 +104,7 @@ def load():
         ("grip_get_state_device", [vp, vp, vp, vp]), ("grip_set_controls_device", [vp, vp, vp]), ("grip_cta_records", [vp, vp, ctypes.c_int64, vp, i32]),
         ("grip_protocol_setup", [vp, vp, vp, vp, vp, vp, vp]), ("grip_protocol_reset", [vp, vp, vp, vp]),
         ("grip_run_rounds", [vp, i32, vp]), ("grip_protocol_read", [vp, vp]),
+        ("grip_run_rounds_async", [vp, i32, vp]), ("grip_rounds_wait", [vp, i32, vp, vp]),
         ("grip_sdf_query", [vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int64, vp, vp])):
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -504,6 +505,19 @@ class DeviceBatch:
         n = ctypes.c_int64()
         check(self.lib.grip_run_rounds(self.h, int(rounds), ctypes.byref(n)))
         return n.value
+
+    def run_rounds_async(self, rounds):
+        """Enqueue `rounds` rounds + an async readout (grip_run_rounds_async); returns a ticket."""
+        t = ctypes.c_int32()
+        check(self.lib.grip_run_rounds_async(self.h, int(rounds), ctypes.byref(t)))
+        return t.value
+
+    def rounds_wait(self, ticket, records=True):
+        """(env-steps, GripTrialOut array or None) of an enqueued call (grip_rounds_wait)."""
+        n = ctypes.c_int64()
+        out = (GripTrialOut * self.n_env)() if records else None
+        check(self.lib.grip_rounds_wait(self.h, int(ticket), ctypes.byref(n), out))
+        return n.value, out
 
     def protocol_read(self):
         out = (GripTrialOut * self.n_env)()

@@ -104,7 +104,19 @@ struct GripBatch {
   size_t dyn_smem = 0;
   static constexpr int NK = 8;
   std::vector<cudaEvent_t> kev;   // pairs
-  std::vector<std::pair<int, int>> pending_k;  // (kernel id, event pair index)
+  std::vector<int> kev_free;      // event pairs whose times were collected
+  std::vector<std::pair<int, int>> pending_k;  // (kernel id, event pair index), in launch order
+  // pipelined device-protocol calls (grip_run_rounds_async / grip_rounds_wait): up to two calls
+  // in flight, each with a pinned readout (env-step counter, flags, protocol records) and an event
+  struct RoundSlot {
+    char* h = nullptr;
+    cudaEvent_t ev = nullptr;
+    bool busy = false;
+    size_t kt_mark = 0;   // pending_k entries of this call (and of calls before it)
+  };
+  RoundSlot rslot[2];
+  int rslot_next = 0;
+  cudaEvent_t ev_reset_st = nullptr, ev_pinit_st = nullptr;   // staging consumed (copy + kernel done)
   double k_ms[NK] = {0};
   long long k_n[NK] = {0};
   cudaEvent_t r0 = nullptr, r1 = nullptr;
@@ -773,6 +785,12 @@ int grip_destroy(GripBatch* b) {
   if (b->h_snap) cudaFreeHost(b->h_snap);
   if (b->h_frame) cudaFreeHost(b->h_frame);
   if (b->h_fmask) cudaFreeHost(b->h_fmask);
+  for (auto& rs : b->rslot) {
+    if (rs.h) cudaFreeHost(rs.h);
+    if (rs.ev) cudaEventDestroy(rs.ev);
+  }
+  if (b->ev_reset_st) cudaEventDestroy(b->ev_reset_st);
+  if (b->ev_pinit_st) cudaEventDestroy(b->ev_pinit_st);
   if (b->h_reset) cudaFreeHost(b->h_reset);
   if (b->h_pinit) cudaFreeHost(b->h_pinit);
   if (b->d_pinit) cudaFree(b->d_pinit);
@@ -817,11 +835,17 @@ enum { K_BEGIN = 0, K_CAND, K_SCAN, K_ELEM, K_ASM, K_LS, K_FIN, K_TET };
 
 static int kt_begin(GripBatch* b, int kid, cudaStream_t st = nullptr) {
   if (!b->prof) return -1;
-  const int pair = (int)b->pending_k.size();
-  while ((int)b->kev.size() < 2 * (pair + 1)) {
-    cudaEvent_t ev;
-    cudaEventCreate(&ev);
-    b->kev.push_back(ev);
+  int pair;
+  if (!b->kev_free.empty()) {
+    pair = b->kev_free.back();
+    b->kev_free.pop_back();
+  } else {
+    pair = (int)b->kev.size() / 2;
+    for (int k = 0; k < 2; ++k) {
+      cudaEvent_t ev;
+      cudaEventCreate(&ev);
+      b->kev.push_back(ev);
+    }
   }
   cudaEventRecord(b->kev[2 * pair], st ? st : b->stream);
   b->pending_k.push_back({kid, pair});
@@ -830,20 +854,26 @@ static int kt_begin(GripBatch* b, int kid, cudaStream_t st = nullptr) {
 static void kt_end(GripBatch* b, int pair, cudaStream_t st = nullptr) {
   if (pair >= 0) cudaEventRecord(b->kev[2 * pair + 1], st ? st : b->stream);
 }
-// fold the recorded launch times into the per-kernel totals (after a stream sync)
-static void kt_collect(GripBatch* b, int n_listed = -1) {
+// fold the recorded launch times into the per-kernel totals: the first `upto` pending launches
+// (all when negative), which must have completed
+static void kt_collect(GripBatch* b, int n_listed = -1, long long upto = -1) {
   static const bool trace = getenv("GRIP_TRACE") != nullptr;
   double per[GripBatch::NK] = {0};
-  for (auto& pk : b->pending_k) {
+  const size_t m = upto < 0 ? b->pending_k.size() : std::min((size_t)upto, b->pending_k.size());
+  for (size_t i = 0; i < m; ++i) {
+    const auto& pk = b->pending_k[i];
     float ms = 0.0f;
     cudaEventElapsedTime(&ms, b->kev[2 * pk.second], b->kev[2 * pk.second + 1]);
     b->k_ms[pk.first] += ms;
     b->k_n[pk.first] += 1;
     per[pk.first] += ms;
+    b->kev_free.push_back(pk.second);
   }
-  if (trace && n_listed >= 0 && !b->pending_k.empty())
+  if (trace && n_listed >= 0 && m)
     fprintf(stderr, "GRIP_TRACE n=%d cand=%.3f elem=%.3f asm=%.3f ls=%.3f\n", n_listed, per[1], per[3], per[4], per[5]);
-  b->pending_k.clear();
+  b->pending_k.erase(b->pending_k.begin(), b->pending_k.begin() + m);
+  for (auto& rs : b->rslot)
+    if (rs.busy) rs.kt_mark = rs.kt_mark > m ? rs.kt_mark - m : 0;
 }
 
 // one Newton sweep over the pending envs (list in b->d_list, n entries); returns new pending count
@@ -1197,7 +1227,7 @@ static int protocol_init_envs(GripBatch* b, const uint8_t* mask, const double* c
   if (L.empty()) return 0;
   const size_t n = L.size();
   const size_t bytes = n * (sizeof(double) * PINIT_D + sizeof(int) * PINIT_I);
-  CK(cudaStreamSynchronize(b->stream));   // the pinned staging buffer may still feed a previous copy
+  if (b->ev_pinit_st) CK(cudaEventSynchronize(b->ev_pinit_st));   // the staging may still feed a previous restart
   if (bytes > b->pinit_cap) {
     if (b->h_pinit) cudaFreeHost(b->h_pinit);
     if (b->d_pinit) cudaFree(b->d_pinit);
@@ -1225,7 +1255,8 @@ static int protocol_init_envs(GripBatch* b, const uint8_t* mask, const double* c
       reinterpret_cast<const int*>(b->d_pinit + n * sizeof(double) * PINIT_D));
   b->launches++;
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(b->stream));
+  if (!b->ev_pinit_st) CK(cudaEventCreateWithFlags(&b->ev_pinit_st, cudaEventDisableTiming));
+  CK(cudaEventRecord(b->ev_pinit_st, b->stream));
   b->snap_valid = false;
   return 0;
 }
@@ -1260,7 +1291,8 @@ int grip_protocol_reset(GripBatch* b, const uint8_t* mask, const double* closing
   return protocol_init_envs(b, mask, closing_dir, max_close, nullptr, nullptr, nullptr);
 }
 
-int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
+// enqueue `rounds` device-protocol rounds over every env and the closing finalize + protocol
+static int enqueue_rounds(GripBatch* b, int rounds) {
   b->ev_now = false;   // a finalize rewrites (or, recording off, invalidates) the event rows
   Dev& D = b->D;
   if (!D.pr_i) {
@@ -1297,40 +1329,51 @@ int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
   k_finalize_protocol<<<E, NT, 0, b->stream>>>(D, b->d_ident);
   kt_end(b, t);
   b->launches += 1;
+  D.round_mode = 0;
   CK(cudaGetLastError());
+  return 0;
+}
+
+// after a call whose flags showed an overflow: drain the stream, grow, clear the flags; the
+// overflowed envs' state is untouched and they resume in the next call
+static int grow_after_overflow(GripBatch* b) {
+  CK(cudaStreamSynchronize(b->stream));
+  if (grow(b)) return -1;
+  CK(cudaMemsetAsync(b->D.flags, 0, sizeof(int) * b->n_env, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  return 0;
+}
+
+int grip_run_rounds(GripBatch* b, int rounds, int64_t* env_steps) {
+  for (auto& rs : b->rslot)
+    if (rs.busy) {
+      g_err = "grip_run_rounds: a pipelined call is in flight (grip_rounds_wait first)";
+      return -1;
+    }
+  if (enqueue_rounds(b, rounds)) return -1;
+  Dev& D = b->D;
+  const int E = b->n_env;
   unsigned long long steps = 0;
   std::vector<int> fl(E);
   CK(cudaMemcpyAsync(&steps, D.pr_steps, sizeof(steps), cudaMemcpyDeviceToHost, b->stream));
   CK(cudaMemcpyAsync(fl.data(), D.flags, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
   CK(cudaStreamSynchronize(b->stream));
   kt_collect(b);
-  D.round_mode = 0;
   bool ovf = false;
   for (int e = 0; e < E; ++e) ovf |= (fl[e] & FLAG_OVERFLOW) != 0;
-  if (ovf) {   // grow; the overflowed envs' state is untouched and they resume next call
-    if (grow(b)) return -1;
-    CK(cudaMemsetAsync(D.flags, 0, sizeof(int) * E, b->stream));
-    CK(cudaStreamSynchronize(b->stream));
-  }
+  if (ovf && grow_after_overflow(b)) return -1;
   if (env_steps) *env_steps = (int64_t)steps;
   return 0;
 }
 
-int grip_protocol_read(GripBatch* b, GripTrialOut* out) {
-  Dev& D = b->D;
-  if (!D.pr_i) {
-    g_err = "grip_protocol_read before grip_protocol_setup";
-    return -1;
-  }
-  const int E = b->n_env;
-  std::vector<int> hi((size_t)E * PI_N);
-  std::vector<double> hd((size_t)E * PD_N);
-  CK(cudaMemcpyAsync(hi.data(), D.pr_i, sizeof(int) * hi.size(), cudaMemcpyDeviceToHost, b->stream));
-  CK(cudaMemcpyAsync(hd.data(), D.pr_d, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, b->stream));
-  CK(cudaStreamSynchronize(b->stream));
+static size_t rslot_bytes(int E) {
+  return 8 + ((4 * (size_t)E * (1 + PI_N) + 7) & ~(size_t)7) + 8 * (size_t)E * PD_N;
+}
+
+static void decode_trial_out(const int* hi, const double* hd, int E, GripTrialOut* out) {
   for (int e = 0; e < E; ++e) {
-    const int* I = hi.data() + (size_t)e * PI_N;
-    const double* R = hd.data() + (size_t)e * PD_N;
+    const int* I = hi + (size_t)e * PI_N;
+    const double* R = hd + (size_t)e * PD_N;
     GripTrialOut& o = out[e];
     o.halt_force[0] = R[PD_HF]; o.halt_force[1] = R[PD_HF + 1];
     for (int k = 0; k < 6; ++k) o.com_disp[k] = R[PD_CDISP + k];
@@ -1349,6 +1392,74 @@ int grip_protocol_read(GripBatch* b, GripTrialOut* out) {
     o.min_distance = R[PD_MIND];
     o.min_J = R[PD_MINJ];
   }
+}
+
+int grip_run_rounds_async(GripBatch* b, int rounds, int32_t* ticket) {
+  GripBatch::RoundSlot& rs = b->rslot[b->rslot_next];
+  if (rs.busy) {
+    g_err = "grip_run_rounds_async: two calls already in flight (grip_rounds_wait first)";
+    return -1;
+  }
+  const int E = b->n_env;
+  if (!rs.h) {
+    CK(cudaMallocHost(&rs.h, rslot_bytes(E)));
+    CK(cudaEventCreateWithFlags(&rs.ev, cudaEventDisableTiming));
+  }
+  if (enqueue_rounds(b, rounds)) return -1;
+  Dev& D = b->D;
+  char* h = rs.h;
+  int* hf = reinterpret_cast<int*>(h + 8);
+  int* hi = hf + E;
+  double* hd = reinterpret_cast<double*>(h + 8 + ((4 * (size_t)E * (1 + PI_N) + 7) & ~(size_t)7));
+  CK(cudaMemcpyAsync(h, D.pr_steps, 8, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(hf, D.flags, sizeof(int) * E, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(hi, D.pr_i, sizeof(int) * (size_t)E * PI_N, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(hd, D.pr_d, sizeof(double) * (size_t)E * PD_N, cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaEventRecord(rs.ev, b->stream));
+  rs.busy = true;
+  rs.kt_mark = b->pending_k.size();
+  *ticket = b->rslot_next;
+  b->rslot_next ^= 1;
+  return 0;
+}
+
+int grip_rounds_wait(GripBatch* b, int32_t ticket, int64_t* env_steps, GripTrialOut* out) {
+  if (ticket < 0 || ticket > 1 || !b->rslot[ticket].busy) {
+    g_err = "grip_rounds_wait: no such call in flight";
+    return -1;
+  }
+  GripBatch::RoundSlot& rs = b->rslot[ticket];
+  CK(cudaEventSynchronize(rs.ev));
+  kt_collect(b, -1, (long long)rs.kt_mark);
+  rs.busy = false;
+  const int E = b->n_env;
+  const char* h = rs.h;
+  unsigned long long steps = 0;
+  memcpy(&steps, h, 8);
+  const int* hf = reinterpret_cast<const int*>(h + 8);
+  const int* hi = hf + E;
+  const double* hd = reinterpret_cast<const double*>(h + 8 + ((4 * (size_t)E * (1 + PI_N) + 7) & ~(size_t)7));
+  if (out) decode_trial_out(hi, hd, E, out);
+  bool ovf = false;
+  for (int e = 0; e < E; ++e) ovf |= (hf[e] & FLAG_OVERFLOW) != 0;
+  if (ovf && grow_after_overflow(b)) return -1;
+  if (env_steps) *env_steps = (int64_t)steps;
+  return 0;
+}
+
+int grip_protocol_read(GripBatch* b, GripTrialOut* out) {
+  Dev& D = b->D;
+  if (!D.pr_i) {
+    g_err = "grip_protocol_read before grip_protocol_setup";
+    return -1;
+  }
+  const int E = b->n_env;
+  std::vector<int> hi((size_t)E * PI_N);
+  std::vector<double> hd((size_t)E * PD_N);
+  CK(cudaMemcpyAsync(hi.data(), D.pr_i, sizeof(int) * hi.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaMemcpyAsync(hd.data(), D.pr_d, sizeof(double) * hd.size(), cudaMemcpyDeviceToHost, b->stream));
+  CK(cudaStreamSynchronize(b->stream));
+  decode_trial_out(hi.data(), hd.data(), E, out);
   return 0;
 }
 
@@ -1513,7 +1624,7 @@ int grip_reset_envs(GripBatch* b, const uint8_t* mask, const GripSceneDesc* d) {
   if (L.empty()) return 0;
   const size_t head = L.size() * (sizeof(int) + sizeof(long long));
   const size_t bytes = ((head + 15) & ~(size_t)15) + n * sizeof(double);
-  CK(cudaStreamSynchronize(b->stream));   // the pinned staging buffer may still feed a previous copy
+  if (b->ev_reset_st) CK(cudaEventSynchronize(b->ev_reset_st));   // the staging may still feed a previous refill
   if (bytes > b->reset_cap) {
     if (b->h_reset) cudaFreeHost(b->h_reset);
     if (b->d_reset) cudaFree(b->d_reset);
@@ -1562,6 +1673,8 @@ int grip_reset_envs(GripBatch* b, const uint8_t* mask, const GripSceneDesc* d) {
       reinterpret_cast<const double*>(dd + ((head + 15) & ~(size_t)15)));
   b->launches++;
   CK(cudaGetLastError());
+  if (!b->ev_reset_st) CK(cudaEventCreateWithFlags(&b->ev_reset_st, cudaEventDisableTiming));
+  CK(cudaEventRecord(b->ev_reset_st, b->stream));
   return 0;
 }
 

@@ -610,6 +610,17 @@ class DeviceProtocolTrials:
         self.env_steps += n
         return n
 
+    def advance_async(self, rounds=1):
+        """Enqueue R device rounds and their readout; returns a ticket for wait()."""
+        return self.dev.run_rounds_async(rounds)
+
+    def wait(self, ticket):
+        """(env-steps, protocol records) of an advance_async call, once it finished."""
+        n, out = self.dev.rounds_wait(ticket)
+        self.group.invalidate()
+        self.env_steps += n
+        return n, out
+
     def record(self, e, out=None):
         """TrialRecord of env e from the device protocol state."""
         o = (out if out is not None else self.dev.protocol_read())[e]

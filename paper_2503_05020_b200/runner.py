@@ -71,6 +71,8 @@ class Lane:
         self.stats = LaneStats(slots=len(first))
         self.started = [True] * len(first)
         self._stop = False
+        self.pending = None   # ticket of the device call in flight (pipelined runner)
+        self.stale = set()    # slots refilled behind the call in flight: its readout predates the refill
 
     def _next_job(self):
         if self.qpos >= len(self.queue):
@@ -85,21 +87,40 @@ class Lane:
     def idle(self):
         return all(j is None for j in self.slot_job)
 
-    def call(self):
+    def call(self, last=False):
         """One host call: R device rounds (device protocol) or one round (host protocol), then
-        collect the finished trials and refill their slots."""
+        collect the finished trials and refill their slots.
+
+        Pipelined (device protocol, runner.pipeline): the next call's rounds are enqueued before
+        this call's results are waited for, so the host's collect-and-refill overlaps the
+        device; refills queue behind the call in flight (a finished slot idles one call longer).
+        last: complete the call in flight without enqueuing another."""
         r = self.runner
         t0 = time.perf_counter()
+        out = None
         if self.mode == "device":
-            n = self.trials.advance(r.rounds_per_call)
-            self.stats.rounds += r.rounds_per_call
             E = self.group.packed.n_env
+            if r.pipeline:
+                if self.pending is None:
+                    self.pending = self.trials.advance_async(r.rounds_per_call)
+                nxt = None if last else self.trials.advance_async(r.rounds_per_call)
+                n, out = self.trials.wait(self.pending)
+                self.pending = nxt
+                skip, self.stale = self.stale, set()
+                self.stats.d2h_bytes += 192 * E                     # the call's protocol records
+            else:
+                n = self.trials.advance(r.rounds_per_call)
+                skip = set()
+            self.stats.rounds += r.rounds_per_call
             self.stats.d2h_bytes += 8 + 4 * E                       # env-step counter, overflow flags
         else:
             n = self.trials.advance_round()
             self.stats.rounds += 1
+            skip = set()
         t1 = time.perf_counter()
-        self._collect_and_refill()
+        refilled = self._collect_and_refill(out, skip)
+        if self.pending is not None:
+            self.stale = set(refilled)
         t2 = time.perf_counter()
         self.stats.calls += 1
         self.stats.env_steps += int(n)
@@ -107,19 +128,27 @@ class Lane:
         self.stats.refill_s += t2 - t1
         self.stats.max_call_ms = max(self.stats.max_call_ms, 1e3 * (t2 - t0))
 
-    def _collect_and_refill(self):
+    def drain(self):
+        """Complete the pipelined call in flight (its trials are collected and refilled)."""
+        if self.pending is not None:
+            self.call(last=True)
+
+    def _collect_and_refill(self, out=None, skip=()):
+        """Finished trials of the readout `out` (slots in `skip` excluded: their readout predates
+        a refill) are recorded and their slots refilled; returns the refilled slots."""
         r = self.runner
         if self.mode == "device":
-            out = self.trials.dev.protocol_read()
             E = self.group.packed.n_env
-            self.stats.d2h_bytes += 192 * E
-            fin = [e for e in range(E) if out[e].phase == 4 and self.slot_job[e] is not None]
+            if out is None:
+                out = self.trials.dev.protocol_read()
+                self.stats.d2h_bytes += 192 * E
+            fin = [e for e in range(E) if out[e].phase == 4 and self.slot_job[e] is not None and e not in skip]
             recs = {e: self.trials.record(e, out) for e in fin}
         else:
             fin = [int(e) for e in np.nonzero(self.trials.phase == 4)[0] if self.slot_job[e] is not None]
             recs = {e: self.trials.records[e] for e in fin}
         if not fin:
-            return
+            return []
         refill, payloads = [], []
         for e in fin:
             job = self.slot_job[e]
@@ -140,6 +169,7 @@ class Lane:
                                              + cnt("body_off") + cnt("edge_off") + cnt("abd_off") + 1) + 12
                 self.stats.h2d_bytes += 48 + 24
             self.trials.refill(refill, payloads)
+        return refill
 
 
 class TrialRunner:
@@ -154,12 +184,14 @@ class TrialRunner:
     cycle:       wrap the queues around (steady state) instead of stopping when they run out
     mode:        "device" (protocol kernel, R rounds per call) or "host" (BatchedGraspTrials)
     on_record:   callback(job, TrialRecord) for every finished trial (e.g. a dataset writer)
+    pipeline:    device protocol: keep the next call enqueued while the host collects and refills
     """
 
     def __init__(self, jobs, scene_of, key_of, slots=None, lanes_per_key=1, rounds_per_call=4, priority=None,
                  cycle=False, device=None, protocol=None, mode="device", record=False, on_record=None,
-                 keep_records=True, prepare=True):
+                 keep_records=True, prepare=True, pipeline=True):
         self.scene_of, self.key_of = scene_of, key_of
+        self.pipeline = bool(pipeline)
         self.rounds_per_call, self.cycle, self.mode, self.record = int(rounds_per_call), bool(cycle), mode, record
         self.protocol = protocol
         self.on_record, self.keep_records = on_record, keep_records
@@ -240,16 +272,20 @@ class TrialRunner:
                     if ln.idle:
                         break
                 elif i == main and main_calls is not None:
-                    if ln.stats.calls - c0 >= main_calls and (min_trials is None
-                                                             or len(self.finished_order) - n0 >= min_trials):
+                    done = ln.stats.calls - c0
+                    if done >= main_calls and (min_trials is None or len(self.finished_order) - n0 >= min_trials):
                         stop.set()
                         break
+                    if min_trials is None and done == main_calls - 1:
+                        ln.call(last=True)   # exactly main_calls calls complete inside the run
+                        continue
                 elif stop.is_set():
                     break
                 elif main_calls is None and min_trials is not None and len(self.finished_order) - n0 >= min_trials:
                     stop.set()
                     break
                 ln.call()
+            ln.drain()
             if timed:
                 ln.stats.device_ms += ln.dev.timer_stop()
 

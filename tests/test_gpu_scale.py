@@ -22,13 +22,14 @@ pytestmark = pytest.mark.gpu
 KIND_PRIORITY = {0: 0, 1: 1, 2: 2}   # box < cylinder < sphere (bench.py's lane priorities)
 
 
-def _cfg2_runner(jobs, slots=None, lanes_per_key=1, rounds_per_call=4):
+def _cfg2_runner(jobs, slots=None, lanes_per_key=1, rounds_per_call=4, pipeline=True):
     from paper_2503_05020_b200 import scene as sc
     from paper_2503_05020_b200.runner import TrialRunner
     c = sc.load_cfg2_candidates()
     kinds = np.asarray(c["kind"])
     return TrialRunner(jobs, lambda j: sc.cfg2_scene(j, c), lambda j: int(kinds[j]), slots=slots,
-                       lanes_per_key=lanes_per_key, rounds_per_call=rounds_per_call, priority=KIND_PRIORITY)
+                       lanes_per_key=lanes_per_key, rounds_per_call=rounds_per_call, priority=KIND_PRIORITY,
+                       pipeline=pipeline)
 
 
 def _assert_record_matches(r, g, key, force_rtol=1e-5):
@@ -65,6 +66,27 @@ def test_refill_bitwise_equals_fresh():
     assert sorted(refilled) == jobs
     for j in jobs:
         assert _same_record(fresh[j], refilled[j]), (j, fresh[j], refilled[j])
+
+
+def test_pipelined_runner_bitwise_equals_synchronous():
+    """The pipelined runner (next call enqueued before the host collects and refills: refills
+    queue behind the call in flight, grip_run_rounds_async / grip_rounds_wait) gives bitwise the
+    trials of the synchronous one (grip_run_rounds + grip_protocol_read), refilled slots included;
+    and a bench-style run of exactly K calls completes exactly K calls per main lane."""
+    jobs = list(range(30))
+    sync = _cfg2_runner(jobs, slots=3, pipeline=False).run()
+    piped_runner = _cfg2_runner(jobs, slots=3, pipeline=True)
+    piped = piped_runner.run()
+    assert sorted(piped) == sorted(sync) == jobs
+    for j in jobs:
+        assert _same_record(sync[j], piped[j]), (j, sync[j], piped[j])
+    r = _cfg2_runner(list(range(9)), slots=3, pipeline=True)
+    r.cycle = True
+    main = r.main_lane
+    c0 = r.lanes[main].stats.calls
+    r.run(main_calls=5)
+    assert r.lanes[main].stats.calls - c0 == 5
+    assert all(ln.pending is None for ln in r.lanes)
 
 
 def test_cfg2_all_400_labels_match_reference(golden):
