@@ -675,7 +675,7 @@ def main():
     ap.add_argument("--global-envs", type=int, default=0, help="strong scaling: total envs split over the ranks")
     ap.add_argument("--sweep", default="", help="config 5: comma-separated env counts, one JSON line each")
     ap.add_argument("--rounds-per-step", type=int, default=16)
-    ap.add_argument("--rounds-per-call", type=int, default=4, help="device protocol: rounds per host call")
+    ap.add_argument("--rounds-per-call", type=int, default=1, help="device protocol: rounds per host call")
     ap.add_argument("--lanes-per-kind", type=int, default=1)
     ap.add_argument("--no-pipeline", action="store_true", help="device protocol: wait for each call before "
                     "enqueuing the next (no host / device overlap)")

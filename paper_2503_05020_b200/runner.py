@@ -187,7 +187,7 @@ class TrialRunner:
     pipeline:    device protocol: keep the next call enqueued while the host collects and refills
     """
 
-    def __init__(self, jobs, scene_of, key_of, slots=None, lanes_per_key=1, rounds_per_call=4, priority=None,
+    def __init__(self, jobs, scene_of, key_of, slots=None, lanes_per_key=1, rounds_per_call=1, priority=None,
                  cycle=False, device=None, protocol=None, mode="device", record=False, on_record=None,
                  keep_records=True, prepare=True, pipeline=True):
         self.scene_of, self.key_of = scene_of, key_of

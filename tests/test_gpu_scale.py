@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 KIND_PRIORITY = {0: 0, 1: 1, 2: 2}   # box < cylinder < sphere (bench.py's lane priorities)
 
 
-def _cfg2_runner(jobs, slots=None, lanes_per_key=1, rounds_per_call=4, pipeline=True):
+def _cfg2_runner(jobs, slots=None, lanes_per_key=1, rounds_per_call=1, pipeline=True):
     from paper_2503_05020_b200 import scene as sc
     from paper_2503_05020_b200.runner import TrialRunner
     c = sc.load_cfg2_candidates()
@@ -91,7 +91,7 @@ def test_pipelined_runner_bitwise_equals_synchronous():
 
 def test_cfg2_all_400_labels_match_reference(golden):
     """All 400 bench envs, the bench's layout (3 lanes by object kind, one slot per env, the
-    device protocol, 4 rounds per call), against the reference's full-protocol trials."""
+    device protocol, 1 round per call, pipelined), against the reference's full-protocol trials."""
     path = golden / "verdicts_cfg2_all.json"
     if not path.exists():
         pytest.skip("verdicts_cfg2_all.json not generated")

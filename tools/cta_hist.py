@@ -41,7 +41,7 @@ def main():
         protocol = "auto"
         record = None
         lanes_per_kind = 1
-        rounds_per_call = 4
+        rounds_per_call = 1
         lane_priority = True
 
     runner, jobs, _, _ = bench.build_runner(A, 2, args.envs, 0, 1)

@@ -39,7 +39,7 @@ def main():
         protocol = "auto"
         record = None
         lanes_per_kind = 1
-        rounds_per_call = 4
+        rounds_per_call = 1
         lane_priority = True
 
     runner, _, _, _ = bench.build_runner(A, 2, 400, 0, 1)
