@@ -36,6 +36,10 @@ import argparse
 import json
 import multiprocessing as mp
 import os
+
+# 9 runner lanes x 3 streams: 32 hardware work queues instead of the default 8 (before any CUDA use;
+# the package sets the same default)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import subprocess
 import sys
 import threading
@@ -676,7 +680,7 @@ def main():
     ap.add_argument("--sweep", default="", help="config 5: comma-separated env counts, one JSON line each")
     ap.add_argument("--rounds-per-step", type=int, default=16)
     ap.add_argument("--rounds-per-call", type=int, default=1, help="device protocol: rounds per host call")
-    ap.add_argument("--lanes-per-kind", type=int, default=1)
+    ap.add_argument("--lanes-per-kind", type=int, default=3)
     ap.add_argument("--no-pipeline", action="store_true", help="device protocol: wait for each call before "
                     "enqueuing the next (no host / device overlap)")
     ap.add_argument("--no-lane-priority", dest="lane_priority", action="store_false")

@@ -1,7 +1,7 @@
 """GPU parity at the bench's own scale and layout.
 
 * every one of the 400 config-2 bench envs (kind i % 3, the reference-sampled candidate of seed
-  i) through the full protocol in the bench's 3-lane layout, against the unmodified reference's
+  i) through the full protocol in the bench's 9-lane layout, against the unmodified reference's
   own trial of the same candidate (tests/golden/verdicts_cfg2_all.json, make_golden.py);
 * config 3 (soft Neo-Hookean box / sphere objects, kinematic fingers, the reference's randomized
   material per trial) against verdicts_cfg3.json;
@@ -90,14 +90,14 @@ def test_pipelined_runner_bitwise_equals_synchronous():
 
 
 def test_cfg2_all_400_labels_match_reference(golden):
-    """All 400 bench envs, the bench's layout (3 lanes by object kind, one slot per env, the
+    """All 400 bench envs, the bench's layout (3 lanes per object kind, one slot per env, the
     device protocol, 1 round per call, pipelined), against the reference's full-protocol trials."""
     path = golden / "verdicts_cfg2_all.json"
     if not path.exists():
         pytest.skip("verdicts_cfg2_all.json not generated")
     ref = {g["i"]: g for g in json.loads(path.read_text())}
-    runner = _cfg2_runner(sorted(ref))
-    assert len(runner.lanes) == 3
+    runner = _cfg2_runner(sorted(ref), lanes_per_key=3)
+    assert len(runner.lanes) == 9
     out = runner.run()
     mix = {}
     for i, g in ref.items():
