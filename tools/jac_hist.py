@@ -38,7 +38,7 @@ def main():
         global_envs = 0
         protocol = "auto"
         record = None
-        lanes_per_kind = 1
+        lanes_per_kind = 3
         rounds_per_call = 1
         lane_priority = True
 
