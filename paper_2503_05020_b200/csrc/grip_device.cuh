@@ -478,7 +478,10 @@ struct BPShared {
 struct BPCl {
   int rank, n;
 };
-constexpr int BP_CL = 4;   // CTAs per env cluster of k_begin / k_candidates / k_linesearch
+#ifndef GRIP_BP_CL
+#define GRIP_BP_CL 4
+#endif
+constexpr int BP_CL = GRIP_BP_CL;   // CTAs per env cluster of k_begin / k_candidates / k_linesearch
 __device__ __forceinline__ BPCl bp_solo() { return BPCl{0, 1}; }
 __device__ __forceinline__ void cl_sync(const BPCl& c) {
   if (c.n > 1) {

@@ -75,7 +75,7 @@ __device__ __forceinline__ void jround2(double* s, double (&Rr)[5][9]) {
 __global__ void __launch_bounds__(TJ) k_tet_jacobi2(const int2* list, const int* n_ptr, const double* Sbuf, double* Wbuf) {
   const int n = *n_ptr;
   const int h = threadIdx.x & 1;
-  for (int idx = (blockIdx.x * TJ + threadIdx.x) >> 1; idx < n; idx += (gridDim.x * TJ) >> 1) {
+  for (int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 1; idx < n; idx += (gridDim.x * blockDim.x) >> 1) {
     const int t = list[idx].x;
     const double* Sg = Sbuf + 45 * (size_t)t;
     double s[45];
