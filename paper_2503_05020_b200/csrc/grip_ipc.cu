@@ -1403,7 +1403,11 @@ int grip_run_rounds_async(GripBatch* b, int rounds, int32_t* ticket) {
   const int E = b->n_env;
   if (!rs.h) {
     CK(cudaMallocHost(&rs.h, rslot_bytes(E)));
-    CK(cudaEventCreateWithFlags(&rs.ev, cudaEventDisableTiming));
+    // the waiting host thread sleeps instead of spinning (9 lanes per rank, up to 8 ranks per
+    // host): the next call is already queued, so the wake-up costs no GPU time (A/B on one GPU:
+    // neutral); GRIP_SPIN_SYNC=1 spins
+    const unsigned fl = cudaEventDisableTiming | (getenv("GRIP_SPIN_SYNC") ? 0u : cudaEventBlockingSync);
+    CK(cudaEventCreateWithFlags(&rs.ev, fl));
   }
   if (enqueue_rounds(b, rounds)) return -1;
   Dev& D = b->D;
