@@ -89,6 +89,20 @@ def test_pipelined_runner_bitwise_equals_synchronous():
     assert all(ln.pending is None for ln in r.lanes)
 
 
+def test_pipelined_growth_bitwise_equals_default_caps(monkeypatch):
+    """Tiny starting capacities (GRIP_SMALL_CAPS: candidates, contacts, anchors, grid cells) make
+    the pipelined calls overflow over and over: grip_rounds_wait drains, grows and clears the
+    flags while the next call is in flight, the overflowed envs' sweeps are redone from the same
+    Jacobi warm starts. The trials are bitwise those of default capacities."""
+    jobs = list(range(18))
+    ref = _cfg2_runner(jobs, slots=2).run()
+    monkeypatch.setenv("GRIP_SMALL_CAPS", "1")
+    small = _cfg2_runner(jobs, slots=2).run()
+    assert sorted(small) == jobs
+    for j in jobs:
+        assert _same_record(ref[j], small[j]), (j, ref[j], small[j])
+
+
 def test_cfg2_all_400_labels_match_reference(golden):
     """All 400 bench envs, the bench's layout (3 lanes per object kind, one slot per env, the
     device protocol, 1 round per call, pipelined), against the reference's full-protocol trials."""
