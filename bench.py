@@ -81,7 +81,8 @@ ASM_BYTES = 1256.0   # per element: its Hessian, gradient and energy read once b
 KGROUPS = {"tets": {"k_tet_scan": 1, "k_tet_front": 1, "k_tet_jacobi2@tet": 1, "k_tet_back": 1},
            "elements": {"k_elements_w": 1, "k_tet_jacobi2@contact": 1, "k_tet_finish": 1},
            "assemble_pcg": {"k_contact_K": 1, "k_assemble_direct": 1}, "candidates": {"k_candidates": 1},
-           "line_search": {"k_linesearch": 1, "k_eig_commit": 1}, "begin": {"k_begin": 1}, "finalize": {"k_finalize": 1}}
+           "line_search": {"k_linesearch": 1}, "begin": {"k_begin": 1},
+           "finalize": {"k_finalize": 1, "k_finalize_protocol": 1}}
 EL_GROUP = {"tets": ("tets",), "elements": ("affine", "contacts", "anchors")}
 NCU_FULL = [ROOT / "profiles" / "r2_ncu_full.json", ROOT / "profiles" / "r1_ncu_full_v5.json"]
 
