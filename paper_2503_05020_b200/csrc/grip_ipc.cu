@@ -116,6 +116,22 @@ struct GripBatch {
   };
   RoundSlot rslot[2];
   int rslot_next = 0;
+  // the pipelined call's launch sequence as a CUDA graph, one per readout slot (a graph's timing
+  // events are not re-recorded before that slot's readout was waited for); re-captured whenever
+  // the kernels' arguments (the Dev struct: buffers grow), the stream, the round count or the
+  // profiling switch change
+  struct RoundGraph {
+    cudaGraphExec_t exec = nullptr;
+    Dev D{};
+    cudaStream_t stream = nullptr;
+    int rounds = 0, env_cap = 0;
+    size_t dyn_smem = 0;
+    bool prof = false;
+    std::vector<std::pair<int, int>> kt;   // the captured timing event pairs
+    long long launches = 0;
+  };
+  RoundGraph rgraph[2];
+  std::vector<char> kev_owned;   // event pair owned by a captured graph (never freed by kt_collect)
   cudaEvent_t ev_reset_st = nullptr, ev_pinit_st = nullptr;   // staging consumed (copy + kernel done)
   double k_ms[NK] = {0};
   long long k_n[NK] = {0};
@@ -789,6 +805,8 @@ int grip_destroy(GripBatch* b) {
     if (rs.h) cudaFreeHost(rs.h);
     if (rs.ev) cudaEventDestroy(rs.ev);
   }
+  for (auto& g : b->rgraph)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (b->ev_reset_st) cudaEventDestroy(b->ev_reset_st);
   if (b->ev_pinit_st) cudaEventDestroy(b->ev_pinit_st);
   if (b->h_reset) cudaFreeHost(b->h_reset);
@@ -833,6 +851,14 @@ int grip_begin_step(GripBatch* b, const uint8_t* active) {
 // kernel ids for grip_kernel_stats
 enum { K_BEGIN = 0, K_CAND, K_SCAN, K_ELEM, K_ASM, K_LS, K_FIN, K_TET };
 
+// a timing event: inside a captured round graph it must be an external record (a real event
+// node, not only a dependency); outside a capture that flag is illegal
+static void kt_record(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+  else cudaEventRecord(ev, st);
+}
 static int kt_begin(GripBatch* b, int kid, cudaStream_t st = nullptr) {
   if (!b->prof) return -1;
   int pair;
@@ -847,12 +873,12 @@ static int kt_begin(GripBatch* b, int kid, cudaStream_t st = nullptr) {
       b->kev.push_back(ev);
     }
   }
-  cudaEventRecord(b->kev[2 * pair], st ? st : b->stream);
+  kt_record(b->kev[2 * pair], st ? st : b->stream);
   b->pending_k.push_back({kid, pair});
   return pair;
 }
 static void kt_end(GripBatch* b, int pair, cudaStream_t st = nullptr) {
-  if (pair >= 0) cudaEventRecord(b->kev[2 * pair + 1], st ? st : b->stream);
+  if (pair >= 0) kt_record(b->kev[2 * pair + 1], st ? st : b->stream);
 }
 // fold the recorded launch times into the per-kernel totals: the first `upto` pending launches
 // (all when negative), which must have completed
@@ -863,11 +889,14 @@ static void kt_collect(GripBatch* b, int n_listed = -1, long long upto = -1) {
   for (size_t i = 0; i < m; ++i) {
     const auto& pk = b->pending_k[i];
     float ms = 0.0f;
-    cudaEventElapsedTime(&ms, b->kev[2 * pk.second], b->kev[2 * pk.second + 1]);
+    if (cudaEventElapsedTime(&ms, b->kev[2 * pk.second], b->kev[2 * pk.second + 1]) != cudaSuccess) {
+      (void)cudaGetLastError();   // a timing gap, never an error of the product path
+      ms = 0.0f;
+    }
     b->k_ms[pk.first] += ms;
     b->k_n[pk.first] += 1;
     per[pk.first] += ms;
-    b->kev_free.push_back(pk.second);
+    if ((size_t)pk.second >= b->kev_owned.size() || !b->kev_owned[pk.second]) b->kev_free.push_back(pk.second);
   }
   if (trace && n_listed >= 0 && m)
     fprintf(stderr, "GRIP_TRACE n=%d cand=%.3f elem=%.3f asm=%.3f ls=%.3f\n", n_listed, per[1], per[3], per[4], per[5]);
@@ -1409,7 +1438,56 @@ int grip_run_rounds_async(GripBatch* b, int rounds, int32_t* ticket) {
     const unsigned fl = cudaEventDisableTiming | (getenv("GRIP_SPIN_SYNC") ? 0u : cudaEventBlockingSync);
     CK(cudaEventCreateWithFlags(&rs.ev, fl));
   }
-  if (enqueue_rounds(b, rounds)) return -1;
+  static const bool graphs = getenv("GRIP_NO_GRAPH") == nullptr && !b->D.cta_rec;
+  if (graphs && !b->D.cta_rec) {
+    GripBatch::RoundGraph& g = b->rgraph[b->rslot_next];
+    Dev cur = b->D;
+    cur.launch_seq = 0;   // diagnostic only (per-CTA timing builds, which do not use graphs)
+    const bool valid = g.exec && g.rounds == rounds && g.prof == b->prof && g.stream == b->stream &&
+                       g.env_cap == b->env_cap && g.dyn_smem == b->dyn_smem && memcmp(&g.D, &cur, sizeof(Dev)) == 0;
+    if (!valid) {
+      if (g.exec) {
+        cudaGraphExecDestroy(g.exec);
+        g.exec = nullptr;
+        for (auto& pk : g.kt) {
+          b->kev_owned[pk.second] = 0;
+          b->kev_free.push_back(pk.second);
+        }
+        g.kt.clear();
+      }
+      const size_t k0 = b->pending_k.size();
+      const long long l0 = b->launches;
+      CK(cudaStreamBeginCapture(b->stream, cudaStreamCaptureModeThreadLocal));
+      const int rc = enqueue_rounds(b, rounds);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(b->stream, &graph);
+      if (rc) return -1;
+      CK(ce);
+      CK(cudaGraphInstantiate(&g.exec, graph, 0));
+      cudaGraphDestroy(graph);
+      g.kt.assign(b->pending_k.begin() + k0, b->pending_k.end());
+      b->pending_k.resize(k0);
+      for (auto& pk : g.kt) {
+        if ((size_t)pk.second >= b->kev_owned.size()) b->kev_owned.resize(pk.second + 1, 0);
+        b->kev_owned[pk.second] = 1;
+      }
+      g.launches = b->launches - l0;
+      b->launches = l0;
+      g.D = cur;
+      g.stream = b->stream;
+      g.rounds = rounds;
+      g.prof = b->prof;
+      g.env_cap = b->env_cap;
+      g.dyn_smem = b->dyn_smem;
+    }
+    b->ev_now = false;
+    b->snap_valid = false;
+    CK(cudaGraphLaunch(g.exec, b->stream));
+    b->pending_k.insert(b->pending_k.end(), g.kt.begin(), g.kt.end());
+    b->launches += g.launches;
+  } else if (enqueue_rounds(b, rounds)) {
+    return -1;
+  }
   Dev& D = b->D;
   char* h = rs.h;
   int* hf = reinterpret_cast<int*>(h + 8);
