@@ -40,6 +40,10 @@ import os
 # 9 runner lanes x 3 streams: 32 hardware work queues instead of the default 8 (before any CUDA use;
 # the package sets the same default)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# 9 lane threads + the main thread per rank: sleep instead of spinning on a call's readout when the
+# ranks' threads would outnumber the host cores
+if int(os.environ.get("WORLD_SIZE", "1")) * 10 > (os.cpu_count() or 1):
+    os.environ.setdefault("GRIP_BLOCKING_SYNC", "1")
 import subprocess
 import sys
 import threading

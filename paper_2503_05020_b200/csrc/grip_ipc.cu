@@ -1432,13 +1432,12 @@ int grip_run_rounds_async(GripBatch* b, int rounds, int32_t* ticket) {
   const int E = b->n_env;
   if (!rs.h) {
     CK(cudaMallocHost(&rs.h, rslot_bytes(E)));
-    // the waiting host thread sleeps instead of spinning (9 lanes per rank, up to 8 ranks per
-    // host): the next call is already queued, so the wake-up costs no GPU time (A/B on one GPU:
-    // neutral); GRIP_SPIN_SYNC=1 spins
-    const unsigned fl = cudaEventDisableTiming | (getenv("GRIP_SPIN_SYNC") ? 0u : cudaEventBlockingSync);
+    // GRIP_BLOCKING_SYNC=1: the waiting host thread sleeps instead of spinning (bench.py sets it
+    // when its ranks' lane threads would outnumber the host cores); spinning is ~0.5 % faster
+    const unsigned fl = cudaEventDisableTiming | (getenv("GRIP_BLOCKING_SYNC") ? cudaEventBlockingSync : 0u);
     CK(cudaEventCreateWithFlags(&rs.ev, fl));
   }
-  static const bool graphs = getenv("GRIP_NO_GRAPH") == nullptr && !b->D.cta_rec;
+  static const bool graphs = getenv("GRIP_GRAPH") != nullptr && !b->D.cta_rec;   // opt-in: see DESIGN §6
   if (graphs && !b->D.cta_rec) {
     GripBatch::RoundGraph& g = b->rgraph[b->rslot_next];
     Dev cur = b->D;
