@@ -1437,7 +1437,7 @@ int grip_run_rounds_async(GripBatch* b, int rounds, int32_t* ticket) {
     const unsigned fl = cudaEventDisableTiming | (getenv("GRIP_BLOCKING_SYNC") ? cudaEventBlockingSync : 0u);
     CK(cudaEventCreateWithFlags(&rs.ev, fl));
   }
-  static const bool graphs = getenv("GRIP_GRAPH") != nullptr && !b->D.cta_rec;   // opt-in: see DESIGN §6
+  const bool graphs = getenv("GRIP_GRAPH") != nullptr && !b->D.cta_rec;   // opt-in: see DESIGN §6
   if (graphs && !b->D.cta_rec) {
     GripBatch::RoundGraph& g = b->rgraph[b->rslot_next];
     Dev cur = b->D;

@@ -103,6 +103,18 @@ def test_pipelined_growth_bitwise_equals_default_caps(monkeypatch):
         assert _same_record(ref[j], small[j]), (j, ref[j], small[j])
 
 
+def test_graph_replay_bitwise(monkeypatch):
+    """GRIP_GRAPH=1 (each pipelined call replayed from a captured CUDA graph, re-captured after
+    buffer growth) gives bitwise the trials of direct launches, from tiny capacities too."""
+    jobs = list(range(12))
+    ref = _cfg2_runner(jobs, slots=2).run()
+    monkeypatch.setenv("GRIP_GRAPH", "1")
+    monkeypatch.setenv("GRIP_SMALL_CAPS", "1")
+    g = _cfg2_runner(jobs, slots=2).run()
+    for j in jobs:
+        assert _same_record(ref[j], g[j]), (j, ref[j], g[j])
+
+
 def test_cfg2_all_400_labels_match_reference(golden):
     """All 400 bench envs, the bench's layout (3 lanes per object kind, one slot per env, the
     device protocol, 1 round per call, pipelined), against the reference's full-protocol trials."""
