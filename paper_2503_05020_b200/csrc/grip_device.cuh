@@ -152,6 +152,9 @@ struct Dev {
                      // on the second stream, concurrently with k_candidates writing flags)
   int* work_off;     // per list position (n+1)
   int* cwork_off;    // per list position (n+1): contact / friction elements only
+  int* asm_key;      // per list position: contact / friction elements (the work scan)
+  int* asm_order;    // the list's envs by descending contact work: the assembly and line search
+                     // launch their heavy envs first (a launch lasts as long as its heaviest CTA)
   int* twork_off;    // per list position (n+1): tets only (k_tet_front)
   int* swork_off;    // per list position (n+1): static 3x3 blocks of H_ff (k_static)
   // anchors (persist across steps)

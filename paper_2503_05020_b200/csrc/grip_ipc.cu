@@ -662,6 +662,8 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
   D.tflag = b->alloc<int>(E);
   D.work_off = b->alloc<int>(E + 1);
   D.cwork_off = b->alloc<int>(E + 1);
+  D.asm_key = b->alloc<int>(E + 1);
+  D.asm_order = b->alloc<int>(E + 1);
   D.twork_off = b->alloc<int>(E + 1);
   D.ev_n = b->alloc<int>(E);
   D.ev_on = 0;
@@ -766,7 +768,7 @@ int grip_create(const GripSceneDesc* d, int device, GripBatch** out) {
         D.pcg_r, D.pcg_z, D.pcg_p, D.pcg_q, D.pcg_b, D.pcg_pinv, D.abd_pinv, D.sb_val, D.c_u, D.c_w, D.ls_y, D.c_r,
         D.inc_ptr, D.inc, D.sv_g, D.body_com, D.max_speed, D.min_J, D.stats, D.fin_done, D.cs_pt, D.cs_ee, D.cs_eid,
         D.cs_n, D.cs_R, D.cs_valid, D.cs_drift, D.md_prev, D.md_kin, D.bp_lc, D.dense_L, D.tet_eig, D.body_tri_lo,
-        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.sb_dst, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n, D.eig_par, D.eig_swept};
+        D.body_tri_hi, D.body_edge_lo, D.body_edge_hi, D.dense_perm, D.dense_fc, D.dense_tail, D.sb_row, D.sb_dst, D.el_K, D.el_kn, D.sc_lst, D.sc_off, D.sv_code, D.tet_S, D.tet_W, D.jac_list, D.jac_n, D.cjac_S, D.cjac_W, D.cjac_list, D.cjac_n, D.eig_par, D.eig_swept, D.asm_key, D.asm_order};
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i)
       if (!ptrs[i]) {
         g_err = "internal: device buffer " + std::to_string(i) + " not allocated";
@@ -1095,14 +1097,14 @@ static void sweep_launch(GripBatch* b, int n, const int* list) {
   if (b->direct) {
     k_contact_K<<<148 * 2, KT, 0, b->stream>>>(D, list, n);
     D.launch_seq = ++b->seq_ctr;
-    k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, list, b->env_cap);
+    k_assemble_direct<<<n, NT, b->dyn_smem, b->stream>>>(D, D.asm_order, b->env_cap);   // heavy envs first
   } else {
     k_assemble_solve<<<n, NT, 0, b->stream>>>(D, list);
   }
   kt_end(b, t);
   t = kt_begin(b, K_LS);
   D.launch_seq = ++b->seq_ctr;
-  k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, list);
+  k_linesearch<<<n * BP_CL, NT, 0, b->stream>>>(D, D.asm_order);   // heavy envs first
   kt_end(b, t);
   b->launches += 6 + 2 + 3 + (b->direct ? 2 : 1) + 1;
   b->sweeps += 1;

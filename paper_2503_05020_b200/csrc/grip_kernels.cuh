@@ -376,6 +376,7 @@ __device__ void work_scan_body(const Dev& D, const int* list, int n, Red& sm) {
         cc += D.n_act[e]; cf += D.n_anc[e]; cn += 1.0;
       }
     }
+    if (i < n) D.asm_key[i] = wc;
     int tot;
     const int pre = block_scan(w, sm, &tot);
     if (i < n) D.work_off[i] = base + pre;
@@ -383,6 +384,17 @@ __device__ void work_scan_body(const Dev& D, const int* list, int n, Red& sm) {
     const int cpre = block_scan(wc, sm, &tot);
     if (i < n) D.cwork_off[i] = cbase + cpre;
     cbase += tot;
+  }
+  __syncthreads();
+  // heavy envs first: rank by (contact work descending, list position ascending)
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const int ki = D.asm_key[i];
+    int r = 0;
+    for (int j = 0; j < n; ++j) {
+      const int kj = D.asm_key[j];
+      r += (kj > ki) || (kj == ki && j < i);
+    }
+    D.asm_order[r] = list[i];
   }
   cc = block_sum(cc, sm); cf = block_sum(cf, sm);
   cn = block_sum(cn, sm);
