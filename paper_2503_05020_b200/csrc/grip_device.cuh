@@ -30,7 +30,10 @@ __device__ unsigned long long g_phase[64];   // diagnostic counters (grip_debug_
 #endif
 constexpr int NT = GRIP_NT;       // threads per env CTA (256; GRIP_NT=512 builds are an A/B experiment)
 constexpr int NWARP = NT / 32;
-constexpr int NT_MINB3 = NT == 256 ? 3 : 1;   // CTAs per SM the heavy CTA-per-env kernels are built for
+#ifndef GRIP_MINB
+#define GRIP_MINB 3
+#endif
+constexpr int NT_MINB3 = NT == 256 ? GRIP_MINB : 1;   // CTAs per SM the heavy CTA-per-env kernels are built for
 constexpr int MAXC = 4096;        // broad-phase grid cells per env
 
 // error / flag bits per env and Newton sweep
