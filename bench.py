@@ -4,9 +4,10 @@ Workload (BASELINE.json configs[1], the default): 400 environments per GPU, each
 UMI-style two-pad gripper grasping a rigid (ABD) box / cylinder / sphere (env i: kind i % 3,
 the reference-sampled antipodal candidate of seed i), run through the reference's validation
 protocol (settle, force-halted closing, hold, six gravity phases; protocol.py:152-277) by
-``runner.TrialRunner``: one device batch ("lane") per object kind, each with its own CUDA stream
-and host thread, the protocol state machine on the device, and every finished trial's slot
-refilled in place with the rank's next candidate (dataset-generation steady state).
+``runner.TrialRunner``: three device batches ("lanes") per object kind, each with its own CUDA
+streams and host thread, the protocol state machine on the device, one round per host call with
+the next call already queued (pipelined), and every finished trial's slot refilled in place with
+the rank's next candidate (dataset-generation steady state).
 ``--config 3`` runs 400 soft Neo-Hookean objects with kinematic fingers and the reference's
 randomized material; ``--config 4`` 200 bimanual envs (two soft grippers, one soft object) with
 the recorder's stress field output every step; ``--sweep`` the config-5 env-count sweep.
