@@ -15,6 +15,11 @@ job of a key goes to that key's lanes.  Results are per job and independent of t
 slot count and refill order (every slot reset returns the env to a fresh state, which the GPU
 tests check bitwise), so the same records come out of 1 lane of 400 slots or 3 lanes of 40.
 
+Each host call runs one device round and is pipelined: the lane enqueues the next call
+(``grip_run_rounds_async``) before it waits for the previous one's readout (``grip_rounds_wait``),
+so recording finished trials and refilling their slots overlaps the device; refills queue behind
+the call in flight, whose readout then predates them (those slots are skipped once).
+
 ``cycle=True`` wraps each key's queue around (steady-state throughput: the bench); otherwise a
 lane stops once its queue is empty and all its slots are idle.
 """
