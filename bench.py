@@ -12,7 +12,7 @@ the rank's next candidate (dataset-generation steady state).
 randomized material; ``--config 4`` 200 bimanual envs (two soft grippers, one soft object) with
 the recorder's stress field output every step; ``--sweep`` the config-5 env-count sweep.
 
-A bench "step" is ``--rounds-per-step`` (16) continuous-batching rounds of the lane with the most
+A bench "step" is ``--rounds-per-step`` (32) continuous-batching rounds of the lane with the most
 envs (one round = one Newton sweep of every unfinished env plus begin / finalize / protocol for
 the envs at a time-step boundary); the other lanes keep running until it is done.  Before the
 W timed-out warm-up steps end, every slot must also have finished one trial (steady phase mix,
@@ -684,7 +684,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="envs per GPU (default: the config's)")
     ap.add_argument("--global-envs", type=int, default=0, help="strong scaling: total envs split over the ranks")
     ap.add_argument("--sweep", default="", help="config 5: comma-separated env counts, one JSON line each")
-    ap.add_argument("--rounds-per-step", type=int, default=16)
+    ap.add_argument("--rounds-per-step", type=int, default=32)
     ap.add_argument("--rounds-per-call", type=int, default=1, help="device protocol: rounds per host call")
     ap.add_argument("--lanes-per-kind", type=int, default=3)
     ap.add_argument("--no-pipeline", action="store_true", help="device protocol: wait for each call before "
