@@ -61,12 +61,12 @@ UNIT = "env-steps/s"
 REF_DIR = ROOT / "baseline" / "_ref"
 
 WORKLOADS = {
-    2: dict(envs=400, mode="device", workload="cfg2: soft 2-pad UMI-style gripper on rigid (ABD) box/cylinder/sphere, "
+    2: dict(envs=400, mode="device", lanes=3, workload="cfg2: soft 2-pad UMI-style gripper on rigid (ABD) box/cylinder/sphere, "
                                               "full grasp protocol, antipodal candidate seed i (kind i % 3)"),
-    3: dict(envs=400, mode="device", workload="cfg3: soft Neo-Hookean box/sphere (kind i % 2) with kinematic fingers, "
+    3: dict(envs=400, mode="device", lanes=6, workload="cfg3: soft Neo-Hookean box/sphere (kind i % 2) with kinematic fingers, "
                                               "randomized material (E log-uniform 1e4-1e7, mu 0.1-1), friction, full "
                                               "grasp protocol"),
-    4: dict(envs=200, mode="host", workload="cfg4: bimanual, two soft 2-pad grippers on one soft cube (yaw i), full "
+    4: dict(envs=200, mode="host", lanes=5, workload="cfg4: bimanual, two soft 2-pad grippers on one soft cube (yaw i), full "
                                             "grasp protocol with 4 halting pads, recorder frames incl. stress field "
                                             "every step"),
 }
@@ -466,7 +466,8 @@ def build_runner(args, cfg, envs, rank, world, writer=None):
     if record:
         mode = "host"
     on_record = None if writer is None else (lambda j, r: writer.put(j, r))
-    runner = TrialRunner(jobs, scene_of, key_of, slots=None, lanes_per_key=args.lanes_per_kind,
+    lanes = args.lanes_per_kind or WORKLOADS[cfg]["lanes"]   # measured best per config
+    runner = TrialRunner(jobs, scene_of, key_of, slots=None, lanes_per_key=lanes,
                          rounds_per_call=args.rounds_per_call, priority=prio if args.lane_priority else None,
                          cycle=True, device=None, mode=mode, record=record, on_record=on_record,
                          pipeline=not getattr(args, "no_pipeline", False))
@@ -686,7 +687,8 @@ def main():
     ap.add_argument("--sweep", default="", help="config 5: comma-separated env counts, one JSON line each")
     ap.add_argument("--rounds-per-step", type=int, default=32)
     ap.add_argument("--rounds-per-call", type=int, default=1, help="device protocol: rounds per host call")
-    ap.add_argument("--lanes-per-kind", type=int, default=3)
+    ap.add_argument("--lanes-per-kind", type=int, default=0,
+                    help="device batches per object kind (default: the config's measured best, 3 / 6 / 5)")
     ap.add_argument("--no-pipeline", action="store_true", help="device protocol: wait for each call before "
                     "enqueuing the next (no host / device overlap)")
     ap.add_argument("--no-lane-priority", dest="lane_priority", action="store_false")
